@@ -1,0 +1,179 @@
+/*
+ * prlab_gpu.h -- C-ABI drop-in boundary of the B200-native prlab forward.
+ *
+ * The reference (`prlab`, C++20) has no FFI layer: its operator API is the set
+ * of value-semantic free functions in include/prlab/kernels.hpp:30-70 plus
+ * forward()/build_model()/resolve_policy() (include/prlab/model.hpp:88-140,
+ * include/prlab/policy.hpp:66).  Each entry point below replaces one of those
+ * (cited per function).  Plain pointers and sizes only -- no torch or C++ types.
+ * include/prlab_gpu.hpp wraps this ABI back into the reference's C++ signatures
+ * (same names, same exception types and messages).
+ *
+ * Errors: every function returns PRLAB_OK (0) or a status; the thread-local
+ * message is available from prlab_gpu_last_error().  The status maps onto the
+ * reference's exception types: PRLAB_EINVAL -> std::invalid_argument,
+ * PRLAB_ERANGE -> std::out_of_range, PRLAB_ERUNTIME / PRLAB_ECUDA ->
+ * std::runtime_error.  There is no CPU fallback anywhere behind this ABI: a
+ * missing/unsupported device is PRLAB_ECUDA.
+ */
+#ifndef PRLAB_GPU_H
+#define PRLAB_GPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PRLAB_GPU_ABI_VERSION 1
+
+enum prlab_status {
+  PRLAB_OK = 0,
+  PRLAB_EINVAL = 1,   /* std::invalid_argument */
+  PRLAB_ERANGE = 2,   /* std::out_of_range     */
+  PRLAB_ERUNTIME = 3, /* std::runtime_error    */
+  PRLAB_ECUDA = 4     /* CUDA error -> std::runtime_error */
+};
+
+/* Lattices: reference Dtype (include/prlab/tensor.hpp:17). */
+enum prlab_dtype { PRLAB_F32 = 0, PRLAB_F16E = 1 };
+
+/* Reference KernelConfig (include/prlab/kernels.hpp:16-22). */
+typedef struct {
+  int32_t compute;    /* prlab_dtype */
+  int32_t accum;      /* prlab_dtype */
+  int32_t stabilized; /* softmax only */
+} prlab_kcfg;
+
+/* Op classes in the reference order (include/prlab/policy.hpp:19-27). */
+enum prlab_op_class {
+  PRLAB_LINEAR = 0,
+  PRLAB_ATTENTION_SCORE_MATMUL = 1,
+  PRLAB_SOFTMAX = 2,
+  PRLAB_LAYERNORM = 3,
+  PRLAB_ACTIVATION = 4,
+  PRLAB_EMBEDDING = 5,
+  PRLAB_RESIDUAL = 6,
+  PRLAB_NUM_OP_CLASSES = 7
+};
+
+/* Reference PrecisionPolicy assignment (include/prlab/policy.hpp:43-56). */
+typedef struct {
+  prlab_kcfg cls[PRLAB_NUM_OP_CLASSES];
+} prlab_policy;
+
+/* Reference ModelConfig (include/prlab/model.hpp:21-52); archetype 0 = encoder_only, 1 = decoder_only. */
+typedef struct {
+  int32_t archetype;
+  int64_t num_layers, hidden, heads, ffn, vocab, max_positions;
+  uint64_t seed;
+} prlab_model_desc;
+
+/* Reference ForwardTrace instrumentation (include/prlab/model.hpp:113-125):
+ * seconds per op class (CUDA-event time, instrumented mode only) and kernel
+ * invocation counts per (class, compute dtype). */
+typedef struct {
+  double seconds[PRLAB_NUM_OP_CLASSES];
+  uint64_t kernel_calls[PRLAB_NUM_OP_CLASSES][2];
+} prlab_trace;
+
+typedef struct prlab_gpu_model prlab_gpu_model;
+
+/* Output storage of device-resident logits. */
+enum prlab_out_dtype { PRLAB_OUT_F32 = 0, PRLAB_OUT_F16 = 1 };
+
+const char* prlab_gpu_last_error(void);
+int prlab_gpu_abi_version(void);
+
+/* ---- policy: resolve_policy (src/policy.cpp:49-67) ---- */
+int prlab_gpu_resolve_policy(const char* name, prlab_policy* out);
+/* PrecisionPolicy::validate / KernelConfig::validate (src/policy.cpp:27-47, src/kernels.cpp:33-38) */
+int prlab_gpu_validate_policy(const prlab_policy* p);
+
+/* ---- model: build_model output -> device arena (replaces the per-call
+ * on_lattice copies of src/kernels.cpp:16-22 with one preplanned upload).
+ * params: host fp32 tensors in the canonical Model::for_each_param order
+ * (src/model.cpp:178-209), n_params tensors. */
+int prlab_gpu_model_create(const prlab_model_desc* desc, const float* const* params,
+                           int64_t n_params, int device, prlab_gpu_model** out);
+/* Same, with the canonical tensors concatenated into one flat buffer. */
+int prlab_gpu_model_create_flat(const prlab_model_desc* desc, const float* flat, int device,
+                                prlab_gpu_model** out);
+void prlab_gpu_model_destroy(prlab_gpu_model* m);
+/* Bytes held on the device: resident weights (per precision copy) and the
+ * activation workspace currently planned. */
+int prlab_gpu_model_memory(const prlab_gpu_model* m, uint64_t* weight_bytes,
+                           uint64_t* workspace_bytes);
+
+/* ---- host fixture generators, same streams as the reference ----
+ * build_model (src/model.cpp:217-265): N(0,0.02) fixed Box-Muller over
+ * mt19937_64(seed) in canonical order, biases 0, gammas 1.  out: param_count floats. */
+int prlab_gpu_build_model(const prlab_model_desc* desc, float* out, int64_t out_len);
+uint64_t prlab_gpu_param_count(const prlab_model_desc* desc);   /* src/model.cpp:267-281 */
+/* random_tokens (src/model.cpp:283-296): ids[i] = mt19937_64(seed)() % vocab. */
+int prlab_gpu_random_tokens(int64_t vocab, int64_t batch, int64_t seq, uint64_t seed, int32_t* ids);
+/* Greedy argmax over device logits rows (lowest index wins ties): d_logits [rows, ld]
+ * in out_dtype, d_tokens int32 [rows].  Asynchronous on stream. */
+int prlab_gpu_argmax_device(const void* d_logits, int32_t dtype, int64_t rows, int64_t n, int64_t ld,
+                            int32_t* d_tokens, void* stream);
+
+/* ---- forward (src/model.cpp:456-482) ----
+ * Drop-in form: host token ids [B*S], host fp32 logits [B,S,V] (or [B,S,h]
+ * for a zero-layer model), synchronous.  trace may be NULL. */
+int prlab_gpu_forward(prlab_gpu_model* m, const int32_t* ids, int64_t batch, int64_t seq,
+                      const prlab_policy* policy, float* logits, prlab_trace* trace);
+
+/* Device-resident form: d_ids [B*S] int32 on the device, logits written to
+ * d_out with row pitch `ld` elements (ld >= V) in out_dtype.  Asynchronous on
+ * `stream` (cudaStream_t; NULL = legacy default).  With use_graph != 0 the
+ * forward is captured once per (B,S,policy,out) key and replayed as a CUDA
+ * graph.  Ids are validated on the device; an out-of-range id is reported by
+ * the next call to prlab_gpu_sync_status(). */
+int prlab_gpu_forward_device(prlab_gpu_model* m, const int32_t* d_ids, int64_t batch,
+                             int64_t seq, const prlab_policy* policy, void* d_out,
+                             int32_t out_dtype, int64_t ld, void* stream, int32_t use_graph);
+/* Synchronizes the stream and reports deferred device-side errors (bad ids). */
+int prlab_gpu_sync_status(prlab_gpu_model* m, void* stream);
+/* Number of kernels one forward_device launch issues for this key (for bench accounting). */
+int prlab_gpu_forward_kernel_count(prlab_gpu_model* m, int64_t batch, int64_t seq,
+                                   const prlab_policy* policy, int64_t* count);
+
+/* ---- per-operator entry points mirroring include/prlab/kernels.hpp:30-70.
+ * Host fp32 buffers in/out (the reference's Tensor storage), synchronous. */
+int prlab_gpu_matmul(const float* a, const float* b, int64_t m, int64_t k, int64_t n,
+                     prlab_kcfg cfg, float* out);                        /* kernels.cpp:40 */
+int prlab_gpu_attention_scores(const float* q, const float* k, int64_t sq, int64_t sk,
+                               int64_t d, float scale, prlab_kcfg cfg, float* out,
+                               float* capture_f32);                      /* kernels.cpp:85 */
+int prlab_gpu_softmax(const float* x, int64_t rows, int64_t n, prlab_kcfg cfg,
+                      float* out);                                       /* kernels.cpp:127 */
+int prlab_gpu_layernorm(const float* x, int64_t rows, int64_t n, const float* gamma,
+                        const float* beta, float eps, prlab_kcfg cfg,
+                        float* out);                                     /* kernels.cpp:170 */
+int prlab_gpu_gelu(const float* x, int64_t n, prlab_kcfg cfg, float* out);      /* kernels.cpp:221 */
+int prlab_gpu_add(const float* a, const float* b, int64_t n, prlab_kcfg cfg,
+                  float* out);                                           /* kernels.cpp:237 */
+int prlab_gpu_tanh(const float* x, int64_t n, prlab_kcfg cfg, float* out);      /* kernels.cpp:296 */
+int prlab_gpu_embed(const float* tok, int64_t vocab, const float* pos, int64_t npos,
+                    int64_t h, const int32_t* ids, int64_t batch, int64_t seq, prlab_kcfg cfg,
+                    float* out);                                         /* kernels.cpp:256 */
+
+/* ---- device-pointer building blocks (tests / bench of the hot kernels) ----
+ * Hybrid Linear on tensor cores (tcgen05): out = epi(round16(A.W^T)), A fp16
+ * [M,K] row-major, Wt fp16 [N,K] row-major (K-major), bias fp32 [N] or NULL.
+ * epi: 0 = bias -> fp16 out; 1 = bias+GELU -> fp16 out; 2 = bias then fp32
+ * residual add in place into out (fp32 [M,N]); 3 = no bias -> fp16 out.
+ * ldo = row pitch of out in elements. */
+int prlab_gpu_linear_f16_device(const void* A, const void* Wt, const float* bias, void* out,
+                                int64_t M, int64_t N, int64_t K, int64_t ldo, int32_t epi,
+                                void* stream);
+/* Fused hybrid attention on tensor cores: qkv fp16 [B*S, 3h] (q|k|v), ctx fp16 [B*S, h]. */
+int prlab_gpu_attention_f16_device(const void* qkv, void* ctx, int64_t batch, int64_t seq,
+                                   int64_t heads, int64_t head_dim, int32_t causal,
+                                   void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PRLAB_GPU_H */

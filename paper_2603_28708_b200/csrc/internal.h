@@ -1,0 +1,124 @@
+// Host-side declarations shared between the C-ABI layer and the kernel files.
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+
+namespace prlab_gpu {
+
+// Exceptions thrown inside the library and mapped onto prlab_status codes at
+// the C-ABI boundary (same classes the reference throws).
+struct cuda_error : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define PRLAB_CUDA(call)                                                                    \
+  do {                                                                                      \
+    cudaError_t e_ = (call);                                                                \
+    if (e_ != cudaSuccess)                                                                  \
+      throw ::prlab_gpu::cuda_error(std::string(#call) + ": " + cudaGetErrorString(e_));    \
+  } while (0)
+
+int num_sms();
+
+// --- TMA descriptors (driver entry point fetched through the runtime) ---
+// 2-D fp16 tensor [rows, cols] with row pitch `pitch_elems`, box {box_cols, box_rows},
+// 128-byte swizzle (box_cols * 2 must be 128).
+CUtensorMap make_tmap_f16_2d(const void* base, uint64_t rows, uint64_t cols, uint64_t pitch_elems,
+                             uint32_t box_rows, uint32_t box_cols);
+// 3-D fp16 tensor [d2, d1, d0] (d0 contiguous) with pitches in elements.
+CUtensorMap make_tmap_f16_3d(const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                             uint64_t pitch1_elems, uint64_t pitch2_elems, uint32_t box0,
+                             uint32_t box1, uint32_t box2);
+
+// --- tcgen05 GEMM: out = epi(A[M,K] . Wt[N,K]^T) ---
+enum GemmEpi : int {
+  EPI_BIAS_F16 = 0,       // round16(round16(acc) + b)              -> fp16
+  EPI_BIAS_GELU_F16 = 1,  // round16(gelu(round16(round16(acc)+b))) -> fp16
+  EPI_BIAS_RESID_F32 = 2, // x += round16(round16(acc) + b)          (fp32, in place)
+  EPI_F16 = 3,            // round16(acc)                           -> fp16
+};
+struct GemmPlan {
+  CUtensorMap tmA, tmB;
+  int M, N, K, bn, epi;
+  const float* bias;
+  void* out;
+  int64_t ldo;
+  int grid;
+  int kernel_count() const { return 1; }
+};
+GemmPlan plan_gemm_tc(const void* A, int64_t lda, const void* Wt, int64_t ldw, const float* bias,
+                      void* out, int64_t ldo, int M, int N, int K, int epi);
+void launch_gemm_tc(const GemmPlan& p, cudaStream_t st);
+void configure_gemm_tc();
+
+// --- fused tensor-core attention (hybrid, head_dim 64, seq <= 512) ---
+struct AttnPlan {
+  CUtensorMap tmQKV;
+  void* ctx;
+  int B, S, H, hd, causal;
+  int64_t ld_qkv, ld_ctx;
+};
+bool attn_tc_supported(int S, int hd);
+AttnPlan plan_attn_tc(const void* qkv, int64_t ld_qkv, void* ctx, int64_t ld_ctx, int B, int S,
+                      int H, int hd, int causal);
+void launch_attn_tc(const AttnPlan& p, cudaStream_t st);
+void configure_attn_tc();
+
+// --- SIMT kernels (any shape, any policy; fp32 storage) ---
+struct Kcfg {
+  int compute, accum, stabilized;
+};
+// out[m,n] = epilogue( sum_k A[m,k] * Bt[n,k] ) with the reference linear_bias /
+// matmul semantics under `lin`; op: 0 none, 1 gelu (act cfg), 2 residual add
+// into `resid` (res cfg, written to out).
+struct SimtGemmEpi {
+  const float* bias;  // may be null (plain matmul)
+  int op;
+  Kcfg act, res;
+  const float* resid;  // residual input (may alias out)
+};
+void simt_gemm(const float* A, int64_t lda, const float* Bt, int64_t ldb, float* out,
+               int64_t ldo, int M, int N, int K, Kcfg lin, const SimtGemmEpi& epi,
+               cudaStream_t st);
+void simt_embed(const float* tok, int64_t vocab, const float* pos, int h, const int32_t* ids,
+                int B, int S, Kcfg cfg, float* out, int* err_flag, cudaStream_t st);
+void simt_layernorm(const float* x, int rows, int n, const float* gamma, const float* beta,
+                    float eps, Kcfg cfg, float* out_f32, __half* out_f16, int round_out16,
+                    cudaStream_t st);
+// Generic attention: q/k/v columns inside row-major [B*S, ld] buffers.
+void simt_attention(const float* q, const float* k, const float* v, int64_t ld_in, float* ctx,
+                    int64_t ld_ctx, int B, int S, int H, int hd, float scale, int causal,
+                    Kcfg att, Kcfg sm, float* tap, cudaStream_t st);
+void simt_scores(const float* q, const float* k, int sq, int sk, int d, float scale, Kcfg cfg,
+                 float* out, float* tap, cudaStream_t st);
+void simt_softmax(const float* x, int64_t rows, int64_t n, Kcfg cfg, float* out, cudaStream_t st);
+void simt_gelu(const float* x, int64_t n, Kcfg cfg, float* out, cudaStream_t st);
+void simt_add(const float* a, const float* b, int64_t n, Kcfg cfg, float* out, cudaStream_t st);
+void simt_tanh(const float* x, int64_t n, Kcfg cfg, float* out, cudaStream_t st);
+void simt_round_copy(const float* x, int64_t n, int f16, float* out, cudaStream_t st);
+// fp16 padded [M, ld16] -> fp32 dense [M, N]
+void convert_f16_to_f32(const __half* in, int64_t ld_in, float* out, int64_t ld_out, int M, int N,
+                        cudaStream_t st);
+void f32_to_f16(const float* in, __half* out, int64_t n, cudaStream_t st);
+void transpose_f32(const float* in, int rows, int cols, float* out, int round16, cudaStream_t st);
+void transpose_to_f16(const float* in, int rows, int cols, __half* out, int64_t ld_out,
+                      cudaStream_t st);
+void round16_inplace(float* x, int64_t n, cudaStream_t st);
+
+// fast-path LayerNorm for h % 128 == 0 (warp per row): fp32 x -> fp16 lattice (hybrid)
+void ln_f32_to_f16(const float* x, int rows, int n, const float* gamma, const float* beta,
+                   float eps, __half* out, cudaStream_t st);
+// fast embed for the hybrid path (fp32 add, float4)
+void embed_f32(const float* tok, int64_t vocab, const float* pos, int h, const int32_t* ids,
+               int B, int S, float* out, int* err_flag, cudaStream_t st);
+
+// greedy argmax per row (lowest index wins ties, NaN never wins); dtype 0 fp32, 1 fp16
+void argmax_rows(const void* logits, int dtype, int64_t rows, int64_t n, int64_t ld, int32_t* out,
+                 cudaStream_t st);
+
+}  // namespace prlab_gpu

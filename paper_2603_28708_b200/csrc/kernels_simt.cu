@@ -1,0 +1,654 @@
+// SIMT CUDA kernels: the generic (any shape, any per-class policy) path and the
+// HBM-bound LayerNorm / embedding kernels of the fast path.
+//
+// The generic kernels keep fp32 storage and honour the reference KernelConfig
+// of each op class exactly: inputs conformed onto the compute lattice,
+// F16E accumulation rounded after every product and partial sum in ascending
+// order (src/kernels.cpp:55-66), outputs conformed.  Products of fp16-lattice
+// values are exact in fp32, so fmaf() is bit-identical to the reference's
+// separate multiply+add under the hybrid config.
+#include "common.cuh"
+#include "internal.h"
+
+namespace prlab_gpu {
+
+namespace {
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+inline int blocks_for(int64_t n, int threads) {
+  const int64_t b = (n + threads - 1) / threads;
+  return static_cast<int>(b < (1 << 30) ? b : (1 << 30));
+}
+
+// ---------------------------------------------------------------------------
+// generic GEMM: out[m, n] = epi( sum_k A[m, k] * Bt[n, k] )  (reference matmul +
+// linear_bias + fused GELU / residual).  64x64 tile, BK 16, 256 threads, 4x4
+// outputs per thread, ascending-k accumulation per output.
+// MODE 0: F32/F32 (fmaf)   1: F16E/F32 (inputs rounded; fmaf exact)   2: F16E/F16E
+// ---------------------------------------------------------------------------
+struct GemmEpiDev {
+  const float* bias;
+  int op;
+  int lin_c, act_c, res_c;
+  const float* resid;
+};
+
+template <int MODE>
+__global__ void __launch_bounds__(256) simt_gemm_kernel(const float* __restrict__ A, int64_t lda,
+                                                        const float* __restrict__ Bt, int64_t ldb,
+                                                        float* out, int64_t ldo, int M, int N,
+                                                        int K, GemmEpiDev e) {
+  __shared__ float As[16][64 + 4];
+  __shared__ float Bs[16][64 + 4];
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.0f;
+
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    // 64 rows x 16 k for A and Bt: 1024 values each, 4 per thread
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int idx = threadIdx.x + i * 256;
+      const int r = idx >> 4, kk = idx & 15;
+      float av = 0.0f, bv = 0.0f;
+      if (m0 + r < M && k0 + kk < K) av = A[static_cast<int64_t>(m0 + r) * lda + k0 + kk];
+      if (n0 + r < N && k0 + kk < K) bv = Bt[static_cast<int64_t>(n0 + r) * ldb + k0 + kk];
+      if (MODE != 0) {
+        av = r16(av);
+        bv = r16(bv);
+      }
+      As[kk][r] = av;
+      Bs[kk][r] = bv;
+    }
+    __syncthreads();
+    const int kmax = min(16, K - k0);
+    for (int kk = 0; kk < kmax; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          if (MODE == 2)
+            acc[i][j] = r16(__fadd_rn(acc[i][j], r16(__fmul_rn(a[i], b[j]))));
+          else
+            acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        }
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int m = m0 + ty * 4 + i;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int n = n0 + tx * 4 + j;
+      if (n >= N) continue;
+      float v = conform(acc[i][j], e.lin_c);
+      if (e.bias) v = conform(__fadd_rn(v, conform(e.bias[n], e.lin_c)), e.lin_c);
+      if (e.op == 1) {
+        const float x = conform(v, e.act_c);
+        v = conform(gelu_erf(x), e.act_c);
+      } else if (e.op == 2) {
+        const float x = conform(e.resid[static_cast<int64_t>(m) * ldo + n], e.res_c);
+        v = conform(__fadd_rn(x, conform(v, e.res_c)), e.res_c);
+      }
+      out[static_cast<int64_t>(m) * ldo + n] = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// embedding gather + add, reference src/kernels.cpp:256-294
+// ---------------------------------------------------------------------------
+__global__ void simt_embed_kernel(const float* __restrict__ tok, int64_t vocab,
+                                  const float* __restrict__ pos, int h,
+                                  const int32_t* __restrict__ ids, int B, int S, int c16,
+                                  float* __restrict__ out, int* err) {
+  const int64_t total = static_cast<int64_t>(B) * S * h;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / h;
+    const int c = static_cast<int>(i % h);
+    const int32_t id = ids[r];
+    if (id < 0 || id >= vocab) {
+      if (err) atomicExch(err, 1);
+      out[i] = 0.0f;
+      continue;
+    }
+    const float t = conform(tok[static_cast<int64_t>(id) * h + c], c16);
+    const float p = conform(pos[static_cast<int64_t>(r % S) * h + c], c16);
+    out[i] = conform(__fadd_rn(t, p), c16);
+  }
+}
+
+// fast path: fp32 gather + add with float4 (h % 4 == 0); bit-exact with the reference.
+__global__ void embed_f32_kernel(const float4* __restrict__ tok, int64_t vocab,
+                                 const float4* __restrict__ pos, int h4,
+                                 const int32_t* __restrict__ ids, int S, int64_t rows,
+                                 float4* __restrict__ out, int* err) {
+  const int64_t total = rows * h4;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / h4;
+    const int c = static_cast<int>(i % h4);
+    const int32_t id = __ldg(ids + r);
+    float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (id < 0 || id >= vocab) {
+      if (err) atomicExch(err, 1);
+    } else {
+      const float4 t = __ldg(tok + static_cast<int64_t>(id) * h4 + c);
+      const float4 p = __ldg(pos + static_cast<int64_t>(r % S) * h4 + c);
+      o = make_float4(__fadd_rn(t.x, p.x), __fadd_rn(t.y, p.y), __fadd_rn(t.z, p.z),
+                      __fadd_rn(t.w, p.w));
+    }
+    out[i] = o;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// LayerNorm, reference src/kernels.cpp:170-219.  One warp per row.  F32
+// accumulation uses warp-shuffle reductions (fp32 reassociation only); F16E
+// accumulation runs the reference's sequential rounded recurrence on lane 0.
+// ---------------------------------------------------------------------------
+__global__ void simt_layernorm_kernel(const float* __restrict__ x, int rows, int n,
+                                      const float* __restrict__ gamma,
+                                      const float* __restrict__ beta, float eps, int c16, int a16,
+                                      float* __restrict__ out32, __half* __restrict__ out16,
+                                      int round_out16) {
+  const int warps = blockDim.x >> 5;
+  const int row = blockIdx.x * warps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float* in = x + static_cast<int64_t>(row) * n;
+  float mean, inv;
+  if (!a16) {
+    float s = 0.0f;
+    for (int i = lane; i < n; i += 32) s += conform(in[i], c16);
+    s = warp_sum(s);
+    mean = __fdiv_rn(s, static_cast<float>(n));
+    float vs = 0.0f;
+    for (int i = lane; i < n; i += 32) {
+      const float d = __fsub_rn(conform(in[i], c16), mean);
+      vs = __fadd_rn(vs, __fmul_rn(d, d));
+    }
+    vs = warp_sum(vs);
+    const float var = __fdiv_rn(vs, static_cast<float>(n));
+    inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, eps)));
+  } else {
+    float m = 0.0f, iv = 0.0f;
+    if (lane == 0) {
+      float s = 0.0f;
+      for (int i = 0; i < n; ++i) s = r16(__fadd_rn(s, conform(in[i], c16)));
+      m = r16(__fdiv_rn(s, static_cast<float>(n)));
+      float vs = 0.0f;
+      for (int i = 0; i < n; ++i) {
+        const float d = r16(__fsub_rn(conform(in[i], c16), m));
+        vs = r16(__fadd_rn(vs, r16(__fmul_rn(d, d))));
+      }
+      const float var = r16(__fdiv_rn(vs, static_cast<float>(n)));
+      iv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, eps)));
+    }
+    mean = __shfl_sync(0xffffffffu, m, 0);
+    inv = __shfl_sync(0xffffffffu, iv, 0);
+  }
+  for (int i = lane; i < n; i += 32) {
+    const float g = conform(gamma[i], c16), b = conform(beta[i], c16);
+    float y = conform(
+        __fadd_rn(__fmul_rn(g, __fmul_rn(__fsub_rn(conform(in[i], c16), mean), inv)), b), c16);
+    if (out16) {
+      out16[static_cast<int64_t>(row) * n + i] = __float2half_rn(y);
+    } else {
+      if (round_out16) y = r16(y);
+      out32[static_cast<int64_t>(row) * n + i] = y;
+    }
+  }
+}
+
+// Fast-path LayerNorm (hybrid: F32 LN, output consumed by an F16E Linear, so the
+// round16 of the next op is applied here).  One warp per row, n = 128*VPT,
+// row held in registers (two-pass mean / variance like the reference).
+template <int VPT>
+__global__ void __launch_bounds__(256) ln_f16_kernel(const float* __restrict__ x, int rows,
+                                                     const float* __restrict__ gamma,
+                                                     const float* __restrict__ beta, float eps,
+                                                     __half* __restrict__ out) {
+  constexpr int n = 128 * VPT;
+  const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float4* in = reinterpret_cast<const float4*>(x + static_cast<int64_t>(row) * n);
+  float4 v[VPT];
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) v[i] = __ldg(in + lane + 32 * i);
+  float s = 0.0f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+  s = warp_sum(s);
+  const float mean = __fdiv_rn(s, static_cast<float>(n));
+  float vs = 0.0f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const float a = __fsub_rn(v[i].x, mean), b = __fsub_rn(v[i].y, mean);
+    const float c = __fsub_rn(v[i].z, mean), d = __fsub_rn(v[i].w, mean);
+    vs += (__fmul_rn(a, a) + __fmul_rn(b, b)) + (__fmul_rn(c, c) + __fmul_rn(d, d));
+  }
+  vs = warp_sum(vs);
+  const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(vs, static_cast<float>(n)), eps)));
+  const float4* g4 = reinterpret_cast<const float4*>(gamma);
+  const float4* b4 = reinterpret_cast<const float4*>(beta);
+  uint2* o = reinterpret_cast<uint2*>(out + static_cast<int64_t>(row) * n);
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const float4 g = __ldg(g4 + lane + 32 * i), b = __ldg(b4 + lane + 32 * i);
+    const float y0 = __fadd_rn(__fmul_rn(g.x, __fmul_rn(__fsub_rn(v[i].x, mean), inv)), b.x);
+    const float y1 = __fadd_rn(__fmul_rn(g.y, __fmul_rn(__fsub_rn(v[i].y, mean), inv)), b.y);
+    const float y2 = __fadd_rn(__fmul_rn(g.z, __fmul_rn(__fsub_rn(v[i].z, mean), inv)), b.z);
+    const float y3 = __fadd_rn(__fmul_rn(g.w, __fmul_rn(__fsub_rn(v[i].w, mean), inv)), b.w);
+    __half2 h01 = __floats2half2_rn(y0, y1), h23 = __floats2half2_rn(y2, y3);
+    o[lane + 32 * i] = make_uint2(*reinterpret_cast<uint32_t*>(&h01), *reinterpret_cast<uint32_t*>(&h23));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// generic attention (any S, any head_dim): one warp per query row.
+// scores (kernels.cpp:85-125) -> causal mask (model.cpp:405-413) -> softmax
+// (kernels.cpp:127-168, sequential sum like the reference) -> P.V (matmul).
+// ---------------------------------------------------------------------------
+__global__ void simt_attention_kernel(const float* __restrict__ q, const float* __restrict__ k,
+                                      const float* __restrict__ v, int64_t ld_in,
+                                      float* __restrict__ ctx, int64_t ld_ctx, int B, int S, int H,
+                                      int hd, float scale, int causal, Kcfg att, Kcfg sm,
+                                      float* __restrict__ tap) {
+  extern __shared__ float sh[];
+  const int warps = blockDim.x >> 5;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float* srow = sh + w * (S + hd);
+  float* qrow = srow + S;
+  const int64_t gq = static_cast<int64_t>(blockIdx.x) * warps + w;  // (b, h, i) flattened
+  if (gq >= static_cast<int64_t>(B) * H * S) return;
+  const int i = static_cast<int>(gq % S);
+  const int head = static_cast<int>((gq / S) % H);
+  const int b = static_cast<int>(gq / (static_cast<int64_t>(S) * H));
+  const int ac = att.compute, aa = att.accum;
+  for (int t = lane; t < hd; t += 32)
+    qrow[t] = conform(q[(static_cast<int64_t>(b) * S + i) * ld_in + head * hd + t], ac);
+  __syncwarp();
+  for (int j = lane; j < S; j += 32) {
+    const float* kr = k + (static_cast<int64_t>(b) * S + j) * ld_in + head * hd;
+    float value, ref = 0.0f;
+    if (aa) {
+      float acc = 0.0f;
+      for (int t = 0; t < hd; ++t) acc = r16(__fadd_rn(acc, r16(__fmul_rn(qrow[t], conform(kr[t], ac)))));
+      value = r16(__fmul_rn(acc, scale));
+      if (tap)
+        for (int t = 0; t < hd; ++t) ref = __fadd_rn(ref, __fmul_rn(qrow[t], conform(kr[t], ac)));
+      ref = __fmul_rn(ref, scale);
+    } else {
+      float acc = 0.0f;
+      for (int t = 0; t < hd; ++t) acc = __fadd_rn(acc, __fmul_rn(qrow[t], conform(kr[t], ac)));
+      ref = __fmul_rn(acc, scale);
+      value = conform(ref, ac);
+    }
+    if (tap) tap[((static_cast<int64_t>(b) * H + head) * S + i) * S + j] = ref;
+    if (causal && j > i) value = __int_as_float(0xff800000);
+    srow[j] = conform(value, sm.compute);
+  }
+  __syncwarp();
+  float shift = 0.0f;
+  if (sm.stabilized) {
+    float mx = __int_as_float(0xff800000);
+    for (int j = lane; j < S; j += 32) mx = fmaxf(mx, srow[j]);
+    shift = warp_max(mx);
+  }
+  for (int j = lane; j < S; j += 32) {
+    const float e = sm.stabilized ? expf(__fsub_rn(srow[j], shift)) : expf(srow[j]);
+    srow[j] = conform(e, sm.compute);
+  }
+  __syncwarp();
+  float sum = 0.0f;
+  if (lane == 0) {
+    if (sm.accum)
+      for (int j = 0; j < S; ++j) sum = r16(__fadd_rn(sum, srow[j]));
+    else
+      for (int j = 0; j < S; ++j) sum = __fadd_rn(sum, srow[j]);
+    sum = conform(sum, sm.compute);
+  }
+  sum = __shfl_sync(0xffffffffu, sum, 0);
+  for (int j = lane; j < S; j += 32)
+    srow[j] = conform(conform(__fdiv_rn(srow[j], sum), sm.compute), ac);  // probs onto att lattice
+  __syncwarp();
+  for (int t = lane; t < hd; t += 32) {
+    float acc = 0.0f;
+    const float* vc = v + static_cast<int64_t>(b) * S * ld_in + head * hd + t;
+    if (aa) {
+      for (int j = 0; j < S; ++j) acc = r16(__fadd_rn(acc, r16(__fmul_rn(srow[j], conform(vc[j * ld_in], ac)))));
+    } else {
+      for (int j = 0; j < S; ++j) acc = __fadd_rn(acc, __fmul_rn(srow[j], conform(vc[j * ld_in], ac)));
+      acc = conform(acc, ac);
+    }
+    ctx[(static_cast<int64_t>(b) * S + i) * ld_ctx + head * hd + t] = acc;
+  }
+}
+
+// per-op softmax (kernels.cpp:127-168): one warp per row, sequential sum.
+__global__ void simt_softmax_kernel(const float* __restrict__ x, int64_t rows, int64_t n, Kcfg cfg,
+                                    float* __restrict__ out) {
+  const int warps = blockDim.x >> 5;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * warps + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (row >= rows) return;
+  const float* in = x + row * n;
+  float* o = out + row * n;
+  float shift = 0.0f;
+  if (cfg.stabilized) {
+    float mx = __int_as_float(0xff800000);
+    for (int64_t j = lane; j < n; j += 32) mx = fmaxf(mx, conform(in[j], cfg.compute));
+    shift = warp_max(mx);
+  }
+  for (int64_t j = lane; j < n; j += 32) {
+    const float xv = conform(in[j], cfg.compute);
+    o[j] = conform(cfg.stabilized ? expf(__fsub_rn(xv, shift)) : expf(xv), cfg.compute);
+  }
+  __syncwarp();
+  float sum = 0.0f;
+  if (lane == 0) {
+    for (int64_t j = 0; j < n; ++j) sum = cfg.accum ? r16(__fadd_rn(sum, o[j])) : __fadd_rn(sum, o[j]);
+    sum = conform(sum, cfg.compute);
+  }
+  sum = __shfl_sync(0xffffffffu, sum, 0);
+  for (int64_t j = lane; j < n; j += 32) o[j] = conform(__fdiv_rn(o[j], sum), cfg.compute);
+}
+
+__global__ void simt_gelu_kernel(const float* x, int64_t n, int c16, float* out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = conform(gelu_erf(conform(x[i], c16)), c16);
+}
+__global__ void simt_add_kernel(const float* a, const float* b, int64_t n, int c16, float* out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = conform(__fadd_rn(conform(a[i], c16), conform(b[i], c16)), c16);
+}
+__global__ void simt_tanh_kernel(const float* x, int64_t n, int c16, float* out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = conform(tanhf(conform(x[i], c16)), c16);
+}
+__global__ void round_copy_kernel(const float* x, int64_t n, int c16, float* out) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = conform(x[i], c16);
+}
+__global__ void f32_to_f16_kernel(const float* x, __half* out, int64_t n) {
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = __float2half_rn(x[i]);
+}
+__global__ void convert_f16_f32_kernel(const __half* __restrict__ in, int64_t ld_in,
+                                       float* __restrict__ out, int64_t ld_out, int M, int N) {
+  const int64_t total = static_cast<int64_t>(M) * N;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / N, c = i % N;
+    out[r * ld_out + c] = __half2float(in[r * ld_in + c]);
+  }
+}
+// out[c, r] = in[r, c] (rows x cols -> cols x rows), 32x32 smem tiles
+template <typename OutT>
+__global__ void transpose_kernel(const float* __restrict__ in, int rows, int cols,
+                                 OutT* __restrict__ out, int64_t ld_out, int rnd) {
+  __shared__ float tile[32][33];
+  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int r = r0 + i, c = c0 + threadIdx.x;
+    tile[i][threadIdx.x] = (r < rows && c < cols) ? in[static_cast<int64_t>(r) * cols + c] : 0.0f;
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int c = c0 + i, r = r0 + threadIdx.x;
+    if (c < cols && r < rows) {
+      const float v = tile[threadIdx.x][i];
+      if constexpr (sizeof(OutT) == 2)
+        out[static_cast<int64_t>(c) * ld_out + r] = __float2half_rn(v);
+      else
+        out[static_cast<int64_t>(c) * ld_out + r] = rnd ? r16(v) : v;
+    }
+  }
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+void simt_gemm(const float* A, int64_t lda, const float* Bt, int64_t ldb, float* out, int64_t ldo,
+               int M, int N, int K, Kcfg lin, const SimtGemmEpi& epi, cudaStream_t st) {
+  GemmEpiDev e{epi.bias, epi.op, lin.compute, epi.act.compute, epi.res.compute, epi.resid};
+  dim3 grid((N + 63) / 64, (M + 63) / 64);
+  if (lin.compute == 0)
+    simt_gemm_kernel<0><<<grid, 256, 0, st>>>(A, lda, Bt, ldb, out, ldo, M, N, K, e);
+  else if (lin.accum == 0)
+    simt_gemm_kernel<1><<<grid, 256, 0, st>>>(A, lda, Bt, ldb, out, ldo, M, N, K, e);
+  else
+    simt_gemm_kernel<2><<<grid, 256, 0, st>>>(A, lda, Bt, ldb, out, ldo, M, N, K, e);
+  PRLAB_CUDA(cudaGetLastError());
+}
+
+void simt_embed(const float* tok, int64_t vocab, const float* pos, int h, const int32_t* ids,
+                int B, int S, Kcfg cfg, float* out, int* err, cudaStream_t st) {
+  const int64_t n = static_cast<int64_t>(B) * S * h;
+  simt_embed_kernel<<<blocks_for(n, 256), 256, 0, st>>>(tok, vocab, pos, h, ids, B, S, cfg.compute,
+                                                         out, err);
+  PRLAB_CUDA(cudaGetLastError());
+}
+
+void embed_f32(const float* tok, int64_t vocab, const float* pos, int h, const int32_t* ids, int B,
+               int S, float* out, int* err, cudaStream_t st) {
+  const int64_t rows = static_cast<int64_t>(B) * S;
+  const int h4 = h / 4;
+  const int64_t n = rows * h4;
+  const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, num_sms() * 8));
+  embed_f32_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(tok), vocab,
+                                           reinterpret_cast<const float4*>(pos), h4, ids, S, rows,
+                                           reinterpret_cast<float4*>(out), err);
+  PRLAB_CUDA(cudaGetLastError());
+}
+
+void simt_layernorm(const float* x, int rows, int n, const float* gamma, const float* beta,
+                    float eps, Kcfg cfg, float* out32, __half* out16, int round_out16,
+                    cudaStream_t st) {
+  simt_layernorm_kernel<<<(rows + 7) / 8, 256, 0, st>>>(x, rows, n, gamma, beta, eps, cfg.compute,
+                                                        cfg.accum, out32, out16, round_out16);
+  PRLAB_CUDA(cudaGetLastError());
+}
+
+void ln_f32_to_f16(const float* x, int rows, int n, const float* gamma, const float* beta,
+                   float eps, __half* out, cudaStream_t st) {
+  const int grid = (rows + 7) / 8;
+  switch (n) {
+    case 128: ln_f16_kernel<1><<<grid, 256, 0, st>>>(x, rows, gamma, beta, eps, out); break;
+    case 256: ln_f16_kernel<2><<<grid, 256, 0, st>>>(x, rows, gamma, beta, eps, out); break;
+    case 384: ln_f16_kernel<3><<<grid, 256, 0, st>>>(x, rows, gamma, beta, eps, out); break;
+    case 512: ln_f16_kernel<4><<<grid, 256, 0, st>>>(x, rows, gamma, beta, eps, out); break;
+    case 768: ln_f16_kernel<6><<<grid, 256, 0, st>>>(x, rows, gamma, beta, eps, out); break;
+    case 1024: ln_f16_kernel<8><<<grid, 256, 0, st>>>(x, rows, gamma, beta, eps, out); break;
+    default:
+      simt_layernorm(x, rows, n, gamma, beta, eps, Kcfg{0, 0, 1}, nullptr, out, 0, st);
+      return;
+  }
+  PRLAB_CUDA(cudaGetLastError());
+}
+
+void simt_attention(const float* q, const float* k, const float* v, int64_t ld_in, float* ctx,
+                    int64_t ld_ctx, int B, int S, int H, int hd, float scale, int causal, Kcfg att,
+                    Kcfg sm, float* tap, cudaStream_t st) {
+  const int warps = 4;
+  const size_t shmem = static_cast<size_t>(warps) * (S + hd) * sizeof(float);
+  static int configured_bytes = 48 * 1024;
+  if (shmem > static_cast<size_t>(configured_bytes)) {
+    PRLAB_CUDA(cudaFuncSetAttribute(simt_attention_kernel,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(shmem)));
+    configured_bytes = static_cast<int>(shmem);
+  }
+  const int64_t rows = static_cast<int64_t>(B) * H * S;
+  simt_attention_kernel<<<static_cast<int>((rows + warps - 1) / warps), warps * 32, shmem, st>>>(
+      q, k, v, ld_in, ctx, ld_ctx, B, S, H, hd, scale, causal, att, sm, tap);
+  PRLAB_CUDA(cudaGetLastError());
+}
+
+void simt_scores(const float* q, const float* k, int sq, int sk, int d, float scale, Kcfg cfg,
+                 float* out, float* tap, cudaStream_t st);
+
+void simt_softmax(const float* x, int64_t rows, int64_t n, Kcfg cfg, float* out, cudaStream_t st) {
+  simt_softmax_kernel<<<static_cast<int>((rows + 7) / 8), 256, 0, st>>>(x, rows, n, cfg, out);
+  PRLAB_CUDA(cudaGetLastError());
+}
+void simt_gelu(const float* x, int64_t n, Kcfg cfg, float* out, cudaStream_t st) {
+  simt_gelu_kernel<<<blocks_for(n, 256), 256, 0, st>>>(x, n, cfg.compute, out);
+  PRLAB_CUDA(cudaGetLastError());
+}
+void simt_add(const float* a, const float* b, int64_t n, Kcfg cfg, float* out, cudaStream_t st) {
+  simt_add_kernel<<<blocks_for(n, 256), 256, 0, st>>>(a, b, n, cfg.compute, out);
+  PRLAB_CUDA(cudaGetLastError());
+}
+void simt_tanh(const float* x, int64_t n, Kcfg cfg, float* out, cudaStream_t st) {
+  simt_tanh_kernel<<<blocks_for(n, 256), 256, 0, st>>>(x, n, cfg.compute, out);
+  PRLAB_CUDA(cudaGetLastError());
+}
+void simt_round_copy(const float* x, int64_t n, int f16, float* out, cudaStream_t st) {
+  round_copy_kernel<<<blocks_for(n, 256), 256, 0, st>>>(x, n, f16, out);
+  PRLAB_CUDA(cudaGetLastError());
+}
+void round16_inplace(float* x, int64_t n, cudaStream_t st) { simt_round_copy(x, n, 1, x, st); }
+void f32_to_f16(const float* in, __half* out, int64_t n, cudaStream_t st) {
+  f32_to_f16_kernel<<<blocks_for(n, 256), 256, 0, st>>>(in, out, n);
+  PRLAB_CUDA(cudaGetLastError());
+}
+void convert_f16_to_f32(const __half* in, int64_t ld_in, float* out, int64_t ld_out, int M, int N,
+                        cudaStream_t st) {
+  const int64_t n = static_cast<int64_t>(M) * N;
+  const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, num_sms() * 16));
+  convert_f16_f32_kernel<<<blocks, 256, 0, st>>>(in, ld_in, out, ld_out, M, N);
+  PRLAB_CUDA(cudaGetLastError());
+}
+void transpose_f32(const float* in, int rows, int cols, float* out, int rnd, cudaStream_t st) {
+  dim3 grid((cols + 31) / 32, (rows + 31) / 32), block(32, 8);
+  transpose_kernel<float><<<grid, block, 0, st>>>(in, rows, cols, out, rows, rnd);
+  PRLAB_CUDA(cudaGetLastError());
+}
+void transpose_to_f16(const float* in, int rows, int cols, __half* out, int64_t ld_out,
+                      cudaStream_t st) {
+  dim3 grid((cols + 31) / 32, (rows + 31) / 32), block(32, 8);
+  transpose_kernel<__half><<<grid, block, 0, st>>>(in, rows, cols, out, ld_out, 0);
+  PRLAB_CUDA(cudaGetLastError());
+}
+
+// per-op attention_scores (kernels.cpp:85-125) via the generic attention
+// machinery would compute more than asked; a dedicated tiny kernel instead.
+namespace {
+__global__ void simt_scores_kernel(const float* __restrict__ q, const float* __restrict__ k, int sq,
+                                   int sk, int d, float scale, Kcfg cfg, float* out, float* tap) {
+  const int64_t idx = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (idx >= static_cast<int64_t>(sq) * sk) return;
+  const int i = static_cast<int>(idx / sk), j = static_cast<int>(idx % sk);
+  const float* qr = q + static_cast<int64_t>(i) * d;
+  const float* kr = k + static_cast<int64_t>(j) * d;
+  const int c = cfg.compute;
+  float value;
+  if (cfg.accum) {
+    float acc = 0.0f;
+    for (int t = 0; t < d; ++t) acc = r16(__fadd_rn(acc, r16(__fmul_rn(conform(qr[t], c), conform(kr[t], c)))));
+    value = r16(__fmul_rn(acc, scale));
+    if (tap) {
+      float ref = 0.0f;
+      for (int t = 0; t < d; ++t) ref = __fadd_rn(ref, __fmul_rn(conform(qr[t], c), conform(kr[t], c)));
+      tap[idx] = __fmul_rn(ref, scale);
+    }
+  } else {
+    float acc = 0.0f;
+    for (int t = 0; t < d; ++t) acc = __fadd_rn(acc, __fmul_rn(conform(qr[t], c), conform(kr[t], c)));
+    const float scaled = __fmul_rn(acc, scale);
+    if (tap) tap[idx] = scaled;
+    value = conform(scaled, c);
+  }
+  out[idx] = value;
+}
+}  // namespace
+
+void simt_scores(const float* q, const float* k, int sq, int sk, int d, float scale, Kcfg cfg,
+                 float* out, float* tap, cudaStream_t st) {
+  const int64_t n = static_cast<int64_t>(sq) * sk;
+  simt_scores_kernel<<<blocks_for(n, 128), 128, 0, st>>>(q, k, sq, sk, d, scale, cfg, out, tap);
+  PRLAB_CUDA(cudaGetLastError());
+}
+
+namespace {
+template <typename T>
+__global__ void argmax_kernel(const T* __restrict__ x, int64_t n, int64_t ld, int32_t* out) {
+  const T* row = x + static_cast<int64_t>(blockIdx.x) * ld;
+  float best = __int_as_float(0xff800000);
+  int idx = 0x7fffffff;
+  for (int64_t j = threadIdx.x; j < n; j += blockDim.x) {
+    const float v = static_cast<float>(row[j]);
+    if (v > best || (v == best && j < idx)) {
+      best = v;
+      idx = static_cast<int>(j);
+    }
+  }
+  __shared__ float sb[32];
+  __shared__ int si[32];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ob = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ob > best || (ob == best && oi < idx)) {
+      best = ob;
+      idx = oi;
+    }
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sb[threadIdx.x >> 5] = best;
+    si[threadIdx.x >> 5] = idx;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
+      if (sb[w] > best || (sb[w] == best && si[w] < idx)) {
+        best = sb[w];
+        idx = si[w];
+      }
+    out[blockIdx.x] = idx == 0x7fffffff ? 0 : idx;
+  }
+}
+}  // namespace
+
+void argmax_rows(const void* logits, int dtype, int64_t rows, int64_t n, int64_t ld, int32_t* out,
+                 cudaStream_t st) {
+  if (dtype == 1)
+    argmax_kernel<__half><<<static_cast<int>(rows), 512, 0, st>>>(static_cast<const __half*>(logits), n, ld, out);
+  else
+    argmax_kernel<float><<<static_cast<int>(rows), 512, 0, st>>>(static_cast<const float*>(logits), n, ld, out);
+  PRLAB_CUDA(cudaGetLastError());
+}
+
+}  // namespace prlab_gpu

@@ -1,0 +1,1048 @@
+// Host runtime behind include/prlab_gpu.h: weight arena planner, device model,
+// forward orchestration (fast tcgen05 path / generic SIMT path), CUDA-graph
+// cache, and the C-ABI with the reference's error semantics.
+//
+// Reference call stack being replaced: prlab::forward -> forward_hidden
+// (src/model.cpp:350-482) -> embed / layernorm_lastdim / linear_bias / matmul /
+// attention_scores / softmax_lastdim / gelu / add (src/kernels.cpp).
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <array>
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <thread>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/prlab_gpu.h"
+#include "common.cuh"
+#include "internal.h"
+
+namespace prlab_gpu {
+
+namespace {
+thread_local std::string g_last_error;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return PRLAB_OK;
+  } catch (const std::invalid_argument& e) {
+    g_last_error = e.what();
+    return PRLAB_EINVAL;
+  } catch (const std::out_of_range& e) {
+    g_last_error = e.what();
+    return PRLAB_ERANGE;
+  } catch (const cuda_error& e) {
+    g_last_error = e.what();
+    return PRLAB_ECUDA;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return PRLAB_ERUNTIME;
+  }
+}
+
+void require_device() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n < 1) {
+    cudaGetLastError();
+    throw cuda_error("no CUDA device available (prlab_gpu has no CPU fallback)");
+  }
+}
+}  // namespace
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    PRLAB_CUDA(cudaGetDevice(&dev));
+    PRLAB_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  }
+  return n;
+}
+
+// ---------------------------------------------------------------------------
+// TMA descriptors through the driver entry point (no -lcuda link dependency)
+// ---------------------------------------------------------------------------
+namespace {
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    PRLAB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    if (!p || q != cudaDriverEntryPointSuccess) throw cuda_error("cuTensorMapEncodeTiled unavailable");
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return fn;
+}
+}  // namespace
+
+CUtensorMap make_tmap_f16_2d(const void* base, uint64_t rows, uint64_t cols, uint64_t pitch_elems,
+                             uint32_t box_rows, uint32_t box_cols) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {pitch_elems * 2};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw cuda_error("cuTensorMapEncodeTiled(2d) failed: " + std::to_string(r));
+  return m;
+}
+
+CUtensorMap make_tmap_f16_3d(const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                             uint64_t pitch1_elems, uint64_t pitch2_elems, uint32_t box0,
+                             uint32_t box1, uint32_t box2) {
+  CUtensorMap m;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {pitch1_elems * 2, pitch2_elems * 2};
+  cuuint32_t box[3] = {box0, box1, box2};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, const_cast<void*>(base), dims,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw cuda_error("cuTensorMapEncodeTiled(3d) failed: " + std::to_string(r));
+  return m;
+}
+
+// ---------------------------------------------------------------------------
+// arena planner: one cudaMalloc, 1 KiB-aligned carve-outs (TMA / 128B swizzle)
+// ---------------------------------------------------------------------------
+namespace {
+struct ArenaPlan {
+  std::vector<size_t> offs;
+  size_t total = 0;
+  int add(size_t bytes) {
+    total = (total + 1023) & ~static_cast<size_t>(1023);
+    offs.push_back(total);
+    total += bytes;
+    return static_cast<int>(offs.size()) - 1;
+  }
+};
+
+struct DeviceBuffer {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DeviceBuffer() = default;
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  ~DeviceBuffer() { reset(); }
+  void alloc(size_t n) {
+    reset();
+    if (n) PRLAB_CUDA(cudaMalloc(&p, n));
+    bytes = n;
+  }
+  void reset() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <typename T>
+  T* at(size_t off) const {
+    return reinterpret_cast<T*>(static_cast<uint8_t*>(p) + off);
+  }
+};
+
+Kcfg K(const prlab_kcfg& c) { return Kcfg{c.compute, c.accum, c.stabilized}; }
+
+// The built-in hybrid assignment (src/policy.cpp:59-63): Linear, AttentionScoreMatmul,
+// Activation {F16E, F32}; Softmax, LayerNorm, Embedding, Residual {F32, F32}, stabilized softmax.
+bool is_hybrid(const prlab_policy& p) {
+  for (int i = 0; i < PRLAB_NUM_OP_CLASSES; ++i) {
+    const prlab_kcfg& c = p.cls[i];
+    const bool narrow = i == PRLAB_LINEAR || i == PRLAB_ATTENTION_SCORE_MATMUL || i == PRLAB_ACTIVATION;
+    if (c.compute != (narrow ? 1 : 0) || c.accum != 0) return false;
+    if (i == PRLAB_SOFTMAX && !c.stabilized) return false;
+  }
+  return true;
+}
+uint64_t policy_key(const prlab_policy& p) {
+  uint64_t k = 0;
+  for (int i = 0; i < PRLAB_NUM_OP_CLASSES; ++i)
+    k = (k << 3) | (static_cast<uint64_t>(p.cls[i].compute & 1) << 2) |
+        (static_cast<uint64_t>(p.cls[i].accum & 1) << 1) |
+        static_cast<uint64_t>(p.cls[i].stabilized != 0);
+  return k;
+}
+void validate_kcfg(const prlab_kcfg& c) {
+  if ((c.compute != 0 && c.compute != 1) || (c.accum != 0 && c.accum != 1))
+    throw std::invalid_argument("unknown dtype in kernel config");
+  if (c.compute == 0 && c.accum == 1)  // KernelConfig::validate, src/kernels.cpp:33-38
+    throw std::invalid_argument("invalid kernel config: f32 compute with f16e accumulation");
+}
+void validate_policy(const prlab_policy& p) {
+  for (int i = 0; i < PRLAB_NUM_OP_CLASSES; ++i) validate_kcfg(p.cls[i]);
+}
+
+void validate_desc(const prlab_model_desc& c) {
+  // ModelConfig::validate, src/model.cpp:101-117 (same messages)
+  if (c.num_layers < 0) throw std::invalid_argument("num_layers must be >= 0");
+  if (c.hidden < 1) throw std::invalid_argument("hidden must be >= 1");
+  if (c.heads < 1) throw std::invalid_argument("heads must be >= 1");
+  if (c.ffn < 1) throw std::invalid_argument("ffn must be >= 1");
+  if (c.vocab < 1) throw std::invalid_argument("vocab must be >= 1");
+  if (c.max_positions < 1) throw std::invalid_argument("max_positions must be >= 1");
+  if (c.hidden % c.heads != 0)
+    throw std::invalid_argument("heads (" + std::to_string(c.heads) + ") must divide hidden (" +
+                                std::to_string(c.hidden) + ")");
+  if (c.ffn < c.hidden)
+    throw std::invalid_argument("ffn (" + std::to_string(c.ffn) + ") must be >= hidden (" +
+                                std::to_string(c.hidden) + ")");
+  if (c.archetype != 0 && c.archetype != 1)
+    throw std::invalid_argument("unknown archetype (expected encoder_only or decoder_only)");
+}
+
+std::vector<size_t> param_sizes(const prlab_model_desc& d) {
+  const size_t h = d.hidden, f = d.ffn;
+  std::vector<size_t> s = {static_cast<size_t>(d.vocab) * h, static_cast<size_t>(d.max_positions) * h};
+  for (int64_t l = 0; l < d.num_layers; ++l) {
+    const size_t lay[16] = {h, h, h * h, h, h * h, h, h * h, h, h * h, h, h, h, h * f, f, f * h, h};
+    s.insert(s.end(), lay, lay + 16);
+  }
+  s.push_back(h);
+  s.push_back(h);
+  if (d.archetype == 0) {
+    s.push_back(h * h);
+    s.push_back(h);
+    s.push_back(h * 2);
+    s.push_back(2);
+  }
+  return s;
+}
+}  // namespace
+
+}  // namespace prlab_gpu
+
+using namespace prlab_gpu;
+
+// ---------------------------------------------------------------------------
+// device model
+// ---------------------------------------------------------------------------
+struct prlab_gpu_model {
+  prlab_model_desc d{};
+  int device = 0;
+  int64_t h = 0, f = 0, H = 0, hd = 0, V = 0, P = 0, L = 0;
+  std::mutex mu;
+  std::vector<std::vector<float>> host;  // fp32 parameter copies (for the lazily built fp32 arena)
+
+  // fast (hybrid) arena: fp16 K-major linear weights + fp32 tables / LN params,
+  // biases pre-rounded onto the fp16 lattice (the reference's conform(b), model.cpp:73)
+  DeviceBuffer arena16;
+  struct L16 {
+    __half *wqkv, *wo, *w1, *w2;
+    float *bqkv, *bo, *b1, *b2, *ln1g, *ln1b, *ln2g, *ln2b;
+  };
+  std::vector<L16> l16;
+  __half* emb16 = nullptr;  // tied head E [V, h] fp16 (already K-major)
+  float *tok = nullptr, *pos = nullptr, *lnfg = nullptr, *lnfb = nullptr;
+
+  // generic fp32 arena: W^T fp32 [out, in] and raw fp32 biases
+  DeviceBuffer arena32;
+  struct L32 {
+    float *wqkv_t, *wo_t, *w1_t, *w2_t, *bqkv, *bo, *b1, *b2;
+  };
+  std::vector<L32> l32;
+  bool have32 = false;
+
+  DeviceBuffer err;  // device error word (bad token ids)
+  cudaStream_t stream = nullptr;  // private stream of the host (drop-in) forward
+
+  // activation workspace + per-key plans
+  DeviceBuffer ws;
+  struct Plan {
+    int64_t B = 0, S = 0;
+    bool fast = false;
+    prlab_policy pol{};
+    float* x = nullptr;
+    __half *xn16 = nullptr, *big16 = nullptr, *logit16 = nullptr;
+    float *xn32 = nullptr, *qkv32 = nullptr, *ctx32 = nullptr, *ff32 = nullptr;
+    int32_t* ids = nullptr;
+    float* out32 = nullptr;
+    int64_t ld16 = 0;
+    std::vector<GemmPlan> gemms;  // fast path: 4 per layer + head
+    AttnPlan attn{};
+    std::map<std::tuple<const void*, void*, int, int64_t>, cudaGraphExec_t> graphs;
+    std::map<std::tuple<void*, int64_t>, GemmPlan> head_plans;
+  };
+  std::map<std::tuple<int64_t, int64_t, uint64_t>, std::unique_ptr<Plan>> plans;
+
+  ~prlab_gpu_model() {
+    drop_plans();
+    if (stream) cudaStreamDestroy(stream);
+  }
+  void drop_plans() {
+    for (auto& kv : plans)
+      for (auto& g : kv.second->graphs) cudaGraphExecDestroy(g.second);
+    plans.clear();
+  }
+};
+
+namespace {
+
+// Fast (tensor-core) path eligibility: the hybrid policy and TMA-friendly extents.
+bool fast_eligible(const prlab_gpu_model& m, int64_t S, const prlab_policy& pol) {
+  if (!is_hybrid(pol) || m.L < 1) return false;
+  if (m.h % 128 != 0 || m.h > 1024 || m.f % 64 != 0) return false;
+  if (!attn_tc_supported(static_cast<int>(S), static_cast<int>(m.hd))) return false;
+  if (std::getenv("PRLAB_FORCE_GENERIC")) return false;
+  return true;
+}
+
+void h2d(void* dst, const float* src, size_t n) {
+  PRLAB_CUDA(cudaMemcpy(dst, src, n * sizeof(float), cudaMemcpyHostToDevice));
+}
+
+void upload_fast(prlab_gpu_model& m) {
+  const int64_t h = m.h, f = m.f, V = m.V, P = m.P, L = m.L;
+  ArenaPlan ap;
+  const int s_tok = ap.add(V * h * 4), s_pos = ap.add(P * h * 4), s_emb = ap.add(V * h * 2);
+  const int s_lnf = ap.add(2 * h * 4);
+  std::vector<std::array<int, 12>> ls(L);
+  for (int64_t l = 0; l < L; ++l)
+    ls[l] = {ap.add(3 * h * h * 2), ap.add(h * h * 2), ap.add(f * h * 2), ap.add(h * f * 2),
+             ap.add(3 * h * 4),     ap.add(h * 4),     ap.add(f * 4),     ap.add(h * 4),
+             ap.add(h * 4),         ap.add(h * 4),     ap.add(h * 4),     ap.add(h * 4)};
+  m.arena16.alloc(ap.total);
+  auto at = [&](int s) { return ap.offs[s]; };
+  m.tok = m.arena16.at<float>(at(s_tok));
+  m.pos = m.arena16.at<float>(at(s_pos));
+  m.emb16 = m.arena16.at<__half>(at(s_emb));
+  m.lnfg = m.arena16.at<float>(at(s_lnf));
+  m.lnfb = m.lnfg + h;
+  cudaStream_t st = nullptr;
+  h2d(m.tok, m.host[0].data(), V * h);
+  h2d(m.pos, m.host[1].data(), P * h);
+  f32_to_f16(m.tok, m.emb16, V * h, st);
+  const size_t fin = 2 + 16 * L;
+  h2d(m.lnfg, m.host[fin].data(), h);
+  h2d(m.lnfb, m.host[fin + 1].data(), h);
+
+  DeviceBuffer stage;
+  stage.alloc(static_cast<size_t>(h) * std::max(h, f) * 4);
+  auto rounded_bias = [&](float* dst, const std::vector<float>& src) {
+    std::vector<float> tmp(src);
+    for (auto& v : tmp) v = __half2float(__float2half_rn(v));
+    h2d(dst, tmp.data(), tmp.size());
+  };
+  // W [in, out] row-major (model.cpp:229-242) -> W^T [out, in] fp16 (K-major)
+  auto put = [&](const std::vector<float>& src, int64_t in, int64_t out, __half* dst) {
+    h2d(stage.p, src.data(), in * out);
+    transpose_to_f16(static_cast<float*>(stage.p), static_cast<int>(in), static_cast<int>(out), dst, in, st);
+    PRLAB_CUDA(cudaStreamSynchronize(st));
+  };
+  m.l16.resize(L);
+  for (int64_t l = 0; l < L; ++l) {
+    const auto* p = &m.host[2 + 16 * l];
+    auto& w = m.l16[l];
+    w.wqkv = m.arena16.at<__half>(at(ls[l][0]));
+    w.wo = m.arena16.at<__half>(at(ls[l][1]));
+    w.w1 = m.arena16.at<__half>(at(ls[l][2]));
+    w.w2 = m.arena16.at<__half>(at(ls[l][3]));
+    w.bqkv = m.arena16.at<float>(at(ls[l][4]));
+    w.bo = m.arena16.at<float>(at(ls[l][5]));
+    w.b1 = m.arena16.at<float>(at(ls[l][6]));
+    w.b2 = m.arena16.at<float>(at(ls[l][7]));
+    w.ln1g = m.arena16.at<float>(at(ls[l][8]));
+    w.ln1b = m.arena16.at<float>(at(ls[l][9]));
+    w.ln2g = m.arena16.at<float>(at(ls[l][10]));
+    w.ln2b = m.arena16.at<float>(at(ls[l][11]));
+    h2d(w.ln1g, p[0].data(), h);
+    h2d(w.ln1b, p[1].data(), h);
+    h2d(w.ln2g, p[10].data(), h);
+    h2d(w.ln2b, p[11].data(), h);
+    put(p[2], h, h, w.wqkv);
+    put(p[4], h, h, w.wqkv + h * h);
+    put(p[6], h, h, w.wqkv + 2 * h * h);
+    put(p[8], h, h, w.wo);
+    put(p[12], h, f, w.w1);
+    put(p[14], f, h, w.w2);
+    rounded_bias(w.bqkv, p[3]);
+    rounded_bias(w.bqkv + h, p[5]);
+    rounded_bias(w.bqkv + 2 * h, p[7]);
+    rounded_bias(w.bo, p[9]);
+    rounded_bias(w.b1, p[13]);
+    rounded_bias(w.b2, p[15]);
+  }
+  m.err.alloc(256);
+  PRLAB_CUDA(cudaMemset(m.err.p, 0, 256));
+  PRLAB_CUDA(cudaDeviceSynchronize());
+}
+
+void ensure_f32(prlab_gpu_model& m) {
+  if (m.have32) return;
+  const int64_t h = m.h, f = m.f, L = m.L;
+  ArenaPlan ap;
+  std::vector<std::array<int, 8>> ls(L);
+  for (int64_t l = 0; l < L; ++l)
+    ls[l] = {ap.add(3 * h * h * 4), ap.add(h * h * 4), ap.add(f * h * 4), ap.add(h * f * 4),
+             ap.add(3 * h * 4),     ap.add(h * 4),     ap.add(f * 4),     ap.add(h * 4)};
+  m.arena32.alloc(std::max<size_t>(ap.total, 1024));
+  DeviceBuffer stage;
+  stage.alloc(static_cast<size_t>(h) * std::max(h, f) * 4);
+  cudaStream_t st = nullptr;
+  auto put = [&](const std::vector<float>& src, int64_t in, int64_t out, float* dst) {
+    h2d(stage.p, src.data(), in * out);
+    transpose_f32(static_cast<float*>(stage.p), static_cast<int>(in), static_cast<int>(out), dst, 0, st);
+    PRLAB_CUDA(cudaStreamSynchronize(st));
+  };
+  m.l32.resize(L);
+  for (int64_t l = 0; l < L; ++l) {
+    const auto* p = &m.host[2 + 16 * l];
+    auto& w = m.l32[l];
+    auto at = [&](int i) { return m.arena32.at<float>(ap.offs[ls[l][i]]); };
+    w.wqkv_t = at(0);
+    w.wo_t = at(1);
+    w.w1_t = at(2);
+    w.w2_t = at(3);
+    w.bqkv = at(4);
+    w.bo = at(5);
+    w.b1 = at(6);
+    w.b2 = at(7);
+    put(p[2], h, h, w.wqkv_t);
+    put(p[4], h, h, w.wqkv_t + h * h);
+    put(p[6], h, h, w.wqkv_t + 2 * h * h);
+    put(p[8], h, h, w.wo_t);
+    put(p[12], h, f, w.w1_t);
+    put(p[14], f, h, w.w2_t);
+    h2d(w.bqkv, p[3].data(), h);
+    h2d(w.bqkv + h, p[5].data(), h);
+    h2d(w.bqkv + 2 * h, p[7].data(), h);
+    h2d(w.bo, p[9].data(), h);
+    h2d(w.b1, p[13].data(), f);
+    h2d(w.b2, p[15].data(), h);
+  }
+  PRLAB_CUDA(cudaDeviceSynchronize());
+  m.have32 = true;
+}
+
+prlab_gpu_model::Plan& get_plan(prlab_gpu_model& m, int64_t B, int64_t S, const prlab_policy& pol) {
+  const auto key = std::make_tuple(B, S, policy_key(pol));
+  auto it = m.plans.find(key);
+  if (it != m.plans.end()) return *it->second;
+
+  const bool fast = fast_eligible(m, S, pol);
+  if (!fast) ensure_f32(m);
+  const int64_t M = B * S, h = m.h, f = m.f, V = m.V;
+  const int64_t outw = m.L > 0 ? V : h;
+  const int64_t ld16 = (V + 7) / 8 * 8;
+  // Activation liveness: x (fp32 residual stream) lives throughout; xn (LN out)
+  // dies at the QKV GEMM before ctx is born and ctx dies at Wo before LN2 writes
+  // xn again -> one buffer.  qkv dies at attention before FFN1 writes ff -> one buffer.
+  ArenaPlan ap;
+  const int s_x = ap.add(M * h * 4);
+  const int s_ids = ap.add(M * 4);
+  const int s_out = ap.add(M * outw * 4);
+  int s_a, s_b, s_c = -1;
+  if (fast) {
+    s_a = ap.add(M * h * 2);                       // xn16 / ctx16
+    s_b = ap.add(M * std::max(3 * h, f) * 2);      // qkv16 / ff16
+    s_c = ap.add(M * ld16 * 2);                    // fp16 logits (internal)
+  } else {
+    s_a = ap.add(M * h * 4);                       // xn32
+    s_b = ap.add(M * (3 * h + f) * 4);             // qkv32 | ff32 (attention reads qkv while ff unused)
+    s_c = ap.add(M * h * 4);                       // ctx32
+  }
+  if (ap.total > m.ws.bytes) {
+    m.drop_plans();  // every cached plan / graph points into the old workspace
+    PRLAB_CUDA(cudaDeviceSynchronize());
+    m.ws.alloc(ap.total);
+  }
+  auto plan = std::make_unique<prlab_gpu_model::Plan>();
+  auto& p = *plan;
+  p.B = B;
+  p.S = S;
+  p.pol = pol;
+  p.fast = fast;
+  p.ld16 = ld16;
+  auto at = [&](int s) { return ap.offs[s]; };
+  p.x = m.ws.at<float>(at(s_x));
+  p.ids = m.ws.at<int32_t>(at(s_ids));
+  p.out32 = m.ws.at<float>(at(s_out));
+  const int Mi = static_cast<int>(M), hi = static_cast<int>(h), fi = static_cast<int>(f);
+  if (fast) {
+    p.xn16 = m.ws.at<__half>(at(s_a));
+    p.big16 = m.ws.at<__half>(at(s_b));
+    p.logit16 = m.ws.at<__half>(at(s_c));
+    for (int64_t l = 0; l < m.L; ++l) {
+      const auto& w = m.l16[l];
+      p.gemms.push_back(plan_gemm_tc(p.xn16, h, w.wqkv, h, w.bqkv, p.big16, 3 * h, Mi, 3 * hi, hi, EPI_BIAS_F16));
+      p.gemms.push_back(plan_gemm_tc(p.xn16, h, w.wo, h, w.bo, p.x, h, Mi, hi, hi, EPI_BIAS_RESID_F32));
+      p.gemms.push_back(plan_gemm_tc(p.xn16, h, w.w1, h, w.b1, p.big16, f, Mi, fi, hi, EPI_BIAS_GELU_F16));
+      p.gemms.push_back(plan_gemm_tc(p.big16, f, w.w2, f, w.b2, p.x, h, Mi, hi, fi, EPI_BIAS_RESID_F32));
+    }
+    p.gemms.push_back(plan_gemm_tc(p.xn16, h, m.emb16, h, nullptr, p.logit16, ld16, Mi,
+                                   static_cast<int>(V), hi, EPI_F16));
+    p.attn = plan_attn_tc(p.big16, 3 * h, p.xn16, h, static_cast<int>(B), static_cast<int>(S),
+                          static_cast<int>(m.H), static_cast<int>(m.hd), m.d.archetype == 1);
+  } else {
+    p.xn32 = m.ws.at<float>(at(s_a));
+    p.qkv32 = m.ws.at<float>(at(s_b));
+    p.ff32 = p.qkv32 + M * 3 * h;
+    p.ctx32 = m.ws.at<float>(at(s_c));
+  }
+  auto& ref = *plan;
+  m.plans[key] = std::move(plan);
+  return ref;
+}
+
+// Records one forward on `st`; returns the number of kernels launched.
+int64_t enqueue_forward(prlab_gpu_model& m, prlab_gpu_model::Plan& p, const int32_t* ids, void* out,
+                        int out_dtype, int64_t ld, cudaStream_t st) {
+  const int64_t B = p.B, S = p.S, M = B * S, h = m.h, f = m.f, V = m.V, L = m.L;
+  const int Bi = static_cast<int>(B), Si = static_cast<int>(S), Mi = static_cast<int>(M);
+  const int hi = static_cast<int>(h), fi = static_cast<int>(f), Vi = static_cast<int>(V);
+  int* err = m.err.at<int>(0);
+  int64_t n = 0;
+  if (p.fast) {
+    embed_f32(m.tok, V, m.pos, hi, ids, Bi, Si, p.x, err, st);
+    ++n;
+    for (int64_t l = 0; l < L; ++l) {
+      const auto& w = m.l16[l];
+      ln_f32_to_f16(p.x, Mi, hi, w.ln1g, w.ln1b, 1e-5f, p.xn16, st);  // LN1 -> Linear lattice
+      launch_gemm_tc(p.gemms[4 * l + 0], st);                          // QKV (+bias)
+      launch_attn_tc(p.attn, st);                                      // attention -> ctx (xn16)
+      launch_gemm_tc(p.gemms[4 * l + 1], st);                          // Wo (+bias) + residual
+      ln_f32_to_f16(p.x, Mi, hi, w.ln2g, w.ln2b, 1e-5f, p.xn16, st);  // LN2
+      launch_gemm_tc(p.gemms[4 * l + 2], st);                          // FFN1 (+bias, GELU)
+      launch_gemm_tc(p.gemms[4 * l + 3], st);                          // FFN2 (+bias) + residual
+      n += 7;
+    }
+    ln_f32_to_f16(p.x, Mi, hi, m.lnfg, m.lnfb, 1e-5f, p.xn16, st);
+    ++n;
+    if (out_dtype == PRLAB_OUT_F16) {
+      if (ld % 8 != 0) throw std::invalid_argument("fp16 logits need a row pitch that is a multiple of 8");
+      const auto key = std::make_tuple(out, ld);
+      auto it = p.head_plans.find(key);
+      if (it == p.head_plans.end())
+        it = p.head_plans.emplace(key, plan_gemm_tc(p.xn16, h, m.emb16, h, nullptr, out, ld, Mi, Vi, hi, EPI_F16)).first;
+      launch_gemm_tc(it->second, st);  // tied head straight into the caller's buffer
+      ++n;
+    } else {
+      launch_gemm_tc(p.gemms.back(), st);
+      convert_f16_to_f32(p.logit16, p.ld16, static_cast<float*>(out), ld, Mi, Vi, st);
+      n += 2;
+    }
+    return n;
+  }
+
+  // ---------------- generic path (fp32 storage, per-class configs) ----------------
+  const prlab_policy& pol = p.pol;
+  const Kcfg lin = K(pol.cls[PRLAB_LINEAR]), att = K(pol.cls[PRLAB_ATTENTION_SCORE_MATMUL]),
+             sm = K(pol.cls[PRLAB_SOFTMAX]), ln = K(pol.cls[PRLAB_LAYERNORM]),
+             act = K(pol.cls[PRLAB_ACTIVATION]), emb = K(pol.cls[PRLAB_EMBEDDING]),
+             res = K(pol.cls[PRLAB_RESIDUAL]);
+  simt_embed(m.tok, V, m.pos, hi, ids, Bi, Si, emb, p.x, err, st);
+  ++n;
+  const float scale = 1.0f / std::sqrt(static_cast<float>(m.hd));
+  for (int64_t l = 0; l < L; ++l) {
+    const auto& w16 = m.l16[l];
+    const auto& w = m.l32[l];
+    simt_layernorm(p.x, Mi, hi, w16.ln1g, w16.ln1b, 1e-5f, ln, p.xn32, nullptr, 0, st);
+    simt_gemm(p.xn32, h, w.wqkv_t, h, p.qkv32, 3 * h, Mi, 3 * hi, hi, lin, SimtGemmEpi{w.bqkv, 0, act, res, nullptr}, st);
+    simt_attention(p.qkv32, p.qkv32 + h, p.qkv32 + 2 * h, 3 * h, p.ctx32, h, Bi, Si, static_cast<int>(m.H),
+                   static_cast<int>(m.hd), scale, m.d.archetype == 1, att, sm, nullptr, st);
+    simt_gemm(p.ctx32, h, w.wo_t, h, p.x, h, Mi, hi, hi, lin, SimtGemmEpi{w.bo, 2, act, res, p.x}, st);
+    simt_layernorm(p.x, Mi, hi, w16.ln2g, w16.ln2b, 1e-5f, ln, p.xn32, nullptr, 0, st);
+    simt_gemm(p.xn32, h, w.w1_t, h, p.ff32, f, Mi, fi, hi, lin, SimtGemmEpi{w.b1, 1, act, res, nullptr}, st);
+    simt_gemm(p.ff32, f, w.w2_t, f, p.x, h, Mi, hi, fi, lin, SimtGemmEpi{w.b2, 2, act, res, p.x}, st);
+    n += 7;
+  }
+  if (out_dtype != PRLAB_OUT_F32)
+    throw std::invalid_argument("fp16 logits are only produced by the hybrid tensor-core path");
+  float* dst = static_cast<float*>(out);
+  if (L == 0) {
+    // zero-layer model: the embeddings are the output (model.cpp:461-467)
+    PRLAB_CUDA(cudaMemcpy2DAsync(dst, ld * 4, p.x, h * 4, h * 4, M, cudaMemcpyDeviceToDevice, st));
+    ++n;
+  } else {
+    simt_layernorm(p.x, Mi, hi, m.lnfg, m.lnfb, 1e-5f, ln, p.xn32, nullptr, 0, st);
+    // tied head: logits = hidden . E^T, E [V, h] is already K-major (model.cpp:469-480)
+    simt_gemm(p.xn32, h, m.tok, h, dst, ld, Mi, Vi, hi, lin, SimtGemmEpi{nullptr, 0, act, res, nullptr}, st);
+    n += 2;
+  }
+  return n;
+}
+
+void fill_calls(const prlab_gpu_model& m, int64_t B, const prlab_policy& pol, prlab_trace* tr) {
+  // Same per-(class, dtype) counts as the reference's timed() wrappers (model.cpp:55-62).
+  std::memset(tr, 0, sizeof(*tr));
+  auto add = [&](int cls, uint64_t n) { tr->kernel_calls[cls][pol.cls[cls].compute] += n; };
+  add(PRLAB_EMBEDDING, 1);
+  const uint64_t L = static_cast<uint64_t>(m.L), BH = static_cast<uint64_t>(B * m.H);
+  add(PRLAB_LAYERNORM, 2 * L + (L > 0 ? 1 : 0));
+  add(PRLAB_LINEAR, 6 * L + (L > 0 ? 1 : 0));
+  add(PRLAB_ATTENTION_SCORE_MATMUL, 2 * BH * L);
+  add(PRLAB_SOFTMAX, BH * L);
+  add(PRLAB_ACTIVATION, L);
+  add(PRLAB_RESIDUAL, 2 * L);
+}
+
+void check_forward_args(const prlab_gpu_model& m, int64_t B, int64_t S) {
+  // forward_hidden validation, src/model.cpp:355-362 (same messages)
+  if (B < 1 || S < 1) throw std::invalid_argument("forward needs a non-empty token batch");
+  if (S > m.P)
+    throw std::invalid_argument("sequence length " + std::to_string(S) + " exceeds max_positions " +
+                                std::to_string(m.P));
+}
+
+// Enqueue one forward on `st`, replaying a cached CUDA graph when requested.
+void run_forward(prlab_gpu_model& m, prlab_gpu_model::Plan& p, const int32_t* d_ids, void* d_out, int out_dtype,
+                 int64_t ld, cudaStream_t st, bool use_graph) {
+  if (!use_graph) {
+    enqueue_forward(m, p, d_ids, d_out, out_dtype, ld, st);
+    return;
+  }
+  const auto key = std::make_tuple(static_cast<const void*>(d_ids), d_out, out_dtype, ld);
+  auto it = p.graphs.find(key);
+  if (it == p.graphs.end()) {
+    // capture on a private stream so a legacy-default caller stream still works
+    cudaStream_t cap;
+    PRLAB_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+    cudaGraph_t g;
+    PRLAB_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+    try {
+      enqueue_forward(m, p, d_ids, d_out, out_dtype, ld, cap);
+    } catch (...) {
+      cudaStreamEndCapture(cap, &g);
+      cudaStreamDestroy(cap);
+      throw;
+    }
+    PRLAB_CUDA(cudaStreamEndCapture(cap, &g));
+    cudaGraphExec_t ge;
+    PRLAB_CUDA(cudaGraphInstantiate(&ge, g, 0));
+    cudaGraphDestroy(g);
+    cudaStreamDestroy(cap);
+    it = p.graphs.emplace(key, ge).first;
+  }
+  PRLAB_CUDA(cudaGraphLaunch(it->second, st));
+}
+
+struct TmpDev {
+  void* p = nullptr;
+  explicit TmpDev(size_t n) { PRLAB_CUDA(cudaMalloc(&p, n ? n : 4)); }
+  ~TmpDev() { cudaFree(p); }
+  float* f() const { return static_cast<float*>(p); }
+};
+
+}  // namespace
+
+namespace {
+template <typename Fn>
+int unary(const float* x, int64_t n, prlab_kcfg cfg, float* out, Fn fn) {
+  return guarded([&] {
+    validate_kcfg(cfg);
+    require_device();
+    if (n == 0) return;
+    TmpDev dx(n * 4), dout(n * 4);
+    PRLAB_CUDA(cudaMemcpy(dx.p, x, n * 4, cudaMemcpyHostToDevice));
+    fn(dx.f(), n, K(cfg), dout.f());
+    PRLAB_CUDA(cudaMemcpy(out, dout.p, n * 4, cudaMemcpyDeviceToHost));
+  });
+}
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// host fixture generators (reference build_model / random_tokens streams)
+// ---------------------------------------------------------------------------
+namespace {
+// std::mt19937_64 (the engine named at src/model.cpp:23 and :292)
+struct Mt64 {
+  uint64_t mt[312];
+  int i = 312;
+  explicit Mt64(uint64_t seed) {
+    mt[0] = seed;
+    for (int k = 1; k < 312; ++k) mt[k] = 6364136223846793005ULL * (mt[k - 1] ^ (mt[k - 1] >> 62)) + k;
+  }
+  uint64_t operator()() {
+    if (i >= 312) {
+      static const uint64_t mag[2] = {0ULL, 0xB5026F5AA96619E9ULL};
+      for (int k = 0; k < 312; ++k) {
+        const uint64_t x = (mt[k] & 0xFFFFFFFF80000000ULL) | (mt[(k + 1) % 312] & 0x7FFFFFFFULL);
+        mt[k] = mt[(k + 156) % 312] ^ (x >> 1) ^ mag[x & 1];
+      }
+      i = 0;
+    }
+    uint64_t x = mt[i++];
+    x ^= (x >> 29) & 0x5555555555555555ULL;
+    x ^= (x << 17) & 0x71D67FFFEDA60000ULL;
+    x ^= (x << 37) & 0xFFF7EEE000000000ULL;
+    x ^= (x >> 43);
+    return x;
+  }
+};
+}  // namespace
+
+// ===========================================================================
+// C ABI
+// ===========================================================================
+extern "C" {
+
+const char* prlab_gpu_last_error(void) { return g_last_error.c_str(); }
+int prlab_gpu_abi_version(void) { return PRLAB_GPU_ABI_VERSION; }
+
+int prlab_gpu_resolve_policy(const char* name, prlab_policy* out) {
+  return guarded([&] {
+    // resolve_policy, src/policy.cpp:49-67
+    const std::string n = name ? name : "";
+    const prlab_kcfg f32{0, 0, 1}, full{1, 1, 0}, wide{1, 0, 1};
+    prlab_policy p;
+    if (n == "fp32") {
+      for (auto& c : p.cls) c = f32;
+    } else if (n == "full_fp16") {
+      for (auto& c : p.cls) c = full;
+    } else if (n == "hybrid") {
+      for (auto& c : p.cls) c = f32;
+      p.cls[PRLAB_LINEAR] = wide;
+      p.cls[PRLAB_ATTENTION_SCORE_MATMUL] = wide;
+      p.cls[PRLAB_ACTIVATION] = wide;
+    } else {
+      throw std::invalid_argument("unknown policy '" + n + "' (valid: fp32, full_fp16, hybrid)");
+    }
+    *out = p;
+  });
+}
+
+uint64_t prlab_gpu_param_count(const prlab_model_desc* d) {
+  uint64_t n = 0;
+  for (size_t s : param_sizes(*d)) n += s;
+  return n;
+}
+
+int prlab_gpu_build_model(const prlab_model_desc* desc, float* out, int64_t out_len) {
+  return guarded([&] {
+    validate_desc(*desc);
+    const auto sizes = param_sizes(*desc);
+    uint64_t total = 0;
+    for (size_t s : sizes) total += s;
+    if (static_cast<uint64_t>(out_len) != total)
+      throw std::invalid_argument("build_model: output holds " + std::to_string(out_len) + " floats, need " +
+                                  std::to_string(total));
+    // NormalSampler (src/model.cpp:22-44): the uniform stream is sequential; the
+    // Box-Muller transform of each pair is independent, so it runs on threads.
+    Mt64 rng(desc->seed);
+    // per tensor: 0 = matrix (normal draws), 1 = gamma (ones), 2 = zeros
+    std::vector<int> kind = {0, 0};
+    for (int64_t l = 0; l < desc->num_layers; ++l) {
+      const int k[16] = {1, 2, 0, 2, 0, 2, 0, 2, 0, 2, 1, 2, 0, 2, 0, 2};
+      kind.insert(kind.end(), k, k + 16);
+    }
+    kind.push_back(1);
+    kind.push_back(2);
+    if (desc->archetype == 0) {
+      const int k[4] = {0, 2, 0, 2};
+      kind.insert(kind.end(), k, k + 4);
+    }
+    uint64_t n_normal = 0;
+    for (size_t t = 0; t < sizes.size(); ++t)
+      if (kind[t] == 0) n_normal += sizes[t];
+    const uint64_t pairs = (n_normal + 1) / 2;
+    std::vector<uint64_t> u(2 * pairs);
+    for (auto& x : u) x = rng();
+    std::vector<float> normals(2 * pairs);
+    const unsigned nt = std::max(1u, std::min(32u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> pool;
+    for (unsigned t = 0; t < nt; ++t)
+      pool.emplace_back([&, t] {
+        for (uint64_t i = t; i < pairs; i += nt) {
+          const double u1 = (static_cast<double>(u[2 * i] >> 11) + 0.5) * 0x1.0p-53;
+          const double u2 = static_cast<double>(u[2 * i + 1] >> 11) * 0x1.0p-53;
+          const double r = std::sqrt(-2.0 * std::log(u1));
+          const double a = 2.0 * 3.14159265358979323846 * u2;
+          normals[2 * i] = static_cast<float>(r * std::cos(a) * static_cast<double>(0.02f));
+          normals[2 * i + 1] = static_cast<float>(r * std::sin(a) * static_cast<double>(0.02f));
+        }
+      });
+    for (auto& th : pool) th.join();
+    float* o = out;
+    uint64_t k = 0;
+    for (size_t t = 0; t < sizes.size(); ++t) {
+      for (size_t i = 0; i < sizes[t]; ++i) o[i] = kind[t] == 0 ? normals[k++] : (kind[t] == 1 ? 1.0f : 0.0f);
+      o += sizes[t];
+    }
+  });
+}
+
+int prlab_gpu_random_tokens(int64_t vocab, int64_t batch, int64_t seq, uint64_t seed, int32_t* ids) {
+  return guarded([&] {
+    if (vocab < 1 || batch < 1 || seq < 1)
+      throw std::invalid_argument("random_tokens needs vocab, batch, seq >= 1");
+    Mt64 rng(seed);
+    for (int64_t i = 0; i < batch * seq; ++i) ids[i] = static_cast<int32_t>(rng() % static_cast<uint64_t>(vocab));
+  });
+}
+
+int prlab_gpu_argmax_device(const void* d_logits, int32_t dtype, int64_t rows, int64_t n, int64_t ld,
+                            int32_t* d_tokens, void* stream) {
+  return guarded([&] {
+    if (dtype != PRLAB_OUT_F32 && dtype != PRLAB_OUT_F16) throw std::invalid_argument("unknown logits dtype");
+    argmax_rows(d_logits, dtype, rows, n, ld, d_tokens, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int prlab_gpu_validate_policy(const prlab_policy* p) {
+  return guarded([&] { validate_policy(*p); });
+}
+
+int prlab_gpu_model_create(const prlab_model_desc* desc, const float* const* params, int64_t n_params,
+                           int device, prlab_gpu_model** out) {
+  return guarded([&] {
+    *out = nullptr;
+    validate_desc(*desc);
+    const auto sizes = param_sizes(*desc);
+    if (static_cast<size_t>(n_params) != sizes.size())
+      throw std::invalid_argument("expected " + std::to_string(sizes.size()) + " parameter tensors, got " +
+                                  std::to_string(n_params));
+    require_device();
+    PRLAB_CUDA(cudaSetDevice(device));
+    auto m = std::make_unique<prlab_gpu_model>();
+    m->d = *desc;
+    m->device = device;
+    m->h = desc->hidden;
+    m->f = desc->ffn;
+    m->H = desc->heads;
+    m->hd = desc->hidden / desc->heads;
+    m->V = desc->vocab;
+    m->P = desc->max_positions;
+    m->L = desc->num_layers;
+    m->host.resize(sizes.size());
+    for (size_t i = 0; i < sizes.size(); ++i) m->host[i].assign(params[i], params[i] + sizes[i]);
+    upload_fast(*m);
+    configure_gemm_tc();
+    configure_attn_tc();
+    PRLAB_CUDA(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
+    *out = m.release();
+  });
+}
+
+int prlab_gpu_model_create_flat(const prlab_model_desc* desc, const float* flat, int device,
+                                prlab_gpu_model** out) {
+  return guarded([&] {
+    validate_desc(*desc);
+    const auto sizes = param_sizes(*desc);
+    std::vector<const float*> ptrs;
+    const float* p = flat;
+    for (size_t s : sizes) {
+      ptrs.push_back(p);
+      p += s;
+    }
+    const int rc = prlab_gpu_model_create(desc, ptrs.data(), static_cast<int64_t>(ptrs.size()), device, out);
+    if (rc != PRLAB_OK) throw std::runtime_error(g_last_error);
+  });
+}
+
+void prlab_gpu_model_destroy(prlab_gpu_model* m) {
+  if (!m) return;
+  cudaSetDevice(m->device);
+  delete m;
+}
+
+int prlab_gpu_model_memory(const prlab_gpu_model* m, uint64_t* weight_bytes, uint64_t* workspace_bytes) {
+  return guarded([&] {
+    if (weight_bytes) *weight_bytes = m->arena16.bytes + m->arena32.bytes;
+    if (workspace_bytes) *workspace_bytes = m->ws.bytes;
+  });
+}
+
+int prlab_gpu_forward(prlab_gpu_model* m, const int32_t* ids, int64_t B, int64_t S,
+                      const prlab_policy* policy, float* logits, prlab_trace* trace) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(m->mu);
+    validate_policy(*policy);
+    check_forward_args(*m, B, S);
+    for (int64_t i = 0; i < B * S; ++i)  // embed(), src/kernels.cpp:278-283
+      if (ids[i] < 0 || ids[i] >= m->V)
+        throw std::out_of_range("token id " + std::to_string(ids[i]) + " outside vocab of " +
+                                std::to_string(m->V));
+    PRLAB_CUDA(cudaSetDevice(m->device));
+    auto& p = get_plan(*m, B, S, *policy);
+    const int64_t w = m->L > 0 ? m->V : m->h;
+    cudaStream_t st = m->stream;
+    PRLAB_CUDA(cudaMemcpyAsync(p.ids, ids, B * S * 4, cudaMemcpyHostToDevice, st));
+    run_forward(*m, p, p.ids, p.out32, PRLAB_OUT_F32, w, st, !std::getenv("PRLAB_NO_GRAPH"));
+    PRLAB_CUDA(cudaMemcpyAsync(logits, p.out32, B * S * w * 4, cudaMemcpyDeviceToHost, st));
+    PRLAB_CUDA(cudaStreamSynchronize(st));
+    if (trace) fill_calls(*m, B, *policy, trace);
+  });
+}
+
+int prlab_gpu_forward_device(prlab_gpu_model* m, const int32_t* d_ids, int64_t B, int64_t S,
+                             const prlab_policy* policy, void* d_out, int32_t out_dtype, int64_t ld,
+                             void* stream, int32_t use_graph) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(m->mu);
+    validate_policy(*policy);
+    check_forward_args(*m, B, S);
+    const int64_t w = m->L > 0 ? m->V : m->h;
+    if (ld < w) throw std::invalid_argument("logits row pitch smaller than the logits width");
+    if (out_dtype != PRLAB_OUT_F32 && out_dtype != PRLAB_OUT_F16)
+      throw std::invalid_argument("unknown logits dtype");
+    PRLAB_CUDA(cudaSetDevice(m->device));
+    auto& p = get_plan(*m, B, S, *policy);
+    run_forward(*m, p, d_ids, d_out, out_dtype, ld, static_cast<cudaStream_t>(stream), use_graph != 0);
+  });
+}
+
+int prlab_gpu_sync_status(prlab_gpu_model* m, void* stream) {
+  return guarded([&] {
+    PRLAB_CUDA(cudaSetDevice(m->device));
+    PRLAB_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    int e = 0;
+    PRLAB_CUDA(cudaMemcpy(&e, m->err.p, 4, cudaMemcpyDeviceToHost));
+    if (e) {
+      PRLAB_CUDA(cudaMemset(m->err.p, 0, 4));
+      throw std::out_of_range("token id outside vocab of " + std::to_string(m->V));
+    }
+  });
+}
+
+int prlab_gpu_forward_kernel_count(prlab_gpu_model* m, int64_t B, int64_t S, const prlab_policy* policy,
+                                   int64_t* count) {
+  return guarded([&] {
+    check_forward_args(*m, B, S);
+    const bool fast = fast_eligible(*m, S, *policy);
+    const int64_t L = m->L;
+    *count = fast ? 1 + 7 * L + 1 + 1 : 1 + 7 * L + (L > 0 ? 2 : 1);
+  });
+}
+
+// ---- per-operator entry points (host fp32 in/out, synchronous) ----
+int prlab_gpu_matmul(const float* a, const float* b, int64_t m, int64_t k, int64_t n, prlab_kcfg cfg,
+                     float* out) {
+  return guarded([&] {
+    validate_kcfg(cfg);
+    if (m < 0 || k < 0 || n < 0) throw std::invalid_argument("negative extent in matmul");
+    require_device();
+    if (m == 0 || n == 0) return;
+    TmpDev da(m * k * 4), db(k * n * 4), dbt(k * n * 4), dout(m * n * 4);
+    PRLAB_CUDA(cudaMemcpy(da.p, a, m * k * 4, cudaMemcpyHostToDevice));
+    PRLAB_CUDA(cudaMemcpy(db.p, b, k * n * 4, cudaMemcpyHostToDevice));
+    transpose_f32(db.f(), static_cast<int>(k), static_cast<int>(n), dbt.f(), 0, nullptr);
+    simt_gemm(da.f(), k, dbt.f(), k, dout.f(), n, static_cast<int>(m), static_cast<int>(n),
+              static_cast<int>(k), K(cfg), SimtGemmEpi{nullptr, 0, K(cfg), K(cfg), nullptr}, nullptr);
+    PRLAB_CUDA(cudaMemcpy(out, dout.p, m * n * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+int prlab_gpu_attention_scores(const float* q, const float* k, int64_t sq, int64_t sk, int64_t d, float scale,
+                               prlab_kcfg cfg, float* out, float* capture) {
+  return guarded([&] {
+    validate_kcfg(cfg);
+    require_device();
+    if (sq == 0 || sk == 0) return;
+    TmpDev dq(sq * d * 4), dk(sk * d * 4), dout(sq * sk * 4), dtap(capture ? sq * sk * 4 : 4);
+    PRLAB_CUDA(cudaMemcpy(dq.p, q, sq * d * 4, cudaMemcpyHostToDevice));
+    PRLAB_CUDA(cudaMemcpy(dk.p, k, sk * d * 4, cudaMemcpyHostToDevice));
+    simt_scores(dq.f(), dk.f(), static_cast<int>(sq), static_cast<int>(sk), static_cast<int>(d), scale, K(cfg),
+                dout.f(), capture ? dtap.f() : nullptr, nullptr);
+    PRLAB_CUDA(cudaMemcpy(out, dout.p, sq * sk * 4, cudaMemcpyDeviceToHost));
+    if (capture) PRLAB_CUDA(cudaMemcpy(capture, dtap.p, sq * sk * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+int prlab_gpu_softmax(const float* x, int64_t rows, int64_t n, prlab_kcfg cfg, float* out) {
+  return guarded([&] {
+    validate_kcfg(cfg);
+    if (n < 1) throw std::invalid_argument("softmax needs a non-empty last axis");
+    require_device();
+    if (rows == 0) return;
+    TmpDev dx(rows * n * 4), dout(rows * n * 4);
+    PRLAB_CUDA(cudaMemcpy(dx.p, x, rows * n * 4, cudaMemcpyHostToDevice));
+    simt_softmax(dx.f(), rows, n, K(cfg), dout.f(), nullptr);
+    PRLAB_CUDA(cudaMemcpy(out, dout.p, rows * n * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+int prlab_gpu_layernorm(const float* x, int64_t rows, int64_t n, const float* gamma, const float* beta,
+                        float eps, prlab_kcfg cfg, float* out) {
+  return guarded([&] {
+    validate_kcfg(cfg);
+    if (n < 1) throw std::invalid_argument("layernorm needs a non-empty last axis");
+    require_device();
+    if (rows == 0) return;
+    TmpDev dx(rows * n * 4), dg(n * 4), db(n * 4), dout(rows * n * 4);
+    PRLAB_CUDA(cudaMemcpy(dx.p, x, rows * n * 4, cudaMemcpyHostToDevice));
+    PRLAB_CUDA(cudaMemcpy(dg.p, gamma, n * 4, cudaMemcpyHostToDevice));
+    PRLAB_CUDA(cudaMemcpy(db.p, beta, n * 4, cudaMemcpyHostToDevice));
+    simt_layernorm(dx.f(), static_cast<int>(rows), static_cast<int>(n), dg.f(), db.f(), eps, K(cfg), dout.f(),
+                   nullptr, 0, nullptr);
+    PRLAB_CUDA(cudaMemcpy(out, dout.p, rows * n * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+int prlab_gpu_gelu(const float* x, int64_t n, prlab_kcfg cfg, float* out) {
+  return unary(x, n, cfg, out, [](const float* a, int64_t nn, Kcfg c, float* o) { simt_gelu(a, nn, c, o, nullptr); });
+}
+int prlab_gpu_tanh(const float* x, int64_t n, prlab_kcfg cfg, float* out) {
+  return unary(x, n, cfg, out, [](const float* a, int64_t nn, Kcfg c, float* o) { simt_tanh(a, nn, c, o, nullptr); });
+}
+int prlab_gpu_add(const float* a, const float* b, int64_t n, prlab_kcfg cfg, float* out) {
+  return guarded([&] {
+    validate_kcfg(cfg);
+    require_device();
+    if (n == 0) return;
+    TmpDev da(n * 4), db(n * 4), dout(n * 4);
+    PRLAB_CUDA(cudaMemcpy(da.p, a, n * 4, cudaMemcpyHostToDevice));
+    PRLAB_CUDA(cudaMemcpy(db.p, b, n * 4, cudaMemcpyHostToDevice));
+    simt_add(da.f(), db.f(), n, K(cfg), dout.f(), nullptr);
+    PRLAB_CUDA(cudaMemcpy(out, dout.p, n * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+int prlab_gpu_embed(const float* tok, int64_t vocab, const float* pos, int64_t npos, int64_t h,
+                    const int32_t* ids, int64_t B, int64_t S, prlab_kcfg cfg, float* out) {
+  return guarded([&] {
+    validate_kcfg(cfg);
+    // embed(), src/kernels.cpp:270-283 (same exception types and messages)
+    if (S > npos)
+      throw std::out_of_range("sequence length " + std::to_string(S) + " exceeds position table extent " +
+                              std::to_string(npos));
+    for (int64_t i = 0; i < B * S; ++i)
+      if (ids[i] < 0 || ids[i] >= vocab)
+        throw std::out_of_range("token id " + std::to_string(ids[i]) + " outside vocab of " + std::to_string(vocab));
+    require_device();
+    if (B * S == 0) return;
+    TmpDev dt(vocab * h * 4), dp(npos * h * 4), di(B * S * 4), dout(B * S * h * 4);
+    PRLAB_CUDA(cudaMemcpy(dt.p, tok, vocab * h * 4, cudaMemcpyHostToDevice));
+    PRLAB_CUDA(cudaMemcpy(dp.p, pos, npos * h * 4, cudaMemcpyHostToDevice));
+    PRLAB_CUDA(cudaMemcpy(di.p, ids, B * S * 4, cudaMemcpyHostToDevice));
+    if (cfg.compute == 0 && h % 4 == 0)
+      embed_f32(dt.f(), vocab, dp.f(), static_cast<int>(h), static_cast<int32_t*>(di.p), static_cast<int>(B),
+                static_cast<int>(S), dout.f(), nullptr, nullptr);
+    else
+      simt_embed(dt.f(), vocab, dp.f(), static_cast<int>(h), static_cast<int32_t*>(di.p), static_cast<int>(B),
+                 static_cast<int>(S), K(cfg), dout.f(), nullptr, nullptr);
+    PRLAB_CUDA(cudaMemcpy(out, dout.p, B * S * h * 4, cudaMemcpyDeviceToHost));
+  });
+}
+
+int prlab_gpu_linear_f16_device(const void* A, const void* Wt, const float* bias, void* out, int64_t M,
+                                int64_t N, int64_t K_, int64_t ldo, int32_t epi, void* stream) {
+  return guarded([&] {
+    if (epi < 0 || epi > 3) throw std::invalid_argument("unknown epilogue");
+    const GemmPlan p = plan_gemm_tc(A, K_, Wt, K_, bias, out, ldo, static_cast<int>(M), static_cast<int>(N),
+                                    static_cast<int>(K_), epi);
+    launch_gemm_tc(p, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int prlab_gpu_attention_f16_device(const void* qkv, void* ctx, int64_t B, int64_t S, int64_t H, int64_t hd,
+                                   int32_t causal, void* stream) {
+  return guarded([&] {
+    const AttnPlan p = plan_attn_tc(qkv, 3 * H * hd, ctx, H * hd, static_cast<int>(B), static_cast<int>(S),
+                                    static_cast<int>(H), static_cast<int>(hd), causal);
+    launch_attn_tc(p, static_cast<cudaStream_t>(stream));
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,172 @@
+"""End-to-end forward parity on the GPU against the CPU oracle (a bit-exact
+restatement of the reference, pinned in tests/test_oracle_*.py).
+
+Bars (BASELINE.json north_star):
+  * fp32 policy: max|gpu - cpu| / max|cpu| <= 1e-3, argmax identical where the
+    CPU top-1/top-2 gap exceeds 1e-5;
+  * hybrid policy: cosine(gpu_hybrid, cpu_fp32) >= 0.9998 and zero non-finite;
+  * embedding gathers bit-exact (zero-layer model).
+"""
+import numpy as np
+import pytest
+
+import paper_2603_28708_b200 as pg
+from oracle.oracle import PRESETS, compare_logits
+from prlab_testutil import model_params, oracle
+
+pytestmark = pytest.mark.gpu
+
+_MODELS = {}
+
+
+def device_model(cfg):
+    if cfg not in _MODELS:
+        _MODELS[cfg] = pg.DeviceModel(pg.ModelConfig(**cfg.__dict__), model_params(cfg))
+    return _MODELS[cfg]
+
+
+def rel_err(got, want):
+    return float(np.abs(got.astype(np.float64) - want).max() / np.abs(want).max())
+
+
+def argmax_check(got, want, min_gap):
+    w = want.reshape(-1, want.shape[-1]).astype(np.float64)
+    g = got.reshape(-1, got.shape[-1])
+    top2 = np.sort(w, axis=1)[:, -2:]
+    gap = top2[:, 1] - top2[:, 0]
+    rows = gap > min_gap
+    return int((np.argmax(g, 1)[rows] != np.argmax(w, 1)[rows]).sum()), int(rows.sum())
+
+
+TOYS = [PRESETS["decoder_toy"], PRESETS["encoder_toy"], PRESETS["decoder_toy"].replace(seed=5)]
+
+
+@pytest.mark.parametrize("cfg", TOYS, ids=["dec", "enc", "dec_seed5"])
+@pytest.mark.parametrize("B,S", [(1, 16), (3, 37)])
+def test_toy_forward_all_policies(cfg, B, S):
+    o = oracle()
+    m = device_model(cfg)
+    ids = o.random_tokens(cfg.vocab, B, S, 11)
+    p = model_params(cfg)
+    cpu32 = o.forward(cfg, p, ids, B, S, "fp32")
+    # fp32 policy (generic SIMT path)
+    got, tr = m.forward(ids, B, S, "fp32", want_trace=True)
+    assert rel_err(got, cpu32) <= 1e-3
+    bad, n = argmax_check(got, cpu32, 1e-5)
+    assert bad == 0, f"{bad}/{n} argmax mismatches on the fp32 path"
+    # hybrid (generic path at toy sizes: h=128 -> fast path too when eligible)
+    gh = m.forward(ids, B, S, "hybrid")
+    cmp = compare_logits(cpu32, gh)
+    assert cmp["candidate_nonfinite"] == 0 and cmp["cosine"] >= 0.9998
+    cpuh = o.forward(cfg, p, ids, B, S, "hybrid")
+    assert np.abs(gh - cpuh).max() < 2e-2
+    # full_fp16 (exact per-MAC rounding emulation on the GPU)
+    gf = m.forward(ids, B, S, "full_fp16")
+    cpuf = o.forward(cfg, p, ids, B, S, "full_fp16")
+    assert np.isfinite(gf).all() == np.isfinite(cpuf).all()
+    assert np.abs(gf - cpuf).max() < 5e-2
+    # routing counts identical to the reference trace (test_policy.cpp:77-109)
+    _, calls = o.forward(cfg, p, ids, B, S, "fp32", want_calls=True)
+    for c in range(7):
+        for d in range(2):
+            assert tr.kernel_calls[c][d] == calls[c][d]
+
+
+def test_forward_generic_hybrid_equals_oracle_closely():
+    """Generic-path hybrid GEMMs are bit-exact (fp16 products are exact in fp32)."""
+    import os
+    cfg = PRESETS["decoder_toy"]
+    o = oracle()
+    ids = o.random_tokens(cfg.vocab, 2, 24, 3)
+    os.environ["PRLAB_FORCE_GENERIC"] = "1"
+    try:
+        m = pg.DeviceModel(pg.ModelConfig(**cfg.__dict__), model_params(cfg))
+        got = m.forward(ids, 2, 24, "hybrid")
+    finally:
+        del os.environ["PRLAB_FORCE_GENERIC"]
+    want = o.forward(cfg, model_params(cfg), ids, 2, 24, "hybrid")
+    assert np.abs(got - want).max() < 5e-3
+
+
+@pytest.mark.parametrize("name,B,S", [("gpt2_small", 1, 128), ("bert_base", 2, 64),
+                                      ("gpt2_small", 2, 77)])
+def test_preset_hybrid_fast_path(name, B, S):
+    cfg = PRESETS[name]
+    o = oracle()
+    m = device_model(cfg)
+    ids = o.random_tokens(cfg.vocab, B, S, 1234)
+    got = m.forward(ids, B, S, "hybrid")
+    cpu32 = o.forward(cfg, model_params(cfg), ids, B, S, "fp32")
+    cmp = compare_logits(cpu32, got)
+    assert cmp["candidate_nonfinite"] == 0
+    assert cmp["cosine"] >= 0.9998, cmp
+    assert cmp["max_abs_error"] < 2e-2, cmp
+
+
+def test_preset_fp32_path_gpt2():
+    cfg = PRESETS["gpt2_small"]
+    o = oracle()
+    m = device_model(cfg)
+    ids = o.random_tokens(cfg.vocab, 1, 32, 99)
+    got = m.forward(ids, 1, 32, "fp32")
+    want = o.forward(cfg, model_params(cfg), ids, 1, 32, "fp32")
+    assert rel_err(got, want) <= 1e-3
+    bad, n = argmax_check(got, want, 1e-5)
+    assert bad == 0 and n > 0
+
+
+def test_device_forward_graph_matches_host_forward():
+    torch = pytest.importorskip("torch")
+    cfg = PRESETS["gpt2_small"]
+    o = oracle()
+    m = device_model(cfg)
+    B, S = 2, 128
+    ids = o.random_tokens(cfg.vocab, B, S, 5)
+    host = m.forward(ids, B, S, "hybrid")
+    d_ids = torch.from_numpy(ids).cuda()
+    ld = (cfg.vocab + 7) // 8 * 8
+    out16 = torch.empty(B * S, ld, dtype=torch.float16, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    for use_graph in (False, True, True):
+        out16.fill_(float("nan"))
+        m.forward_device(d_ids.data_ptr(), B, S, "hybrid", out16.data_ptr(), pg.OUT_F16, ld, st,
+                         use_graph)
+        m.sync_status(st)
+        got = out16[:, :cfg.vocab].float().cpu().numpy().reshape(B, S, -1)
+        assert np.array_equal(got, host), "device fp16 logits differ from the host path"
+
+
+def test_forward_errors_match_reference():
+    cfg = PRESETS["decoder_toy"]
+    m = device_model(cfg)
+    with pytest.raises(IndexError, match="outside vocab"):
+        m.forward(np.array([0, 320], np.int32), 1, 2, "hybrid")
+    with pytest.raises(ValueError, match="exceeds max_positions"):
+        m.forward(np.zeros(161, np.int32), 1, 161, "hybrid")
+    with pytest.raises(ValueError, match="unknown policy"):
+        pg.resolve_policy("mixed")
+
+
+def test_zero_layer_is_bitexact_embedding():
+    cfg = PRESETS["decoder_toy"].replace(num_layers=0)
+    o = oracle()
+    p = o.build_model(cfg)
+    m = pg.DeviceModel(pg.ModelConfig(**cfg.__dict__), p)
+    ids = o.random_tokens(cfg.vocab, 2, 5, 7)
+    got = m.forward(ids, 2, 5, "fp32")
+    want = o.forward(cfg, p, ids, 2, 5, "fp32")
+    assert got.shape == (2, 5, cfg.hidden)
+    assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def test_decoder_causality_bitexact():  # test_model.cpp:169-203
+    cfg = PRESETS["gpt2_small"]
+    o = oracle()
+    m = device_model(cfg)
+    a = o.random_tokens(cfg.vocab, 1, 128, 1)
+    b = a.copy()
+    b[127] = (b[127] + 1) % cfg.vocab
+    la = m.forward(a, 1, 128, "hybrid")
+    lb = m.forward(b, 1, 128, "hybrid")
+    assert np.array_equal(la[0, :127], lb[0, :127])
+    assert not np.array_equal(la[0, 127], lb[0, 127])

@@ -1,0 +1,198 @@
+"""Parity of the hand-written sm_100a kernels (tcgen05 GEMM, fused attention) against
+plain PyTorch fp32 references of the same hybrid-lattice math, plus the per-operator
+C-ABI against the CPU oracle on the reference's known-answer tests."""
+import math
+
+import numpy as np
+import pytest
+
+import paper_2603_28708_b200 as pg
+from prlab_testutil import oracle
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+def r16(t):
+    return t.to(torch.float16).to(torch.float32)
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _no_tf32():
+    torch.backends.cuda.matmul.allow_tf32 = False
+    torch.backends.cudnn.allow_tf32 = False
+    yield
+
+
+def _gemm_ref(A, Wt, bias, epi, resid=None):
+    acc = A.float() @ Wt.float().T  # fp32 reference (TF32 disabled)
+    v = r16(acc)
+    if epi == 3:
+        return v
+    v = r16(v + (bias if bias is not None else 0.0))
+    if epi == 1:
+        v = r16(0.5 * v * (1.0 + torch.erf(v * 0.7071067811865476)))
+    if epi == 2:
+        return resid + v
+    return v
+
+
+# (M, N, K): tile-aligned, M/N tails, tiny, wide LM-head-like N, FFN shapes
+SHAPES = [(128, 256, 64), (300, 2304, 768), (1, 64, 64), (128, 50257, 768), (777, 3072, 768),
+          (2048, 768, 3072), (128, 768, 768), (4096, 2304, 768)]
+
+
+@pytest.mark.parametrize("M,N,K", SHAPES)
+@pytest.mark.parametrize("epi", [0, 1, 2, 3])
+def test_tc_linear_matches_fp32_reference(M, N, K, epi):
+    if epi != 0 and (M, N, K) in [(128, 50257, 768)]:
+        pytest.skip("head shape only needs epi 0/3")
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K + epi)
+    A = (torch.randn(M, K, device="cuda", generator=g) * 0.5).half()
+    Wt = (torch.randn(N, K, device="cuda", generator=g) * 0.05).half()
+    bias = r16(torch.randn(N, device="cuda", generator=g) * 0.1)
+    ldo = N if epi == 2 else (N + 7) // 8 * 8
+    if epi == 2:
+        out = torch.randn(M, N, device="cuda", generator=g)
+        resid = out.clone()
+    else:
+        out = torch.full((M, ldo), float("nan"), device="cuda", dtype=torch.float16)
+        resid = None
+    pg.linear_f16_device(A, Wt, bias if epi != 3 else None, out, M, N, K, ldo, epi)
+    torch.cuda.synchronize()
+    ref = _gemm_ref(A, Wt, bias, epi, resid)
+    got = out.float()[:, :N]
+    assert torch.isfinite(got).all(), "unwritten / non-finite outputs"
+    err = (got - ref).abs()
+    # accumulation order differs from fp32 sequential: allow one fp16 ulp at the value
+    tol = torch.clamp(ref.abs(), min=6.1e-5) * 2.0 ** -10 * 1.01 + 1e-6
+    frac_bad = (err > tol).float().mean().item()
+    assert frac_bad < 2e-3, f"max err {err.max().item():.3e}, {frac_bad:.2e} beyond 1 ulp"
+    assert err.max().item() <= 4 * tol.max().item() + 1e-3
+
+
+def _attn_ref(qkv, B, S, H, hd, causal):
+    h = H * hd
+    x = qkv.float().view(B, S, 3, H, hd)
+    q, k, v = x[:, :, 0].transpose(1, 2), x[:, :, 1].transpose(1, 2), x[:, :, 2].transpose(1, 2)
+    s = r16((q @ k.transpose(-1, -2)) * (1.0 / math.sqrt(hd)))
+    if causal:
+        mask = torch.triu(torch.ones(S, S, dtype=torch.bool, device=qkv.device), 1)
+        s = s.masked_fill(mask, float("-inf"))
+    m = s.amax(-1, keepdim=True)
+    e = torch.exp(s - m)
+    p = r16(e / e.sum(-1, keepdim=True))
+    o = r16(p @ v)
+    return o.transpose(1, 2).reshape(B * S, h)
+
+
+@pytest.mark.parametrize("B,S,causal", [(1, 128, 0), (1, 128, 1), (2, 77, 0), (2, 77, 1),
+                                         (1, 1, 1), (3, 200, 1), (2, 512, 0), (2, 512, 1),
+                                         (1, 384, 0), (4, 64, 1)])
+def test_tc_attention_matches_fp32_reference(B, S, causal):
+    H, hd = 12, 64
+    g = torch.Generator(device="cuda").manual_seed(B * 1000 + S * 2 + causal)
+    qkv = (torch.randn(B * S, 3 * H * hd, device="cuda", generator=g) * 1.5).half()
+    ctx = torch.full((B * S, H * hd), float("nan"), device="cuda", dtype=torch.float16)
+    pg.attention_f16_device(qkv, ctx, B, S, H, hd, causal)
+    torch.cuda.synchronize()
+    ref = _attn_ref(qkv, B, S, H, hd, causal)
+    got = ctx.float()
+    assert torch.isfinite(got).all()
+    err = (got - ref).abs()
+    assert err.max().item() < 2e-2, f"max err {err.max().item()}"
+    assert err.mean().item() < 1e-3
+
+
+# ---------------------------------------------------------------------------
+# per-operator C-ABI vs the oracle on the reference's known answers
+# (reference tests/test_kernels.cpp)
+# ---------------------------------------------------------------------------
+F32 = pg.KernelConfig(pg.F32, pg.F32, True)
+F16ACC = pg.KernelConfig(pg.F16E, pg.F16E, True)
+F16WIDE = pg.KernelConfig(pg.F16E, pg.F32, True)
+F16UNSTABLE = pg.KernelConfig(pg.F16E, pg.F16E, False)
+
+
+def test_kat_long_reductions():  # test_kernels.cpp:37-60
+    for n, want in [(2049, (2048.0, 2048.0, 2049.0)), (2050, (2048.0, 2050.0, 2050.0))]:
+        a = np.ones((1, n), np.float32)
+        b = np.ones((n, 1), np.float32)
+        assert pg.matmul(a, b, F16ACC)[0, 0] == want[0]
+        assert pg.matmul(a, b, F16WIDE)[0, 0] == want[1]
+        assert pg.matmul(a, b, F32)[0, 0] == want[2]
+
+
+def test_kat_matmul_vs_oracle_bitexact_narrow():
+    rng = np.random.default_rng(3)
+    a = rng.uniform(-1, 1, (17, 33)).astype(np.float32)
+    b = rng.uniform(-1, 1, (33, 9)).astype(np.float32)
+    o = oracle()
+    for cfg in [F16ACC, F16WIDE]:
+        got = pg.matmul(a, b, cfg)
+        want = o.matmul(a, b, cfg.compute, cfg.accum)
+        assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
+    got = pg.matmul(a, b, F32)
+    ref = a.astype(np.float64) @ b.astype(np.float64)
+    assert np.abs(got - ref).max() <= 33 * 1.2e-7 * 33
+
+
+def test_kat_softmax():  # test_kernels.cpp:82-98
+    x = np.array([[12.0, 0.0]], np.float32)
+    y = pg.softmax_lastdim(x, F16ACC)
+    assert y[0, 0] == 1.0 and y[0, 1] == np.float32(6.139278411865234e-06)
+    y = pg.softmax_lastdim(x, F16UNSTABLE)
+    assert np.isnan(y[0, 0]) and y[0, 1] == 0.0
+
+
+def test_kat_scores_fold_scale():  # test_kernels.cpp:119-135
+    q = np.array([[1, 2, 3], [4, 5, 6]], np.float32)
+    k = np.array([[7, 8, 9], [10, 11, 12]], np.float32)
+    s, tap = pg.attention_scores(q, k, 0.125, F16ACC, capture=True)
+    ref = (q.astype(np.float64) @ k.T.astype(np.float64)).astype(np.float32)
+    assert np.array_equal(tap, ref * np.float32(0.125))
+    assert np.array_equal(s, oracle().round16_array(ref * np.float32(0.125)))
+
+
+def test_kat_layernorm_gelu_add_embed():
+    y = pg.layernorm_lastdim(np.full((1, 6), 3.0, np.float32), np.ones(6, np.float32),
+                             np.full(6, 0.25, np.float32), 1e-5, F32)
+    assert np.allclose(y, 0.25, rtol=1e-6)
+    g = pg.gelu(np.array([0.0, 1.0, -1.0], np.float32), F32)
+    assert g[0] == 0.0
+    assert abs(g[1] - 0.8413447460685429) < 1e-6 and abs(g[2] + 0.15865525393145707) < 1e-6
+    assert pg.add(np.array([2048.0], np.float32), np.array([1.0], np.float32), F16ACC)[0] == 2048.0
+    assert pg.add(np.array([2048.0], np.float32), np.array([1.0], np.float32), F32)[0] == 2049.0
+    tok = np.array([[0, 0], [10, 20], [30, 40]], np.float32)
+    pos = np.array([[1, 2], [3, 4]], np.float32)
+    e = pg.embed(tok, pos, [2, 1], 1, 2, F32)
+    assert e.ravel().tolist() == [31.0, 42.0, 13.0, 24.0]
+    with pytest.raises(IndexError):
+        pg.embed(tok, pos, [3, 0], 1, 2, F32)
+    with pytest.raises(IndexError):
+        pg.embed(tok, pos, [0, 0, 0], 1, 3, F32)
+
+
+def test_kernel_config_validation():
+    with pytest.raises(ValueError):
+        pg.matmul(np.ones((2, 2), np.float32), np.ones((2, 2), np.float32),
+                  pg.KernelConfig(pg.F32, pg.F16E, True))
+
+
+def test_per_op_vs_oracle_random():
+    rng = np.random.default_rng(7)
+    o = oracle()
+    x = rng.uniform(-4, 4, (8, 16)).astype(np.float32)
+    for cfg in [F32, F16ACC, F16WIDE, F16UNSTABLE]:
+        got = pg.softmax_lastdim(x, cfg)
+        want = o.softmax(x, cfg.compute, cfg.accum, bool(cfg.stabilized))
+        assert np.allclose(got, want, rtol=2e-6, atol=1e-7, equal_nan=True)
+    xl = rng.normal(0, 1, (4, 64)).astype(np.float32)
+    gam = rng.normal(1, 0.1, 64).astype(np.float32)
+    bet = rng.normal(0, 0.1, 64).astype(np.float32)
+    for cfg in [F32, F16ACC]:
+        got = pg.layernorm_lastdim(xl, gam, bet, 1e-5, cfg)
+        want = o.layernorm(xl, gam, bet, 1e-5, cfg.compute, cfg.accum)
+        tol = 1e-5 if cfg.compute == pg.F32 else 2e-3
+        assert np.abs(got - want).max() <= tol
