@@ -94,6 +94,16 @@ class ClockSampler:
             except Exception:
                 self.proc.kill()
 
+    def wait_samples(self, n, timeout=5.0, busy=None):
+        """Block (optionally running `busy()` to keep the GPU loaded) until n new samples."""
+        start = len(self.lines)
+        t0 = time.time()
+        while len(self.lines) < start + n and time.time() - t0 < timeout:
+            if busy is not None:
+                busy()
+            else:
+                time.sleep(0.01)
+
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -271,14 +281,24 @@ def run_ours(args, wl):
 
     # ---- timed region: device-resident inputs; weights (0.25 GB) exceed L2 ----
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
-    barrier()
+
+    def busy():
+        for _ in range(8):
+            step()
+        torch.cuda.synchronize()
+
     with ClockSampler(local) as clk:
+        # the sampler brackets the timed region: >= 2 samples under load before it and
+        # one after it (a short timed region can fall between two 100 ms samples)
+        clk.wait_samples(2, busy=busy)
+        barrier()
         evs[0].record(stream)
         for i in range(args.steps):
             step()
             evs[i + 1].record(stream)
         torch.cuda.synchronize()
-    barrier()
+        barrier()
+        clk.wait_samples(1, busy=busy)
     per_step = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
     total_ms = evs[0].elapsed_time(evs[-1])
     model.sync_status(sp)

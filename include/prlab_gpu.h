@@ -168,10 +168,20 @@ int prlab_gpu_embed(const float* tok, int64_t vocab, const float* pos, int64_t n
 int prlab_gpu_linear_f16_device(const void* A, const void* Wt, const float* bias, void* out,
                                 int64_t M, int64_t N, int64_t K, int64_t ldo, int32_t epi,
                                 void* stream);
+/* Same with an explicit tile configuration (tuning sweeps): bn in {0 (auto), 64, 128, 256},
+ * splits (0 = auto), lean (0 = auto, 1 = half-depth pipeline, -1 = full depth). */
+int prlab_gpu_linear_f16_device_ex(const void* A, const void* Wt, const float* bias, void* out,
+                                   int64_t M, int64_t N, int64_t K, int64_t ldo, int32_t epi,
+                                   int32_t bn, int32_t splits, int32_t lean, void* stream);
 /* Fused hybrid attention on tensor cores: qkv fp16 [B*S, 3h] (q|k|v), ctx fp16 [B*S, h]. */
 int prlab_gpu_attention_f16_device(const void* qkv, void* ctx, int64_t batch, int64_t seq,
                                    int64_t heads, int64_t head_dim, int32_t causal,
                                    void* stream);
+
+/* Debug variant: dbg (device, [grid][8] int64) receives clock64() phase stamps per CTA. */
+int prlab_gpu_attention_f16_device_dbg(const void* qkv, void* ctx, int64_t batch, int64_t seq,
+                                       int64_t heads, int64_t head_dim, int32_t causal,
+                                       void* stream, long long* dbg);
 
 #ifdef __cplusplus
 }

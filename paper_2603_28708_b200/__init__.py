@@ -166,8 +166,13 @@ EXPORTS = [
                                   C.c_int64, KernelConfig, _FP]),
     ("prlab_gpu_linear_f16_device", C.c_int, [_P, _P, _P, _P, C.c_int64, C.c_int64, C.c_int64,
                                               C.c_int64, C.c_int32, _P]),
+    ("prlab_gpu_linear_f16_device_ex", C.c_int, [_P, _P, _P, _P, C.c_int64, C.c_int64, C.c_int64,
+                                                 C.c_int64, C.c_int32, C.c_int32, C.c_int32,
+                                                 C.c_int32, _P]),
     ("prlab_gpu_attention_f16_device", C.c_int, [_P, _P, C.c_int64, C.c_int64, C.c_int64,
                                                  C.c_int64, C.c_int32, _P]),
+    ("prlab_gpu_attention_f16_device_dbg", C.c_int, [_P, _P, C.c_int64, C.c_int64, C.c_int64,
+                                                     C.c_int64, C.c_int32, _P, _P]),
 ]
 
 
@@ -422,6 +427,13 @@ def linear_f16_device(A, Wt, bias, out, M, N, K, ldo, epi, stream=0):
     _check(lib().prlab_gpu_linear_f16_device(C.c_void_p(_ptr(A)), C.c_void_p(_ptr(Wt)),
                                              C.c_void_p(_ptr(bias)), C.c_void_p(_ptr(out)), M, N,
                                              K, ldo, epi, C.c_void_p(stream)))
+
+
+def linear_f16_device_ex(A, Wt, bias, out, M, N, K, ldo, epi, bn=0, splits=0, lean=0, stream=0):
+    _check(lib().prlab_gpu_linear_f16_device_ex(C.c_void_p(_ptr(A)), C.c_void_p(_ptr(Wt)),
+                                                C.c_void_p(_ptr(bias)), C.c_void_p(_ptr(out)), M,
+                                                N, K, ldo, epi, bn, splits, lean,
+                                                C.c_void_p(stream)))
 
 
 def attention_f16_device(qkv, ctx, B, S, H, hd, causal, stream=0):

@@ -32,6 +32,7 @@ struct AttnArgs {
   int h;  // hidden = H * hd (column offset of K; V at 2h)
   __half* ctx;
   int64_t ld_ctx;
+  long long* dbg;  // optional per-CTA phase timestamps [grid][8] (clock64), null = off
 };
 
 struct Smem {
@@ -66,6 +67,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int nkb_all = (a.S + 127) / 128;
   const int nkb = a.causal ? min(qt + 1, nkb_all) : nkb_all;  // key blocks that matter
   const uint32_t warp = warp_id(), lane = lane_id();
+  long long* dbg = a.dbg ? a.dbg + static_cast<int64_t>(blockIdx.x) * 8 : nullptr;
+  if (dbg && threadIdx.x == 0) dbg[0] = clock64();
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm);
@@ -79,20 +82,26 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_trigger();
   const uint32_t tmem = *tmem_slot;
+  if (dbg && threadIdx.x == 0) dbg[1] = clock64();
+  // V tiles get their own buffers when K uses at most half of the KV region
+  // (S <= 256): then V streams in concurrently with Q.K^T instead of after it.
+  const int v_slot0 = nkb <= kMaxKB / 2 ? kMaxKB / 2 : 0;
 
   if (warp == 0) {
     if (lane == 0) {
+      pdl_wait();  // q/k/v are written by the upstream QKV GEMM
       mbar_expect_tx(q_full, kTile);
       tma_load_3d(smem + Smem::Q, &tm, q_full, head * 64, qt * 128, b);
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_expect_tx(&k_full[kb], kTile);
         tma_load_3d(smem + Smem::KV + kb * kTile, &tm, &k_full[kb], a.h + head * 64, kb * 128, b);
       }
-      mbar_wait(s_full, 0);  // QK^T done reading K: reuse the buffers for V
+      if (v_slot0 == 0) mbar_wait(s_full, 0);  // QK^T done reading K: reuse the buffers for V
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_expect_tx(&v_full[kb], kTile);
-        tma_load_3d(smem + Smem::KV + kb * kTile, &tm, &v_full[kb], 2 * a.h + head * 64,
+        tma_load_3d(smem + Smem::KV + (v_slot0 + kb) * kTile, &tm, &v_full[kb], 2 * a.h + head * 64,
                     kb * 128, b);
       }
     }
@@ -102,6 +111,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // ---- S = Q . K^T : M=128 queries, N=128 keys per block, K = 64 (4 x 16)
       constexpr uint32_t idesc_s = idesc_f16_f32(128, 128, 0, 0);
       mbar_wait(q_full, 0);
+      if (dbg) dbg[2] = clock64();
       const uint32_t q0 = smem_u32(smem + Smem::Q);
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&k_full[kb], 0);
@@ -121,7 +131,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kb = 0; kb < nkb; ++kb) {
         mbar_wait(&v_full[kb], 0);
         tc_fence_after();
-        const uint32_t v0 = smem_u32(smem + Smem::KV + kb * kTile);
+        const uint32_t v0 = smem_u32(smem + Smem::KV + (v_slot0 + kb) * kTile);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {  // 16 keys per MMA
           const uint32_t pa = p0 + (kb * 2 + kk / 4) * kTile + (kk % 4) * 32;
@@ -148,46 +158,74 @@ __global__ void __launch_bounds__(kThreads, 1)
 
     mbar_wait(s_full, 0);
     tc_fence_after();
+    const bool stamp = dbg && sw == 0 && lane == 0;
+    if (stamp) dbg[3] = clock64();
+    // the mask only matters on chunks that cross the sequence end or the diagonal
+    // (warp-uniform test: rows of this warp are qt*128 + quad*32 + [0, 32))
+    const int row_lo = qt * 128 + quad * 32;
+    auto chunk_unmasked = [&](int c) { return c + 32 <= a.S && (!a.causal || c + 31 <= row_lo); };
     // pass 1: row max of round16(acc * 0.125) with the mask applied
     float mx = NEG_INF;
     for (int c = c_begin; c < c_end; c += 32) {
       uint32_t v[32];
       tmem_ld32(lane_addr + c, v);
       tmem_wait_ld();
+      if (chunk_unmasked(c)) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int j = c + i;
-        float s = r16(__fmul_rn(__uint_as_float(v[i]), 0.125f));
-        const bool valid = j < a.S && (!a.causal || j <= qrow);
-        mx = fmaxf(mx, valid ? s : NEG_INF);
+        for (int i = 0; i < 32; ++i) mx = fmaxf(mx, r16(__fmul_rn(__uint_as_float(v[i]), 0.125f)));
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int j = c + i;
+          float s = r16(__fmul_rn(__uint_as_float(v[i]), 0.125f));
+          const bool valid = j < a.S && (!a.causal || j <= qrow);
+          mx = fmaxf(mx, valid ? s : NEG_INF);
+        }
       }
     }
     red_max[grp * 128 + r] = mx;
     named_bar_sync(1, kSoftmaxWarps * 32);
     mx = fmaxf(fmaxf(red_max[r], red_max[128 + r]), fmaxf(red_max[256 + r], red_max[384 + r]));
-    // pass 2: e = exp(s - max) kept in TMEM (fp32), partial sums in key order
+    if (stamp) dbg[4] = clock64();
+    // pass 2: e = exp(s - max) kept in TMEM (fp32), partial sums in key order.
+    // exp(s - mx) = 2^(s*log2e - mx*log2e): one FFMA + one SFU op per element.
+    constexpr float LOG2E = 1.4426950408889634f;
+    const float mxl = __fmul_rn(mx, LOG2E);
     float sum = 0.0f;
     for (int c = c_begin; c < c_end; c += 32) {
       uint32_t v[32];
       tmem_ld32(lane_addr + c, v);
       tmem_wait_ld();
+      if (chunk_unmasked(c)) {
 #pragma unroll
-      for (int i = 0; i < 32; ++i) {
-        const int j = c + i;
-        const float s = r16(__fmul_rn(__uint_as_float(v[i]), 0.125f));
-        const bool valid = j < a.S && (!a.causal || j <= qrow);
-        const float e = valid ? expf(__fsub_rn(s, mx)) : 0.0f;
-        sum = __fadd_rn(sum, e);
-        v[i] = __float_as_uint(e);
+        for (int i = 0; i < 32; ++i) {
+          const float s = r16(__fmul_rn(__uint_as_float(v[i]), 0.125f));
+          const float e = ex2_approx(fmaf(s, LOG2E, -mxl));
+          sum = __fadd_rn(sum, e);
+          v[i] = __float_as_uint(e);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const int j = c + i;
+          const float s = r16(__fmul_rn(__uint_as_float(v[i]), 0.125f));
+          const bool valid = j < a.S && (!a.causal || j <= qrow);
+          const float e = valid ? ex2_approx(fmaf(s, LOG2E, -mxl)) : 0.0f;
+          sum = __fadd_rn(sum, e);
+          v[i] = __float_as_uint(e);
+        }
       }
       tmem_st32(lane_addr + c, v);
     }
     tmem_wait_st();
+    if (stamp) dbg[5] = clock64();
     red_sum[grp * 128 + r] = sum;
     named_bar_sync(1, kSoftmaxWarps * 32);
     sum = __fadd_rn(__fadd_rn(__fadd_rn(red_sum[r], red_sum[128 + r]), red_sum[256 + r]),
                     red_sum[384 + r]);
     // pass 3: p = round16(e / sum) -> fp16 into the swizzled P operand
+    // (e * (1/sum): one correctly rounded reciprocal per row instead of a divide per element)
+    const float inv = __frcp_rn(sum);
     uint8_t* prow = smem + Smem::P;
     for (int c = c_begin; c < c_end; c += 32) {
       uint32_t v[32];
@@ -196,8 +234,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       uint32_t pk[16];
 #pragma unroll
       for (int i = 0; i < 16; ++i) {
-        const float p0 = __fdiv_rn(__uint_as_float(v[2 * i]), sum);
-        const float p1 = __fdiv_rn(__uint_as_float(v[2 * i + 1]), sum);
+        const float p0 = __fmul_rn(__uint_as_float(v[2 * i]), inv);
+        const float p1 = __fmul_rn(__uint_as_float(v[2 * i + 1]), inv);
         __half2 h2 = __floats2half2_rn(p0, p1);
         pk[i] = *reinterpret_cast<uint32_t*>(&h2);
       }
@@ -215,10 +253,12 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(p_ready);
+    if (stamp) dbg[6] = clock64();
 
     // epilogue: O (128 x 64 fp32 in TMEM cols 0..63) -> round16 -> ctx
     mbar_wait(o_full, 0);
     tc_fence_after();
+    if (stamp) dbg[7] = clock64();
     if (grp < 2) {
       uint32_t v[32];
       tmem_ld32(lane_addr + grp * 32, v);
@@ -287,9 +327,9 @@ void launch_attn_tc(const AttnPlan& p, cudaStream_t st) {
   a.h = p.H * p.hd;
   a.ctx = reinterpret_cast<__half*>(p.ctx);
   a.ld_ctx = p.ld_ctx;
+  a.dbg = p.dbg;
   const int grid = p.B * p.H * a.nqt;
-  attn_tc_kernel<<<grid, kThreads, kSmemBytes, st>>>(p.tmQKV, a);
-  PRLAB_CUDA(cudaGetLastError());
+  launch_pdl(attn_tc_kernel, dim3(grid), dim3(kThreads), kSmemBytes, st, p.tmQKV, a);
 }
 
 }  // namespace prlab_gpu

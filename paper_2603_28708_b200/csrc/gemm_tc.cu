@@ -6,12 +6,20 @@
 //   out[m, n] = epi( sum_k A[m, k] * Wt[n, k] )      A: [M, K] fp16, Wt: [N, K] fp16
 //
 // Persistent, warp-specialised kernel, one CTA per SM:
-//   warp 0      TMA producer: 128x64 A tile + BNx64 W tile per stage (128B swizzle)
+//   warp 0      TMA producer: 128x64 A tile + BNx64 W tile per stage (128B swizzle).
+//               The first stages' weight tiles are fetched BEFORE griddepcontrol.wait:
+//               weights never depend on the upstream kernel, so with programmatic
+//               dependent launch their HBM latency hides under the previous kernel.
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (M=128, N=BN, K=16)
 //   warps 2..5  epilogue: tcgen05.ld (thread = output row), fused bias / GELU /
 //               residual, fp16 or fp32 stores
-// Two TMEM accumulator stages (2*BN columns) let the epilogue of tile i overlap
-// the main loop of tile i+1.
+// Two TMEM accumulator stages (2*BN columns) let the epilogue of unit i overlap
+// the main loop of unit i+1.
+//
+// Split-K (small M, e.g. batch-1 latency): a work unit is (tile, k-split).  Each
+// unit writes its fp32 partial tile to a workspace; the last unit of a tile to
+// arrive (atomic ticket) sums the partials in split order -- deterministic --
+// and applies the epilogue, so the rounding points are those of the full sum.
 #include "common.cuh"
 #include "internal.h"
 
@@ -20,39 +28,53 @@ namespace prlab_gpu {
 namespace {
 
 constexpr int BM = 128, BK = 64;
-constexpr int kThreads = 192;
 
 struct GemmArgs {
   int M, N, K;
   int num_m_blocks, num_n_blocks, num_tiles, num_k_blocks;
+  int splits, kb_per_split;
   const float* bias;
   void* out;
   int64_t ldo;
+  float* ws;      // split-K partials [tile*splits + split][BM][BN]
+  int* tickets;   // per-tile arrival counters (left at zero after every launch)
 };
 
-template <int BN>
+// LEAN: half-depth pipeline (~100 KB smem) so two CTAs -- this kernel's and the
+// next PDL-launched kernel's -- can be co-resident on an SM at batch-1 sizes.
+template <int BN, bool LEAN, int EPI = 0>
 struct Cfg {
-  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 6 : 8);
+  static constexpr int STAGES = (BN == 256 ? 4 : (BN == 128 ? 6 : 8)) / (LEAN ? 2 : 1);
+  // epilogue warps: 1, 2 or 4 per TMEM lane quadrant; the erf-heavy GELU epilogue gets
+  // the most so it keeps pace with the tensor core
+  static constexpr int EPI_WARPS = BN >= 256 && EPI == EPI_BIAS_GELU_F16 ? 16 : (BN >= 128 ? 8 : 4);
+  static constexpr int THREADS = 64 + 32 * EPI_WARPS;
+  static constexpr int COLS_PER_WARP = BN / (EPI_WARPS / 4);
   static constexpr uint32_t A_BYTES = BM * BK * 2;
   static constexpr uint32_t B_BYTES = BN * BK * 2;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-  static constexpr size_t SMEM = 1024 + STAGES * STAGE_BYTES + 256;
+  static constexpr uint32_t BIAS_OFF = STAGES * STAGE_BYTES + 256;  // per-warp bias slices
+  static constexpr size_t SMEM = 1024 + BIAS_OFF + EPI_WARPS * COLS_PER_WARP * 4;
 };
 
+// sbias: the 32 (pre-rounded) bias values of columns col0..col0+31 in shared memory, or null.
 template <int EPI>
-__device__ __forceinline__ void epilogue_chunk(const uint32_t (&r)[32], const GemmArgs& g, int row,
-                                               int col0) {
+__device__ __forceinline__ void epilogue_chunk(const float (&acc)[32], const GemmArgs& g, int row,
+                                               int col0, const float* sbias) {
   if (row >= g.M) return;
   const bool full = col0 + 32 <= g.N;
   float v[32];
+  float bias[32];
+  if (EPI != EPI_F16) {
+#pragma unroll
+    for (int i = 0; i < 32; ++i) bias[i] = sbias != nullptr ? sbias[i] : 0.0f;
+  }
 #pragma unroll
   for (int i = 0; i < 32; ++i) {
-    float a = r16(__uint_as_float(r[i]));  // round16(fp32 acc): matmul output lattice
+    float a = r16(acc[i]);  // round16(fp32 acc): matmul output lattice
     if (EPI != EPI_F16) {
-      const int c = col0 + i;
-      const float b = (g.bias != nullptr && c < g.N) ? __ldg(g.bias + c) : 0.0f;
-      a = r16(__fadd_rn(a, b));  // conform(row + conform(b)), bias stored pre-rounded
+      a = r16(__fadd_rn(a, bias[i]));  // conform(row + conform(b)), bias stored pre-rounded
       if (EPI == EPI_BIAS_GELU_F16) a = r16(gelu_erf(a));
     }
     v[i] = a;
@@ -92,11 +114,32 @@ __device__ __forceinline__ void epilogue_chunk(const uint32_t (&r)[32], const Ge
   }
 }
 
-template <int BN, int EPI>
-__global__ void __launch_bounds__(kThreads, 1)
+// Tile rasterization: bands of up to 16 m-blocks; inside a band the n-blocks
+// advance slowest, so the CTAs resident at any moment share one band of A
+// (<= 2048 rows) and a few weight tiles -- both stay in L2 (A is read from DRAM once).
+__device__ __forceinline__ void tile_coords(const GemmArgs& g, int tile, int& m_blk, int& n_blk) {
+  constexpr int GROUP_M = 16;
+  const int band = tile / (GROUP_M * g.num_n_blocks);
+  const int m0 = band * GROUP_M;
+  const int rows = min(GROUP_M, g.num_m_blocks - m0);
+  const int local = tile - band * GROUP_M * g.num_n_blocks;
+  n_blk = local / rows;
+  m_blk = m0 + local % rows;
+}
+
+__device__ __forceinline__ void unit_range(const GemmArgs& g, int unit, int& tile, int& split,
+                                           int& kb0, int& kb1) {
+  tile = unit / g.splits;
+  split = unit - tile * g.splits;
+  kb0 = split * g.kb_per_split;
+  kb1 = min(g.num_k_blocks, kb0 + g.kb_per_split);
+}
+
+template <int BN, bool LEAN, int EPI>
+__global__ void __launch_bounds__(Cfg<BN, LEAN, EPI>::THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                    const GemmArgs g) {
-  using C = Cfg<BN>;
+  using C = Cfg<BN, LEAN, EPI>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
@@ -107,8 +150,10 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  int* last_flag = reinterpret_cast<int*>(tmem_slot + 1);
 
   const uint32_t warp = warp_id(), lane = lane_id();
+  const int total_units = g.num_tiles * g.splits;
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
@@ -118,7 +163,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], 4);
+      mbar_init(&tempty[s], C::EPI_WARPS);
     }
     fence_barrier_init();
   }
@@ -129,34 +174,59 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  pdl_trigger();
   const uint32_t tmem_base = *tmem_slot;
 
   if (warp == 0) {
     // ---------------- TMA producer ----------------
-    uint32_t stage = 0, phase = 0;
-    for (int tile = blockIdx.x; tile < g.num_tiles; tile += gridDim.x) {
-      const int m_blk = tile % g.num_m_blocks, n_blk = tile / g.num_m_blocks;
-      for (int kb = 0; kb < g.num_k_blocks; ++kb) {
-        mbar_wait(&empty[stage], phase ^ 1);
-        if (lane == 0) {
-          mbar_expect_tx(&full[stage], C::STAGE_BYTES);
-          tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
-          tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, n_blk * BN);
+    if (lane == 0) {
+      int pre = 0;
+      if (static_cast<int>(blockIdx.x) < total_units) {
+        int tile, split, kb0, kb1;
+        unit_range(g, blockIdx.x, tile, split, kb0, kb1);
+        int m_blk0, n_blk;
+        tile_coords(g, tile, m_blk0, n_blk);
+        pre = min(C::STAGES, kb1 - kb0);
+        for (int i = 0; i < pre; ++i) {  // weights: independent of the upstream kernel
+          mbar_expect_tx(&full[i], C::STAGE_BYTES);
+          tma_load_2d(sB + i * C::B_BYTES, &tmB, &full[i], (kb0 + i) * BK, n_blk * BN);
         }
-        __syncwarp();
-        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
+      pdl_wait();  // activations below are produced by the upstream kernel
+      uint32_t stage = 0, phase = 0;
+      bool first = true;
+      for (int unit = blockIdx.x; unit < total_units; unit += gridDim.x) {
+        int tile, split, kb0, kb1;
+        unit_range(g, unit, tile, split, kb0, kb1);
+        int m_blk, n_blk;
+      tile_coords(g, tile, m_blk, n_blk);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          if (first && kb - kb0 < pre) {
+            tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
+          } else {
+            mbar_wait(&empty[stage], phase ^ 1);
+            mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+            tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
+            tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, n_blk * BN);
+          }
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        first = false;
       }
     }
+    __syncwarp();
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
     constexpr uint32_t idesc = idesc_f16_f32(BM, BN, 0, 0);
     uint32_t stage = 0, phase = 0, t = 0;
-    for (int tile = blockIdx.x; tile < g.num_tiles; tile += gridDim.x, ++t) {
+    for (int unit = blockIdx.x; unit < total_units; unit += gridDim.x, ++t) {
+      int tile, split, kb0, kb1;
+      unit_range(g, unit, tile, split, kb0, kb1);
       const uint32_t acc = t & 1, acc_phase = (t >> 1) & 1;
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d_tmem = tmem_base + acc * BN;
-      for (int kb = 0; kb < g.num_k_blocks; ++kb) {
+      for (int kb = kb0; kb < kb1; ++kb) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
         if (lane == 0) {
@@ -165,7 +235,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k)
             umma_f16_ss(d_tmem, sw128_desc(a0 + k * 32, 0, 1024), sw128_desc(b0 + k * 32, 0, 1024),
-                        idesc, (kb | k) != 0);
+                        idesc, (kb > kb0 || k > 0) ? 1u : 0u);
           umma_commit(&empty[stage]);
         }
         __syncwarp();
@@ -176,24 +246,107 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ---------------- epilogue ----------------
-    const uint32_t quad = warp & 3;  // TMEM lane quadrant this warp may access
+    const uint32_t quad = warp & 3;                     // TMEM lane quadrant this warp may access
+    const int cbase = ((warp - 2) >> 2) * C::COLS_PER_WARP;  // this warp's column slice
+    const int r = quad * 32 + lane;                     // row within the tile
+    const int tid = (warp - 2) * 32 + lane;
+    float* sbias = reinterpret_cast<float*>(smem + C::BIAS_OFF) + (warp - 2) * C::COLS_PER_WARP;
     uint32_t t = 0;
-    for (int tile = blockIdx.x; tile < g.num_tiles; tile += gridDim.x, ++t) {
-      const int m_blk = tile % g.num_m_blocks, n_blk = tile / g.num_m_blocks;
+    for (int unit = blockIdx.x; unit < total_units; unit += gridDim.x, ++t) {
+      int tile, split, kb0, kb1;
+      unit_range(g, unit, tile, split, kb0, kb1);
+      int m_blk, n_blk;
+      tile_coords(g, tile, m_blk, n_blk);
       const uint32_t acc = t & 1, acc_phase = (t >> 1) & 1;
+      // stage this warp's bias slice while the accumulator is still being produced
+      const bool has_bias = EPI != EPI_F16 && g.bias != nullptr;
+      if (has_bias) {
+        __syncwarp();
+        for (int c = lane; c < C::COLS_PER_WARP; c += 32) {
+          const int col = n_blk * BN + cbase + c;
+          sbias[c] = col < g.N ? __ldg(g.bias + col) : 0.0f;
+        }
+        __syncwarp();
+      }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
-      const int row = m_blk * BM + quad * 32 + lane;
+      const int row = m_blk * BM + r;
+      if (g.splits == 1) {
 #pragma unroll 1
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tmem_base + ((quad * 32) << 16) + acc * BN + c * 32, r);
-        tmem_wait_ld();
-        epilogue_chunk<EPI>(r, g, row, n_blk * BN + c * 32);
+        for (int c = cbase; c < cbase + C::COLS_PER_WARP; c += 32) {
+          uint32_t u[32];
+          tmem_ld32(tmem_base + ((quad * 32) << 16) + acc * BN + c, u);
+          tmem_wait_ld();
+          float v[32];
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(u[i]);
+          epilogue_chunk<EPI>(v, g, row, n_blk * BN + c, has_bias ? sbias + (c - cbase) : nullptr);
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+      } else {
+        // partial tile -> workspace (row-contiguous, 16B stores), then release TMEM
+        float* wrow = g.ws + (static_cast<int64_t>(unit) * BM + r) * BN;
+#pragma unroll 1
+        for (int c = cbase; c < cbase + C::COLS_PER_WARP; c += 32) {
+          uint32_t u[32];
+          tmem_ld32(tmem_base + ((quad * 32) << 16) + acc * BN + c, u);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; i += 4)
+            __stcg(reinterpret_cast<float4*>(wrow + c + i),
+                   make_float4(__uint_as_float(u[i]), __uint_as_float(u[i + 1]),
+                               __uint_as_float(u[i + 2]), __uint_as_float(u[i + 3])));
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+        __threadfence();
+        named_bar_sync(1, 32 * C::EPI_WARPS);
+        if (tid == 0) {
+          const int prev = atomicAdd(&g.tickets[tile], 1);
+          const int last = prev == g.splits - 1;
+          if (last) g.tickets[tile] = 0;  // ready for the next launch
+          *last_flag = last;
+        }
+        named_bar_sync(1, 32 * C::EPI_WARPS);
+        const int last = *last_flag;
+        named_bar_sync(1, 32 * C::EPI_WARPS);  // flag consumed before the next unit overwrites it
+        if (last) {
+          __threadfence();
+          const float* base = g.ws + (static_cast<int64_t>(tile) * g.splits * BM + r) * BN;
+#pragma unroll 1
+          for (int c = cbase; c < cbase + C::COLS_PER_WARP; c += 32) {
+            float v[32];
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] = 0.0f;
+#pragma unroll 1
+            for (int s0 = 0; s0 < g.splits; s0 += 2) {  // fixed split order: deterministic sum
+              float4 p[2][8];
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                const int s = s0 + j < g.splits ? s0 + j : s0;
+                const float4* src = reinterpret_cast<const float4*>(base + static_cast<int64_t>(s) * BM * BN + c);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) p[j][i] = __ldcg(src + i);
+              }
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                if (s0 + j >= g.splits) break;
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                  v[4 * i] = __fadd_rn(v[4 * i], p[j][i].x);
+                  v[4 * i + 1] = __fadd_rn(v[4 * i + 1], p[j][i].y);
+                  v[4 * i + 2] = __fadd_rn(v[4 * i + 2], p[j][i].z);
+                  v[4 * i + 3] = __fadd_rn(v[4 * i + 3], p[j][i].w);
+                }
+              }
+            }
+            epilogue_chunk<EPI>(v, g, row, n_blk * BN + c, has_bias ? sbias + (c - cbase) : nullptr);
+          }
+        }
       }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
     }
   }
   __syncthreads();
@@ -203,51 +356,340 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Cluster split-K (small M).  grid = tiles * splits, cluster = (splits, 1, 1):
+// the CTAs of one cluster own the k-slices of one output tile.  Each writes its
+// fp32 partial tile to its own shared memory; after a cluster barrier every CTA
+// reduces 1/splits of the tile's rows across all peers through DSMEM (fixed
+// split order -> deterministic) and applies the epilogue.  No global partials,
+// no atomics, the reduction is spread over all CTAs of the cluster.
+// ---------------------------------------------------------------------------
+template <int BN>
+struct CCfg {
+  static constexpr int STAGES = 4;
+  static constexpr uint32_t A_BYTES = BM * BK * 2;
+  static constexpr uint32_t B_BYTES = BN * BK * 2;
+  static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int PSTRIDE = BN + 4;  // partial row stride (floats), skews banks
+  static constexpr uint32_t PART_BYTES = BM * PSTRIDE * 4;
+  static constexpr uint32_t DATA = STAGES * STAGE_BYTES > PART_BYTES ? STAGES * STAGE_BYTES : PART_BYTES;
+  static constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+  static constexpr size_t SMEM = 1024 + DATA + 256;
+  static constexpr int THREADS = 192;
+};
+
+template <int EPI>
+__device__ __forceinline__ void epilogue_vec4(float4 a, const GemmArgs& g, int row, int col) {
+  if (row >= g.M || col >= g.N) return;
+  float v[4] = {a.x, a.y, a.z, a.w};
+  const bool full = col + 4 <= g.N;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float x = r16(v[i]);
+    if (EPI != EPI_F16) {
+      const float b = (g.bias != nullptr && col + i < g.N) ? __ldg(g.bias + col + i) : 0.0f;
+      x = r16(__fadd_rn(x, b));
+      if (EPI == EPI_BIAS_GELU_F16) x = r16(gelu_erf(x));
+    }
+    v[i] = x;
+  }
+  if (EPI == EPI_BIAS_RESID_F32) {
+    float* o = reinterpret_cast<float*>(g.out) + static_cast<int64_t>(row) * g.ldo + col;
+    if (full && (g.ldo % 4) == 0) {
+      float4 x = *reinterpret_cast<float4*>(o);
+      x.x = __fadd_rn(x.x, v[0]);
+      x.y = __fadd_rn(x.y, v[1]);
+      x.z = __fadd_rn(x.z, v[2]);
+      x.w = __fadd_rn(x.w, v[3]);
+      *reinterpret_cast<float4*>(o) = x;
+    } else {
+      for (int i = 0; i < 4 && col + i < g.N; ++i) o[i] = __fadd_rn(o[i], v[i]);
+    }
+  } else {
+    __half* o = reinterpret_cast<__half*>(g.out) + static_cast<int64_t>(row) * g.ldo + col;
+    if (full && (g.ldo % 4) == 0) {
+      __half2 h01 = __floats2half2_rn(v[0], v[1]), h23 = __floats2half2_rn(v[2], v[3]);
+      *reinterpret_cast<uint2*>(o) = make_uint2(*reinterpret_cast<uint32_t*>(&h01), *reinterpret_cast<uint32_t*>(&h23));
+    } else {
+      for (int i = 0; i < 4 && col + i < g.N; ++i) o[i] = __float2half_rn(v[i]);
+    }
+  }
+}
+
 template <int BN, int EPI>
+__global__ void __launch_bounds__(CCfg<BN>::THREADS, 1)
+    gemm_splitk_cluster_kernel(const __grid_constant__ CUtensorMap tmA,
+                               const __grid_constant__ CUtensorMap tmB, const GemmArgs g) {
+  using C = CCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  float* part = reinterpret_cast<float*>(smem);  // reuses the stage buffers after the MMAs
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::DATA);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int split = static_cast<int>(cluster_ctarank());
+  const int tile = blockIdx.x / g.splits;
+  const int kb0 = split * g.kb_per_split;
+  const int kb1 = min(g.num_k_blocks, kb0 + g.kb_per_split);
+  int m_blk, n_blk;
+      tile_coords(g, tile, m_blk, n_blk);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tfull, 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, C::TMEM_COLS);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_trigger();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const int pre = min(C::STAGES, kb1 - kb0);
+      for (int i = 0; i < pre; ++i) {  // weights first: independent of the upstream kernel
+        mbar_expect_tx(&full[i], C::STAGE_BYTES);
+        tma_load_2d(sB + i * C::B_BYTES, &tmB, &full[i], (kb0 + i) * BK, n_blk * BN);
+      }
+      pdl_wait();
+      uint32_t stage = 0, phase = 0;
+      for (int kb = kb0; kb < kb1; ++kb) {
+        if (kb - kb0 < pre) {
+          tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
+        } else {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], C::STAGE_BYTES);
+          tma_load_2d(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
+          tma_load_2d(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, n_blk * BN);
+        }
+        if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    constexpr uint32_t idesc = idesc_f16_f32(BM, BN, 0, 0);
+    uint32_t stage = 0, phase = 0;
+    for (int kb = kb0; kb < kb1; ++kb) {
+      mbar_wait(&full[stage], phase);
+      tc_fence_after();
+      if (lane == 0) {
+        const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
+        const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+        for (int k = 0; k < BK / 16; ++k)
+          umma_f16_ss(tmem_base, sw128_desc(a0 + k * 32, 0, 1024), sw128_desc(b0 + k * 32, 0, 1024), idesc,
+                      (kb > kb0 || k > 0) ? 1u : 0u);
+        umma_commit(&empty[stage]);
+      }
+      __syncwarp();
+      if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+    }
+    if (lane == 0) umma_commit(tfull);
+    __syncwarp();
+  } else {
+    // accumulator -> own shared memory (row r, padded stride)
+    const uint32_t quad = warp & 3;
+    const int r = quad * 32 + lane;
+    mbar_wait(tfull, 0);
+    tc_fence_after();
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      uint32_t u[32];
+      tmem_ld32(tmem_base + ((quad * 32) << 16) + c, u);
+      tmem_wait_ld();
+      float* dst = part + r * C::PSTRIDE + c;
+#pragma unroll
+      for (int i = 0; i < 32; i += 4)
+        *reinterpret_cast<float4*>(dst + i) = make_float4(__uint_as_float(u[i]), __uint_as_float(u[i + 1]),
+                                                          __uint_as_float(u[i + 2]), __uint_as_float(u[i + 3]));
+    }
+    tc_fence_before();
+  }
+  cluster_sync_all();  // every CTA's partial is complete and visible cluster-wide
+  if (warp >= 2) {
+    const int tid = (warp - 2) * 32 + lane;
+    const int rows_per = (BM + g.splits - 1) / g.splits;
+    const int r0 = split * rows_per, r1 = min(BM, r0 + rows_per);
+    const uint32_t base = smem_u32(part);
+    constexpr int C4 = BN / 4;
+    // each thread's column quad is fixed (128 % C4 == 0): stage its bias once
+    const int c4 = tid % C4;
+    const int col = n_blk * BN + c4 * 4;
+    for (int e = tid; e < (r1 - r0) * C4; e += 128) {
+      const int rr = r0 + e / C4;
+      const uint32_t off = static_cast<uint32_t>((rr * C::PSTRIDE + c4 * 4) * 4);
+      float4 p[8];
+#pragma unroll
+      for (int s = 0; s < 8; ++s)  // all peer loads in flight before the (ordered) sum
+        if (s < g.splits) p[s] = ld_dsmem_f4(mapa_shared(base + off, static_cast<uint32_t>(s)));
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+      for (int s = 0; s < 8; ++s) {  // fixed order: deterministic
+        if (s < g.splits) {
+          acc.x = __fadd_rn(acc.x, p[s].x);
+          acc.y = __fadd_rn(acc.y, p[s].y);
+          acc.z = __fadd_rn(acc.z, p[s].z);
+          acc.w = __fadd_rn(acc.w, p[s].w);
+        }
+      }
+      epilogue_vec4<EPI>(acc, g, m_blk * BM + rr, col);
+    }
+  }
+  cluster_sync_all();  // peers are done reading this CTA's shared memory
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C::TMEM_COLS);
+  }
+}
+
+template <int BN, int EPI>
+void configure_cluster_one() {
+  auto k = gemm_splitk_cluster_kernel<BN, EPI>;
+  PRLAB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(CCfg<BN>::SMEM)));
+  PRLAB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+}
+
+template <int BN>
+void configure_cluster_bn() {
+  configure_cluster_one<BN, EPI_BIAS_F16>();
+  configure_cluster_one<BN, EPI_BIAS_GELU_F16>();
+  configure_cluster_one<BN, EPI_BIAS_RESID_F32>();
+  configure_cluster_one<BN, EPI_F16>();
+}
+
+template <int BN, int EPI>
+void launch_cluster_one(const GemmPlan& p, const GemmArgs& g, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.grid);
+  cfg.blockDim = dim3(CCfg<BN>::THREADS);
+  cfg.dynamicSmemBytes = CCfg<BN>::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = p.splits;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  PRLAB_CUDA(cudaLaunchKernelEx(&cfg, gemm_splitk_cluster_kernel<BN, EPI>, p.tmA, p.tmB, g));
+}
+
+template <int BN>
+void launch_cluster_bn(const GemmPlan& p, const GemmArgs& g, cudaStream_t st) {
+  switch (p.epi) {
+    case EPI_BIAS_F16: launch_cluster_one<BN, EPI_BIAS_F16>(p, g, st); break;
+    case EPI_BIAS_GELU_F16: launch_cluster_one<BN, EPI_BIAS_GELU_F16>(p, g, st); break;
+    case EPI_BIAS_RESID_F32: launch_cluster_one<BN, EPI_BIAS_RESID_F32>(p, g, st); break;
+    case EPI_F16: launch_cluster_one<BN, EPI_F16>(p, g, st); break;
+    default: throw std::invalid_argument("unknown gemm epilogue");
+  }
+}
+
+template <int BN, bool LEAN, int EPI>
 void configure_one() {
-  PRLAB_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(Cfg<BN>::SMEM)));
+  PRLAB_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, LEAN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(Cfg<BN, LEAN, EPI>::SMEM)));
 }
 
-template <int BN, int EPI>
-void launch_one(const GemmPlan& p, const GemmArgs& g, cudaStream_t st) {
-  gemm_tc_kernel<BN, EPI><<<p.grid, kThreads, Cfg<BN>::SMEM, st>>>(p.tmA, p.tmB, g);
-  PRLAB_CUDA(cudaGetLastError());
-}
-
-template <int BN>
+template <int BN, bool LEAN>
 void configure_bn() {
-  configure_one<BN, EPI_BIAS_F16>();
-  configure_one<BN, EPI_BIAS_GELU_F16>();
-  configure_one<BN, EPI_BIAS_RESID_F32>();
-  configure_one<BN, EPI_F16>();
+  configure_one<BN, LEAN, EPI_BIAS_F16>();
+  configure_one<BN, LEAN, EPI_BIAS_GELU_F16>();
+  configure_one<BN, LEAN, EPI_BIAS_RESID_F32>();
+  configure_one<BN, LEAN, EPI_F16>();
 }
 
-template <int BN>
+template <int BN, bool LEAN, int EPI>
+void launch_one(const GemmPlan& p, const GemmArgs& g, cudaStream_t st) {
+  using C = Cfg<BN, LEAN, EPI>;
+  launch_pdl(gemm_tc_kernel<BN, LEAN, EPI>, dim3(p.grid), dim3(C::THREADS), C::SMEM, st, p.tmA, p.tmB, g);
+}
+
+template <int BN, bool LEAN>
 void launch_bn(const GemmPlan& p, const GemmArgs& g, cudaStream_t st) {
   switch (p.epi) {
-    case EPI_BIAS_F16: launch_one<BN, EPI_BIAS_F16>(p, g, st); break;
-    case EPI_BIAS_GELU_F16: launch_one<BN, EPI_BIAS_GELU_F16>(p, g, st); break;
-    case EPI_BIAS_RESID_F32: launch_one<BN, EPI_BIAS_RESID_F32>(p, g, st); break;
-    case EPI_F16: launch_one<BN, EPI_F16>(p, g, st); break;
+    case EPI_BIAS_F16: launch_one<BN, LEAN, EPI_BIAS_F16>(p, g, st); break;
+    case EPI_BIAS_GELU_F16: launch_one<BN, LEAN, EPI_BIAS_GELU_F16>(p, g, st); break;
+    case EPI_BIAS_RESID_F32: launch_one<BN, LEAN, EPI_BIAS_RESID_F32>(p, g, st); break;
+    case EPI_F16: launch_one<BN, LEAN, EPI_F16>(p, g, st); break;
     default: throw std::invalid_argument("unknown gemm epilogue");
   }
 }
 
 }  // namespace
 
+SplitScratch& global_split_scratch() {
+  static SplitScratch s;
+  if (!s.ws) {
+    s.ws_floats = static_cast<size_t>(2 * num_sms()) * BM * 128;
+    PRLAB_CUDA(cudaMalloc(&s.ws, s.ws_floats * sizeof(float)));
+    s.n_tickets = 4096;
+    PRLAB_CUDA(cudaMalloc(&s.tickets, s.n_tickets * sizeof(int)));
+    PRLAB_CUDA(cudaMemset(s.tickets, 0, s.n_tickets * sizeof(int)));
+  }
+  return s;
+}
+
 GemmPlan plan_gemm_tc(const void* A, int64_t lda, const void* Wt, int64_t ldw, const float* bias,
-                      void* out, int64_t ldo, int M, int N, int K, int epi) {
+                      void* out, int64_t ldo, int M, int N, int K, int epi, const SplitScratch* scratch,
+                      int force_bn, int force_splits, int force_lean) {
   if (M < 1 || N < 1 || K < 1) throw std::invalid_argument("tc gemm: empty extent");
   if (K % 8 != 0 || lda % 8 != 0 || ldw % 8 != 0)
     throw std::invalid_argument("tc gemm: K and row pitches must be multiples of 8");
   GemmPlan p{};
   const int sms = num_sms();
   const int mb = (M + BM - 1) / BM;
-  // Pick the widest N tile that still gives every SM work; narrow tiles stream
-  // the weights through more SMs when M is small (weight-bandwidth bound).
+  const int nkb = (K + BK - 1) / BK;
+  // Widest N tile that still gives every SM work; narrower tiles stream the
+  // weights through more SMs when M is small (weight-bandwidth bound).
   int bn = 256;
   while (bn > 64 && static_cast<int64_t>(mb) * ((N + bn - 1) / bn) < sms) bn /= 2;
+  if (force_bn) bn = force_bn;
+  const int tiles = mb * ((N + bn - 1) / bn);
+  // Split K while the grid is far below one wave (batch-1 latency shapes): the
+  // cluster split-K kernel reduces partials through DSMEM (cluster <= 8 CTAs).
+  int splits = 1;
+  bool cluster = false;
+  if (bn <= 128 && tiles * 2 <= sms && nkb > 1) {
+    splits = std::min(std::min(nkb, 8), std::max(1, sms / tiles));
+    cluster = splits > 1;
+  }
+  if (force_splits) {
+    splits = std::min(std::abs(force_splits), nkb);
+    cluster = force_splits > 0 && splits > 1;  // negative: the global-workspace split-K path
+  }
+  if (splits > 1) {
+    const int kps = (nkb + splits - 1) / splits;
+    splits = (nkb + kps - 1) / kps;
+    if (splits == 1) cluster = false;
+  }
+  if (!cluster && splits > 1 &&
+      (!scratch || static_cast<size_t>(tiles) * splits * BM * bn > scratch->ws_floats || tiles > scratch->n_tickets))
+    splits = 1;
+  // lean pipelines when the whole grid fits in one wave: every CTA then runs a
+  // single short unit and the next kernel's CTAs can share its SM (PDL overlap)
+  p.lean = (tiles * splits <= sms);
+  if (force_lean) p.lean = force_lean > 0;
+  p.cluster = cluster;
   p.M = M;
   p.N = N;
   p.K = K;
@@ -256,19 +698,34 @@ GemmPlan plan_gemm_tc(const void* A, int64_t lda, const void* Wt, int64_t ldw, c
   p.bias = bias;
   p.out = out;
   p.ldo = ldo;
+  p.splits = splits;
+  p.kb_per_split = (nkb + splits - 1) / splits;
+  p.splits = (nkb + p.kb_per_split - 1) / p.kb_per_split;
+  if (p.splits > 1 && !p.cluster) {
+    if (!scratch || static_cast<size_t>(tiles) * p.splits * BM * bn > scratch->ws_floats ||
+        tiles > scratch->n_tickets)
+      throw std::invalid_argument("tc gemm: split-K workspace too small");
+    p.ws = scratch->ws;
+    p.tickets = scratch->tickets;
+  }
   p.tmA = make_tmap_f16_2d(A, M, K, lda, BM, BK);
   p.tmB = make_tmap_f16_2d(Wt, N, K, ldw, bn, BK);
-  const int tiles = mb * ((N + bn - 1) / bn);
-  p.grid = tiles < sms ? tiles : sms;
+  const int units = tiles * p.splits;
+  p.grid = p.cluster ? units : (units < sms ? units : sms);
   return p;
 }
 
 void configure_gemm_tc() {
   static bool done = false;  // per process; the library drives one device per process
   if (done) return;
-  configure_bn<256>();
-  configure_bn<128>();
-  configure_bn<64>();
+  configure_bn<256, false>();
+  configure_bn<128, false>();
+  configure_bn<64, false>();
+  configure_bn<256, true>();
+  configure_bn<128, true>();
+  configure_bn<64, true>();
+  configure_cluster_bn<64>();
+  configure_cluster_bn<128>();
   done = true;
 }
 
@@ -282,13 +739,29 @@ void launch_gemm_tc(const GemmPlan& p, cudaStream_t st) {
   g.num_n_blocks = (p.N + p.bn - 1) / p.bn;
   g.num_tiles = g.num_m_blocks * g.num_n_blocks;
   g.num_k_blocks = (p.K + BK - 1) / BK;
+  g.splits = p.splits;
+  g.kb_per_split = p.kb_per_split;
   g.bias = p.bias;
   g.out = p.out;
   g.ldo = p.ldo;
-  switch (p.bn) {
-    case 256: launch_bn<256>(p, g, st); break;
-    case 128: launch_bn<128>(p, g, st); break;
-    case 64: launch_bn<64>(p, g, st); break;
+  g.ws = p.ws;
+  g.tickets = p.tickets;
+  if (p.cluster) {
+    if (p.bn == 64)
+      launch_cluster_bn<64>(p, g, st);
+    else if (p.bn == 128)
+      launch_cluster_bn<128>(p, g, st);
+    else
+      throw std::invalid_argument("cluster split-K supports tile widths 64 and 128");
+    return;
+  }
+  switch (p.bn * 2 + (p.lean ? 1 : 0)) {
+    case 512: launch_bn<256, false>(p, g, st); break;
+    case 256: launch_bn<128, false>(p, g, st); break;
+    case 128: launch_bn<64, false>(p, g, st); break;
+    case 513: launch_bn<256, true>(p, g, st); break;
+    case 257: launch_bn<128, true>(p, g, st); break;
+    case 129: launch_bn<64, true>(p, g, st); break;
     default: throw std::invalid_argument("bad tile width");
   }
 }

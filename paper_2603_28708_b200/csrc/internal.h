@@ -7,6 +7,7 @@
 
 #include <stdexcept>
 #include <string>
+#include <utility>
 
 namespace prlab_gpu {
 
@@ -24,6 +25,25 @@ struct cuda_error : std::runtime_error {
   } while (0)
 
 int num_sms();
+bool pdl_enabled();
+
+// Launch with programmatic stream serialization (PDL) so the kernel's prologue
+// overlaps the tail of the previous kernel in the stream / graph.
+template <typename... KArgs, typename... Args>
+void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  PRLAB_CUDA(cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...));
+}
 
 // --- TMA descriptors (driver entry point fetched through the runtime) ---
 // 2-D fp16 tensor [rows, cols] with row pitch `pitch_elems`, box {box_cols, box_rows},
@@ -45,14 +65,29 @@ enum GemmEpi : int {
 struct GemmPlan {
   CUtensorMap tmA, tmB;
   int M, N, K, bn, epi;
+  int splits, kb_per_split;
+  bool lean;
+  bool cluster;  // split-K reduced through DSMEM inside a thread-block cluster
   const float* bias;
   void* out;
   int64_t ldo;
+  float* ws;
+  int* tickets;
   int grid;
-  int kernel_count() const { return 1; }
 };
+// Split-K scratch: fp32 partial tiles + per-tile tickets (zero between launches).
+// One per model: kernels of one forward run in stream order, so they share it.
+struct SplitScratch {
+  float* ws = nullptr;
+  size_t ws_floats = 0;
+  int* tickets = nullptr;
+  int n_tickets = 0;
+};
+SplitScratch& global_split_scratch();
 GemmPlan plan_gemm_tc(const void* A, int64_t lda, const void* Wt, int64_t ldw, const float* bias,
-                      void* out, int64_t ldo, int M, int N, int K, int epi);
+                      void* out, int64_t ldo, int M, int N, int K, int epi,
+                      const SplitScratch* scratch, int force_bn = 0, int force_splits = 0,
+                      int force_lean = 0);
 void launch_gemm_tc(const GemmPlan& p, cudaStream_t st);
 void configure_gemm_tc();
 
@@ -62,6 +97,7 @@ struct AttnPlan {
   void* ctx;
   int B, S, H, hd, causal;
   int64_t ld_qkv, ld_ctx;
+  long long* dbg = nullptr;  // phase timestamps (debug)
 };
 bool attn_tc_supported(int S, int hd);
 AttnPlan plan_attn_tc(const void* qkv, int64_t ld_qkv, void* ctx, int64_t ld_ctx, int B, int S,

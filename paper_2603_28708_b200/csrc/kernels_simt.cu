@@ -145,6 +145,8 @@ __global__ void embed_f32_kernel(const float4* __restrict__ tok, int64_t vocab,
                                  const float4* __restrict__ pos, int h4,
                                  const int32_t* __restrict__ ids, int S, int64_t rows,
                                  float4* __restrict__ out, int* err) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t total = rows * h4;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -234,6 +236,8 @@ __global__ void __launch_bounds__(256) ln_f16_kernel(const float* __restrict__ x
   constexpr int n = 128 * VPT;
   const int row = blockIdx.x * 8 + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
+  pdl_trigger();
+  pdl_wait();  // x is produced by the upstream residual GEMM
   if (row >= rows) return;
   const float4* in = reinterpret_cast<const float4*>(x + static_cast<int64_t>(row) * n);
   float4 v[VPT];
@@ -405,6 +409,8 @@ __global__ void f32_to_f16_kernel(const float* x, __half* out, int64_t n) {
 }
 __global__ void convert_f16_f32_kernel(const __half* __restrict__ in, int64_t ld_in,
                                        float* __restrict__ out, int64_t ld_out, int M, int N) {
+  pdl_trigger();
+  pdl_wait();
   const int64_t total = static_cast<int64_t>(M) * N;
   for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
@@ -467,10 +473,8 @@ void embed_f32(const float* tok, int64_t vocab, const float* pos, int h, const i
   const int h4 = h / 4;
   const int64_t n = rows * h4;
   const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, num_sms() * 8));
-  embed_f32_kernel<<<blocks, 256, 0, st>>>(reinterpret_cast<const float4*>(tok), vocab,
-                                           reinterpret_cast<const float4*>(pos), h4, ids, S, rows,
-                                           reinterpret_cast<float4*>(out), err);
-  PRLAB_CUDA(cudaGetLastError());
+  launch_pdl(embed_f32_kernel, dim3(blocks), dim3(256), 0, st, reinterpret_cast<const float4*>(tok), vocab,
+             reinterpret_cast<const float4*>(pos), h4, ids, S, rows, reinterpret_cast<float4*>(out), err);
 }
 
 void simt_layernorm(const float* x, int rows, int n, const float* gamma, const float* beta,
@@ -485,17 +489,16 @@ void ln_f32_to_f16(const float* x, int rows, int n, const float* gamma, const fl
                    float eps, __half* out, cudaStream_t st) {
   const int grid = (rows + 7) / 8;
   switch (n) {
-    case 128: ln_f16_kernel<1><<<grid, 256, 0, st>>>(x, rows, gamma, beta, eps, out); break;
-    case 256: ln_f16_kernel<2><<<grid, 256, 0, st>>>(x, rows, gamma, beta, eps, out); break;
-    case 384: ln_f16_kernel<3><<<grid, 256, 0, st>>>(x, rows, gamma, beta, eps, out); break;
-    case 512: ln_f16_kernel<4><<<grid, 256, 0, st>>>(x, rows, gamma, beta, eps, out); break;
-    case 768: ln_f16_kernel<6><<<grid, 256, 0, st>>>(x, rows, gamma, beta, eps, out); break;
-    case 1024: ln_f16_kernel<8><<<grid, 256, 0, st>>>(x, rows, gamma, beta, eps, out); break;
+    case 128: launch_pdl(ln_f16_kernel<1>, dim3(grid), dim3(256), 0, st, x, rows, gamma, beta, eps, out); break;
+    case 256: launch_pdl(ln_f16_kernel<2>, dim3(grid), dim3(256), 0, st, x, rows, gamma, beta, eps, out); break;
+    case 384: launch_pdl(ln_f16_kernel<3>, dim3(grid), dim3(256), 0, st, x, rows, gamma, beta, eps, out); break;
+    case 512: launch_pdl(ln_f16_kernel<4>, dim3(grid), dim3(256), 0, st, x, rows, gamma, beta, eps, out); break;
+    case 768: launch_pdl(ln_f16_kernel<6>, dim3(grid), dim3(256), 0, st, x, rows, gamma, beta, eps, out); break;
+    case 1024: launch_pdl(ln_f16_kernel<8>, dim3(grid), dim3(256), 0, st, x, rows, gamma, beta, eps, out); break;
     default:
       simt_layernorm(x, rows, n, gamma, beta, eps, Kcfg{0, 0, 1}, nullptr, out, 0, st);
       return;
   }
-  PRLAB_CUDA(cudaGetLastError());
 }
 
 void simt_attention(const float* q, const float* k, const float* v, int64_t ld_in, float* ctx,
@@ -548,8 +551,7 @@ void convert_f16_to_f32(const __half* in, int64_t ld_in, float* out, int64_t ld_
                         cudaStream_t st) {
   const int64_t n = static_cast<int64_t>(M) * N;
   const int blocks = static_cast<int>(std::min<int64_t>((n + 255) / 256, num_sms() * 16));
-  convert_f16_f32_kernel<<<blocks, 256, 0, st>>>(in, ld_in, out, ld_out, M, N);
-  PRLAB_CUDA(cudaGetLastError());
+  launch_pdl(convert_f16_f32_kernel, dim3(blocks), dim3(256), 0, st, in, ld_in, out, ld_out, M, N);
 }
 void transpose_f32(const float* in, int rows, int cols, float* out, int rnd, cudaStream_t st) {
   dim3 grid((cols + 31) / 32, (rows + 31) / 32), block(32, 8);

@@ -68,6 +68,11 @@ int num_sms() {
   return n;
 }
 
+bool pdl_enabled() {
+  static const bool on = std::getenv("PRLAB_NO_PDL") == nullptr;
+  return on;
+}
+
 // ---------------------------------------------------------------------------
 // TMA descriptors through the driver entry point (no -lcuda link dependency)
 // ---------------------------------------------------------------------------
@@ -256,6 +261,8 @@ struct prlab_gpu_model {
   bool have32 = false;
 
   DeviceBuffer err;  // device error word (bad token ids)
+  DeviceBuffer split_ws, split_tickets;
+  SplitScratch scratch;
   cudaStream_t stream = nullptr;  // private stream of the host (drop-in) forward
 
   // activation workspace + per-key plans
@@ -376,6 +383,13 @@ void upload_fast(prlab_gpu_model& m) {
   }
   m.err.alloc(256);
   PRLAB_CUDA(cudaMemset(m.err.p, 0, 256));
+  m.scratch.ws_floats = static_cast<size_t>(2 * num_sms()) * 128 * 128;
+  m.split_ws.alloc(m.scratch.ws_floats * sizeof(float));
+  m.scratch.ws = static_cast<float*>(m.split_ws.p);
+  m.scratch.n_tickets = 4096;
+  m.split_tickets.alloc(m.scratch.n_tickets * sizeof(int));
+  PRLAB_CUDA(cudaMemset(m.split_tickets.p, 0, m.scratch.n_tickets * sizeof(int)));
+  m.scratch.tickets = static_cast<int*>(m.split_tickets.p);
   PRLAB_CUDA(cudaDeviceSynchronize());
 }
 
@@ -476,13 +490,13 @@ prlab_gpu_model::Plan& get_plan(prlab_gpu_model& m, int64_t B, int64_t S, const 
     p.logit16 = m.ws.at<__half>(at(s_c));
     for (int64_t l = 0; l < m.L; ++l) {
       const auto& w = m.l16[l];
-      p.gemms.push_back(plan_gemm_tc(p.xn16, h, w.wqkv, h, w.bqkv, p.big16, 3 * h, Mi, 3 * hi, hi, EPI_BIAS_F16));
-      p.gemms.push_back(plan_gemm_tc(p.xn16, h, w.wo, h, w.bo, p.x, h, Mi, hi, hi, EPI_BIAS_RESID_F32));
-      p.gemms.push_back(plan_gemm_tc(p.xn16, h, w.w1, h, w.b1, p.big16, f, Mi, fi, hi, EPI_BIAS_GELU_F16));
-      p.gemms.push_back(plan_gemm_tc(p.big16, f, w.w2, f, w.b2, p.x, h, Mi, hi, fi, EPI_BIAS_RESID_F32));
+      p.gemms.push_back(plan_gemm_tc(p.xn16, h, w.wqkv, h, w.bqkv, p.big16, 3 * h, Mi, 3 * hi, hi, EPI_BIAS_F16, &m.scratch));
+      p.gemms.push_back(plan_gemm_tc(p.xn16, h, w.wo, h, w.bo, p.x, h, Mi, hi, hi, EPI_BIAS_RESID_F32, &m.scratch));
+      p.gemms.push_back(plan_gemm_tc(p.xn16, h, w.w1, h, w.b1, p.big16, f, Mi, fi, hi, EPI_BIAS_GELU_F16, &m.scratch));
+      p.gemms.push_back(plan_gemm_tc(p.big16, f, w.w2, f, w.b2, p.x, h, Mi, hi, fi, EPI_BIAS_RESID_F32, &m.scratch));
     }
     p.gemms.push_back(plan_gemm_tc(p.xn16, h, m.emb16, h, nullptr, p.logit16, ld16, Mi,
-                                   static_cast<int>(V), hi, EPI_F16));
+                                   static_cast<int>(V), hi, EPI_F16, &m.scratch));
     p.attn = plan_attn_tc(p.big16, 3 * h, p.xn16, h, static_cast<int>(B), static_cast<int>(S),
                           static_cast<int>(m.H), static_cast<int>(m.hd), m.d.archetype == 1);
   } else {
@@ -525,7 +539,7 @@ int64_t enqueue_forward(prlab_gpu_model& m, prlab_gpu_model::Plan& p, const int3
       const auto key = std::make_tuple(out, ld);
       auto it = p.head_plans.find(key);
       if (it == p.head_plans.end())
-        it = p.head_plans.emplace(key, plan_gemm_tc(p.xn16, h, m.emb16, h, nullptr, out, ld, Mi, Vi, hi, EPI_F16)).first;
+        it = p.head_plans.emplace(key, plan_gemm_tc(p.xn16, h, m.emb16, h, nullptr, out, ld, Mi, Vi, hi, EPI_F16, &m.scratch)).first;
       launch_gemm_tc(it->second, st);  // tied head straight into the caller's buffer
       ++n;
     } else {
@@ -1031,16 +1045,34 @@ int prlab_gpu_linear_f16_device(const void* A, const void* Wt, const float* bias
   return guarded([&] {
     if (epi < 0 || epi > 3) throw std::invalid_argument("unknown epilogue");
     const GemmPlan p = plan_gemm_tc(A, K_, Wt, K_, bias, out, ldo, static_cast<int>(M), static_cast<int>(N),
-                                    static_cast<int>(K_), epi);
+                                    static_cast<int>(K_), epi, &global_split_scratch());
+    launch_gemm_tc(p, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int prlab_gpu_linear_f16_device_ex(const void* A, const void* Wt, const float* bias, void* out, int64_t M,
+                                   int64_t N, int64_t K_, int64_t ldo, int32_t epi, int32_t bn, int32_t splits,
+                                   int32_t lean, void* stream) {
+  return guarded([&] {
+    if (epi < 0 || epi > 3) throw std::invalid_argument("unknown epilogue");
+    if (bn != 0 && bn != 64 && bn != 128 && bn != 256) throw std::invalid_argument("bn must be 64, 128 or 256");
+    const GemmPlan p = plan_gemm_tc(A, K_, Wt, K_, bias, out, ldo, static_cast<int>(M), static_cast<int>(N),
+                                    static_cast<int>(K_), epi, &global_split_scratch(), bn, splits, lean);
     launch_gemm_tc(p, static_cast<cudaStream_t>(stream));
   });
 }
 
 int prlab_gpu_attention_f16_device(const void* qkv, void* ctx, int64_t B, int64_t S, int64_t H, int64_t hd,
                                    int32_t causal, void* stream) {
+  return prlab_gpu_attention_f16_device_dbg(qkv, ctx, B, S, H, hd, causal, stream, nullptr);
+}
+
+int prlab_gpu_attention_f16_device_dbg(const void* qkv, void* ctx, int64_t B, int64_t S, int64_t H, int64_t hd,
+                                       int32_t causal, void* stream, long long* dbg) {
   return guarded([&] {
-    const AttnPlan p = plan_attn_tc(qkv, 3 * H * hd, ctx, H * hd, static_cast<int>(B), static_cast<int>(S),
-                                    static_cast<int>(H), static_cast<int>(hd), causal);
+    AttnPlan p = plan_attn_tc(qkv, 3 * H * hd, ctx, H * hd, static_cast<int>(B), static_cast<int>(S),
+                              static_cast<int>(H), static_cast<int>(hd), causal);
+    p.dbg = dbg;
     launch_attn_tc(p, static_cast<cudaStream_t>(stream));
   });
 }
