@@ -697,6 +697,34 @@ struct Mt64 {
 };
 }  // namespace
 
+prlab_gpu_model* create_model(const prlab_model_desc& desc, const float* const* params, int64_t n_params,
+                              int device) {
+  validate_desc(desc);
+  const auto sizes = param_sizes(desc);
+  if (static_cast<size_t>(n_params) != sizes.size())
+    throw std::invalid_argument("expected " + std::to_string(sizes.size()) + " parameter tensors, got " +
+                                std::to_string(n_params));
+  require_device();
+  PRLAB_CUDA(cudaSetDevice(device));
+  auto m = std::make_unique<prlab_gpu_model>();
+  m->d = desc;
+  m->device = device;
+  m->h = desc.hidden;
+  m->f = desc.ffn;
+  m->H = desc.heads;
+  m->hd = desc.hidden / desc.heads;
+  m->V = desc.vocab;
+  m->P = desc.max_positions;
+  m->L = desc.num_layers;
+  m->host.resize(sizes.size());
+  for (size_t i = 0; i < sizes.size(); ++i) m->host[i].assign(params[i], params[i] + sizes[i]);
+  upload_fast(*m);
+  configure_gemm_tc();
+  configure_attn_tc();
+  PRLAB_CUDA(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
+  return m.release();
+}
+
 // ===========================================================================
 // C ABI
 // ===========================================================================
@@ -810,33 +838,7 @@ int prlab_gpu_validate_policy(const prlab_policy* p) {
 
 int prlab_gpu_model_create(const prlab_model_desc* desc, const float* const* params, int64_t n_params,
                            int device, prlab_gpu_model** out) {
-  return guarded([&] {
-    *out = nullptr;
-    validate_desc(*desc);
-    const auto sizes = param_sizes(*desc);
-    if (static_cast<size_t>(n_params) != sizes.size())
-      throw std::invalid_argument("expected " + std::to_string(sizes.size()) + " parameter tensors, got " +
-                                  std::to_string(n_params));
-    require_device();
-    PRLAB_CUDA(cudaSetDevice(device));
-    auto m = std::make_unique<prlab_gpu_model>();
-    m->d = *desc;
-    m->device = device;
-    m->h = desc->hidden;
-    m->f = desc->ffn;
-    m->H = desc->heads;
-    m->hd = desc->hidden / desc->heads;
-    m->V = desc->vocab;
-    m->P = desc->max_positions;
-    m->L = desc->num_layers;
-    m->host.resize(sizes.size());
-    for (size_t i = 0; i < sizes.size(); ++i) m->host[i].assign(params[i], params[i] + sizes[i]);
-    upload_fast(*m);
-    configure_gemm_tc();
-    configure_attn_tc();
-    PRLAB_CUDA(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
-    *out = m.release();
-  });
+  return guarded([&] { *out = create_model(*desc, params, n_params, device); });
 }
 
 int prlab_gpu_model_create_flat(const prlab_model_desc* desc, const float* flat, int device,
@@ -850,8 +852,7 @@ int prlab_gpu_model_create_flat(const prlab_model_desc* desc, const float* flat,
       ptrs.push_back(p);
       p += s;
     }
-    const int rc = prlab_gpu_model_create(desc, ptrs.data(), static_cast<int64_t>(ptrs.size()), device, out);
-    if (rc != PRLAB_OK) throw std::runtime_error(g_last_error);
+    *out = create_model(*desc, ptrs.data(), static_cast<int64_t>(ptrs.size()), device);
   });
 }
 
