@@ -20,6 +20,8 @@
 // unit writes its fp32 partial tile to a workspace; the last unit of a tile to
 // arrive (atomic ticket) sums the partials in split order -- deterministic --
 // and applies the epilogue, so the rounding points are those of the full sum.
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -38,24 +40,32 @@ struct GemmArgs {
   int64_t ldo;
   float* ws;      // split-K partials [tile*splits + split][BM][BN]
   int* tickets;   // per-tile arrival counters (left at zero after every launch)
+  int tma_store;  // epilogue through smem staging + TMA store / reduce-add
 };
 
 // LEAN: half-depth pipeline (~100 KB smem) so two CTAs -- this kernel's and the
 // next PDL-launched kernel's -- can be co-resident on an SM at batch-1 sizes.
 template <int BN, bool LEAN, int EPI = 0>
 struct Cfg {
-  static constexpr int STAGES = (BN == 256 ? 4 : (BN == 128 ? 6 : 8)) / (LEAN ? 2 : 1);
+  static constexpr int STAGES0 = (BN == 256 ? 4 : (BN == 128 ? 6 : 8)) / (LEAN ? 2 : 1);
   // epilogue warps: 1, 2 or 4 per TMEM lane quadrant; the erf-heavy GELU epilogue gets
   // the most so it keeps pace with the tensor core
-  static constexpr int EPI_WARPS = BN >= 256 && EPI == EPI_BIAS_GELU_F16 ? 16 : (BN >= 128 ? 8 : 4);
+  static constexpr int EPI_WARPS = BN >= 128 ? 8 : 4;
   static constexpr int THREADS = 64 + 32 * EPI_WARPS;
   static constexpr int COLS_PER_WARP = BN / (EPI_WARPS / 4);
   static constexpr uint32_t A_BYTES = BM * BK * 2;
   static constexpr uint32_t B_BYTES = BN * BK * 2;
   static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-  static constexpr uint32_t BIAS_OFF = STAGES * STAGE_BYTES + 256;  // per-warp bias slices
-  static constexpr size_t SMEM = 1024 + BIAS_OFF + EPI_WARPS * COLS_PER_WARP * 4;
+  // TMA-store epilogue: two 32-row x 128-byte staging buffers per epilogue warp
+  static constexpr uint32_t EPI_BYTES = EPI_WARPS * 2 * 4096;
+  static constexpr uint32_t BIAS_BYTES = EPI_WARPS * COLS_PER_WARP * 4;
+  static constexpr uint32_t SMEM_BUDGET = 227 * 1024 - 1024 - 256 - EPI_BYTES - BIAS_BYTES;
+  static constexpr int STAGES = STAGES0 * STAGE_BYTES <= SMEM_BUDGET ? STAGES0 : SMEM_BUDGET / STAGE_BYTES;
+  static constexpr uint32_t EPI_OFF = STAGES * STAGE_BYTES;           // 1024-aligned (stage sizes are)
+  static constexpr uint32_t BAR_OFF = EPI_OFF + EPI_BYTES;
+  static constexpr uint32_t BIAS_OFF = BAR_OFF + 256;                 // per-warp bias slices
+  static constexpr size_t SMEM = 1024 + BIAS_OFF + BIAS_BYTES;
 };
 
 // sbias: the 32 (pre-rounded) bias values of columns col0..col0+31 in shared memory, or null.
@@ -127,6 +137,22 @@ __device__ __forceinline__ void tile_coords(const GemmArgs& g, int tile, int& m_
   m_blk = m0 + local % rows;
 }
 
+// The Linear-class epilogue numerics on one 32-column chunk of fp32 accumulators:
+// round16(acc) [+ round16(b), round16] [GELU, round16]  (kernels.cpp:78, model.cpp:73,
+// kernels.cpp:232).  The residual add itself happens in the store path.
+template <int EPI>
+__device__ __forceinline__ void epilogue_values(const uint32_t (&u)[32], const float* sbias, float (&v)[32]) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    float a = r16(__uint_as_float(u[i]));
+    if (EPI != EPI_F16) {
+      a = r16(__fadd_rn(a, sbias != nullptr ? sbias[i] : 0.0f));
+      if (EPI == EPI_BIAS_GELU_F16) a = r16(gelu_erf(a));
+    }
+    v[i] = a;
+  }
+}
+
 __device__ __forceinline__ void unit_range(const GemmArgs& g, int unit, int& tile, int& split,
                                            int& kb0, int& kb1) {
   tile = unit / g.splits;
@@ -138,14 +164,14 @@ __device__ __forceinline__ void unit_range(const GemmArgs& g, int unit, int& til
 template <int BN, bool LEAN, int EPI>
 __global__ void __launch_bounds__(Cfg<BN, LEAN, EPI>::THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                   const GemmArgs g) {
+                   const __grid_constant__ CUtensorMap tmC, const GemmArgs g) {
   using C = Cfg<BN, LEAN, EPI>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~static_cast<uintptr_t>(1023));
   uint8_t* sA = smem;
   uint8_t* sB = smem + C::STAGES * C::A_BYTES;
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE_BYTES);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
   uint64_t* empty = full + C::STAGES;
   uint64_t* tfull = empty + C::STAGES;
   uint64_t* tempty = tfull + 2;
@@ -252,6 +278,7 @@ __global__ void __launch_bounds__(Cfg<BN, LEAN, EPI>::THREADS, 1)
     const int tid = (warp - 2) * 32 + lane;
     float* sbias = reinterpret_cast<float*>(smem + C::BIAS_OFF) + (warp - 2) * C::COLS_PER_WARP;
     uint32_t t = 0;
+    uint32_t store_k = 0;  // TMA-store staging buffer parity (per warp, across tiles)
     for (int unit = blockIdx.x; unit < total_units; unit += gridDim.x, ++t) {
       int tile, split, kb0, kb1;
       unit_range(g, unit, tile, split, kb0, kb1);
@@ -271,7 +298,57 @@ __global__ void __launch_bounds__(Cfg<BN, LEAN, EPI>::THREADS, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = m_blk * BM + r;
-      if (g.splits == 1) {
+      if (g.splits == 1 && g.tma_store) {
+        // fp16 out: 64-column store chunks (2 TMEM loads); fp32 residual: 32-column
+        // chunks added into x by the TMA engine (cp.reduce.async.bulk .add.f32)
+        constexpr bool F32OUT = EPI == EPI_BIAS_RESID_F32;
+        constexpr int SC = F32OUT ? 32 : 64;
+        uint8_t* ebuf = smem + C::EPI_OFF + (warp - 2) * 2 * 4096;
+#pragma unroll 1
+        for (int c = cbase; c < cbase + C::COLS_PER_WARP; c += SC, ++store_k) {
+          uint8_t* buf = ebuf + (store_k & 1) * 4096;
+          if (lane == 0) bulk_wait_read<1>();  // this buffer's previous store has been read
+          __syncwarp();
+          uint8_t* rowp = buf + lane * 128;
+#pragma unroll
+          for (int h = 0; h < SC; h += 32) {
+            uint32_t u[32];
+            tmem_ld32(tmem_base + ((quad * 32) << 16) + acc * BN + c + h, u);
+            tmem_wait_ld();
+            float v[32];
+            epilogue_values<EPI>(u, has_bias ? sbias + (c - cbase) + h : nullptr, v);
+            if (F32OUT) {
+#pragma unroll
+              for (int j = 0; j < 8; ++j)
+                *reinterpret_cast<float4*>(rowp + ((j ^ (lane & 7)) * 16)) =
+                    make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+            } else {
+              uint32_t pk[16];
+#pragma unroll
+              for (int i = 0; i < 16; ++i) {
+                __half2 h2 = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+                pk[i] = *reinterpret_cast<uint32_t*>(&h2);
+              }
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                *reinterpret_cast<uint4*>(rowp + ((((h >> 3) + j) ^ (lane & 7)) * 16)) =
+                    make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+            }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            if (F32OUT)
+              tma_reduce_add_2d(&tmC, buf, n_blk * BN + c, m_blk * BM + quad * 32);
+            else
+              tma_store_2d(&tmC, buf, n_blk * BN + c, m_blk * BM + quad * 32);
+            bulk_commit();
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+      } else if (g.splits == 1) {
 #pragma unroll 1
         for (int c = cbase; c < cbase + C::COLS_PER_WARP; c += 32) {
           uint32_t u[32];
@@ -348,6 +425,8 @@ __global__ void __launch_bounds__(Cfg<BN, LEAN, EPI>::THREADS, 1)
         }
       }
     }
+    if (lane == 0) bulk_wait<0>();  // TMA stores complete before the CTA retires
+    __syncwarp();
   }
   __syncthreads();
   if (warp == 1) {
@@ -621,7 +700,7 @@ void configure_bn() {
 template <int BN, bool LEAN, int EPI>
 void launch_one(const GemmPlan& p, const GemmArgs& g, cudaStream_t st) {
   using C = Cfg<BN, LEAN, EPI>;
-  launch_pdl(gemm_tc_kernel<BN, LEAN, EPI>, dim3(p.grid), dim3(C::THREADS), C::SMEM, st, p.tmA, p.tmB, g);
+  launch_pdl(gemm_tc_kernel<BN, LEAN, EPI>, dim3(p.grid), dim3(C::THREADS), C::SMEM, st, p.tmA, p.tmB, p.tmC, g);
 }
 
 template <int BN, bool LEAN>
@@ -710,6 +789,13 @@ GemmPlan plan_gemm_tc(const void* A, int64_t lda, const void* Wt, int64_t ldw, c
   }
   p.tmA = make_tmap_f16_2d(A, M, K, lda, BM, BK);
   p.tmB = make_tmap_f16_2d(Wt, N, K, ldw, bn, BK);
+  // TMA-store epilogue when the output rows are 16-byte aligned (TMA clips the M/N tails)
+  const bool f32out = epi == EPI_BIAS_RESID_F32;
+  const int64_t row_bytes = ldo * (f32out ? 4 : 2);
+  p.tma_store = !std::getenv("PRLAB_NO_TMA_STORE") && (row_bytes % 16 == 0) &&
+                (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+  if (p.tma_store)
+    p.tmC = f32out ? make_tmap_f32_2d(out, M, N, ldo, 32, 32) : make_tmap_f16_2d(out, M, N, ldo, 32, 64);
   const int units = tiles * p.splits;
   p.grid = p.cluster ? units : (units < sms ? units : sms);
   return p;
@@ -746,6 +832,7 @@ void launch_gemm_tc(const GemmPlan& p, cudaStream_t st) {
   g.ldo = p.ldo;
   g.ws = p.ws;
   g.tickets = p.tickets;
+  g.tma_store = p.tma_store ? 1 : 0;
   if (p.cluster) {
     if (p.bn == 64)
       launch_cluster_bn<64>(p, g, st);

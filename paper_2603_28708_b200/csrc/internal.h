@@ -51,6 +51,9 @@ void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cuda
 CUtensorMap make_tmap_f16_2d(const void* base, uint64_t rows, uint64_t cols, uint64_t pitch_elems,
                              uint32_t box_rows, uint32_t box_cols);
 // 3-D fp16 tensor [d2, d1, d0] (d0 contiguous) with pitches in elements.
+// 2-D fp32 tensor [rows, cols], box {box_cols, box_rows}, 128-byte swizzle (box_cols*4 == 128)
+CUtensorMap make_tmap_f32_2d(const void* base, uint64_t rows, uint64_t cols, uint64_t pitch_elems,
+                             uint32_t box_rows, uint32_t box_cols);
 CUtensorMap make_tmap_f16_3d(const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
                              uint64_t pitch1_elems, uint64_t pitch2_elems, uint32_t box0,
                              uint32_t box1, uint32_t box2);
@@ -63,7 +66,8 @@ enum GemmEpi : int {
   EPI_F16 = 3,            // round16(acc)                           -> fp16
 };
 struct GemmPlan {
-  CUtensorMap tmA, tmB;
+  CUtensorMap tmA, tmB, tmC;  // tmC: output map for the TMA-store epilogue
+  bool tma_store;
   int M, N, K, bn, epi;
   int splits, kb_per_split;
   bool lean;

@@ -105,6 +105,21 @@ CUtensorMap make_tmap_f16_2d(const void* base, uint64_t rows, uint64_t cols, uin
   return m;
 }
 
+CUtensorMap make_tmap_f32_2d(const void* base, uint64_t rows, uint64_t cols, uint64_t pitch_elems,
+                             uint32_t box_rows, uint32_t box_cols) {
+  CUtensorMap m;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {pitch_elems * 4};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims,
+                           strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) throw cuda_error("cuTensorMapEncodeTiled(f32 2d) failed: " + std::to_string(r));
+  return m;
+}
+
 CUtensorMap make_tmap_f16_3d(const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
                              uint64_t pitch1_elems, uint64_t pitch2_elems, uint32_t box0,
                              uint32_t box1, uint32_t box2) {
