@@ -183,6 +183,10 @@ int prlab_gpu_attention_f16_device_dbg(const void* qkv, void* ctx, int64_t batch
                                        int64_t heads, int64_t head_dim, int32_t causal,
                                        void* stream, long long* dbg);
 
+/* Debug: GEMM launches after this call write %globaltimer phase stamps ([grid][8] int64,
+ * device memory) into dbg (NULL switches the stamps off). */
+int prlab_gpu_debug_gemm_stamps(long long* dbg);
+
 #ifdef __cplusplus
 }
 #endif

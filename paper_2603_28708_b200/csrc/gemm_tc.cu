@@ -41,6 +41,7 @@ struct GemmArgs {
   float* ws;      // split-K partials [tile*splits + split][BM][BN]
   int* tickets;   // per-tile arrival counters (left at zero after every launch)
   int tma_store;  // epilogue through smem staging + TMA store / reduce-add
+  long long* dbg; // optional per-CTA %globaltimer stamps [grid][8] (debug), null = off
 };
 
 // LEAN: half-depth pipeline (~100 KB smem) so two CTAs -- this kernel's and the
@@ -496,6 +497,39 @@ __device__ __forceinline__ void epilogue_vec4(float4 a, const GemmArgs& g, int r
   }
 }
 
+// full-width quad with the bias and residual already in registers
+template <int EPI>
+__device__ __forceinline__ void epilogue_vec4_fast(float4 a, float4 b, float4 x, const GemmArgs& g, int row,
+                                                   int col) {
+  float v[4] = {a.x, a.y, a.z, a.w};
+  const float bb[4] = {b.x, b.y, b.z, b.w};
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    float t = r16(v[i]);
+    if (EPI != EPI_F16) {
+      t = r16(__fadd_rn(t, bb[i]));
+      if (EPI == EPI_BIAS_GELU_F16) t = r16(gelu_erf(t));
+    }
+    v[i] = t;
+  }
+  if (EPI == EPI_BIAS_RESID_F32) {
+    float* o = reinterpret_cast<float*>(g.out) + static_cast<int64_t>(row) * g.ldo + col;
+    *reinterpret_cast<float4*>(o) =
+        make_float4(__fadd_rn(x.x, v[0]), __fadd_rn(x.y, v[1]), __fadd_rn(x.z, v[2]), __fadd_rn(x.w, v[3]));
+  } else {
+    __half* o = reinterpret_cast<__half*>(g.out) + static_cast<int64_t>(row) * g.ldo + col;
+    __half2 h01 = __floats2half2_rn(v[0], v[1]), h23 = __floats2half2_rn(v[2], v[3]);
+    if ((g.ldo % 4) == 0)
+      *reinterpret_cast<uint2*>(o) = make_uint2(*reinterpret_cast<uint32_t*>(&h01), *reinterpret_cast<uint32_t*>(&h23));
+    else {
+      o[0] = __low2half(h01);
+      o[1] = __high2half(h01);
+      o[2] = __low2half(h23);
+      o[3] = __high2half(h23);
+    }
+  }
+}
+
 template <int BN, int EPI>
 __global__ void __launch_bounds__(CCfg<BN>::THREADS, 1)
     gemm_splitk_cluster_kernel(const __grid_constant__ CUtensorMap tmA,
@@ -513,6 +547,8 @@ __global__ void __launch_bounds__(CCfg<BN>::THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
 
   const uint32_t warp = warp_id(), lane = lane_id();
+  long long* dbg = g.dbg ? g.dbg + static_cast<int64_t>(blockIdx.x) * 8 : nullptr;
+  if (dbg && threadIdx.x == 0) dbg[0] = globaltimer();
   const int split = static_cast<int>(cluster_ctarank());
   const int tile = blockIdx.x / g.splits;
   const int kb0 = split * g.kb_per_split;
@@ -539,6 +575,7 @@ __global__ void __launch_bounds__(CCfg<BN>::THREADS, 1)
   tc_fence_after();
   pdl_trigger();
   const uint32_t tmem_base = *tmem_slot;
+  if (dbg && threadIdx.x == 0) dbg[1] = globaltimer();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -548,6 +585,7 @@ __global__ void __launch_bounds__(CCfg<BN>::THREADS, 1)
         tma_load_2d(sB + i * C::B_BYTES, &tmB, &full[i], (kb0 + i) * BK, n_blk * BN);
       }
       pdl_wait();
+      if (dbg) dbg[2] = globaltimer();
       uint32_t stage = 0, phase = 0;
       for (int kb = kb0; kb < kb1; ++kb) {
         if (kb - kb0 < pre) {
@@ -588,6 +626,7 @@ __global__ void __launch_bounds__(CCfg<BN>::THREADS, 1)
     const int r = quad * 32 + lane;
     mbar_wait(tfull, 0);
     tc_fence_after();
+    if (dbg && warp == 2 && lane == 0) dbg[3] = globaltimer();
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
       uint32_t u[32];
@@ -601,17 +640,41 @@ __global__ void __launch_bounds__(CCfg<BN>::THREADS, 1)
     }
     tc_fence_before();
   }
-  cluster_sync_all();  // every CTA's partial is complete and visible cluster-wide
+  // Hoist this thread's global reads (bias quad, residual x) above the cluster
+  // barrier: their latency overlaps the wait instead of serialising the reduce.
+  constexpr int C4 = BN / 4;
+  constexpr int MAXIT = 8;  // (rows_per * C4) / 128 <= 8 for splits >= 2 at BN 64, >= 4 at BN 128
+  const int tid = static_cast<int>(threadIdx.x) - 64;
+  const int rows_per = (BM + g.splits - 1) / g.splits;
+  const int r0 = split * rows_per, r1 = min(BM, r0 + rows_per);
+  const int c4 = (tid >= 0 ? tid : 0) % C4;  // each thread's column quad is fixed (128 % C4 == 0)
+  const int col = n_blk * BN + c4 * 4;
+  const int nit = tid >= 0 ? ((r1 - r0) * C4 - tid + 127) / 128 : 0;
+  float4 bias4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  float4 xres[MAXIT];
   if (warp >= 2) {
-    const int tid = (warp - 2) * 32 + lane;
-    const int rows_per = (BM + g.splits - 1) / g.splits;
-    const int r0 = split * rows_per, r1 = min(BM, r0 + rows_per);
+    if (EPI != EPI_F16 && g.bias != nullptr && col + 4 <= g.N) bias4 = __ldg(reinterpret_cast<const float4*>(g.bias + col));
+    if (EPI == EPI_BIAS_RESID_F32) {
+#pragma unroll
+      for (int it = 0; it < MAXIT; ++it) {
+        const int rr = r0 + (tid + it * 128) / C4;
+        const int row = m_blk * BM + rr;
+        xres[it] = (it < nit && row < g.M && col + 4 <= g.N && (g.ldo % 4) == 0)
+                       ? *reinterpret_cast<const float4*>(reinterpret_cast<const float*>(g.out) +
+                                                          static_cast<int64_t>(row) * g.ldo + col)
+                       : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+    }
+  }
+  if (dbg && threadIdx.x == 64) dbg[4] = globaltimer();
+  cluster_sync_all();  // every CTA's partial is complete and visible cluster-wide
+  if (dbg && threadIdx.x == 64) dbg[5] = globaltimer();
+  if (warp >= 2) {
     const uint32_t base = smem_u32(part);
-    constexpr int C4 = BN / 4;
-    // each thread's column quad is fixed (128 % C4 == 0): stage its bias once
-    const int c4 = tid % C4;
-    const int col = n_blk * BN + c4 * 4;
-    for (int e = tid; e < (r1 - r0) * C4; e += 128) {
+#pragma unroll
+    for (int it = 0; it < MAXIT; ++it) {
+      if (it >= nit) break;
+      const int e = tid + it * 128;
       const int rr = r0 + e / C4;
       const uint32_t off = static_cast<uint32_t>((rr * C::PSTRIDE + c4 * 4) * 4);
       float4 p[8];
@@ -628,10 +691,30 @@ __global__ void __launch_bounds__(CCfg<BN>::THREADS, 1)
           acc.w = __fadd_rn(acc.w, p[s].w);
         }
       }
+      const int row = m_blk * BM + rr;
+      if (col + 4 <= g.N && row < g.M && (EPI != EPI_BIAS_RESID_F32 || (g.ldo % 4) == 0)) {
+        epilogue_vec4_fast<EPI>(acc, bias4, xres[it], g, row, col);
+      } else {
+        epilogue_vec4<EPI>(acc, g, row, col);
+      }
+    }
+    for (int it = MAXIT; it < nit; ++it) {  // tall slices (few splits, wide tiles): no prefetch
+      const int rr = r0 + (tid + it * 128) / C4;
+      const uint32_t off = static_cast<uint32_t>((rr * C::PSTRIDE + c4 * 4) * 4);
+      float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int s = 0; s < g.splits; ++s) {
+        const float4 p = ld_dsmem_f4(mapa_shared(base + off, static_cast<uint32_t>(s)));
+        acc.x = __fadd_rn(acc.x, p.x);
+        acc.y = __fadd_rn(acc.y, p.y);
+        acc.z = __fadd_rn(acc.z, p.z);
+        acc.w = __fadd_rn(acc.w, p.w);
+      }
       epilogue_vec4<EPI>(acc, g, m_blk * BM + rr, col);
     }
   }
+  if (dbg && threadIdx.x == 64) dbg[6] = globaltimer();
   cluster_sync_all();  // peers are done reading this CTA's shared memory
+  if (dbg && threadIdx.x == 64) dbg[7] = globaltimer();
   if (warp == 1) {
     tc_fence_after();
     tmem_dealloc(tmem_base, C::TMEM_COLS);
@@ -715,6 +798,11 @@ void launch_bn(const GemmPlan& p, const GemmArgs& g, cudaStream_t st) {
 }
 
 }  // namespace
+
+long long*& debug_stamps() {
+  static long long* p = nullptr;
+  return p;
+}
 
 SplitScratch& global_split_scratch() {
   static SplitScratch s;
@@ -833,6 +921,7 @@ void launch_gemm_tc(const GemmPlan& p, cudaStream_t st) {
   g.ws = p.ws;
   g.tickets = p.tickets;
   g.tma_store = p.tma_store ? 1 : 0;
+  g.dbg = debug_stamps();
   if (p.cluster) {
     if (p.bn == 64)
       launch_cluster_bn<64>(p, g, st);

@@ -88,6 +88,7 @@ struct SplitScratch {
   int n_tickets = 0;
 };
 SplitScratch& global_split_scratch();
+long long*& debug_stamps();  // GEMM phase stamps target (debug; null = off)
 GemmPlan plan_gemm_tc(const void* A, int64_t lda, const void* Wt, int64_t ldw, const float* bias,
                       void* out, int64_t ldo, int M, int N, int K, int epi,
                       const SplitScratch* scratch, int force_bn = 0, int force_splits = 0,

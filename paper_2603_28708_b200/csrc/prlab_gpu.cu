@@ -1078,6 +1078,10 @@ int prlab_gpu_linear_f16_device_ex(const void* A, const void* Wt, const float* b
   });
 }
 
+int prlab_gpu_debug_gemm_stamps(long long* dbg) {
+  return guarded([&] { debug_stamps() = dbg; });
+}
+
 int prlab_gpu_attention_f16_device(const void* qkv, void* ctx, int64_t B, int64_t S, int64_t H, int64_t hd,
                                    int32_t causal, void* stream) {
   return prlab_gpu_attention_f16_device_dbg(qkv, ctx, B, S, H, hd, causal, stream, nullptr);
