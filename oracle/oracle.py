@@ -295,6 +295,24 @@ class Oracle:
         return out
 
 
+def make_adversarial_params(orc: "Oracle", c: ModelConfig, probe_ids, batch: int, seq: int,
+                            target: float = 30.0) -> np.ndarray:
+    """Restatement of make_adversarial_model (src/fidelity.cpp:282-312) on the oracle:
+    rescale layer-0 Wq/bq/Wk/bk by sqrt(target / max|layer-0 fp32 score|)."""
+    if c.num_layers < 1:
+        raise ValueError("adversarial construction needs >= 1 layer")
+    p = orc.build_model(c)
+    _, tap = orc.forward(c, p, probe_ids, batch, seq, "fp32", retain_scores=True)
+    max_score = float(np.abs(tap[0].astype(np.float64)).max())
+    if max_score == 0.0:
+        raise ValueError("probe produced all-zero layer-0 scores; cannot rescale")
+    s = np.float32(np.sqrt(target / max_score))
+    views = dict(split_params(c, p))
+    for name in ("layers.0.attn.wq", "layers.0.attn.bq", "layers.0.attn.wk", "layers.0.attn.bk"):
+        views[name][...] = views[name] * s
+    return p
+
+
 class Reference:
     """The unmodified reference, compiled by oracle/Makefile (oracle/_ref/libprlab_ref.so)."""
 
@@ -363,6 +381,17 @@ class Reference:
             msg = self.lib.ref_last_error().decode()
             raise (IndexError if rc == -2 else ValueError)(msg)
         return (logits, calls.reshape(7, 2)) if want_calls else logits
+
+    def make_adversarial_model(self, c: ModelConfig, probe_ids, batch, seq, target=30.0):
+        L = self.lib
+        L.ref_make_adversarial_model.argtypes = ([C.c_int] + [C.c_int64] * 6 +
+                                                 [C.c_uint64, C.POINTER(C.c_int32), C.c_int64,
+                                                  C.c_int64, C.c_float, C.POINTER(C.c_float)])
+        out = np.empty(self.param_count(c), dtype=np.float32)
+        ids = np.ascontiguousarray(probe_ids, np.int32)
+        if L.ref_make_adversarial_model(*self._c(c), c.seed, _ip(ids), batch, seq, target, _fp(out)):
+            raise ValueError(L.ref_last_error().decode())
+        return out
 
     def matmul(self, a, b, compute, accum):
         a = np.ascontiguousarray(a, np.float32)

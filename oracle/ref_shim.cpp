@@ -160,6 +160,27 @@ int ref_forward(int archetype, int64_t L, int64_t h, int64_t H, int64_t f, int64
   }
 }
 
+// make_adversarial_model (src/fidelity.cpp:282-312) -> flat canonical params
+int ref_make_adversarial_model(int archetype, int64_t L, int64_t h, int64_t H, int64_t f, int64_t V,
+                               int64_t P, uint64_t seed, const int32_t* probe_ids, int64_t B, int64_t S,
+                               float target, float* out) {
+  try {
+    prlab::TokenBatch tb;
+    tb.batch = B;
+    tb.seq = S;
+    tb.ids.assign(probe_ids, probe_ids + B * S);
+    const prlab::Model m = prlab::make_adversarial_model(make_cfg(archetype, L, h, H, f, V, P, seed), tb, target);
+    float* o = out;
+    m.for_each_param([&o](const std::string&, const prlab::Tensor& t) {
+      std::memcpy(o, t.data.data(), t.data.size() * sizeof(float));
+      o += t.data.size();
+    });
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, -1);
+  }
+}
+
 // --- per-operator entry points (src/kernels.cpp) for KAT cross-checks ---
 int ref_matmul(const float* a, const float* b, int64_t m, int64_t k, int64_t n, int compute,
                int accum, float* out) {

@@ -118,3 +118,20 @@ def test_round16_matches_reference_on_random_bits():
     for x in rng.integers(0, 2 ** 32, 20_000, dtype=np.uint64).astype(np.uint32).view(np.float32):
         a, b = o.round16(float(x)), r.lib.ref_round16(float(x))
         assert (np.isnan(a) and np.isnan(b)) or u32(a) == u32(b)
+
+
+@needs_ref
+@pytest.mark.parametrize("name", ["decoder_toy", "encoder_toy"])
+def test_adversarial_construction_matches_reference(name):
+    from oracle.oracle import make_adversarial_params
+    r = reference()
+    cfg = PRESETS[name].replace(seed=4)
+    probe = o.random_tokens(cfg.vocab, 1, 32, 5)
+    a = make_adversarial_params(o, cfg, probe, 1, 32, 30.0)
+    b = r.make_adversarial_model(cfg, probe, 1, 32, 30.0)
+    assert np.array_equal(u32(a), u32(b))
+    # the NaN mechanism (test_fidelity.cpp:175-195): full_fp16 overflows, hybrid/fp32 stay finite
+    ids = o.random_tokens(cfg.vocab, 1, 32, 5)
+    assert not np.isfinite(o.forward(cfg, a, ids, 1, 32, "full_fp16")).all()
+    assert np.isfinite(o.forward(cfg, a, ids, 1, 32, "hybrid")).all()
+    assert np.isfinite(o.forward(cfg, a, ids, 1, 32, "fp32")).all()
