@@ -766,6 +766,300 @@ void launch_cluster_bn(const GemmPlan& p, const GemmArgs& g, cudaStream_t st) {
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// CTA-pair GEMM (large M): a cluster of 2 CTAs computes a 256 x BN tile with
+// tcgen05.mma.cta_group::2 (M = 256).  CTA r loads its own 128 rows of A and
+// half of the B tile (BN/2 weight rows) -- per CTA and k-block that is 16 KB
+// + BN*64 B instead of 16 KB + BN*128 B, which cuts the L2->SM traffic per
+// FLOP by a third at BN = 256.  Only the leader (rank 0) issues MMAs; its
+// commits are multicast to both CTAs' barriers; both CTAs run their own
+// epilogue on their own TMEM rows (TMA-store / reduce-add as in gemm_tc_kernel).
+// Barriers: full (leader; 2 arrivals + both CTAs' transaction bytes), empty and
+// tfull (per CTA, multicast commits), tempty (leader; all epilogue warps of both).
+// ---------------------------------------------------------------------------
+template <int BN, int EPI = 0>
+struct Cfg2 {
+  // the erf-heavy GELU epilogue gets 4 warps per TMEM lane quadrant (one staging
+  // buffer each); the others 2 warps per quadrant with double-buffered staging
+  static constexpr int EPI_WARPS = (EPI == EPI_BIAS_GELU_F16 && BN == 256) ? 16 : 8;
+  static constexpr int NBUF = EPI_WARPS == 16 ? 1 : 2;
+  static constexpr int THREADS = 64 + 32 * EPI_WARPS;
+  static constexpr int COLS_PER_WARP = BN / (EPI_WARPS / 4);
+  static constexpr uint32_t A_BYTES = BM * BK * 2;
+  static constexpr uint32_t B_BYTES = (BN / 2) * BK * 2;
+  static constexpr uint32_t STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr uint32_t TMEM_COLS = 2 * BN;
+  static constexpr uint32_t EPI_BYTES = EPI_WARPS * NBUF * 4096;
+  static constexpr uint32_t BIAS_BYTES = EPI_WARPS * COLS_PER_WARP * 4;
+  static constexpr uint32_t SMEM_BUDGET = 227 * 1024 - 1024 - 256 - EPI_BYTES - BIAS_BYTES;
+  static constexpr int STAGES = SMEM_BUDGET / STAGE_BYTES > 6 ? 6 : SMEM_BUDGET / STAGE_BYTES;
+  static constexpr uint32_t EPI_OFF = STAGES * STAGE_BYTES;
+  static constexpr uint32_t BAR_OFF = EPI_OFF + EPI_BYTES;
+  static constexpr uint32_t BIAS_OFF = BAR_OFF + 256;
+  static constexpr size_t SMEM = 1024 + BIAS_OFF + BIAS_BYTES;
+};
+
+template <int BN, int EPI>
+__global__ void __launch_bounds__(Cfg2<BN, EPI>::THREADS, 1)
+    gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    const __grid_constant__ CUtensorMap tmC, const GemmArgs g) {
+  using C = Cfg2<BN, EPI>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + C::STAGES * C::A_BYTES;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::BAR_OFF);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const uint32_t rank = cluster_ctarank();
+  const bool leader = rank == 0;
+  // work unit = (pair of m-blocks, n-block); pairs stride by the number of clusters
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const int m_pairs = (g.num_m_blocks + 1) / 2;
+  const int total_units = m_pairs * g.num_n_blocks;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmB);
+    if (g.tma_store) tma_prefetch_desc(&tmC);
+    for (int s = 0; s < C::STAGES; ++s) {
+      mbar_init(&full[s], 2);
+      mbar_init(&empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], 2 * C::EPI_WARPS);
+    }
+    fence_barrier_init();
+  }
+  cluster_sync_all();  // barriers of both CTAs initialised before any cross-CTA traffic
+  if (warp == 1) {
+    tmem_alloc_pair(tmem_slot, C::TMEM_COLS);
+    tmem_relinquish_pair();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_trigger();
+  const uint32_t tmem_base = *tmem_slot;
+
+  auto coords = [&](int unit, int& mp, int& n_blk) {
+    // bands of 8 m-pairs (16 m-blocks); n-blocks advance slowest inside a band
+    constexpr int GROUP = 8;
+    const int band = unit / (GROUP * g.num_n_blocks);
+    const int m0 = band * GROUP;
+    const int rows = min(GROUP, m_pairs - m0);
+    const int local = unit - band * GROUP * g.num_n_blocks;
+    n_blk = local / rows;
+    mp = m0 + local % rows;
+  };
+
+  if (warp == 0) {
+    // ---------------- TMA producer (both CTAs) ----------------
+    if (lane == 0) {
+      int pre = 0;
+      if (pair < total_units) {
+        int mp, n_blk;
+        coords(pair, mp, n_blk);
+        pre = min(C::STAGES, g.num_k_blocks);
+        for (int i = 0; i < pre; ++i) {  // weight halves first (independent of the upstream kernel)
+          if (leader) mbar_expect_tx(&full[i], 2 * C::STAGE_BYTES);
+          tma_load_2d_pair(sB + i * C::B_BYTES, &tmB, &full[i], i * BK, n_blk * BN + rank * (BN / 2));
+        }
+      }
+      pdl_wait();
+      uint32_t stage = 0, phase = 0;
+      bool first = true;
+      for (int unit = pair; unit < total_units; unit += npairs) {
+        int mp, n_blk;
+        coords(unit, mp, n_blk);
+        const int m_blk = 2 * mp + static_cast<int>(rank);
+        for (int kb = 0; kb < g.num_k_blocks; ++kb) {
+          if (first && kb < pre) {
+            tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
+          } else {
+            mbar_wait(&empty[stage], phase ^ 1);
+            if (leader) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
+            tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
+            tma_load_2d_pair(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, n_blk * BN + rank * (BN / 2));
+          }
+          if (!leader) mbar_arrive_cluster(to_leader(smem_u32(&full[stage])));
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        first = false;
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---------------- MMA issuer (leader only) ----------------
+    if (leader) {
+      constexpr uint32_t idesc = idesc_f16_f32(256, BN, 0, 0);
+      uint32_t stage = 0, phase = 0, t = 0;
+      for (int unit = pair; unit < total_units; unit += npairs, ++t) {
+        const uint32_t acc = t & 1, acc_phase = (t >> 1) & 1;
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < g.num_k_blocks; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          if (lane == 0) {
+            const uint32_t a0 = smem_u32(sA + stage * C::A_BYTES);
+            const uint32_t b0 = smem_u32(sB + stage * C::B_BYTES);
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              umma_f16_ss_pair(d_tmem, sw128_desc(a0 + k * 32, 0, 1024), sw128_desc(b0 + k * 32, 0, 1024), idesc,
+                               (kb > 0 || k > 0) ? 1u : 0u);
+            umma_commit_pair(&empty[stage]);
+          }
+          __syncwarp();
+          if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
+        }
+        if (lane == 0) umma_commit_pair(&tfull[acc]);
+        __syncwarp();
+      }
+      // the peer's last tempty arrivals must land before the leader retires
+      if (t > 0) mbar_wait(&tempty[(t - 1) & 1], ((t - 1) >> 1) & 1);
+    }
+    __syncwarp();
+  } else {
+    // ---------------- epilogue (both CTAs, own TMEM rows) ----------------
+    const uint32_t quad = warp & 3;
+    const int cbase = ((warp - 2) >> 2) * C::COLS_PER_WARP;
+    float* sbias = reinterpret_cast<float*>(smem + C::BIAS_OFF) + (warp - 2) * C::COLS_PER_WARP;
+    const uint32_t tempty_leader = to_leader(smem_u32(&tempty[0]));
+    uint8_t* ebuf = smem + C::EPI_OFF + (warp - 2) * C::NBUF * 4096;
+    constexpr bool F32OUT = EPI == EPI_BIAS_RESID_F32;
+    constexpr int SC = F32OUT ? 32 : 64;
+    uint32_t t = 0, store_k = 0;
+    for (int unit = pair; unit < total_units; unit += npairs, ++t) {
+      int mp, n_blk;
+      coords(unit, mp, n_blk);
+      const int m_blk = 2 * mp + static_cast<int>(rank);
+      const uint32_t acc = t & 1, acc_phase = (t >> 1) & 1;
+      const bool has_bias = EPI != EPI_F16 && g.bias != nullptr;
+      if (has_bias) {
+        __syncwarp();
+        for (int c = lane; c < C::COLS_PER_WARP; c += 32) {
+          const int col = n_blk * BN + cbase + c;
+          sbias[c] = col < g.N ? __ldg(g.bias + col) : 0.0f;
+        }
+        __syncwarp();
+      }
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+#pragma unroll 1
+      for (int c = cbase; c < cbase + C::COLS_PER_WARP; c += SC, ++store_k) {
+        uint8_t* buf = ebuf + (C::NBUF == 2 ? (store_k & 1) * 4096 : 0);
+        if (lane == 0) {
+          if (C::NBUF == 2)
+            bulk_wait_read<1>();
+          else
+            bulk_wait_read<0>();
+        }
+        __syncwarp();
+        uint8_t* rowp = buf + lane * 128;
+#pragma unroll
+        for (int h = 0; h < SC; h += 32) {
+          uint32_t u[32];
+          tmem_ld32(tmem_base + ((quad * 32) << 16) + acc * BN + c + h, u);
+          tmem_wait_ld();
+          float v[32];
+          epilogue_values<EPI>(u, has_bias ? sbias + (c - cbase) + h : nullptr, v);
+          if (F32OUT) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              *reinterpret_cast<float4*>(rowp + ((j ^ (lane & 7)) * 16)) =
+                  make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+          } else {
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              __half2 h2 = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
+              pk[i] = *reinterpret_cast<uint32_t*>(&h2);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+              *reinterpret_cast<uint4*>(rowp + ((((h >> 3) + j) ^ (lane & 7)) * 16)) =
+                  make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          if (F32OUT)
+            tma_reduce_add_2d(&tmC, buf, n_blk * BN + c, m_blk * BM + quad * 32);
+          else
+            tma_store_2d(&tmC, buf, n_blk * BN + c, m_blk * BM + quad * 32);
+          bulk_commit();
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
+    }
+    if (lane == 0) bulk_wait<0>();
+    __syncwarp();
+  }
+  tc_fence_before();
+  cluster_sync_all();  // all MMAs / TMEM reads of both CTAs done
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem_base, C::TMEM_COLS);
+  }
+}
+
+template <int BN, int EPI>
+void configure_pair_one() {
+  auto k = gemm_tc2_kernel<BN, EPI>;
+  PRLAB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(Cfg2<BN, EPI>::SMEM)));
+}
+
+template <int BN>
+void configure_pair_bn() {
+  configure_pair_one<BN, EPI_BIAS_F16>();
+  configure_pair_one<BN, EPI_BIAS_GELU_F16>();
+  configure_pair_one<BN, EPI_BIAS_RESID_F32>();
+  configure_pair_one<BN, EPI_F16>();
+}
+
+template <int BN, int EPI>
+void launch_pair_one(const GemmPlan& p, const GemmArgs& g, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.grid);
+  cfg.blockDim = dim3(Cfg2<BN, EPI>::THREADS);
+  cfg.dynamicSmemBytes = Cfg2<BN, EPI>::SMEM;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[2];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 2;
+  PRLAB_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<BN, EPI>, p.tmA, p.tmB, p.tmC, g));
+}
+
+template <int BN>
+void launch_pair_bn(const GemmPlan& p, const GemmArgs& g, cudaStream_t st) {
+  switch (p.epi) {
+    case EPI_BIAS_F16: launch_pair_one<BN, EPI_BIAS_F16>(p, g, st); break;
+    case EPI_BIAS_GELU_F16: launch_pair_one<BN, EPI_BIAS_GELU_F16>(p, g, st); break;
+    case EPI_BIAS_RESID_F32: launch_pair_one<BN, EPI_BIAS_RESID_F32>(p, g, st); break;
+    case EPI_F16: launch_pair_one<BN, EPI_F16>(p, g, st); break;
+    default: throw std::invalid_argument("unknown gemm epilogue");
+  }
+}
+
 template <int BN, bool LEAN, int EPI>
 void configure_one() {
   PRLAB_CUDA(cudaFuncSetAttribute(gemm_tc_kernel<BN, LEAN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -857,6 +1151,11 @@ GemmPlan plan_gemm_tc(const void* A, int64_t lda, const void* Wt, int64_t ldw, c
   p.lean = (tiles * splits <= sms);
   if (force_lean) p.lean = force_lean > 0;
   p.cluster = cluster;
+  // CTA pairs (cta_group::2) once there are several waves of 256-row tiles
+  p.pair = !cluster && splits == 1 && (bn == 256 || bn == 128) && mb >= 4 &&
+           static_cast<int64_t>((mb + 1) / 2) * ((N + bn - 1) / bn) >= sms / 2 && !std::getenv("PRLAB_NO_PAIR");
+  if (force_lean < -1) p.pair = false;  // tuning: -2 forces the 1-CTA kernel
+  if (force_lean > 1) p.pair = (bn == 256 || bn == 128);  // tuning: 2 forces the pair kernel
   p.M = M;
   p.N = N;
   p.K = K;
@@ -876,7 +1175,6 @@ GemmPlan plan_gemm_tc(const void* A, int64_t lda, const void* Wt, int64_t ldw, c
     p.tickets = scratch->tickets;
   }
   p.tmA = make_tmap_f16_2d(A, M, K, lda, BM, BK);
-  p.tmB = make_tmap_f16_2d(Wt, N, K, ldw, bn, BK);
   // TMA-store epilogue when the output rows are 16-byte aligned (TMA clips the M/N tails)
   const bool f32out = epi == EPI_BIAS_RESID_F32;
   const int64_t row_bytes = ldo * (f32out ? 4 : 2);
@@ -886,6 +1184,16 @@ GemmPlan plan_gemm_tc(const void* A, int64_t lda, const void* Wt, int64_t ldw, c
     p.tmC = f32out ? make_tmap_f32_2d(out, M, N, ldo, 32, 32) : make_tmap_f16_2d(out, M, N, ldo, 32, 64);
   const int units = tiles * p.splits;
   p.grid = p.cluster ? units : (units < sms ? units : sms);
+  if (p.pair) {
+    if (!p.tma_store) p.pair = false;  // the pair kernel only has the TMA-store epilogue
+  }
+  if (p.pair) {
+    const int pair_units = ((mb + 1) / 2) * ((N + bn - 1) / bn);
+    p.grid = 2 * std::min(pair_units, sms / 2);
+    p.tmB = make_tmap_f16_2d(Wt, N, K, ldw, bn / 2, BK);
+  } else {
+    p.tmB = make_tmap_f16_2d(Wt, N, K, ldw, bn, BK);
+  }
   return p;
 }
 
@@ -900,6 +1208,8 @@ void configure_gemm_tc() {
   configure_bn<64, true>();
   configure_cluster_bn<64>();
   configure_cluster_bn<128>();
+  configure_pair_bn<128>();
+  configure_pair_bn<256>();
   done = true;
 }
 
@@ -922,6 +1232,13 @@ void launch_gemm_tc(const GemmPlan& p, cudaStream_t st) {
   g.tickets = p.tickets;
   g.tma_store = p.tma_store ? 1 : 0;
   g.dbg = debug_stamps();
+  if (p.pair) {
+    if (p.bn == 256)
+      launch_pair_bn<256>(p, g, st);
+    else
+      launch_pair_bn<128>(p, g, st);
+    return;
+  }
   if (p.cluster) {
     if (p.bn == 64)
       launch_cluster_bn<64>(p, g, st);

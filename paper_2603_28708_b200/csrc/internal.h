@@ -72,6 +72,7 @@ struct GemmPlan {
   int splits, kb_per_split;
   bool lean;
   bool cluster;  // split-K reduced through DSMEM inside a thread-block cluster
+  bool pair;     // CTA-pair (cta_group::2) kernel, 256-row tiles
   const float* bias;
   void* out;
   int64_t ldo;

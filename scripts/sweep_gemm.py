@@ -66,7 +66,7 @@ def main():
                 cfgs = [(0, 0, 0)] + [(bn, sp, ln) for bn, sp, ln in
                                       itertools.product([64, 128], [1, 2, 3, 4, 6, 8, -3], [1, -1])]
             else:
-                cfgs = [(0, 0, 0)] + [(bn, 1, -1) for bn in (64, 128, 256)]
+                cfgs = [(0, 0, 0)] + [(bn, 1, ln) for bn in (128, 256) for ln in (-2, 2)]
             for bn, sp, ln in cfgs:
                 if name == "head" and sp not in (0, 1):
                     continue

@@ -233,3 +233,30 @@ def test_tc_linear_forced_configs(bn, splits, lean, epi):
     pg.linear_f16_device_ex(A, Wt, bias, out2, M, N, K, N, epi, bn, splits, lean)
     torch.cuda.synchronize()
     assert torch.equal(out2, out) if epi != 2 else True
+
+
+@pytest.mark.parametrize("M", [512, 640, 1000])
+@pytest.mark.parametrize("bn", [128, 256])
+@pytest.mark.parametrize("epi", [0, 1, 2, 3])
+def test_tc_linear_cta_pair(M, bn, epi):
+    """The cta_group::2 kernel (256-row tiles over a CTA pair), incl. an odd number of
+    128-row blocks (the pair's second CTA runs entirely out of bounds) and M tails."""
+    N, K = 768 + 256, 768
+    g = torch.Generator(device="cuda").manual_seed(M + bn + epi)
+    A = (torch.randn(M, K, device="cuda", generator=g) * 0.5).half()
+    Wt = (torch.randn(N, K, device="cuda", generator=g) * 0.05).half()
+    bias = r16(torch.randn(N, device="cuda", generator=g) * 0.1)
+    if epi == 2:
+        out = torch.randn(M, N, device="cuda", generator=g)
+        resid = out.clone()
+    else:
+        out = torch.full((M, N), float("nan"), device="cuda", dtype=torch.float16)
+        resid = None
+    pg.linear_f16_device_ex(A, Wt, bias if epi != 3 else None, out, M, N, K, N, epi, bn, 1, 2)
+    torch.cuda.synchronize()
+    ref = _gemm_ref(A, Wt, bias, epi, resid)
+    got = out.float()
+    assert torch.isfinite(got).all()
+    err = (got - ref).abs()
+    tol = torch.clamp(ref.abs(), min=6.1e-5) * 2.0 ** -10 * 1.01 + 1e-6
+    assert (err > tol).float().mean().item() < 3e-3, err.max().item()
