@@ -34,6 +34,95 @@ __device__ __forceinline__ float gelu_erf(float v) {
 }
 
 // ---------------------------------------------------------------------------
+// Packed pair arithmetic (sm_100: FFMA2 / FMUL2 / FADD2 on .f32x2, HADD2 on f16x2).
+// A pair is two fp32 lanes in one 64-bit register; every op rounds each lane RN,
+// exactly as the scalar op would.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint64_t f2_pack(float lo, float hi) {
+  uint64_t r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+__device__ __forceinline__ void f2_unpack(uint64_t v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+__device__ __forceinline__ uint64_t f2_fma(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_mul(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+__device__ __forceinline__ uint64_t f2_add(uint64_t a, uint64_t b) {
+  uint64_t d;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(a), "l"(b));
+  return d;
+}
+// (round16(lo), round16(hi)) packed as f16x2 (lo in the low half)
+__device__ __forceinline__ uint32_t h2_pack_rn(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+// binary16 RNE add of two f16x2 words: equals round16(fp32(a) + fp32(b)) lane-wise for
+// every pair of binary16 inputs (24 >= 2*11+2, so the fp32 sum rounded again to
+// binary16 is the correctly rounded binary16 sum -- SURVEY App. C.2).
+__device__ __forceinline__ uint32_t h2_add_rn(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("add.rn.f16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+__device__ __forceinline__ void h2_unpack(uint32_t v, float& lo, float& hi) {
+  const __half2 h = *reinterpret_cast<const __half2*>(&v);
+  lo = __low2float(h);
+  hi = __high2float(h);
+}
+
+// GELU of two binary16-lattice values in the reference's expression order
+// 0.5f * v * (1.0f + erf(v * 0.70710678f)) (src/kernels.cpp:221-235), with erf
+// evaluated branch-free on the FMA pipe as sign(u) * (1 - erfc|u|),
+// erfc(t) = 2^(-t^2 log2 e + P(t)) for t = min(|u|, 4.5) and P a degree-12 fit of
+// log2(erfc(t) e^(t^2)) (abs. error 4e-7 in the exponent).  The 1 + erf sum and the
+// products are the reference's fp32 operations, so the result differs from the
+// correctly rounded reference formula only where erf's last fp32 bit flips the fp16
+// rounding of the output (5 of the 63 488 finite binary16 inputs in a double-precision
+// emulation; scripts/gelu_fit.py).  ~14 issue slots per element instead of ~30.
+__device__ __forceinline__ void gelu2_fast(float& x0, float& x1) {
+  const uint64_t x = f2_pack(x0, x1);
+  const uint64_t u = f2_mul(x, f2_pack(0.70710678118654752440f, 0.70710678118654752440f));
+  float u0, u1;
+  f2_unpack(u, u0, u1);
+  const uint64_t t = f2_pack(fminf(fabsf(u0), 4.5f), fminf(fabsf(u1), 4.5f));
+  const uint64_t xc = f2_fma(t, f2_pack(2.0f / 4.5f, 2.0f / 4.5f), f2_pack(-1.0f, -1.0f));
+  auto C = [](float c) { return f2_pack(c, c); };
+  uint64_t p = C(-2.227836521e-04f);
+  p = f2_fma(p, xc, C(5.317298928e-04f));
+  p = f2_fma(p, xc, C(-2.733187575e-04f));
+  p = f2_fma(p, xc, C(-4.225545854e-04f));
+  p = f2_fma(p, xc, C(1.940271002e-03f));
+  p = f2_fma(p, xc, C(-6.848694291e-03f));
+  p = f2_fma(p, xc, C(1.920940541e-02f));
+  p = f2_fma(p, xc, C(-4.619692266e-02f));
+  p = f2_fma(p, xc, C(1.024701148e-01f));
+  p = f2_fma(p, xc, C(-2.187634408e-01f));
+  p = f2_fma(p, xc, C(4.757040143e-01f));
+  p = f2_fma(p, xc, C(-1.242962837e+00f));
+  p = f2_fma(p, xc, C(-2.113490343e+00f));
+  const uint64_t e = f2_fma(f2_mul(t, t), C(-1.4426950408889634f), p);
+  float e0, e1;
+  f2_unpack(e, e0, e1);
+  const uint64_t q = f2_pack(ex2_approx(e0), ex2_approx(e1));  // erfc(|u|)
+  float a0, a1;
+  f2_unpack(f2_fma(q, C(-1.0f), C(1.0f)), a0, a1);  // erf|u| = 1 - erfc|u|
+  const uint64_t erf2 = f2_pack(copysignf(a0, u0), copysignf(a1, u1));
+  const uint64_t g = f2_mul(f2_mul(C(0.5f), x), f2_add(C(1.0f), erf2));
+  f2_unpack(g, x0, x1);
+}
+
+// ---------------------------------------------------------------------------
 // shared-memory / mbarrier
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {

@@ -41,6 +41,7 @@ struct GemmArgs {
   float* ws;      // split-K partials [tile*splits + split][BM][BN]
   int* tickets;   // per-tile arrival counters (left at zero after every launch)
   int tma_store;  // epilogue through smem staging + TMA store / reduce-add
+  int group_m;    // raster band height in m-blocks (A band kept L2-resident)
   long long* dbg; // optional per-CTA %globaltimer stamps [grid][8] (debug), null = off
 };
 
@@ -69,6 +70,33 @@ struct Cfg {
   static constexpr size_t SMEM = 1024 + BIAS_OFF + BIAS_BYTES;
 };
 
+// Pairs go through the packed pipes: cvt.rn.f16x2 (= round16 of both lanes), then the
+// bias add as a binary16 RNE add (= round16(round16(acc) + b) since b is on the lattice).
+template <int EPI>
+__device__ __forceinline__ uint32_t epilogue_pair(float a0, float a1, float b0, float b1) {
+  uint32_t h = h2_pack_rn(a0, a1);
+  if (EPI != EPI_F16) {
+    h = h2_add_rn(h, h2_pack_rn(b0, b1));  // exact repack: biases are pre-rounded (0 when absent)
+    if (EPI == EPI_BIAS_GELU_F16) {
+      float x0, x1;
+      h2_unpack(h, x0, x1);
+      gelu2_fast(x0, x1);
+      h = h2_pack_rn(x0, x1);
+    }
+  }
+  return h;
+}
+template <int EPI>
+__device__ __forceinline__ uint32_t epilogue_pair(float a0, float a1, const float* sbias, int i) {
+  float b0 = 0.0f, b1 = 0.0f;
+  if (EPI != EPI_F16 && sbias != nullptr) {
+    const float2 b = *reinterpret_cast<const float2*>(sbias + i);
+    b0 = b.x;
+    b1 = b.y;
+  }
+  return epilogue_pair<EPI>(a0, a1, b0, b1);
+}
+
 // sbias: the 32 (pre-rounded) bias values of columns col0..col0+31 in shared memory, or null.
 template <int EPI>
 __device__ __forceinline__ void epilogue_chunk(const float (&acc)[32], const GemmArgs& g, int row,
@@ -76,20 +104,9 @@ __device__ __forceinline__ void epilogue_chunk(const float (&acc)[32], const Gem
   if (row >= g.M) return;
   const bool full = col0 + 32 <= g.N;
   float v[32];
-  float bias[32];
-  if (EPI != EPI_F16) {
 #pragma unroll
-    for (int i = 0; i < 32; ++i) bias[i] = sbias != nullptr ? sbias[i] : 0.0f;
-  }
-#pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    float a = r16(acc[i]);  // round16(fp32 acc): matmul output lattice
-    if (EPI != EPI_F16) {
-      a = r16(__fadd_rn(a, bias[i]));  // conform(row + conform(b)), bias stored pre-rounded
-      if (EPI == EPI_BIAS_GELU_F16) a = r16(gelu_erf(a));
-    }
-    v[i] = a;
-  }
+  for (int i = 0; i < 16; ++i)  // round16(acc) [+ conform(b), round16] [GELU, round16]
+    h2_unpack(epilogue_pair<EPI>(acc[2 * i], acc[2 * i + 1], sbias, 2 * i), v[2 * i], v[2 * i + 1]);
   if (EPI == EPI_BIAS_RESID_F32) {
     float* o = reinterpret_cast<float*>(g.out) + static_cast<int64_t>(row) * g.ldo + col0;
     if (full && (g.ldo % 4) == 0) {
@@ -129,7 +146,7 @@ __device__ __forceinline__ void epilogue_chunk(const float (&acc)[32], const Gem
 // advance slowest, so the CTAs resident at any moment share one band of A
 // (<= 2048 rows) and a few weight tiles -- both stay in L2 (A is read from DRAM once).
 __device__ __forceinline__ void tile_coords(const GemmArgs& g, int tile, int& m_blk, int& n_blk) {
-  constexpr int GROUP_M = 16;
+  const int GROUP_M = g.group_m;
   const int band = tile / (GROUP_M * g.num_n_blocks);
   const int m0 = band * GROUP_M;
   const int rows = min(GROUP_M, g.num_m_blocks - m0);
@@ -141,17 +158,20 @@ __device__ __forceinline__ void tile_coords(const GemmArgs& g, int tile, int& m_
 // The Linear-class epilogue numerics on one 32-column chunk of fp32 accumulators:
 // round16(acc) [+ round16(b), round16] [GELU, round16]  (kernels.cpp:78, model.cpp:73,
 // kernels.cpp:232).  The residual add itself happens in the store path.
+// fp16 outputs: 16 packed f16x2 words
+template <int EPI>
+__device__ __forceinline__ void epilogue_packed(const uint32_t (&u)[32], const float* sbias, uint32_t (&pk)[16]) {
+#pragma unroll
+  for (int i = 0; i < 16; ++i)
+    pk[i] = epilogue_pair<EPI>(__uint_as_float(u[2 * i]), __uint_as_float(u[2 * i + 1]), sbias, 2 * i);
+}
+
 template <int EPI>
 __device__ __forceinline__ void epilogue_values(const uint32_t (&u)[32], const float* sbias, float (&v)[32]) {
 #pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    float a = r16(__uint_as_float(u[i]));
-    if (EPI != EPI_F16) {
-      a = r16(__fadd_rn(a, sbias != nullptr ? sbias[i] : 0.0f));
-      if (EPI == EPI_BIAS_GELU_F16) a = r16(gelu_erf(a));
-    }
-    v[i] = a;
-  }
+  for (int i = 0; i < 16; ++i)
+    h2_unpack(epilogue_pair<EPI>(__uint_as_float(u[2 * i]), __uint_as_float(u[2 * i + 1]), sbias, 2 * i),
+              v[2 * i], v[2 * i + 1]);
 }
 
 __device__ __forceinline__ void unit_range(const GemmArgs& g, int unit, int& tile, int& split,
@@ -316,20 +336,17 @@ __global__ void __launch_bounds__(Cfg<BN, LEAN, EPI>::THREADS, 1)
             uint32_t u[32];
             tmem_ld32(tmem_base + ((quad * 32) << 16) + acc * BN + c + h, u);
             tmem_wait_ld();
-            float v[32];
-            epilogue_values<EPI>(u, has_bias ? sbias + (c - cbase) + h : nullptr, v);
+            const float* sb = has_bias ? sbias + (c - cbase) + h : nullptr;
             if (F32OUT) {
+              float v[32];
+              epilogue_values<EPI>(u, sb, v);
 #pragma unroll
               for (int j = 0; j < 8; ++j)
                 *reinterpret_cast<float4*>(rowp + ((j ^ (lane & 7)) * 16)) =
                     make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
             } else {
               uint32_t pk[16];
-#pragma unroll
-              for (int i = 0; i < 16; ++i) {
-                __half2 h2 = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
-                pk[i] = *reinterpret_cast<uint32_t*>(&h2);
-              }
+              epilogue_packed<EPI>(u, sb, pk);
 #pragma unroll
               for (int j = 0; j < 4; ++j)
                 *reinterpret_cast<uint4*>(rowp + ((((h >> 3) + j) ^ (lane & 7)) * 16)) =
@@ -464,16 +481,12 @@ __device__ __forceinline__ void epilogue_vec4(float4 a, const GemmArgs& g, int r
   if (row >= g.M || col >= g.N) return;
   float v[4] = {a.x, a.y, a.z, a.w};
   const bool full = col + 4 <= g.N;
+  float bb[4];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    float x = r16(v[i]);
-    if (EPI != EPI_F16) {
-      const float b = (g.bias != nullptr && col + i < g.N) ? __ldg(g.bias + col + i) : 0.0f;
-      x = r16(__fadd_rn(x, b));
-      if (EPI == EPI_BIAS_GELU_F16) x = r16(gelu_erf(x));
-    }
-    v[i] = x;
-  }
+  for (int i = 0; i < 4; ++i) bb[i] = (g.bias != nullptr && col + i < g.N) ? __ldg(g.bias + col + i) : 0.0f;
+#pragma unroll
+  for (int i = 0; i < 4; i += 2)
+    h2_unpack(epilogue_pair<EPI>(v[i], v[i + 1], bb[i], bb[i + 1]), v[i], v[i + 1]);
   if (EPI == EPI_BIAS_RESID_F32) {
     float* o = reinterpret_cast<float*>(g.out) + static_cast<int64_t>(row) * g.ldo + col;
     if (full && (g.ldo % 4) == 0) {
@@ -504,14 +517,8 @@ __device__ __forceinline__ void epilogue_vec4_fast(float4 a, float4 b, float4 x,
   float v[4] = {a.x, a.y, a.z, a.w};
   const float bb[4] = {b.x, b.y, b.z, b.w};
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    float t = r16(v[i]);
-    if (EPI != EPI_F16) {
-      t = r16(__fadd_rn(t, bb[i]));
-      if (EPI == EPI_BIAS_GELU_F16) t = r16(gelu_erf(t));
-    }
-    v[i] = t;
-  }
+  for (int i = 0; i < 4; i += 2)
+    h2_unpack(epilogue_pair<EPI>(v[i], v[i + 1], bb[i], bb[i + 1]), v[i], v[i + 1]);
   if (EPI == EPI_BIAS_RESID_F32) {
     float* o = reinterpret_cast<float*>(g.out) + static_cast<int64_t>(row) * g.ldo + col;
     *reinterpret_cast<float4*>(o) =
@@ -850,8 +857,8 @@ __global__ void __launch_bounds__(Cfg2<BN, EPI>::THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   auto coords = [&](int unit, int& mp, int& n_blk) {
-    // bands of 8 m-pairs (16 m-blocks); n-blocks advance slowest inside a band
-    constexpr int GROUP = 8;
+    // bands of group_m/2 m-pairs; n-blocks advance slowest inside a band
+    const int GROUP = g.group_m >> 1;
     const int band = unit / (GROUP * g.num_n_blocks);
     const int m0 = band * GROUP;
     const int rows = min(GROUP, m_pairs - m0);
@@ -970,20 +977,17 @@ __global__ void __launch_bounds__(Cfg2<BN, EPI>::THREADS, 1)
           uint32_t u[32];
           tmem_ld32(tmem_base + ((quad * 32) << 16) + acc * BN + c + h, u);
           tmem_wait_ld();
-          float v[32];
-          epilogue_values<EPI>(u, has_bias ? sbias + (c - cbase) + h : nullptr, v);
+          const float* sb = has_bias ? sbias + (c - cbase) + h : nullptr;
           if (F32OUT) {
+            float v[32];
+            epilogue_values<EPI>(u, sb, v);
 #pragma unroll
             for (int j = 0; j < 8; ++j)
               *reinterpret_cast<float4*>(rowp + ((j ^ (lane & 7)) * 16)) =
                   make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
           } else {
             uint32_t pk[16];
-#pragma unroll
-            for (int i = 0; i < 16; ++i) {
-              __half2 h2 = __floats2half2_rn(v[2 * i], v[2 * i + 1]);
-              pk[i] = *reinterpret_cast<uint32_t*>(&h2);
-            }
+            epilogue_packed<EPI>(u, sb, pk);
 #pragma unroll
             for (int j = 0; j < 4; ++j)
               *reinterpret_cast<uint4*>(rowp + ((((h >> 3) + j) ^ (lane & 7)) * 16)) =
@@ -1156,6 +1160,19 @@ GemmPlan plan_gemm_tc(const void* A, int64_t lda, const void* Wt, int64_t ldw, c
            static_cast<int64_t>((mb + 1) / 2) * ((N + bn - 1) / bn) >= sms / 2 && !std::getenv("PRLAB_NO_PAIR");
   if (force_lean < -1) p.pair = false;  // tuning: -2 forces the 1-CTA kernel
   if (force_lean > 1) p.pair = (bn == 256 || bn == 128);  // tuning: 2 forces the pair kernel
+  // Raster band: inside a band the n-blocks advance slowest, so the band's rows of A
+  // are re-read from L2 once per n-block and each weight tile is fetched once per band.
+  // When all of A fits comfortably in L2 (e.g. the LM head: A 25 MB, E 77 MB at C4)
+  // one band covers every m-block and the weights stream from DRAM exactly once;
+  // otherwise bands of 16 m-blocks (2048 rows).
+  {
+    const int64_t a_bytes = static_cast<int64_t>(M) * K * 2;
+    const int64_t w_bytes = static_cast<int64_t>(N) * K * 2;
+    int grp = 16;
+    if (a_bytes <= (48ll << 20) && w_bytes > a_bytes) grp = mb;
+    grp = std::max(2, (grp + 1) / 2 * 2);  // the pair kernel bands by m-pairs
+    p.group_m = grp;
+  }
   p.M = M;
   p.N = N;
   p.K = K;
@@ -1231,6 +1248,7 @@ void launch_gemm_tc(const GemmPlan& p, cudaStream_t st) {
   g.ws = p.ws;
   g.tickets = p.tickets;
   g.tma_store = p.tma_store ? 1 : 0;
+  g.group_m = p.group_m;
   g.dbg = debug_stamps();
   if (p.pair) {
     if (p.bn == 256)

@@ -79,6 +79,7 @@ struct GemmPlan {
   float* ws;
   int* tickets;
   int grid;
+  int group_m;  // raster band height (m-blocks)
 };
 // Split-K scratch: fp32 partial tiles + per-tile tickets (zero between launches).
 // One per model: kernels of one forward run in stream order, so they share it.
