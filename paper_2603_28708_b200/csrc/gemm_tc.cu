@@ -42,6 +42,7 @@ struct GemmArgs {
   int* tickets;   // per-tile arrival counters (left at zero after every launch)
   int tma_store;  // epilogue through smem staging + TMA store / reduce-add
   int group_m;    // raster band height in m-blocks (A band kept L2-resident)
+  int dbg_noload; // debug: after the first fill, skip the TMA loads (MMA/epilogue pacing probe)
   long long* dbg; // optional per-CTA %globaltimer stamps [grid][8] (debug), null = off
 };
 
@@ -890,6 +891,16 @@ __global__ void __launch_bounds__(Cfg2<BN, EPI>::THREADS, 1)
         for (int kb = 0; kb < g.num_k_blocks; ++kb) {
           if (first && kb < pre) {
             tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
+          } else if (g.dbg_noload) {  // debug probe: 3 = no operand loads, 1 = no A, 2 = no B
+            mbar_wait(&empty[stage], phase ^ 1);
+            const uint32_t bytes = ((g.dbg_noload & 1) ? 0u : C::A_BYTES) + ((g.dbg_noload & 2) ? 0u : C::B_BYTES);
+            if (leader) {
+              if (bytes) mbar_expect_tx(&full[stage], 2 * bytes);
+              else mbar_arrive(&full[stage]);
+            }
+            if (!(g.dbg_noload & 1)) tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
+            if (!(g.dbg_noload & 2))
+              tma_load_2d_pair(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, n_blk * BN + rank * (BN / 2));
           } else {
             mbar_wait(&empty[stage], phase ^ 1);
             if (leader) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
@@ -1249,6 +1260,7 @@ void launch_gemm_tc(const GemmPlan& p, cudaStream_t st) {
   g.tickets = p.tickets;
   g.tma_store = p.tma_store ? 1 : 0;
   g.group_m = p.group_m;
+  g.dbg_noload = std::getenv("PRLAB_DBG_GEMM_NOLOAD") ? std::atoi(std::getenv("PRLAB_DBG_GEMM_NOLOAD")) : 0;
   g.dbg = debug_stamps();
   if (p.pair) {
     if (p.bn == 256)
