@@ -81,6 +81,34 @@ __device__ __forceinline__ void h2_unpack(uint32_t v, float& lo, float& hi) {
   hi = __high2float(h);
 }
 
+// 2^x for a pair on the FMA pipe (offloads the SFU in the softmax): x clamped to
+// [-125, 0] (the callers' exponents are <= 0; below -125 the result is < 2^-125,
+// which is 0 after any fp16 rounding and negligible in an fp32 row sum),
+// n = rint(x) by the 1.5*2^23 trick, 2^f on [-0.5, 0.5] by a degree-5 minimax
+// polynomial (rel. error 3.5e-7, ex2.approx is ~2^-22), exponent added as an integer.
+__device__ __forceinline__ uint64_t exp2_pair_poly(float x0, float x1) {
+  const uint64_t x = f2_pack(fmaxf(x0, -125.0f), fmaxf(x1, -125.0f));
+  const uint64_t M = f2_pack(12582912.0f, 12582912.0f);
+  const uint64_t j = f2_add(x, M);
+  const uint64_t nM = f2_pack(-12582912.0f, -12582912.0f);
+  const uint64_t n = f2_add(j, nM);
+  float n0, n1;
+  f2_unpack(n, n0, n1);
+  const uint64_t f = f2_add(x, f2_pack(-n0, -n1));
+  auto C = [](float c) { return f2_pack(c, c); };
+  uint64_t p = C(1.339528011e-03f);
+  p = f2_fma(p, f, C(9.670763277e-03f));
+  p = f2_fma(p, f, C(5.550340563e-02f));
+  p = f2_fma(p, f, C(2.402221113e-01f));
+  p = f2_fma(p, f, C(6.931471825e-01f));
+  p = f2_fma(p, f, C(1.0f));
+  float p0, p1, j0, j1;
+  f2_unpack(p, p0, p1);
+  f2_unpack(j, j0, j1);
+  return f2_pack(__uint_as_float(__float_as_uint(p0) + (__float_as_uint(j0) << 23)),
+                 __uint_as_float(__float_as_uint(p1) + (__float_as_uint(j1) << 23)));
+}
+
 // GELU of two binary16-lattice values in the reference's expression order
 // 0.5f * v * (1.0f + erf(v * 0.70710678f)) (src/kernels.cpp:221-235), with erf
 // evaluated branch-free on the FMA pipe as sign(u) * (1 - erfc|u|),
@@ -283,6 +311,15 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
         "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
         "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
         "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, "
+      "%12, %13, %14, %15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+        "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+        "=r"(r[14]), "=r"(r[15])
       : "r"(taddr));
 }
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {

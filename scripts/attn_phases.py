@@ -11,13 +11,13 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2603_28708_b200 as pg  # noqa: E402
 
-PH = ["s_wait", "pass1", "pass2", "pass3", "o_wait", "epi"]
+PH = ["s_wait+pass1", "pass2", "sum_bar", "pass3", "o_wait", "epilogue"]
 
 
 def run(B, S, causal, H=12, hd=64):
     qkv = (torch.randn(B * S, 3 * H * hd, device="cuda") * 1.5).half()
     ctx = torch.empty(B * S, H * hd, device="cuda", dtype=torch.float16)
-    dbg = torch.zeros(max(B * H, 148), 128, dtype=torch.int64, device="cuda")
+    dbg = torch.zeros(max(B * H, 148), 256, dtype=torch.int64, device="cuda")
     for _ in range(3):
         pg.attention_f16_device(qkv, ctx, B, S, H, hd, causal)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -44,9 +44,21 @@ def run(B, S, causal, H=12, hd=64):
         if st[0] == 0:
             break
         ph = {PH[i]: int(st[i + 1] - st[i]) for i in range(6)}
-        ph["mma_q_ready_rel"] = int(st[7] - st[0])
+        if t > 0:
+            ph["since_prev_tile"] = int(st[0] - c0[8 + (t - 1) * 8])
+        ms = c0[8 + 14 * 8 + t * 4: 8 + 14 * 8 + t * 4 + 4]
+        if ms[0] > 0:  # MMA thread, relative to the softmax tile start
+            ph["mma_qk_begin"] = int(ms[0] - st[0])
+            ph["mma_qk_issued"] = int(ms[1] - st[0])
+            ph["mma_pv_first"] = int(ms[2] - st[0])
+            ph["mma_pv_last"] = int(ms[3] - st[0])
+            ph["softmax_pass3_end"] = int(st[4] - st[0])
         tiles.append(ph)
     out["cta0_tiles"] = tiles
+    t1 = c0[8 + 8]
+    if t1 > 0:
+        out["t1_pass3_end_per_warp"] = [int(c0[200 + w] - t1) for w in range(16)]
+        out["t1_pv_issue"] = [int(c0[224 + q] - t1) for q in range(4)]
     print(json.dumps(out), flush=True)
 
 
