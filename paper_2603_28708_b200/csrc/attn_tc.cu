@@ -7,36 +7,32 @@
 //   o_i  = round16( fp32dot(round16(p_i), v) )            AttentionScoreMatmul {F16E, F32}
 // The whole score row is resident (S <= 512 -> 128 x 512 fp32 = all of TMEM), so
 // the softmax is the reference's exact two-pass form (max, then exp/sum, then
-// normalise-then-round), not an online rescaling; e is computed once and kept.
+// normalise-then-round), not an online rescaling.
 //
 // Persistent CTAs (one per SM): CTA c owns the (batch, head) items c, c + grid, ...
 // and runs every 128-query tile of an item back to back (last tile first), so K and
-// V of the item are loaded into shared memory once; Q is double-buffered so the next
-// tile's Q (and the next item's K / V) stream in under the current softmax.
-// Warp roles (576 threads):
+// V of the item are loaded into shared memory once and Q is double-buffered: the
+// next tile's Q -- and, across items, the next item's K (after the last Q.K^T) and V
+// (after the last P.V) -- stream in under the current tile's softmax.
+// Warp roles:
 //   warp 0       TMA producer (Q ring of 2, K[4], V[4])
 //   warp 1       TMEM owner + tcgen05.mma issuer: S = Q.K^T one 128-key block at a
-//                time (s_full[kb]), then O = P.V one block at a time as soon as that
-//                block's P exists (p_full[kb]), P read straight from TMEM
-//   warps 2..17  softmax + epilogue.  Warp (quad q = warp & 3, group g) owns rows
-//                32q..32q+31 (its TMEM lane quadrant) and keys 32g..32g+31 of every
-//                128-key block, so all 16 warps work on every block in block order
-//                for any causal block count:
-//     pass 1  per block as its S lands: row max of the raw accumulators (FMNMX3;
-//             round16(x*0.125) is monotone, so the max is rounded once at the end)
-//     pass 2  e = 2^(s*log2e - max*log2e), s = round16(acc*0.125) (FMUL2, cvt.f16x2,
-//             FFMA2, SFU), stored back over S (fp32), row sums (FADD2); the next
-//             block's TMEM load is in flight while a block computes
-//     pass 3  per block: p = round16(e * (1/sum)) packed 2 x fp16 per column into the
-//             first half of the block's columns (after the 4 warps of the quadrant
-//             have read the block), then p_full[kb]: the block's P.V MMAs overlap
-//             the next block's pass 3
-//   Key chunks wholly above the causal diagonal or past the sequence end skip the
-//   arithmetic (P = 0); only chunks crossing them mask per element.
-// TMEM columns: S / e block kb at [128kb, 128kb+128); P_kb packed in [128kb, 128kb+64);
-// O (128 x 64 fp32) in [64, 128) once P_0 is written.
-#include <cstdlib>
-
+//                time (s_full[kb] per block, so the softmax starts on block 0 while
+//                later blocks multiply), then O = P.V with P read from TMEM
+//   warps 2..17  softmax + epilogue: 4 warps per TMEM lane quadrant.
+//     pass 1  row max of the raw accumulators (3-input FMNMX; round16(x*0.125) is
+//             monotone, so the max is rounded once at the end)
+//     pass 2  s = round16(acc*0.125) (FMUL2 + cvt.f16x2), e = 2^(s*log2e - max*log2e)
+//             (FFMA2 + SFU), stored back over S (fp32), partial sums (FADD2)
+//     pass 3  p = round16(e * (1/sum)) packed 2 x fp16 per TMEM column over the
+//             already-consumed part of S -> the A operand of the P.V MMA
+//   Chunks of 32 keys wholly above the causal diagonal or past the sequence end skip
+//   passes 1-2 and store P = 0; only chunks crossing the diagonal test per element.
+//
+// TMEM columns: S block kb at [128kb, 128kb+128).  "wide" mode (>= 3 key blocks):
+// column group g owns key block g and writes P_g into [128g, 128g+64); O lives in
+// [64, 128).  "narrow" mode (<= 2 key blocks): group g owns 32*nkb contiguous keys,
+// P goes to [256, 256 + 64*nkb), O to [384, 448).
 #include "common.cuh"
 #include "internal.h"
 
@@ -48,16 +44,13 @@ constexpr int kSoftmaxWarps = 16;
 constexpr int kThreads = 64 + kSoftmaxWarps * 32;  // 576
 constexpr int kMaxKB = 4;                          // S <= 512
 constexpr uint32_t kTile = 128 * 64 * 2;           // one 128 x 64 fp16 tile, 16 KB
-// kPolyPairs (template): pairs (of the 8 per 16-key unit) whose exponentials run on
-// the FMA pipe instead of the SFU -- balances the 16/clk/SM SFU against issue slots.
-constexpr uint32_t kPolyDefault = 0x22;
 
 struct AttnArgs {
   int B, S, H, hd, causal, nqt;
   int h;  // hidden = H * hd (column offset of K; V at 2h)
   __half* ctx;
   int64_t ld_ctx;
-  long long* dbg;  // optional per-CTA stamps [grid][256] (clock64), null = off
+  long long* dbg;  // optional per-CTA stamps [grid][128] (clock64), null = off
 };
 
 struct Smem {
@@ -76,14 +69,13 @@ enum : int {
   B_QEMPTY = 2,   // [2]
   B_KFULL = 4,    // [4]
   B_VFULL = 8,    // [4]
-  B_SFULL = 12,   // [4] S block kb in TMEM
-  B_PFULL = 16,   // [4] P block kb in TMEM (16 softmax warps)
-  B_PVDONE = 20,  // [4] the P.V MMAs of block kb completed (TMEM block reusable)
-  B_KEMPTY = 24,
-  B_VEMPTY = 25,
-  B_OFULL = 26,
-  B_OFREE = 27,   // 16 softmax warps: O of the tile read into registers
-  B_COUNT = 28
+  B_SFULL = 12,   // [4]
+  B_KEMPTY = 16,
+  B_VEMPTY = 17,
+  B_PREADY = 18,  // 16 softmax warps
+  B_OFULL = 19,
+  B_TFREE = 20,   // 16 softmax warps: TMEM of the tile consumed
+  B_COUNT = 21
 };
 
 // D[tmem] (+)= A[tmem] * B[smem], kind::f16
@@ -97,14 +89,6 @@ __device__ __forceinline__ void umma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, ui
       : "memory");
 }
 
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
-      "%11, %12, %13, %14, %15, %16};" ::"r"(taddr),
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
-      "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
-      : "memory");
-}
 
 __device__ __forceinline__ float fmax3(float a, float b, float c) {
   float d;
@@ -119,7 +103,6 @@ __device__ __forceinline__ int nkb_of(const AttnArgs& a, int qt) {
   return a.causal ? min(qt + 1, nkb_all) : nkb_all;
 }
 
-template <uint32_t kPolyPairs>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm, const AttnArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -133,13 +116,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   const int items = a.B * a.H;
   const int nkb_all = (a.S + 127) / 128;
   const uint32_t warp = warp_id(), lane = lane_id();
-  long long* dbg = a.dbg ? a.dbg + static_cast<int64_t>(blockIdx.x) * 256 : nullptr;
+  long long* dbg = a.dbg ? a.dbg + static_cast<int64_t>(blockIdx.x) * 128 : nullptr;
   if (dbg && threadIdx.x == 0) dbg[0] = clock64();
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm);
     for (int i = 0; i < B_COUNT; ++i)
-      mbar_init(&bars[i], ((i >= B_PFULL && i < B_PFULL + 4) || i == B_OFREE) ? kSoftmaxWarps : 1);
+      mbar_init(&bars[i], (i == B_PREADY || i == B_TFREE) ? kSoftmaxWarps : 1);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -186,28 +169,21 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       constexpr uint32_t idesc_s = idesc_f16_f32(128, 128, 0, 0);
       constexpr uint32_t idesc_o = idesc_f16_f32(128, 64, 0, 1);
-      // parity bits per barrier of a block ring: p_full[kb] and pv_done[kb]
-      uint32_t pph = 0, dph = 0, t = 0, it = 0;
-      int nkb_prev = 0;  // previous tile: its P blocks and (in its last block) its O
+      uint32_t t = 0, it = 0;
       for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
         for (int j = 0; j < a.nqt; ++j, ++t) {
-          const int nkb = nkb_of(a, tile_of(a, j));
-          const int L = nkb - 1;  // O of this tile lives in the upper half of block L
+          const int qt = tile_of(a, j);
+          const int nkb = nkb_of(a, qt);
+          const bool wide = nkb > 2;
+          const uint32_t o_col = wide ? 64u : 384u;
           const uint32_t qb = t & 1;
+          if (t > 0) mbar_wait(&bars[B_TFREE], (t - 1) & 1);  // previous tile's TMEM consumed
           mbar_wait(&bars[B_QFULL + qb], (t >> 1) & 1);
           tc_fence_after();
+          if (dbg && t < 14) dbg[8 + t * 8 + 7] = clock64();
           const uint32_t q0 = smem_u32(smem + Smem::Q + qb * kTile);
-          // ---- S = Q . K^T : M=128 queries, N=128 keys per block, K = 64 (4 x 16).
-          // Block kb's columns are reusable once the previous tile's P.V of that block
-          // finished and, for the block that held its O, once O was read.
-          long long* ms = (dbg && t < 14) ? dbg + 8 + 14 * 8 + t * 4 : nullptr;  // MMA-thread stamps
-          if (ms) ms[0] = clock64();
+          // ---- S = Q . K^T : M=128 queries, N=128 keys per block, K = 64 (4 x 16)
           for (int kb = 0; kb < nkb; ++kb) {
-            if (kb < nkb_prev) {
-              mbar_wait(&bars[B_PVDONE + kb], (dph >> kb) & 1);
-              dph ^= 1u << kb;
-              if (kb == nkb_prev - 1) mbar_wait(&bars[B_OFREE], (t - 1) & 1);
-            }
             mbar_wait(&bars[B_KFULL + kb], it & 1);
             tc_fence_after();
             const uint32_t k0 = smem_u32(smem + Smem::K + kb * kTile);
@@ -217,209 +193,152 @@ __global__ void __launch_bounds__(kThreads, 1)
                           sw128_desc(k0 + k * 32, 0, 1024), idesc_s, k != 0);
             umma_commit(&bars[B_SFULL + kb]);
           }
-          // blocks the previous tile used but this one does not: retire their pv_done phase
-          for (int kb = nkb; kb < nkb_prev; ++kb) {
-            mbar_wait(&bars[B_PVDONE + kb], (dph >> kb) & 1);
-            dph ^= 1u << kb;
-          }
-          if (ms) ms[1] = clock64();
           umma_commit(&bars[B_QEMPTY + qb]);
           if (j == a.nqt - 1) umma_commit(&bars[B_KEMPTY]);
-          // ---- O = P . V block by block (last block first: its upper half then holds O),
-          // M=128, N=64 (V MN-major in smem), P in TMEM
-          const uint32_t o_col = 128u * L + 64u;
-          for (int q = 0; q < nkb; ++q) {
-            const int kb = q == 0 ? L : q - 1;
-            mbar_wait(&bars[B_PFULL + kb], (pph >> kb) & 1);
+          // ---- O = P . V : M=128, N=64 (head dim, V MN-major in smem), K = keys, P in TMEM
+          mbar_wait(&bars[B_PREADY], t & 1);
+          tc_fence_after();
+          for (int kb = 0; kb < nkb; ++kb) {
             mbar_wait(&bars[B_VFULL + kb], it & 1);
             tc_fence_after();
             const uint32_t v0 = smem_u32(smem + Smem::V + kb * kTile);
+            const uint32_t pcol = wide ? 128u * kb : 256u + 64u * kb;
 #pragma unroll
             for (int kk = 0; kk < 8; ++kk)  // 16 keys per MMA = 8 packed TMEM columns of P
-              umma_f16_ts(tmem + o_col, tmem + kb * 128 + 8 * kk, sw128_desc(v0 + kk * 2048, 128 * 128, 1024),
-                          idesc_o, (q | kk) != 0);
-            umma_commit(&bars[B_PVDONE + kb]);
-            if (ms && q == 0) ms[2] = clock64();
-            if (dbg && t == 1) dbg[224 + q] = clock64();
+              umma_f16_ts(tmem + o_col, tmem + pcol + 8 * kk, sw128_desc(v0 + kk * 2048, 128 * 128, 1024),
+                          idesc_o, (kb | kk) != 0);
           }
-          if (ms) ms[3] = clock64();
-          pph ^= (1u << nkb) - 1;
           umma_commit(&bars[B_OFULL]);
           if (j == a.nqt - 1) umma_commit(&bars[B_VEMPTY]);
-          nkb_prev = nkb;
         }
       }
     }
     __syncwarp();
   } else {
     // ---------------- softmax + epilogue warps ----------------
-    const uint32_t quad = warp & 3;        // TMEM lane quadrant accessible to this warp
-    const uint32_t grp = (warp - 2) >> 2;  // 32-key chunk of every block
-    const int r = quad * 32 + lane;        // row within the tile (TMEM lane)
+    const uint32_t sw = warp - 2;
+    const uint32_t quad = warp & 3;  // TMEM lane quadrant accessible to this warp
+    const uint32_t grp = sw >> 2;    // column group 0..3
+    const int r = quad * 32 + lane;  // row within the tile (TMEM lane)
     const uint32_t lane_addr = tmem + ((quad * 32) << 16);
     const float NEG_INF = __int_as_float(0xff800000);
     constexpr float LOG2E = 1.4426950408889634f;
-    const uint64_t k8 = f2_pack(0.125f, 0.125f), kl = f2_pack(LOG2E, LOG2E);
     uint32_t t = 0, sph = 0;  // sph: parity bit per s_full barrier
-    // the previous tile's epilogue runs inside this tile's pass 1 (its O sits in the
-    // upper half of its last block; the next tile overwrites that block only if it
-    // has more blocks, and then the epilogue goes right before that block's wait)
-    int pv_b = -1, pv_head = 0, pv_qt = 0, pv_L = 0;
-    auto epilogue = [&](uint32_t tt) {
-      mbar_wait(&bars[B_OFULL], tt & 1);
-      tc_fence_after();
-      if (grp < 2) {
-        uint32_t v[32];
-        tmem_ld32(lane_addr + 128u * pv_L + 64u + grp * 32, v);
-        tmem_wait_ld();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bars[B_OFREE]);  // O is in registers
-        const int erow = pv_qt * 128 + r;
-        if (erow < a.S) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int i = 0; i < 16; ++i) pk[i] = h2_pack_rn(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
-          uint4* dst = reinterpret_cast<uint4*>(a.ctx + (static_cast<int64_t>(pv_b) * a.S + erow) * a.ld_ctx +
-                                                pv_head * 64 + grp * 32);
-#pragma unroll
-          for (int q = 0; q < 4; ++q) dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
-        }
-      } else {
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bars[B_OFREE]);
-      }
-      pv_b = -1;
-    };
     for (int item = blockIdx.x; item < items; item += gridDim.x) {
       const int head = item % a.H, b = item / a.H;
       for (int j = 0; j < a.nqt; ++j, ++t) {
         const int qt = tile_of(a, j);
         const int nkb = nkb_of(a, qt);
+        const bool wide = nkb > 2;
+        const uint32_t o_col = wide ? 64u : 384u;
         const int qrow = qt * 128 + r;
-        const int row_lo = qt * 128 + quad * 32, row_hi = row_lo + 31;  // this warp's rows
-        long long* ts = (dbg && warp == 2 && lane == 0 && t < 14) ? dbg + 8 + t * 8 : nullptr;
+        long long* ts = (dbg && sw == 0 && lane == 0 && t < 14) ? dbg + 8 + t * 8 : nullptr;
         if (ts) ts[0] = clock64();
-        auto cbase = [&](int kb) { return kb * 128 + static_cast<int>(grp) * 32; };  // first key of chunk
-        auto dead = [&](int kb) { const int c0 = cbase(kb); return c0 >= a.S || (a.causal && c0 > row_hi); };
-        auto full = [&](int kb) { const int c0 = cbase(kb); return c0 + 32 <= a.S && (!a.causal || c0 + 31 <= row_lo); };
-        auto valid = [&](int jj) { return jj < a.S && (!a.causal || jj <= qrow); };
-        const uint32_t col = grp * 32;  // this warp's columns inside a block
-        // ---- pass 1: max of the raw accumulators, block by block as S lands
+        int c_begin, c_end;
+        if (wide) {  // group g owns key block g (idle when g >= nkb)
+          const bool own = grp < static_cast<uint32_t>(nkb);
+          c_begin = own ? static_cast<int>(grp) * 128 : 0;
+          c_end = own ? c_begin + 128 : 0;
+        } else {
+          const int cpg = nkb * 32;
+          c_begin = static_cast<int>(grp) * cpg;
+          c_end = c_begin + cpg;
+        }
+        // wait for the S blocks this group reads (every block in narrow mode: cheap)
+        if (wide) {
+          if (grp < static_cast<uint32_t>(nkb)) mbar_wait(&bars[B_SFULL + grp], (sph >> grp) & 1);
+        } else {
+          for (int kb = 0; kb < nkb; ++kb) mbar_wait(&bars[B_SFULL + kb], (sph >> kb) & 1);
+        }
+        sph ^= (1u << nkb) - 1;  // every block of this tile completed one phase
+        tc_fence_after();
+        if (ts) ts[1] = clock64();
+        // chunk classes (warp-uniform: rows of this warp are qt*128 + quad*32 + [0, 32))
+        const int row_lo = qt * 128 + quad * 32, row_hi = row_lo + 31;
+        auto chunk_full = [&](int c) { return c + 32 <= a.S && (!a.causal || c + 31 <= row_lo); };
+        auto chunk_dead = [&](int c) { return c >= a.S || (a.causal && c > row_hi); };
+        // pass 1: max of the raw accumulators over the unmasked keys
         float m0 = NEG_INF, m1 = NEG_INF;
-        for (int kb = 0; kb < nkb; ++kb) {
-          if (pv_b >= 0 && kb == pv_L) epilogue(t - 1);  // this block still holds the previous O
-          mbar_wait(&bars[B_SFULL + kb], (sph >> kb) & 1);
-          tc_fence_after();
-          if (dead(kb)) continue;
+        for (int c = c_begin; c < c_end; c += 32) {
+          if (chunk_dead(c)) continue;
           uint32_t v[32];
-          tmem_ld32(lane_addr + kb * 128 + col, v);
+          tmem_ld32(lane_addr + c, v);
           tmem_wait_ld();
-          if (full(kb)) {
+          if (chunk_full(c)) {
 #pragma unroll
             for (int i = 0; i < 32; i += 4) {
               m0 = fmax3(m0, __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
               m1 = fmax3(m1, __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
             }
           } else {
-            const int c0 = cbase(kb);
 #pragma unroll
-            for (int i = 0; i < 32; ++i) m0 = fmaxf(m0, valid(c0 + i) ? __uint_as_float(v[i]) : NEG_INF);
+            for (int i = 0; i < 32; ++i) {
+              const int jj = c + i;
+              const bool valid = jj < a.S && (!a.causal || jj <= qrow);
+              m0 = fmaxf(m0, valid ? __uint_as_float(v[i]) : NEG_INF);
+            }
           }
         }
-        sph ^= (1u << nkb) - 1;
         red_max[grp * 128 + r] = fmaxf(m0, m1);
-        if (pv_b >= 0) epilogue(t - 1);
-        if (ts) ts[1] = clock64();
         named_bar_sync(1, kSoftmaxWarps * 32);
         const float mraw = fmaxf(fmaxf(red_max[r], red_max[128 + r]), fmaxf(red_max[256 + r], red_max[384 + r]));
         const float mx = r16(__fmul_rn(mraw, 0.125f));  // == max_j round16(acc_j * 0.125)
-        const uint64_t nm = f2_pack(-__fmul_rn(mx, LOG2E), -__fmul_rn(mx, LOG2E));
-        // ---- pass 2: e = exp(s - max) kept in TMEM (fp32), row sums; next block's load in flight
+        if (ts) ts[2] = clock64();
+        // pass 2: e = exp(s - max) kept in TMEM (fp32), partial sums in key order.
+        // exp(s - mx) = 2^(s*log2e - mx*log2e): one FFMA + one SFU op per element.
+        const float mxl = __fmul_rn(mx, LOG2E);
+        const uint64_t k8 = f2_pack(0.125f, 0.125f), kl = f2_pack(LOG2E, LOG2E), nm = f2_pack(-mxl, -mxl);
         uint64_t sum2 = f2_pack(0.0f, 0.0f);
-        {
-          // units u = 2*kb + half (16 columns each); ping-pong buffers, the load of
-          // unit u+1 is in flight while unit u computes
-          uint32_t va[16], vb[16];
-          auto live = [&](int u) { return (u >> 1) < nkb && !dead(u >> 1); };
-          auto ld_unit = [&](int u, uint32_t (&buf)[16]) {
-            tmem_ld16(lane_addr + (u >> 1) * 128 + col + (u & 1) * 16, buf);
-          };
-          auto compute = [&](int u, uint32_t (&v)[16]) {
-            const int kb = u >> 1;
-            const int c0 = cbase(kb) + (u & 1) * 16;
-            float e[16];
-            if (full(kb)) {  // hot path: no masks
+        for (int c = c_begin; c < c_end; c += 32) {
+          if (chunk_dead(c)) continue;
+          uint32_t v[32];
+          tmem_ld32(lane_addr + c, v);
+          tmem_wait_ld();
+          const bool full = chunk_full(c);
 #pragma unroll
-              for (int i = 0; i < 16; i += 2) {
-                float s0, s1;
-                f2_unpack(f2_mul(f2_pack(__uint_as_float(v[i]), __uint_as_float(v[i + 1])), k8), s0, s1);
-                h2_unpack(h2_pack_rn(s0, s1), s0, s1);  // s = round16(acc * 0.125)
-                float x0, x1;
-                f2_unpack(f2_fma(f2_pack(s0, s1), kl, nm), x0, x1);
-                if ((kPolyPairs >> (i / 2)) & 1) {  // this pair's exponentials on the FMA pipe
-                  f2_unpack(exp2_pair_poly(x0, x1), e[i], e[i + 1]);
-                } else {
-                  e[i] = ex2_approx(x0);
-                  e[i + 1] = ex2_approx(x1);
-                }
-              }
-            } else {
-#pragma unroll
-              for (int i = 0; i < 16; i += 2) {
-                float s0, s1;
-                f2_unpack(f2_mul(f2_pack(__uint_as_float(v[i]), __uint_as_float(v[i + 1])), k8), s0, s1);
-                h2_unpack(h2_pack_rn(s0, s1), s0, s1);
-                float x0, x1;
-                f2_unpack(f2_fma(f2_pack(s0, s1), kl, nm), x0, x1);
-                e[i] = valid(c0 + i) ? ex2_approx(x0) : 0.0f;
-                e[i + 1] = valid(c0 + i + 1) ? ex2_approx(x1) : 0.0f;
-              }
+          for (int i = 0; i < 32; i += 2) {
+            float s0, s1;
+            const uint64_t sc = f2_mul(f2_pack(__uint_as_float(v[i]), __uint_as_float(v[i + 1])), k8);
+            f2_unpack(sc, s0, s1);
+            h2_unpack(h2_pack_rn(s0, s1), s0, s1);  // s = round16(acc * 0.125)
+            const uint64_t x = f2_fma(f2_pack(s0, s1), kl, nm);
+            float x0, x1;
+            f2_unpack(x, x0, x1);
+            float e0 = ex2_approx(x0), e1 = ex2_approx(x1);
+            if (!full) {
+              const int jj = c + i;
+              e0 = (jj < a.S && (!a.causal || jj <= qrow)) ? e0 : 0.0f;
+              e1 = (jj + 1 < a.S && (!a.causal || jj + 1 <= qrow)) ? e1 : 0.0f;
             }
-#pragma unroll
-            for (int i = 0; i < 16; i += 2) {
-              sum2 = f2_add(sum2, f2_pack(e[i], e[i + 1]));
-              v[i] = __float_as_uint(e[i]);
-              v[i + 1] = __float_as_uint(e[i + 1]);
-            }
-            tmem_st16(lane_addr + kb * 128 + col + (u & 1) * 16, v);
-          };
-          if (live(0)) {
-            ld_unit(0, va);
-            tmem_wait_ld();
+            const uint64_t e2 = f2_pack(e0, e1);
+            sum2 = f2_add(sum2, e2);
+            v[i] = __float_as_uint(e0);
+            v[i + 1] = __float_as_uint(e1);
           }
-#pragma unroll
-          for (int u = 0; u < 2 * kMaxKB; ++u) {
-            uint32_t(&cur)[16] = (u & 1) ? vb : va;
-            uint32_t(&nxt)[16] = (u & 1) ? va : vb;
-            const bool ln = u + 1 < 2 * kMaxKB && live(u + 1);
-            if (ln) ld_unit(u + 1, nxt);
-            if (live(u)) compute(u, cur);
-            if (ln) tmem_wait_ld();
-          }
+          tmem_st32(lane_addr + c, v);
         }
         tmem_wait_st();
         float sa, sb;
         f2_unpack(sum2, sa, sb);
         red_sum[grp * 128 + r] = __fadd_rn(sa, sb);
-        if (ts) ts[2] = clock64();
         named_bar_sync(1, kSoftmaxWarps * 32);
         const float sum = __fadd_rn(__fadd_rn(__fadd_rn(red_sum[r], red_sum[128 + r]), red_sum[256 + r]),
                                     red_sum[384 + r]);
+        // pass 3: p = round16(e * (1/sum)), packed fp16 pairs into TMEM (the P.V A operand)
         if (ts) ts[3] = clock64();
-        // ---- pass 3: p = round16(e * (1/sum)) -> first half of the block's columns
         const float inv = __frcp_rn(sum);
         const uint64_t inv2 = f2_pack(inv, inv);
-        for (int q = 0; q < nkb; ++q) {
-          const int kb = q == 0 ? nkb - 1 : q - 1;  // last block first: it will hold O
+        for (int c = c_begin; c < c_end; c += 32) {
+          const uint32_t pcol = wide ? static_cast<uint32_t>((c / 128) * 128 + (c % 128) / 2)
+                                     : 256u + static_cast<uint32_t>(c / 2);
           uint32_t pk[16];
-          if (dead(kb)) {
+          if (chunk_dead(c)) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) pk[i] = 0u;
           } else {
             uint32_t v[32];
-            tmem_ld32(lane_addr + kb * 128 + col, v);
-            tmem_wait_ld();
+            tmem_ld32(lane_addr + c, v);
+            tmem_wait_ld();  // the whole chunk is in registers before P overwrites S columns
 #pragma unroll
             for (int i = 0; i < 16; ++i) {
               float p0, p1;
@@ -427,24 +346,41 @@ __global__ void __launch_bounds__(kThreads, 1)
               pk[i] = h2_pack_rn(p0, p1);
             }
           }
-          // the quadrant's 4 warps have read block kb before its P overwrites e columns
-          named_bar_sync(2 + quad, 128);
-          tmem_st16(lane_addr + kb * 128 + grp * 16, pk);
-          tmem_wait_st();
+          tmem_st16(lane_addr + pcol, pk);
+        }
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars[B_PREADY]);
+        if (ts) ts[4] = clock64();
+
+        // epilogue: O (128 x 64 fp32 in TMEM) -> round16 -> ctx
+        mbar_wait(&bars[B_OFULL], t & 1);
+        tc_fence_after();
+        if (ts) ts[5] = clock64();
+        if (grp < 2) {
+          uint32_t v[32];
+          tmem_ld32(lane_addr + o_col + grp * 32, v);
+          tmem_wait_ld();
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&bars[B_PFULL + kb]);
+          if (lane == 0) mbar_arrive(&bars[B_TFREE]);  // O is in registers: TMEM free
+          if (ts) ts[6] = clock64();
+          if (qrow < a.S) {
+            uint32_t pk[16];
+#pragma unroll
+            for (int i = 0; i < 16; ++i) pk[i] = h2_pack_rn(__uint_as_float(v[2 * i]), __uint_as_float(v[2 * i + 1]));
+            uint4* dst = reinterpret_cast<uint4*>(a.ctx + (static_cast<int64_t>(b) * a.S + qrow) * a.ld_ctx +
+                                                  head * 64 + grp * 32);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) dst[q] = make_uint4(pk[4 * q], pk[4 * q + 1], pk[4 * q + 2], pk[4 * q + 3]);
+          }
+        } else {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&bars[B_TFREE]);
         }
-        if (ts) ts[4] = clock64();
-        if (dbg && t == 1 && lane == 0) dbg[200 + (warp - 2)] = clock64();  // pass-3 end per warp
-        pv_b = b;
-        pv_head = head;
-        pv_qt = qt;
-        pv_L = nkb - 1;
-        if (ts) ts[5] = ts[6] = clock64();
       }
     }
-    if (pv_b >= 0) epilogue(t - 1);
   }
   tc_fence_before();
   __syncthreads();
@@ -480,8 +416,8 @@ AttnPlan plan_attn_tc(const void* qkv, int64_t ld_qkv, void* ctx, int64_t ld_ctx
 void configure_attn_tc() {
   static bool done = false;
   if (done) return;
-  for (auto k : {attn_tc_kernel<kPolyDefault>, attn_tc_kernel<0u>, attn_tc_kernel<0x55u>})
-    PRLAB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes)));
+  PRLAB_CUDA(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  static_cast<int>(kSmemBytes)));
   done = true;
 }
 
@@ -499,14 +435,7 @@ void launch_attn_tc(const AttnPlan& p, cudaStream_t st) {
   a.ld_ctx = p.ld_ctx;
   a.dbg = p.dbg;
   const int grid = std::min(p.B * p.H, num_sms());
-  // tuning knob: PRLAB_ATTN_POLY=0 (all exponentials on the SFU) / 0x55 (half on the FMA pipe)
-  static const int poly = std::getenv("PRLAB_ATTN_POLY") ? std::atoi(std::getenv("PRLAB_ATTN_POLY")) : -1;
-  if (poly == 0)
-    launch_pdl(attn_tc_kernel<0u>, dim3(grid), dim3(kThreads), kSmemBytes, st, p.tmQKV, a);
-  else if (poly == 0x55)
-    launch_pdl(attn_tc_kernel<0x55u>, dim3(grid), dim3(kThreads), kSmemBytes, st, p.tmQKV, a);
-  else
-    launch_pdl(attn_tc_kernel<kPolyDefault>, dim3(grid), dim3(kThreads), kSmemBytes, st, p.tmQKV, a);
+  launch_pdl(attn_tc_kernel, dim3(grid), dim3(kThreads), kSmemBytes, st, p.tmQKV, a);
 }
 
 }  // namespace prlab_gpu

@@ -11,7 +11,7 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2603_28708_b200 as pg  # noqa: E402
 
-PH = ["s_wait+pass1", "pass2", "sum_bar", "pass3", "o_wait", "epilogue"]
+PH = ["s_wait+pass1+prev_epilogue", "max_bar+pass2", "sum_bar", "pass3"]
 
 
 def run(B, S, causal, H=12, hd=64):
@@ -43,22 +43,12 @@ def run(B, S, causal, H=12, hd=64):
         st = c0[8 + t * 8: 16 + t * 8]
         if st[0] == 0:
             break
-        ph = {PH[i]: int(st[i + 1] - st[i]) for i in range(6)}
+        ph = {PH[i]: int(st[i + 1] - st[i]) for i in range(4)}
         if t > 0:
             ph["since_prev_tile"] = int(st[0] - c0[8 + (t - 1) * 8])
-        ms = c0[8 + 14 * 8 + t * 4: 8 + 14 * 8 + t * 4 + 4]
-        if ms[0] > 0:  # MMA thread, relative to the softmax tile start
-            ph["mma_qk_begin"] = int(ms[0] - st[0])
-            ph["mma_qk_issued"] = int(ms[1] - st[0])
-            ph["mma_pv_first"] = int(ms[2] - st[0])
-            ph["mma_pv_last"] = int(ms[3] - st[0])
-            ph["softmax_pass3_end"] = int(st[4] - st[0])
         tiles.append(ph)
     out["cta0_tiles"] = tiles
-    t1 = c0[8 + 8]
-    if t1 > 0:
-        out["t1_pass3_end_per_warp"] = [int(c0[200 + w] - t1) for w in range(16)]
-        out["t1_pv_issue"] = [int(c0[224 + q] - t1) for q in range(4)]
+
     print(json.dumps(out), flush=True)
 
 
