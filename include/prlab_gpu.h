@@ -124,6 +124,24 @@ int prlab_gpu_argmax_device(const void* d_logits, int32_t dtype, int64_t rows, i
 int prlab_gpu_forward(prlab_gpu_model* m, const int32_t* ids, int64_t batch, int64_t seq,
                       const prlab_policy* policy, float* logits, prlab_trace* trace);
 
+/* forward with the reference's optional outputs (src/model.cpp:456-482):
+ * flags PRLAB_FWD_RETAIN_SCORES -> scores (host fp32 [L][B][H][S][S]) receives every
+ *   layer's fp32 pre-mask scaled scores (ForwardTrace::layer_scores, kernels.cpp:108-118);
+ * flags PRLAB_FWD_TIMED -> trace->seconds holds CUDA-event time per op class (the
+ *   reference's timed() wrappers, model.cpp:55-62; fused kernels count for the class
+ *   that produces their output, the fused attention for AttentionScoreMatmul).
+ * Without flags this is prlab_gpu_forward. */
+enum prlab_fwd_flags { PRLAB_FWD_RETAIN_SCORES = 1, PRLAB_FWD_TIMED = 2 };
+int prlab_gpu_forward_ex(prlab_gpu_model* m, const int32_t* ids, int64_t batch, int64_t seq,
+                         const prlab_policy* policy, int32_t flags, float* logits, prlab_trace* trace,
+                         float* scores);
+
+/* classifier_probs (src/model.cpp:484-526): mean-pooled final hidden states, tanh
+ * pooler, 2-way head, softmax; probs[b] = positive-class probability.  encoder_only
+ * models only (PRLAB_EINVAL otherwise, with the reference's message). */
+int prlab_gpu_classifier_probs(prlab_gpu_model* m, const int32_t* ids, int64_t batch, int64_t seq,
+                               const prlab_policy* policy, float* probs);
+
 /* Device-resident form: d_ids [B*S] int32 on the device, logits written to
  * d_out with row pitch `ld` elements (ld >= V) in out_dtype.  Asynchronous on
  * `stream` (cudaStream_t; NULL = legacy default).  With use_graph != 0 the

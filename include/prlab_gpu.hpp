@@ -100,12 +100,11 @@ DeviceModel& device_model_for(const Model& m, int device = 0) {
 }
 
 // prlab::forward (model.cpp:456-482): same signature, same ForwardTrace fields
-// (logits [B,S,V] fp32 storage; kernel_calls per class/dtype).
+// (logits [B,S,V] fp32 storage; kernel_calls per class/dtype; seconds per class from
+// CUDA events like the reference's timed() wrappers; layer_scores when retained).
 template <class Model, class TokenBatch, class PrecisionPolicy>
 auto forward(const Model& model, const TokenBatch& tokens, const PrecisionPolicy& policy,
              bool retain_scores = false) {
-  if (retain_scores)
-    throw std::invalid_argument("retain_scores is not supported by the GPU forward yet");
   DeviceModel& dm = device_model_for(model);
   const prlab_policy pol = to_c_policy(policy);
   decltype(prlab::forward(model, tokens, policy)) trace;  // the reference's ForwardTrace type
@@ -113,13 +112,35 @@ auto forward(const Model& model, const TokenBatch& tokens, const PrecisionPolicy
   trace.logits.shape = {tokens.batch, tokens.seq, w};
   trace.logits.data.resize(static_cast<size_t>(tokens.batch * tokens.seq * w));
   prlab_trace tr{};
-  check(prlab_gpu_forward(dm.get(), tokens.ids.data(), tokens.batch, tokens.seq, &pol,
-                          trace.logits.data.data(), &tr));
+  const int64_t heads = model.config.heads, S = tokens.seq, B = tokens.batch;
+  std::vector<float> scores;
+  if (retain_scores) scores.resize(static_cast<size_t>(dm.layers() * B * heads * S * S));
+  check(prlab_gpu_forward_ex(dm.get(), tokens.ids.data(), B, S, &pol,
+                             PRLAB_FWD_TIMED | (retain_scores ? PRLAB_FWD_RETAIN_SCORES : 0),
+                             trace.logits.data.data(), &tr, retain_scores ? scores.data() : nullptr));
   for (int c = 0; c < PRLAB_NUM_OP_CLASSES; ++c) {
     trace.seconds[static_cast<size_t>(c)] = tr.seconds[c];
     for (int d = 0; d < 2; ++d) trace.kernel_calls[static_cast<size_t>(c)][static_cast<size_t>(d)] = tr.kernel_calls[c][d];
   }
+  if (retain_scores) {
+    const size_t per = static_cast<size_t>(B * heads * S * S);
+    for (int64_t l = 0; l < dm.layers(); ++l) {
+      decltype(trace.logits) t({B, heads, S, S});
+      std::copy(scores.begin() + l * per, scores.begin() + (l + 1) * per, t.data.begin());
+      trace.layer_scores.push_back(std::move(t));
+    }
+  }
   return trace;
+}
+
+// prlab::classifier_probs (model.cpp:484-526): positive-class probability per batch row.
+template <class Model, class TokenBatch, class PrecisionPolicy>
+std::vector<float> classifier_probs(const Model& model, const TokenBatch& tokens, const PrecisionPolicy& policy) {
+  DeviceModel& dm = device_model_for(model);
+  const prlab_policy pol = to_c_policy(policy);
+  std::vector<float> out(static_cast<size_t>(tokens.batch));
+  check(prlab_gpu_classifier_probs(dm.get(), tokens.ids.data(), tokens.batch, tokens.seq, &pol, out.data()));
+  return out;
 }
 
 // ---- per-operator mirrors of include/prlab/kernels.hpp:30-70 ----

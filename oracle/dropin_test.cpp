@@ -7,6 +7,7 @@
 // non-finite, the reference's exception types, and the KATs of test_kernels.cpp.
 // Built by oracle/Makefile into oracle/_ref/dropin_test; run on the GPU box by
 // tests/test_gpu_dropin.py.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <stdexcept>
@@ -53,6 +54,54 @@ int main() {
   for (int c = 0; c < kNumOpClasses; ++c)
     for (int d = 0; d < 2; ++d) calls_equal &= cpu_h.kernel_calls[c][d] == gpu.kernel_calls[c][d];
   CHECK(calls_equal, "ForwardTrace kernel_calls identical to the reference");
+
+  // --- ForwardTrace::seconds filled (CUDA-event time per op class, timed() wrappers)
+  CHECK(gpu.seconds[static_cast<int>(OpClass::Linear)] > 0.0 &&
+            gpu.seconds[static_cast<int>(OpClass::LayerNorm)] > 0.0,
+        "ForwardTrace seconds per op class measured on the device");
+
+  // --- retain_scores: layer_scores [B,H,S,S] fp32 pre-mask taps (model.cpp:393-427)
+  {
+    const ForwardTrace cpu_t = forward(model, tokens, resolve_policy("hybrid"), true);
+    const auto gpu_t = gpu::forward(model, tokens, resolve_policy("hybrid"), true);
+    bool shape_ok = gpu_t.layer_scores.size() == cpu_t.layer_scores.size();
+    double md = 0.0, mref = 0.0;
+    for (size_t l = 0; shape_ok && l < cpu_t.layer_scores.size(); ++l) {
+      shape_ok &= gpu_t.layer_scores[l].shape == cpu_t.layer_scores[l].shape;
+      for (size_t i = 0; shape_ok && i < cpu_t.layer_scores[l].data.size(); ++i) {
+        md = std::max(md, std::fabs(static_cast<double>(gpu_t.layer_scores[l].data[i]) - cpu_t.layer_scores[l].data[i]));
+        mref = std::max(mref, std::fabs(static_cast<double>(cpu_t.layer_scores[l].data[i])));
+      }
+    }
+    std::printf("       layer_scores max |gpu-cpu| %.3e (max |score| %.3e)\n", md, mref);
+    CHECK(shape_ok && md <= 2e-2 * std::max(mref, 1e-3), "retain_scores layer_scores match the reference taps");
+  }
+
+  // --- classifier_probs (model.cpp:484-526) on a BERT-shaped encoder
+  {
+    ModelConfig ec = ModelConfig::bert_base();
+    ec.num_layers = 2;
+    ec.vocab = 4096;
+    const Model enc = build_model(ec);
+    const TokenBatch et = random_tokens(ec.vocab, 3, 48, 11);
+    const std::vector<float> want = classifier_probs(enc, et, resolve_policy("fp32"));
+    const std::vector<float> got = gpu::classifier_probs(enc, et, resolve_policy("hybrid"));
+    const std::vector<float> got32 = gpu::classifier_probs(enc, et, resolve_policy("fp32"));
+    double d16 = 0.0, d32 = 0.0;
+    for (size_t i = 0; i < want.size(); ++i) {
+      d16 = std::max(d16, std::fabs(static_cast<double>(got[i]) - want[i]));
+      d32 = std::max(d32, std::fabs(static_cast<double>(got32[i]) - want[i]));
+    }
+    std::printf("       classifier |hybrid-cpu32| %.3e |fp32-cpu32| %.3e\n", d16, d32);
+    CHECK(got.size() == want.size() && d16 <= 2e-3 && d32 <= 1e-5, "classifier_probs matches the reference");
+    bool dec = false;
+    try {
+      gpu::classifier_probs(model, tokens, resolve_policy("hybrid"));
+    } catch (const std::invalid_argument&) {
+      dec = true;
+    }
+    CHECK(dec, "classifier_probs on a decoder -> std::invalid_argument");
+  }
 
   // --- exceptions: same types as the reference
   TokenBatch bad = tokens;

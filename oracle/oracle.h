@@ -88,6 +88,11 @@ int or_forward(const or_model_cfg* c, const float* params, const int32_t* ids, i
                int64_t seq, const or_policy* policy, float* logits, uint64_t* kernel_calls,
                float* scores_tap);
 
+/* classifier_probs (src/model.cpp:484-526): out[b] = positive-class probability.
+ * encoder_only models only (-1 otherwise). */
+int or_classifier_probs(const or_model_cfg* c, const float* params, const int32_t* ids, int64_t batch,
+                        int64_t seq, const or_policy* policy, float* out);
+
 /* OpenMP thread count used by the oracle loops (results are independent of it). */
 void or_set_threads(int n);
 

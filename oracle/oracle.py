@@ -158,6 +158,9 @@ class Oracle:
                                C.c_int64, C.POINTER(C.c_int32), C.c_int64, C.c_int64, _Kcfg,
                                C.POINTER(C.c_float)]
         L.or_set_threads.argtypes = [C.c_int]
+        L.or_classifier_probs.argtypes = [C.POINTER(_ModelCfg), C.POINTER(C.c_float),
+                                          C.POINTER(C.c_int32), C.c_int64, C.c_int64,
+                                          C.POINTER(_Policy), C.POINTER(C.c_float)]
 
     # --- lattice
     def round16(self, x: float) -> float:
@@ -224,6 +227,17 @@ class Oracle:
         return out[0] if len(out) == 1 else tuple(out)
 
     # --- operators
+    def classifier_probs(self, c: ModelConfig, params: np.ndarray, ids: np.ndarray, batch: int,
+                         seq: int, policy: str) -> np.ndarray:
+        """classifier_probs, src/model.cpp:484-526 (encoder_only)."""
+        out = np.empty(batch, dtype=np.float32)
+        pol = self.policy(policy)
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        if self.lib.or_classifier_probs(C.byref(_mcfg(c)), _fp(params), _ip(ids), batch, seq,
+                                        C.byref(pol), _fp(out)):
+            raise ValueError("or_classifier_probs failed (encoder_only model, valid config)")
+        return out
+
     @staticmethod
     def _k(compute, accum, stabilized=True):
         return _Kcfg(compute, accum, int(stabilized))
@@ -381,6 +395,35 @@ class Reference:
             msg = self.lib.ref_last_error().decode()
             raise (IndexError if rc == -2 else ValueError)(msg)
         return (logits, calls.reshape(7, 2)) if want_calls else logits
+
+    def forward_scores(self, c: ModelConfig, params, ids, batch, seq, policy):
+        """prlab::forward(..., retain_scores=true): (logits, [L,B,H,S,S] fp32 taps)."""
+        L = self.lib
+        L.ref_forward_scores.argtypes = ([C.c_int] + [C.c_int64] * 6 +
+                                         [C.POINTER(C.c_float), C.POINTER(C.c_int32), C.c_int64,
+                                          C.c_int64, C.c_char_p, C.POINTER(C.c_float),
+                                          C.POINTER(C.c_float)])
+        width = c.vocab if c.num_layers > 0 else c.hidden
+        logits = np.empty((batch, seq, width), dtype=np.float32)
+        taps = np.empty((c.num_layers, batch, c.heads, seq, seq), dtype=np.float32)
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        if L.ref_forward_scores(*self._c(c), _fp(params), _ip(ids), batch, seq, policy.encode(),
+                                _fp(logits), _fp(taps)):
+            raise ValueError(L.ref_last_error().decode())
+        return logits, taps
+
+    def classifier_probs(self, c: ModelConfig, params, ids, batch, seq, policy):
+        """prlab::classifier_probs (src/model.cpp:484-526)."""
+        L = self.lib
+        L.ref_classifier_probs.argtypes = ([C.c_int] + [C.c_int64] * 6 +
+                                           [C.POINTER(C.c_float), C.POINTER(C.c_int32), C.c_int64,
+                                            C.c_int64, C.c_char_p, C.POINTER(C.c_float)])
+        out = np.empty(batch, dtype=np.float32)
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        if L.ref_classifier_probs(*self._c(c), _fp(params), _ip(ids), batch, seq, policy.encode(),
+                                  _fp(out)):
+            raise ValueError(L.ref_last_error().decode())
+        return out
 
     def make_adversarial_model(self, c: ModelConfig, probe_ids, batch, seq, target=30.0):
         L = self.lib

@@ -482,10 +482,11 @@ static void lattice_inplace(float* x, int64_t n, int d) {
     for (i = 0; i < n; ++i) x[i] = or_round16(x[i]);
 }
 
-/* forward_hidden + forward, src/model.cpp:350-482 */
-int or_forward(const or_model_cfg* c, const float* params, const int32_t* ids, int64_t B,
-               int64_t S, const or_policy* pol, float* logits, uint64_t* calls,
-               float* scores_tap) {
+/* forward_hidden + forward, src/model.cpp:350-482.  hidden_out (optional): the final
+ * LayerNorm output [B*S, h] (forward_hidden's result) -- then no head is computed. */
+static int forward_impl(const or_model_cfg* c, const float* params, const int32_t* ids, int64_t B,
+                        int64_t S, const or_policy* pol, float* logits, uint64_t* calls,
+                        float* scores_tap, float* hidden_out) {
   int i;
   if (or_validate_config(c)) return -1;
   for (i = 0; i < OR_NUM_CLASSES; ++i)
@@ -626,7 +627,15 @@ int or_forward(const or_model_cfg* c, const float* params, const int32_t* ids, i
 #undef LIN
   }
 
-  if (c->num_layers == 0) {
+  if (hidden_out) {
+    /* forward_hidden (model.cpp:445-451): zero layers -> the embeddings, else final LN */
+    if (c->num_layers == 0) {
+      memcpy(hidden_out, x, (size_t)(M * h) * sizeof(float));
+    } else {
+      COUNT(OR_LAYERNORM, ln);
+      or_layernorm(x, M, h, fin, fin + h, 1e-5f, ln, hidden_out);
+    }
+  } else if (c->num_layers == 0) {
     memcpy(logits, x, (size_t)(M * h) * sizeof(float));
   } else {
     /* final LN (model.cpp:449-451) and tied head (model.cpp:469-480):
@@ -641,5 +650,56 @@ int or_forward(const or_model_cfg* c, const float* params, const int32_t* ids, i
   }
 #undef COUNT
   free(x); free(xn); free(q); free(k); free(v); free(ctx); free(br); free(ff); free(wt);
+  return 0;
+}
+
+int or_forward(const or_model_cfg* c, const float* params, const int32_t* ids, int64_t B,
+               int64_t S, const or_policy* pol, float* logits, uint64_t* calls,
+               float* scores_tap) {
+  return forward_impl(c, params, ids, B, S, pol, logits, calls, scores_tap, NULL);
+}
+
+/* classifier_probs, src/model.cpp:484-526: mean-pool (Linear accumulation contract),
+ * tanh pooler, 2-way head, softmax; out[b] = P(class 1). */
+int or_classifier_probs(const or_model_cfg* c, const float* params, const int32_t* ids, int64_t B,
+                        int64_t S, const or_policy* pol, float* out) {
+  if (c->archetype != 0) return -1; /* encoder_only only (model.cpp:486-488) */
+  if (or_validate_config(c)) return -1;
+  const int64_t h = c->hidden, f = c->ffn, V = c->vocab;
+  const or_kcfg lin = pol->cls[OR_LINEAR], act = pol->cls[OR_ACTIVATION], sm = pol->cls[OR_SOFTMAX];
+  float* hidden = (float*)malloc((size_t)(B * S * h) * sizeof(float));
+  int rc = forward_impl(c, params, ids, B, S, pol, NULL, NULL, NULL, hidden);
+  if (rc) { free(hidden); return rc; }
+  const int64_t per_layer = 4 * h + 4 * (h * h + h) + (h * f + f) + (f * h + h);
+  const float* fin = params + V * h + c->max_positions * h + c->num_layers * per_layer;
+  const float *pw = fin + 2 * h, *pb = pw + h * h, *cw = pb + h, *cb = cw + h * 2;
+  float* pooled = (float*)malloc((size_t)(B * h) * sizeof(float));
+  float* pre = (float*)malloc((size_t)(B * h) * sizeof(float));
+  float* wt = (float*)malloc((size_t)(h * h) * sizeof(float));
+  float logits2[2], probs2[2];
+  int64_t b, cc, t, r;
+  const int narrow = lin.accum == OR_F16E;
+  for (b = 0; b < B; ++b)
+    for (cc = 0; cc < h; ++cc) {
+      float acc = 0.0f;
+      for (t = 0; t < S; ++t) {
+        const float xv = conform(hidden[(b * S + t) * h + cc], lin.compute);
+        acc = narrow ? or_round16(acc + xv) : acc + xv;
+      }
+      pooled[b * h + cc] = conform(acc / (float)S, lin.compute);
+    }
+  for (r = 0; r < h; ++r)
+    for (cc = 0; cc < h; ++cc) wt[cc * h + r] = conform(pw[r * h + cc], lin.compute);
+  linear_bias(pooled, wt, pb, B, h, h, lin, pre);
+  or_tanh(pre, B * h, act, pre);
+  lattice_inplace(pre, B * h, lin.compute);
+  for (r = 0; r < h; ++r)
+    for (cc = 0; cc < 2; ++cc) wt[cc * h + r] = conform(cw[r * 2 + cc], lin.compute);
+  for (b = 0; b < B; ++b) {
+    linear_bias(pre + b * h, wt, cb, 1, h, 2, lin, logits2);
+    or_softmax(logits2, 1, 2, sm, probs2);
+    out[b] = probs2[1];
+  }
+  free(hidden); free(pooled); free(pre); free(wt);
   return 0;
 }

@@ -160,6 +160,49 @@ int ref_forward(int archetype, int64_t L, int64_t h, int64_t H, int64_t f, int64
   }
 }
 
+// prlab::forward with retain_scores: logits + the [L][B][H][S][S] fp32 pre-mask score taps
+int ref_forward_scores(int archetype, int64_t L, int64_t h, int64_t H, int64_t f, int64_t V, int64_t P,
+                       const float* params, const int32_t* ids, int64_t B, int64_t S, const char* policy,
+                       float* logits, float* scores) {
+  try {
+    const prlab::Model m = model_from_flat(make_cfg(archetype, L, h, H, f, V, P, 0), params);
+    prlab::TokenBatch tb;
+    tb.batch = B;
+    tb.seq = S;
+    tb.ids.assign(ids, ids + B * S);
+    const prlab::ForwardTrace tr = prlab::forward(m, tb, prlab::resolve_policy(policy), true);
+    std::memcpy(logits, tr.logits.data.data(), tr.logits.data.size() * sizeof(float));
+    float* o = scores;
+    for (const auto& t : tr.layer_scores) {
+      std::memcpy(o, t.data.data(), t.data.size() * sizeof(float));
+      o += t.data.size();
+    }
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, -1);
+  }
+}
+
+// prlab::classifier_probs (src/model.cpp:484-526)
+int ref_classifier_probs(int archetype, int64_t L, int64_t h, int64_t H, int64_t f, int64_t V, int64_t P,
+                         const float* params, const int32_t* ids, int64_t B, int64_t S, const char* policy,
+                         float* out) {
+  try {
+    const prlab::Model m = model_from_flat(make_cfg(archetype, L, h, H, f, V, P, 0), params);
+    prlab::TokenBatch tb;
+    tb.batch = B;
+    tb.seq = S;
+    tb.ids.assign(ids, ids + B * S);
+    const std::vector<float> pr = prlab::classifier_probs(m, tb, prlab::resolve_policy(policy));
+    std::memcpy(out, pr.data(), pr.size() * sizeof(float));
+    return 0;
+  } catch (const std::invalid_argument& e) {
+    return fail(e, -1);
+  } catch (const std::exception& e) {
+    return fail(e, -3);
+  }
+}
+
 // make_adversarial_model (src/fidelity.cpp:282-312) -> flat canonical params
 int ref_make_adversarial_model(int archetype, int64_t L, int64_t h, int64_t H, int64_t f, int64_t V,
                                int64_t P, uint64_t seed, const int32_t* probe_ids, int64_t B, int64_t S,

@@ -28,6 +28,7 @@ F32, F16E = 0, 1
 OP_CLASSES = ["Linear", "AttentionScoreMatmul", "Softmax", "LayerNorm", "Activation",
               "Embedding", "Residual"]
 OUT_F32, OUT_F16 = 0, 1
+FWD_RETAIN_SCORES, FWD_TIMED = 1, 2
 
 PRLAB_OK, PRLAB_EINVAL, PRLAB_ERANGE, PRLAB_ERUNTIME, PRLAB_ECUDA = range(5)
 
@@ -146,6 +147,10 @@ EXPORTS = [
     ("prlab_gpu_argmax_device", C.c_int, [_P, C.c_int32, C.c_int64, C.c_int64, C.c_int64, _P, _P]),
     ("prlab_gpu_forward", C.c_int, [_P, _IP, C.c_int64, C.c_int64, C.POINTER(PrecisionPolicy),
                                     _FP, C.POINTER(Trace)]),
+    ("prlab_gpu_forward_ex", C.c_int, [_P, _IP, C.c_int64, C.c_int64, C.POINTER(PrecisionPolicy),
+                                       C.c_int32, _FP, C.POINTER(Trace), _FP]),
+    ("prlab_gpu_classifier_probs", C.c_int, [_P, _IP, C.c_int64, C.c_int64,
+                                             C.POINTER(PrecisionPolicy), _FP]),
     ("prlab_gpu_forward_device", C.c_int, [_P, _P, C.c_int64, C.c_int64,
                                            C.POINTER(PrecisionPolicy), _P, C.c_int32, C.c_int64,
                                            _P, C.c_int32]),
@@ -314,6 +319,33 @@ class DeviceModel:
         _check(lib().prlab_gpu_forward(self._h, ids.ctypes.data_as(_IP), batch, seq,
                                        C.byref(pol), _f(logits), C.byref(tr)))
         return (logits, tr) if want_trace else logits
+
+    def forward_ex(self, ids, batch: int, seq: int, policy="hybrid", retain_scores=False,
+                   timed=False):
+        """forward with the reference's optional outputs: (logits, Trace, layer_scores or None);
+        layer_scores [L,B,H,S,S] fp32 pre-mask taps (ForwardTrace::layer_scores)."""
+        cfg = self.config
+        ids = _arr(ids, np.int32)
+        width = cfg.vocab if cfg.num_layers > 0 else cfg.hidden
+        logits = np.empty((batch, seq, width), np.float32)
+        scores = (np.empty((cfg.num_layers, batch, cfg.heads, seq, seq), np.float32)
+                  if retain_scores else None)
+        tr = Trace()
+        pol = _policy(policy)
+        flags = (FWD_RETAIN_SCORES if retain_scores else 0) | (FWD_TIMED if timed else 0)
+        _check(lib().prlab_gpu_forward_ex(self._h, ids.ctypes.data_as(_IP), batch, seq,
+                                          C.byref(pol), flags, _f(logits), C.byref(tr),
+                                          _f(scores) if scores is not None else None))
+        return logits, tr, scores
+
+    def classifier_probs(self, ids, batch: int, seq: int, policy="hybrid") -> np.ndarray:
+        """classifier_probs (src/model.cpp:484-526): positive-class probability per row."""
+        ids = _arr(ids, np.int32)
+        out = np.empty(batch, np.float32)
+        pol = _policy(policy)
+        _check(lib().prlab_gpu_classifier_probs(self._h, ids.ctypes.data_as(_IP), batch, seq,
+                                                C.byref(pol), _f(out)))
+        return out
 
     def forward_device(self, d_ids: int, batch: int, seq: int, policy, d_out: int,
                        out_dtype: int, ld: int, stream: int = 0, use_graph: bool = True):

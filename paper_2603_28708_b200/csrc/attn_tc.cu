@@ -47,6 +47,7 @@ constexpr uint32_t kTile = 128 * 64 * 2;           // one 128 x 64 fp16 tile, 16
 
 struct AttnArgs {
   int B, S, H, hd, causal, nqt;
+  float* tap;  // optional [B][H][S][S] fp32 pre-mask scores acc * 0.125 (retain_scores), null = off
   int h;  // hidden = H * hd (column offset of K; V at 2h)
   __half* ctx;
   int64_t ld_ctx;
@@ -100,7 +101,8 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
 __device__ __forceinline__ int tile_of(const AttnArgs& a, int j) { return a.nqt - 1 - j; }
 __device__ __forceinline__ int nkb_of(const AttnArgs& a, int qt) {
   const int nkb_all = (a.S + 127) / 128;
-  return a.causal ? min(qt + 1, nkb_all) : nkb_all;
+  // the retain_scores tap needs every key block (the mask is applied after the tap)
+  return (a.causal && a.tap == nullptr) ? min(qt + 1, nkb_all) : nkb_all;
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -260,10 +262,16 @@ __global__ void __launch_bounds__(kThreads, 1)
         // pass 1: max of the raw accumulators over the unmasked keys
         float m0 = NEG_INF, m1 = NEG_INF;
         for (int c = c_begin; c < c_end; c += 32) {
-          if (chunk_dead(c)) continue;
+          if (chunk_dead(c) && a.tap == nullptr) continue;
           uint32_t v[32];
           tmem_ld32(lane_addr + c, v);
           tmem_wait_ld();
+          if (a.tap != nullptr && qrow < a.S) {  // retain_scores: fp32 acc * scale, pre-mask
+            float* trow = a.tap + ((static_cast<int64_t>(b) * a.H + head) * a.S + qrow) * a.S;
+            for (int i = 0; i < 32; ++i)
+              if (c + i < a.S) trow[c + i] = __fmul_rn(__uint_as_float(v[i]), 0.125f);
+          }
+          if (chunk_dead(c)) continue;
           if (chunk_full(c)) {
 #pragma unroll
             for (int i = 0; i < 32; i += 4) {
@@ -421,7 +429,7 @@ void configure_attn_tc() {
   done = true;
 }
 
-void launch_attn_tc(const AttnPlan& p, cudaStream_t st) {
+void launch_attn_tc(const AttnPlan& p, cudaStream_t st, float* tap) {
   configure_attn_tc();
   AttnArgs a;
   a.B = p.B;
@@ -434,6 +442,7 @@ void launch_attn_tc(const AttnPlan& p, cudaStream_t st) {
   a.ctx = reinterpret_cast<__half*>(p.ctx);
   a.ld_ctx = p.ld_ctx;
   a.dbg = p.dbg;
+  a.tap = tap;
   const int grid = std::min(p.B * p.H, num_sms());
   launch_pdl(attn_tc_kernel, dim3(grid), dim3(kThreads), kSmemBytes, st, p.tmQKV, a);
 }

@@ -109,7 +109,8 @@ struct AttnPlan {
 bool attn_tc_supported(int S, int hd);
 AttnPlan plan_attn_tc(const void* qkv, int64_t ld_qkv, void* ctx, int64_t ld_ctx, int B, int S,
                       int H, int hd, int causal);
-void launch_attn_tc(const AttnPlan& p, cudaStream_t st);
+// tap (optional): [B][H][S][S] fp32 pre-mask scores (the reference's retain_scores capture)
+void launch_attn_tc(const AttnPlan& p, cudaStream_t st, float* tap = nullptr);
 void configure_attn_tc();
 
 // --- SIMT kernels (any shape, any policy; fp32 storage) ---
@@ -143,6 +144,9 @@ void simt_softmax(const float* x, int64_t rows, int64_t n, Kcfg cfg, float* out,
 void simt_gelu(const float* x, int64_t n, Kcfg cfg, float* out, cudaStream_t st);
 void simt_add(const float* a, const float* b, int64_t n, Kcfg cfg, float* out, cudaStream_t st);
 void simt_tanh(const float* x, int64_t n, Kcfg cfg, float* out, cudaStream_t st);
+// classifier mean pool over the sequence (x32 or x16 [B*S, h]) -> out [B, h] fp32
+void simt_pool_mean(const float* x32, const __half* x16, int B, int S, int h, Kcfg lin, float* out,
+                    cudaStream_t st);
 void simt_round_copy(const float* x, int64_t n, int f16, float* out, cudaStream_t st);
 // fp16 padded [M, ld16] -> fp32 dense [M, N]
 void convert_f16_to_f32(const __half* in, int64_t ld_in, float* out, int64_t ld_out, int M, int N,

@@ -534,6 +534,25 @@ void simt_add(const float* a, const float* b, int64_t n, Kcfg cfg, float* out, c
   simt_add_kernel<<<blocks_for(n, 256), 256, 0, st>>>(a, b, n, cfg.compute, out);
   PRLAB_CUDA(cudaGetLastError());
 }
+// classifier_probs mean pool (src/model.cpp:496-511): one thread per (batch row, column),
+// tokens summed in order under the Linear accumulation contract, then conform(acc / S).
+__global__ void pool_mean_kernel(const float* x32, const __half* x16, int B, int S, int h, int c16, int a16,
+                                 float* out) {
+  const int b = blockIdx.y, c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B || c >= h) return;
+  float acc = 0.0f;
+  for (int t = 0; t < S; ++t) {
+    const int64_t i = (static_cast<int64_t>(b) * S + t) * h + c;
+    const float xv = conform(x16 ? __half2float(x16[i]) : x32[i], c16);
+    acc = a16 ? r16(__fadd_rn(acc, xv)) : __fadd_rn(acc, xv);
+  }
+  out[static_cast<int64_t>(b) * h + c] = conform(__fdiv_rn(acc, static_cast<float>(S)), c16);
+}
+void simt_pool_mean(const float* x32, const __half* x16, int B, int S, int h, Kcfg lin, float* out,
+                    cudaStream_t st) {
+  pool_mean_kernel<<<dim3((h + 127) / 128, B), 128, 0, st>>>(x32, x16, B, S, h, lin.compute, lin.accum, out);
+  PRLAB_CUDA(cudaGetLastError());
+}
 void simt_tanh(const float* x, int64_t n, Kcfg cfg, float* out, cudaStream_t st) {
   simt_tanh_kernel<<<blocks_for(n, 256), 256, 0, st>>>(x, n, cfg.compute, out);
   PRLAB_CUDA(cudaGetLastError());

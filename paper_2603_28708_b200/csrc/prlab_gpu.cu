@@ -275,6 +275,11 @@ struct prlab_gpu_model {
   std::vector<L32> l32;
   bool have32 = false;
 
+  // encoder classifier head (pooler [h,h], classifier [h,2]) as fp32 W^T + biases,
+  // uploaded on the first classifier_probs call
+  DeviceBuffer cls_arena;
+  float *pool_wt = nullptr, *pool_b = nullptr, *cls_wt = nullptr, *cls_b = nullptr;
+
   DeviceBuffer err;  // device error word (bad token ids)
   DeviceBuffer split_ws, split_tickets;
   SplitScratch scratch;
@@ -525,42 +530,66 @@ prlab_gpu_model::Plan& get_plan(prlab_gpu_model& m, int64_t B, int64_t S, const 
   return ref;
 }
 
+// Options of one forward recording (the drop-in's retain_scores / instrumented /
+// classifier variants; the default is the plain logits forward).
+struct FwdOpts {
+  float* tap = nullptr;      // device [L][B][H][S][S] fp32 pre-mask scores (retain_scores)
+  bool hidden_only = false;  // stop after forward_hidden (classifier_probs)
+  // instrumented mode: one (op class, start, end) event triple per launch
+  std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>>* timing = nullptr;
+};
+
 // Records one forward on `st`; returns the number of kernels launched.
 int64_t enqueue_forward(prlab_gpu_model& m, prlab_gpu_model::Plan& p, const int32_t* ids, void* out,
-                        int out_dtype, int64_t ld, cudaStream_t st) {
+                        int out_dtype, int64_t ld, cudaStream_t st, const FwdOpts& o = FwdOpts()) {
   const int64_t B = p.B, S = p.S, M = B * S, h = m.h, f = m.f, V = m.V, L = m.L;
   const int Bi = static_cast<int>(B), Si = static_cast<int>(S), Mi = static_cast<int>(M);
   const int hi = static_cast<int>(h), fi = static_cast<int>(f), Vi = static_cast<int>(V);
   int* err = m.err.at<int>(0);
   int64_t n = 0;
-  if (p.fast) {
-    embed_f32(m.tok, V, m.pos, hi, ids, Bi, Si, p.x, err, st);
+  // instrumented mode: bracket each launch with events attributed to the reference op
+  // class (fused kernels count for the class that produces their output; the fused
+  // attention kernel for AttentionScoreMatmul)
+  auto T = [&](int cls, auto&& launch) {
+    if (o.timing) {
+      cudaEvent_t a, b;
+      PRLAB_CUDA(cudaEventCreate(&a));
+      PRLAB_CUDA(cudaEventCreate(&b));
+      PRLAB_CUDA(cudaEventRecord(a, st));
+      launch();
+      PRLAB_CUDA(cudaEventRecord(b, st));
+      o.timing->emplace_back(cls, a, b);
+    } else {
+      launch();
+    }
     ++n;
+  };
+  const int64_t tap_stride = B * m.H * S * S;
+  if (p.fast) {
+    T(PRLAB_EMBEDDING, [&] { embed_f32(m.tok, V, m.pos, hi, ids, Bi, Si, p.x, err, st); });
     for (int64_t l = 0; l < L; ++l) {
       const auto& w = m.l16[l];
-      ln_f32_to_f16(p.x, Mi, hi, w.ln1g, w.ln1b, 1e-5f, p.xn16, st);  // LN1 -> Linear lattice
-      launch_gemm_tc(p.gemms[4 * l + 0], st);                          // QKV (+bias)
-      launch_attn_tc(p.attn, st);                                      // attention -> ctx (xn16)
-      launch_gemm_tc(p.gemms[4 * l + 1], st);                          // Wo (+bias) + residual
-      ln_f32_to_f16(p.x, Mi, hi, w.ln2g, w.ln2b, 1e-5f, p.xn16, st);  // LN2
-      launch_gemm_tc(p.gemms[4 * l + 2], st);                          // FFN1 (+bias, GELU)
-      launch_gemm_tc(p.gemms[4 * l + 3], st);                          // FFN2 (+bias) + residual
-      n += 7;
+      float* tap = o.tap ? o.tap + l * tap_stride : nullptr;
+      T(PRLAB_LAYERNORM, [&] { ln_f32_to_f16(p.x, Mi, hi, w.ln1g, w.ln1b, 1e-5f, p.xn16, st); });  // LN1
+      T(PRLAB_LINEAR, [&] { launch_gemm_tc(p.gemms[4 * l + 0], st); });                          // QKV (+bias)
+      T(PRLAB_ATTENTION_SCORE_MATMUL, [&] { launch_attn_tc(p.attn, st, tap); });                // -> ctx (xn16)
+      T(PRLAB_LINEAR, [&] { launch_gemm_tc(p.gemms[4 * l + 1], st); });                          // Wo + residual
+      T(PRLAB_LAYERNORM, [&] { ln_f32_to_f16(p.x, Mi, hi, w.ln2g, w.ln2b, 1e-5f, p.xn16, st); });  // LN2
+      T(PRLAB_LINEAR, [&] { launch_gemm_tc(p.gemms[4 * l + 2], st); });                          // FFN1 + GELU
+      T(PRLAB_LINEAR, [&] { launch_gemm_tc(p.gemms[4 * l + 3], st); });                          // FFN2 + residual
     }
-    ln_f32_to_f16(p.x, Mi, hi, m.lnfg, m.lnfb, 1e-5f, p.xn16, st);
-    ++n;
+    T(PRLAB_LAYERNORM, [&] { ln_f32_to_f16(p.x, Mi, hi, m.lnfg, m.lnfb, 1e-5f, p.xn16, st); });
+    if (o.hidden_only) return n;  // forward_hidden: r16(final LN) in xn16 (the Linear lattice)
     if (out_dtype == PRLAB_OUT_F16) {
       if (ld % 8 != 0) throw std::invalid_argument("fp16 logits need a row pitch that is a multiple of 8");
       const auto key = std::make_tuple(out, ld);
       auto it = p.head_plans.find(key);
       if (it == p.head_plans.end())
         it = p.head_plans.emplace(key, plan_gemm_tc(p.xn16, h, m.emb16, h, nullptr, out, ld, Mi, Vi, hi, EPI_F16, &m.scratch)).first;
-      launch_gemm_tc(it->second, st);  // tied head straight into the caller's buffer
-      ++n;
+      T(PRLAB_LINEAR, [&] { launch_gemm_tc(it->second, st); });  // tied head straight into the caller's buffer
     } else {
-      launch_gemm_tc(p.gemms.back(), st);
-      convert_f16_to_f32(p.logit16, p.ld16, static_cast<float*>(out), ld, Mi, Vi, st);
-      n += 2;
+      T(PRLAB_LINEAR, [&] { launch_gemm_tc(p.gemms.back(), st); });
+      T(PRLAB_LINEAR, [&] { convert_f16_to_f32(p.logit16, p.ld16, static_cast<float*>(out), ld, Mi, Vi, st); });
     }
     return n;
   }
@@ -571,21 +600,29 @@ int64_t enqueue_forward(prlab_gpu_model& m, prlab_gpu_model::Plan& p, const int3
              sm = K(pol.cls[PRLAB_SOFTMAX]), ln = K(pol.cls[PRLAB_LAYERNORM]),
              act = K(pol.cls[PRLAB_ACTIVATION]), emb = K(pol.cls[PRLAB_EMBEDDING]),
              res = K(pol.cls[PRLAB_RESIDUAL]);
-  simt_embed(m.tok, V, m.pos, hi, ids, Bi, Si, emb, p.x, err, st);
-  ++n;
+  T(PRLAB_EMBEDDING, [&] { simt_embed(m.tok, V, m.pos, hi, ids, Bi, Si, emb, p.x, err, st); });
   const float scale = 1.0f / std::sqrt(static_cast<float>(m.hd));
   for (int64_t l = 0; l < L; ++l) {
     const auto& w16 = m.l16[l];
     const auto& w = m.l32[l];
-    simt_layernorm(p.x, Mi, hi, w16.ln1g, w16.ln1b, 1e-5f, ln, p.xn32, nullptr, 0, st);
-    simt_gemm(p.xn32, h, w.wqkv_t, h, p.qkv32, 3 * h, Mi, 3 * hi, hi, lin, SimtGemmEpi{w.bqkv, 0, act, res, nullptr}, st);
-    simt_attention(p.qkv32, p.qkv32 + h, p.qkv32 + 2 * h, 3 * h, p.ctx32, h, Bi, Si, static_cast<int>(m.H),
-                   static_cast<int>(m.hd), scale, m.d.archetype == 1, att, sm, nullptr, st);
-    simt_gemm(p.ctx32, h, w.wo_t, h, p.x, h, Mi, hi, hi, lin, SimtGemmEpi{w.bo, 2, act, res, p.x}, st);
-    simt_layernorm(p.x, Mi, hi, w16.ln2g, w16.ln2b, 1e-5f, ln, p.xn32, nullptr, 0, st);
-    simt_gemm(p.xn32, h, w.w1_t, h, p.ff32, f, Mi, fi, hi, lin, SimtGemmEpi{w.b1, 1, act, res, nullptr}, st);
-    simt_gemm(p.ff32, f, w.w2_t, f, p.x, h, Mi, hi, fi, lin, SimtGemmEpi{w.b2, 2, act, res, p.x}, st);
-    n += 7;
+    float* tap = o.tap ? o.tap + l * tap_stride : nullptr;
+    T(PRLAB_LAYERNORM, [&] { simt_layernorm(p.x, Mi, hi, w16.ln1g, w16.ln1b, 1e-5f, ln, p.xn32, nullptr, 0, st); });
+    T(PRLAB_LINEAR, [&] {
+      simt_gemm(p.xn32, h, w.wqkv_t, h, p.qkv32, 3 * h, Mi, 3 * hi, hi, lin, SimtGemmEpi{w.bqkv, 0, act, res, nullptr}, st);
+    });
+    T(PRLAB_ATTENTION_SCORE_MATMUL, [&] {
+      simt_attention(p.qkv32, p.qkv32 + h, p.qkv32 + 2 * h, 3 * h, p.ctx32, h, Bi, Si, static_cast<int>(m.H),
+                     static_cast<int>(m.hd), scale, m.d.archetype == 1, att, sm, tap, st);
+    });
+    T(PRLAB_LINEAR, [&] { simt_gemm(p.ctx32, h, w.wo_t, h, p.x, h, Mi, hi, hi, lin, SimtGemmEpi{w.bo, 2, act, res, p.x}, st); });
+    T(PRLAB_LAYERNORM, [&] { simt_layernorm(p.x, Mi, hi, w16.ln2g, w16.ln2b, 1e-5f, ln, p.xn32, nullptr, 0, st); });
+    T(PRLAB_LINEAR, [&] { simt_gemm(p.xn32, h, w.w1_t, h, p.ff32, f, Mi, fi, hi, lin, SimtGemmEpi{w.b1, 1, act, res, nullptr}, st); });
+    T(PRLAB_LINEAR, [&] { simt_gemm(p.ff32, f, w.w2_t, f, p.x, h, Mi, hi, fi, lin, SimtGemmEpi{w.b2, 2, act, res, p.x}, st); });
+  }
+  if (o.hidden_only) {
+    // forward_hidden: zero layers -> the embeddings (p.x), else the final LN in xn32
+    if (L > 0) T(PRLAB_LAYERNORM, [&] { simt_layernorm(p.x, Mi, hi, m.lnfg, m.lnfb, 1e-5f, ln, p.xn32, nullptr, 0, st); });
+    return n;
   }
   if (out_dtype != PRLAB_OUT_F32)
     throw std::invalid_argument("fp16 logits are only produced by the hybrid tensor-core path");
@@ -595,10 +632,11 @@ int64_t enqueue_forward(prlab_gpu_model& m, prlab_gpu_model::Plan& p, const int3
     PRLAB_CUDA(cudaMemcpy2DAsync(dst, ld * 4, p.x, h * 4, h * 4, M, cudaMemcpyDeviceToDevice, st));
     ++n;
   } else {
-    simt_layernorm(p.x, Mi, hi, m.lnfg, m.lnfb, 1e-5f, ln, p.xn32, nullptr, 0, st);
+    T(PRLAB_LAYERNORM, [&] { simt_layernorm(p.x, Mi, hi, m.lnfg, m.lnfb, 1e-5f, ln, p.xn32, nullptr, 0, st); });
     // tied head: logits = hidden . E^T, E [V, h] is already K-major (model.cpp:469-480)
-    simt_gemm(p.xn32, h, m.tok, h, dst, ld, Mi, Vi, hi, lin, SimtGemmEpi{nullptr, 0, act, res, nullptr}, st);
-    n += 2;
+    T(PRLAB_LINEAR, [&] {
+      simt_gemm(p.xn32, h, m.tok, h, dst, ld, Mi, Vi, hi, lin, SimtGemmEpi{nullptr, 0, act, res, nullptr}, st);
+    });
   }
   return n;
 }
@@ -903,6 +941,111 @@ int prlab_gpu_forward(prlab_gpu_model* m, const int32_t* ids, int64_t B, int64_t
     PRLAB_CUDA(cudaMemcpyAsync(logits, p.out32, B * S * w * 4, cudaMemcpyDeviceToHost, st));
     PRLAB_CUDA(cudaStreamSynchronize(st));
     if (trace) fill_calls(*m, B, *policy, trace);
+  });
+}
+
+int prlab_gpu_forward_ex(prlab_gpu_model* m, const int32_t* ids, int64_t B, int64_t S,
+                         const prlab_policy* policy, int32_t flags, float* logits, prlab_trace* trace,
+                         float* scores) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(m->mu);
+    validate_policy(*policy);
+    check_forward_args(*m, B, S);
+    for (int64_t i = 0; i < B * S; ++i)  // embed(), src/kernels.cpp:278-283
+      if (ids[i] < 0 || ids[i] >= m->V)
+        throw std::out_of_range("token id " + std::to_string(ids[i]) + " outside vocab of " +
+                                std::to_string(m->V));
+    const bool retain = (flags & PRLAB_FWD_RETAIN_SCORES) != 0, timed = (flags & PRLAB_FWD_TIMED) != 0;
+    if (retain && scores == nullptr) throw std::invalid_argument("retain_scores needs a scores buffer");
+    PRLAB_CUDA(cudaSetDevice(m->device));
+    auto& p = get_plan(*m, B, S, *policy);
+    const int64_t w = m->L > 0 ? m->V : m->h;
+    cudaStream_t st = m->stream;
+    PRLAB_CUDA(cudaMemcpyAsync(p.ids, ids, B * S * 4, cudaMemcpyHostToDevice, st));
+    FwdOpts o;
+    const int64_t tap_n = m->L * B * m->H * S * S;
+    TmpDev tap(retain ? static_cast<size_t>(tap_n) * 4 : 0);
+    if (retain) o.tap = tap.f();
+    std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> ev;
+    if (timed) o.timing = &ev;
+    if (!retain && !timed)
+      run_forward(*m, p, p.ids, p.out32, PRLAB_OUT_F32, w, st, !std::getenv("PRLAB_NO_GRAPH"));
+    else
+      enqueue_forward(*m, p, p.ids, p.out32, PRLAB_OUT_F32, w, st, o);
+    PRLAB_CUDA(cudaMemcpyAsync(logits, p.out32, B * S * w * 4, cudaMemcpyDeviceToHost, st));
+    if (retain) PRLAB_CUDA(cudaMemcpyAsync(scores, tap.p, tap_n * 4, cudaMemcpyDeviceToHost, st));
+    PRLAB_CUDA(cudaStreamSynchronize(st));
+    if (trace) {
+      fill_calls(*m, B, *policy, trace);
+      for (auto& e : ev) {
+        float ms = 0.0f;
+        PRLAB_CUDA(cudaEventElapsedTime(&ms, std::get<1>(e), std::get<2>(e)));
+        trace->seconds[std::get<0>(e)] += 1e-3 * ms;
+      }
+    }
+    for (auto& e : ev) {
+      cudaEventDestroy(std::get<1>(e));
+      cudaEventDestroy(std::get<2>(e));
+    }
+  });
+}
+
+int prlab_gpu_classifier_probs(prlab_gpu_model* m, const int32_t* ids, int64_t B, int64_t S,
+                               const prlab_policy* policy, float* probs) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(m->mu);
+    if (m->d.archetype != 0) throw std::invalid_argument("classifier_probs needs an encoder_only model");
+    validate_policy(*policy);
+    check_forward_args(*m, B, S);
+    for (int64_t i = 0; i < B * S; ++i)
+      if (ids[i] < 0 || ids[i] >= m->V)
+        throw std::out_of_range("token id " + std::to_string(ids[i]) + " outside vocab of " +
+                                std::to_string(m->V));
+    PRLAB_CUDA(cudaSetDevice(m->device));
+    const int64_t h = m->h;
+    if (m->pool_wt == nullptr) {
+      // canonical order: ..., final_ln.{gamma,beta}, pooler.{weight [h,h], bias}, classifier.{weight [h,2], bias}
+      const size_t base = 2 + 16 * static_cast<size_t>(m->L) + 2;
+      const auto& pw = m->host[base];
+      const auto& pb = m->host[base + 1];
+      const auto& cw = m->host[base + 2];
+      const auto& cb = m->host[base + 3];
+      std::vector<float> buf(static_cast<size_t>(h * h + h + 2 * h + 2));
+      for (int64_t r = 0; r < h; ++r)
+        for (int64_t c = 0; c < h; ++c) buf[c * h + r] = pw[r * h + c];  // W^T [out, in]
+      std::copy(pb.begin(), pb.end(), buf.begin() + h * h);
+      for (int64_t r = 0; r < h; ++r)
+        for (int64_t c = 0; c < 2; ++c) buf[h * h + h + c * h + r] = cw[r * 2 + c];
+      std::copy(cb.begin(), cb.end(), buf.begin() + h * h + 3 * h);
+      m->cls_arena.alloc(buf.size() * 4);
+      h2d(m->cls_arena.p, buf.data(), buf.size());
+      float* a = static_cast<float*>(m->cls_arena.p);
+      m->pool_wt = a;
+      m->pool_b = a + h * h;
+      m->cls_wt = a + h * h + h;
+      m->cls_b = a + h * h + 3 * h;
+    }
+    auto& p = get_plan(*m, B, S, *policy);
+    cudaStream_t st = m->stream;
+    PRLAB_CUDA(cudaMemcpyAsync(p.ids, ids, B * S * 4, cudaMemcpyHostToDevice, st));
+    FwdOpts o;
+    o.hidden_only = true;
+    enqueue_forward(*m, p, p.ids, nullptr, PRLAB_OUT_F32, 0, st, o);
+    const Kcfg lin = K(policy->cls[PRLAB_LINEAR]), act = K(policy->cls[PRLAB_ACTIVATION]),
+               sm = K(policy->cls[PRLAB_SOFTMAX]), res = K(policy->cls[PRLAB_RESIDUAL]);
+    const int Bi = static_cast<int>(B), hi = static_cast<int>(h);
+    TmpDev pooled(B * h * 4), pre(B * h * 4), logit(B * 2 * 4), pr(B * 2 * 4);
+    const bool f16 = p.fast;  // fast path: r16(final LN) in fp16; generic: fp32 (or embeddings at L = 0)
+    const float* x32 = f16 ? nullptr : (m->L > 0 ? p.xn32 : p.x);
+    simt_pool_mean(x32, f16 ? p.xn16 : nullptr, Bi, static_cast<int>(S), hi, lin, pooled.f(), st);
+    simt_gemm(pooled.f(), h, m->pool_wt, h, pre.f(), h, Bi, hi, hi, lin, SimtGemmEpi{m->pool_b, 0, act, res, nullptr}, st);
+    simt_tanh(pre.f(), B * h, act, pre.f(), st);
+    simt_gemm(pre.f(), h, m->cls_wt, h, logit.f(), 2, Bi, 2, hi, lin, SimtGemmEpi{m->cls_b, 0, act, res, nullptr}, st);
+    simt_softmax(logit.f(), B, 2, sm, pr.f(), st);
+    std::vector<float> host(static_cast<size_t>(2 * B));
+    PRLAB_CUDA(cudaMemcpyAsync(host.data(), pr.p, B * 2 * 4, cudaMemcpyDeviceToHost, st));
+    PRLAB_CUDA(cudaStreamSynchronize(st));
+    for (int64_t b = 0; b < B; ++b) probs[b] = host[2 * b + 1];
   });
 }
 

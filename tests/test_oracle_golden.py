@@ -135,3 +135,25 @@ def test_adversarial_construction_matches_reference(name):
     assert not np.isfinite(o.forward(cfg, a, ids, 1, 32, "full_fp16")).all()
     assert np.isfinite(o.forward(cfg, a, ids, 1, 32, "hybrid")).all()
     assert np.isfinite(o.forward(cfg, a, ids, 1, 32, "fp32")).all()
+
+
+@pytest.mark.skipif(not have_reference_lib(), reason="oracle/_ref not built (needs /root/reference)")
+@pytest.mark.parametrize("policy", ["fp32", "hybrid", "full_fp16"])
+def test_oracle_classifier_and_taps_bit_identical_to_reference(policy):
+    """classifier_probs (model.cpp:484-526) and the retain_scores taps (model.cpp:393-427)
+    of the restatement equal the compiled reference bit for bit."""
+    from oracle.oracle import ModelConfig
+    o, r = oracle(), reference()
+    enc = ModelConfig(archetype=0, num_layers=2, hidden=128, heads=4, ffn=256, vocab=320,
+                      max_positions=160, seed=3)
+    p = o.build_model(enc)
+    ids = o.random_tokens(enc.vocab, 3, 40, 5)
+    a = o.classifier_probs(enc, p, ids, 3, 40, policy)
+    b = r.classifier_probs(enc, p, ids, 3, 40, policy)
+    assert np.array_equal(a.view(np.uint32), b.view(np.uint32))
+    dec = enc.replace(archetype=1)
+    p = o.build_model(dec)
+    lo, to = o.forward(dec, p, ids, 3, 40, policy, retain_scores=True)
+    lr, tr = r.forward_scores(dec, p, ids, 3, 40, policy)
+    assert np.array_equal(to.view(np.uint32), tr.view(np.uint32))
+    assert np.array_equal(np.nan_to_num(lo).view(np.uint32), np.nan_to_num(lr).view(np.uint32))
