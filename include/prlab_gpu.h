@@ -118,6 +118,31 @@ int prlab_gpu_random_tokens(int64_t vocab, int64_t batch, int64_t seq, uint64_t 
 int prlab_gpu_argmax_device(const void* d_logits, int32_t dtype, int64_t rows, int64_t n, int64_t ld,
                             int32_t* d_tokens, void* stream);
 
+/* ---- device-side logits reductions (src/fidelity.cpp) ----
+ * Per row of device logits [rows, ld] (out_dtype): d_nll (double, may be NULL) =
+ * -log_softmax(row)[d_targets[row]] evaluated like window_nll_sum (fidelity.cpp:213-240:
+ * max-stabilised, double accumulation; NaN when the row holds NaN/+inf; 0 when the
+ * target is < 0), d_argmax (may be NULL) = first index of the row maximum.  Async. */
+int prlab_gpu_row_nll_device(const void* d_logits, int32_t dtype, int64_t rows, int64_t n, int64_t ld,
+                              const int32_t* d_targets, double* d_nll, int32_t* d_argmax, void* stream);
+
+/* compare_logits (src/fidelity.cpp:11-37) of two device logit tensors; synchronous. */
+typedef struct {
+  double max_abs_error, mean_abs_error, cosine;
+  int32_t has_cosine; /* std::optional<double> cosine engaged */
+  uint64_t finite_pairs, candidate_nonfinite;
+  int32_t nan_affected;
+} prlab_logit_comparison;
+int prlab_gpu_compare_logits_device(const void* d_base, int32_t base_dtype, int64_t ld_base, const void* d_cand,
+                                    int32_t cand_dtype, int64_t ld_cand, int64_t rows, int64_t n, void* stream,
+                                    prlab_logit_comparison* out);
+
+/* perplexity (src/fidelity.cpp:248-279): sliding windows of context_len over a host
+ * token stream, forwards batched on the device, next-token NLL reduced on the device
+ * (only one double per row crosses PCIe).  Same validation and messages. */
+int prlab_gpu_perplexity(prlab_gpu_model* m, const int32_t* tokens, int64_t n_tokens, int64_t context_len,
+                         const prlab_policy* policy, double* ppl);
+
 /* ---- forward (src/model.cpp:456-482) ----
  * Drop-in form: host token ids [B*S], host fp32 logits [B,S,V] (or [B,S,h]
  * for a zero-layer model), synchronous.  trace may be NULL. */

@@ -425,6 +425,19 @@ class Reference:
             raise ValueError(L.ref_last_error().decode())
         return out
 
+    def perplexity(self, c: ModelConfig, params, stream, context_len, policy) -> float:
+        """prlab::perplexity (src/fidelity.cpp:248-279)."""
+        L = self.lib
+        L.ref_perplexity.argtypes = ([C.c_int] + [C.c_int64] * 6 +
+                                     [C.POINTER(C.c_float), C.POINTER(C.c_int32), C.c_int64, C.c_int64,
+                                      C.c_char_p, C.POINTER(C.c_double)])
+        out = C.c_double()
+        stream = np.ascontiguousarray(stream, dtype=np.int32)
+        if L.ref_perplexity(*self._c(c), _fp(params), _ip(stream), stream.size, context_len,
+                            policy.encode(), C.byref(out)):
+            raise ValueError(L.ref_last_error().decode())
+        return out.value
+
     def make_adversarial_model(self, c: ModelConfig, probe_ids, batch, seq, target=30.0):
         L = self.lib
         L.ref_make_adversarial_model.argtypes = ([C.c_int] + [C.c_int64] * 6 +
@@ -508,3 +521,33 @@ def compare_logits(baseline: np.ndarray, candidate: np.ndarray) -> dict:
         if na > 0 and nb > 0:
             r["cosine"] = float((b * c).sum() / (np.sqrt(na) * np.sqrt(nb)))
     return r
+
+
+def window_nll_sum(logits: np.ndarray, window: np.ndarray) -> float:
+    """window_nll_sum (src/fidelity.cpp:213-240) restated in numpy double: positions
+    0..S-2 predict their successors; max-stabilised log-softmax; a non-finite row max
+    poisons the sum with NaN."""
+    seq, vocab = logits.shape[-2], logits.shape[-1]
+    rows = logits.reshape(seq, vocab)
+    nll = 0.0
+    for t in range(seq - 1):
+        row = rows[t].astype(np.float64)
+        mx = np.max(row) if not np.isnan(row).all() else np.nan
+        if not np.isfinite(mx):
+            return float("nan")
+        denom = float(np.sum(np.exp(row - mx)))
+        nll -= (row[int(window[t + 1])] - mx) - np.log(denom)
+    return float(nll)
+
+
+def perplexity_windows(forward_fn, stream: np.ndarray, context_len: int) -> float:
+    """perplexity (src/fidelity.cpp:248-279) over a forward_fn(ids, seq) -> [1, seq, V]."""
+    nll, predicted = 0.0, 0
+    for off in range(0, len(stream), context_len):
+        n = min(context_len, len(stream) - off)
+        if n < 2:
+            break
+        w = stream[off:off + n]
+        nll += window_nll_sum(forward_fn(w, n), w)
+        predicted += n - 1
+    return float(np.exp(nll / predicted))

@@ -10,6 +10,7 @@
 // No reference source is copied here; this file only calls its public API
 // (include/prlab/{kernels,model,policy,fidelity}.hpp).
 #include <cstring>
+#include <span>
 #include <exception>
 #include <stdexcept>
 #include <string>
@@ -200,6 +201,20 @@ int ref_classifier_probs(int archetype, int64_t L, int64_t h, int64_t H, int64_t
     return fail(e, -1);
   } catch (const std::exception& e) {
     return fail(e, -3);
+  }
+}
+
+// prlab::perplexity (src/fidelity.cpp:248-279)
+int ref_perplexity(int archetype, int64_t L, int64_t h, int64_t H, int64_t f, int64_t V, int64_t P,
+                   const float* params, const int32_t* stream, int64_t n, int64_t context_len, const char* policy,
+                   double* out) {
+  try {
+    const prlab::Model m = model_from_flat(make_cfg(archetype, L, h, H, f, V, P, 0), params);
+    *out = prlab::perplexity(m, std::span<const int32_t>(stream, static_cast<size_t>(n)), context_len,
+                             prlab::resolve_policy(policy));
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, -1);
   }
 }
 

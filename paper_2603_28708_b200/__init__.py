@@ -64,6 +64,20 @@ class _ModelDesc(C.Structure):
                 ("max_positions", C.c_int64), ("seed", C.c_uint64)]
 
 
+class LogitComparison(C.Structure):
+    """compare_logits result (include/prlab/fidelity.hpp:20-27)."""
+    _fields_ = [("max_abs_error", C.c_double), ("mean_abs_error", C.c_double), ("cosine", C.c_double),
+                ("has_cosine", C.c_int32), ("finite_pairs", C.c_uint64),
+                ("candidate_nonfinite", C.c_uint64), ("nan_affected", C.c_int32)]
+
+    def as_dict(self):
+        return {"max_abs_error": self.max_abs_error, "mean_abs_error": self.mean_abs_error,
+                "cosine": self.cosine if self.has_cosine else None,
+                "finite_pairs": int(self.finite_pairs),
+                "candidate_nonfinite": int(self.candidate_nonfinite),
+                "nan_affected": bool(self.nan_affected)}
+
+
 class Trace(C.Structure):
     """Reference ForwardTrace instrumentation (include/prlab/model.hpp:113-125)."""
     _fields_ = [("seconds", C.c_double * 7), ("kernel_calls", (C.c_uint64 * 2) * 7)]
@@ -149,6 +163,12 @@ EXPORTS = [
                                     _FP, C.POINTER(Trace)]),
     ("prlab_gpu_forward_ex", C.c_int, [_P, _IP, C.c_int64, C.c_int64, C.POINTER(PrecisionPolicy),
                                        C.c_int32, _FP, C.POINTER(Trace), _FP]),
+    ("prlab_gpu_row_nll_device", C.c_int, [_P, C.c_int32, C.c_int64, C.c_int64, C.c_int64, _P, _P,
+                                           _P, _P]),
+    ("prlab_gpu_compare_logits_device", C.c_int, [_P, C.c_int32, C.c_int64, _P, C.c_int32, C.c_int64,
+                                                  C.c_int64, C.c_int64, _P, C.POINTER(LogitComparison)]),
+    ("prlab_gpu_perplexity", C.c_int, [_P, _IP, C.c_int64, C.c_int64, C.POINTER(PrecisionPolicy),
+                                       C.POINTER(C.c_double)]),
     ("prlab_gpu_classifier_probs", C.c_int, [_P, _IP, C.c_int64, C.c_int64,
                                              C.POINTER(PrecisionPolicy), _FP]),
     ("prlab_gpu_forward_device", C.c_int, [_P, _P, C.c_int64, C.c_int64,
@@ -347,6 +367,15 @@ class DeviceModel:
                                                 C.byref(pol), _f(out)))
         return out
 
+    def perplexity(self, tokens, context_len: int, policy="hybrid") -> float:
+        """perplexity (src/fidelity.cpp:248-279) with the NLL reduced on the device."""
+        tokens = _arr(tokens, np.int32)
+        out = C.c_double()
+        pol = _policy(policy)
+        _check(lib().prlab_gpu_perplexity(self._h, tokens.ctypes.data_as(_IP), tokens.size, context_len,
+                                          C.byref(pol), C.byref(out)))
+        return float(out.value)
+
     def forward_device(self, d_ids: int, batch: int, seq: int, policy, d_out: int,
                        out_dtype: int, ld: int, stream: int = 0, use_graph: bool = True):
         """Device-resident forward: raw device pointers (e.g. torch .data_ptr())."""
@@ -488,3 +517,28 @@ def header_symbols(path: str = HEADER_PATH) -> Sequence[str]:
     import re
     src = open(path).read()
     return sorted(set(re.findall(r"\b(prlab_gpu_[a-z0-9_]+)\s*\(", src)))
+
+
+def row_nll_device(logits, targets, nll, argmax=None, rows=None, n=None, ld=None, stream=0):
+    """Per-row next-token NLL / argmax over device logits (torch tensors on cuda)."""
+    import torch  # noqa: F401  (device tensors)
+    dtype = OUT_F16 if str(logits.dtype) == "torch.float16" else OUT_F32
+    rows = logits.shape[0] if rows is None else rows
+    ld = logits.shape[1] if ld is None else ld
+    n = ld if n is None else n
+    _check(lib().prlab_gpu_row_nll_device(C.c_void_p(logits.data_ptr()), dtype, rows, n, ld,
+                                          C.c_void_p(targets.data_ptr()) if targets is not None else None,
+                                          C.c_void_p(nll.data_ptr()) if nll is not None else None,
+                                          C.c_void_p(argmax.data_ptr()) if argmax is not None else None,
+                                          C.c_void_p(stream)))
+
+
+def compare_logits_device(base, cand, rows, n, stream=0) -> dict:
+    """compare_logits (src/fidelity.cpp:11-37) of two device logit tensors [rows, ld]."""
+    def dt(t):
+        return OUT_F16 if str(t.dtype) == "torch.float16" else OUT_F32
+    r = LogitComparison()
+    _check(lib().prlab_gpu_compare_logits_device(C.c_void_p(base.data_ptr()), dt(base), base.shape[1],
+                                                 C.c_void_p(cand.data_ptr()), dt(cand), cand.shape[1],
+                                                 rows, n, C.c_void_p(stream), C.byref(r)))
+    return r.as_dict()

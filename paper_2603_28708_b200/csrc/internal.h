@@ -144,6 +144,12 @@ void simt_softmax(const float* x, int64_t rows, int64_t n, Kcfg cfg, float* out,
 void simt_gelu(const float* x, int64_t n, Kcfg cfg, float* out, cudaStream_t st);
 void simt_add(const float* a, const float* b, int64_t n, Kcfg cfg, float* out, cudaStream_t st);
 void simt_tanh(const float* x, int64_t n, Kcfg cfg, float* out, cudaStream_t st);
+// device logits reductions (logits_reduce.cu): per row NLL of targets[row] (skipped
+// when < 0; double) and argmax; compare_logits partials [rows][7]
+void row_nll(const void* logits, int dtype, int64_t rows, int64_t n, int64_t ld, const int32_t* targets,
+             double* nll, int32_t* amax, cudaStream_t st);
+void compare_rows(const void* base, int base_dtype, int64_t ldb, const void* cand, int cand_dtype, int64_t ldc,
+                  int64_t rows, int64_t n, double* part, cudaStream_t st);
 // classifier mean pool over the sequence (x32 or x16 [B*S, h]) -> out [B, h] fp32
 void simt_pool_mean(const float* x32, const __half* x16, int B, int S, int h, Kcfg lin, float* out,
                     cudaStream_t st);

@@ -885,6 +885,116 @@ int prlab_gpu_argmax_device(const void* d_logits, int32_t dtype, int64_t rows, i
   });
 }
 
+int prlab_gpu_row_nll_device(const void* d_logits, int32_t dtype, int64_t rows, int64_t n, int64_t ld,
+                              const int32_t* d_targets, double* d_nll, int32_t* d_argmax, void* stream) {
+  return guarded([&] {
+    if (dtype != PRLAB_OUT_F32 && dtype != PRLAB_OUT_F16) throw std::invalid_argument("unknown logits dtype");
+    if (n < 1 || ld < n) throw std::invalid_argument("logits row extent / pitch");
+    row_nll(d_logits, dtype, rows, n, ld, d_targets, d_nll, d_argmax, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int prlab_gpu_compare_logits_device(const void* d_base, int32_t base_dtype, int64_t ld_base, const void* d_cand,
+                                    int32_t cand_dtype, int64_t ld_cand, int64_t rows, int64_t n, void* stream,
+                                    prlab_logit_comparison* out) {
+  return guarded([&] {
+    for (int d : {base_dtype, cand_dtype})
+      if (d != PRLAB_OUT_F32 && d != PRLAB_OUT_F16) throw std::invalid_argument("unknown logits dtype");
+    if (rows < 0 || n < 0 || ld_base < n || ld_cand < n) throw std::invalid_argument("logits extents / pitches");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    std::vector<double> h(static_cast<size_t>(rows * 7));
+    if (rows > 0 && n > 0) {
+      TmpDev part(rows * 7 * sizeof(double));
+      compare_rows(d_base, base_dtype, ld_base, d_cand, cand_dtype, ld_cand, rows, n, static_cast<double*>(part.p), st);
+      PRLAB_CUDA(cudaMemcpyAsync(h.data(), part.p, h.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+      PRLAB_CUDA(cudaStreamSynchronize(st));
+    }
+    // fold the rows in order (compare_logits, src/fidelity.cpp:11-37)
+    double mx = 0.0, se = 0.0, dot = 0.0, na = 0.0, nb = 0.0;
+    uint64_t fin = 0, bad = 0;
+    for (int64_t r = 0; r < rows; ++r) {
+      const double* q = &h[static_cast<size_t>(r * 7)];
+      mx = std::max(mx, q[0]);
+      se += q[1];
+      dot += q[2];
+      na += q[3];
+      nb += q[4];
+      fin += static_cast<uint64_t>(q[5]);
+      bad += static_cast<uint64_t>(q[6]);
+    }
+    std::memset(out, 0, sizeof(*out));
+    out->max_abs_error = mx;
+    out->finite_pairs = fin;
+    out->candidate_nonfinite = bad;
+    out->nan_affected = bad > 0;
+    if (fin > 0) {
+      out->mean_abs_error = se / static_cast<double>(fin);
+      if (na > 0.0 && nb > 0.0) {
+        out->cosine = dot / (std::sqrt(na) * std::sqrt(nb));
+        out->has_cosine = 1;
+      }
+    }
+  });
+}
+
+int prlab_gpu_perplexity(prlab_gpu_model* m, const int32_t* tokens, int64_t n_tokens, int64_t context_len,
+                         const prlab_policy* policy, double* ppl) {
+  return guarded([&] {
+    // validation and messages as perplexity() (src/fidelity.cpp:248-263)
+    if (m->d.archetype != 1) throw std::invalid_argument("perplexity needs a decoder_only model");
+    if (context_len < 2) throw std::invalid_argument("context_len must be >= 2");
+    if (context_len > m->P)
+      throw std::invalid_argument("context_len " + std::to_string(context_len) + " exceeds max_positions " +
+                                  std::to_string(m->P));
+    if (n_tokens <= context_len)
+      throw std::invalid_argument("token stream of " + std::to_string(n_tokens) +
+                                  " is too short for context_len " + std::to_string(context_len) +
+                                  " (need context_len + 1)");
+    for (int64_t i = 0; i < n_tokens; ++i)
+      if (tokens[i] < 0 || tokens[i] >= m->V)
+        throw std::out_of_range("token id " + std::to_string(tokens[i]) + " outside vocab of " +
+                                std::to_string(m->V));
+    std::lock_guard<std::mutex> lk(m->mu);
+    validate_policy(*policy);
+    PRLAB_CUDA(cudaSetDevice(m->device));
+    cudaStream_t st = m->stream;
+    const int64_t V = m->V;
+    // windows [off, off + len): full ones batched (bounded logits buffer), then the tail
+    const int64_t nfull = n_tokens / context_len;
+    const int64_t tail = n_tokens - nfull * context_len;
+    double nll_sum = 0.0;
+    uint64_t predicted = 0;
+    auto run = [&](int64_t off, int64_t nwin, int64_t len) {
+      const int64_t rows = nwin * len;
+      auto& p = get_plan(*m, nwin, len, *policy);
+      std::vector<int32_t> tg(static_cast<size_t>(rows));
+      for (int64_t w = 0; w < nwin; ++w)
+        for (int64_t t = 0; t < len; ++t)
+          tg[static_cast<size_t>(w * len + t)] = t + 1 < len ? tokens[off + w * len + t + 1] : -1;
+      TmpDev dtg(rows * 4), dnll(rows * sizeof(double));
+      PRLAB_CUDA(cudaMemcpyAsync(p.ids, tokens + off, rows * 4, cudaMemcpyHostToDevice, st));
+      PRLAB_CUDA(cudaMemcpyAsync(dtg.p, tg.data(), rows * 4, cudaMemcpyHostToDevice, st));
+      enqueue_forward(*m, p, p.ids, p.out32, PRLAB_OUT_F32, V, st);  // logits stay on the device
+      row_nll(p.out32, 0, rows, V, V, static_cast<const int32_t*>(dtg.p), static_cast<double*>(dnll.p), nullptr, st);
+      std::vector<double> h(static_cast<size_t>(rows));
+      PRLAB_CUDA(cudaMemcpyAsync(h.data(), dnll.p, rows * sizeof(double), cudaMemcpyDeviceToHost, st));
+      PRLAB_CUDA(cudaStreamSynchronize(st));
+      for (int64_t w = 0; w < nwin; ++w) {  // window by window, positions in order
+        double win = 0.0;
+        for (int64_t t = 0; t + 1 < len; ++t) win += h[static_cast<size_t>(w * len + t)];
+        nll_sum += win;
+        predicted += static_cast<uint64_t>(len - 1);
+      }
+    };
+    const int64_t max_rows = std::max<int64_t>(context_len, (int64_t(1) << 31) / (V * 2));  // <= 2 GB of logits
+    const int64_t per_batch = std::max<int64_t>(1, std::min<int64_t>(64, max_rows / context_len));
+    for (int64_t w = 0; w < nfull; w += per_batch)
+      run(w * context_len, std::min(per_batch, nfull - w), context_len);
+    if (tail >= 2) run(nfull * context_len, 1, tail);
+    *ppl = std::exp(nll_sum / static_cast<double>(predicted));
+  });
+}
+
 int prlab_gpu_validate_policy(const prlab_policy* p) {
   return guarded([&] { validate_policy(*p); });
 }

@@ -157,3 +157,19 @@ def test_oracle_classifier_and_taps_bit_identical_to_reference(policy):
     lr, tr = r.forward_scores(dec, p, ids, 3, 40, policy)
     assert np.array_equal(to.view(np.uint32), tr.view(np.uint32))
     assert np.array_equal(np.nan_to_num(lo).view(np.uint32), np.nan_to_num(lr).view(np.uint32))
+
+
+@pytest.mark.skipif(not have_reference_lib(), reason="oracle/_ref not built (needs /root/reference)")
+@pytest.mark.parametrize("policy", ["fp32", "hybrid"])
+def test_perplexity_restatement_matches_reference(policy):
+    """perplexity / window_nll_sum (fidelity.cpp:213-279) restated over the oracle's
+    forward equals the compiled reference (double-precision log-softmax; numpy's exp may
+    differ from glibc's in the last ulp)."""
+    from oracle.oracle import perplexity_windows
+    o, r = oracle(), reference()
+    cfg = PRESETS["decoder_toy"]
+    p = o.build_model(cfg)
+    stream = o.random_tokens(cfg.vocab, 1, 150, 9)
+    want = r.perplexity(cfg, p, stream, 64, policy)
+    got = perplexity_windows(lambda w, n: o.forward(cfg, p, w, 1, n, policy), stream, 64)
+    assert abs(got - want) <= 1e-12 * want
