@@ -101,6 +101,12 @@ int prlab_gpu_model_create(const prlab_model_desc* desc, const float* const* par
 int prlab_gpu_model_create_flat(const prlab_model_desc* desc, const float* flat, int device,
                                 prlab_gpu_model** out);
 void prlab_gpu_model_destroy(prlab_gpu_model* m);
+/* load_checkpoint (src/checkpoint.cpp:133-162): a PRLABCKP v1 file (config JSON + tensor
+ * records in canonical order, f32 or f16 payloads) straight into the device arena; the
+ * file's config is returned in *desc (may be NULL).  Same checks and messages as the
+ * reference (PRLAB_ERUNTIME for format errors). */
+int prlab_gpu_model_load_checkpoint(const char* path, int device, prlab_model_desc* desc,
+                                    prlab_gpu_model** out);
 /* Bytes held on the device: resident weights (per precision copy) and the
  * activation workspace currently planned. */
 int prlab_gpu_model_memory(const prlab_gpu_model* m, uint64_t* weight_bytes,

@@ -180,8 +180,15 @@ class Oracle:
         self.lib.or_set_threads(n)
 
     # --- policies
-    def policy(self, name: str) -> _Policy:
+    def policy(self, name) -> _Policy:
+        """A named policy (resolve_policy, src/policy.cpp:49-67) or a custom per-class
+        assignment given as 7 (compute, accum, stabilized) triples in OpClass order
+        (the outcome of policy_from_spec, src/policy.cpp:69-116)."""
         p = _Policy()
+        if not isinstance(name, str):
+            for i, (cmp_, acc, stab) in enumerate(name):
+                p.cls[i] = _Kcfg(int(cmp_), int(acc), int(stab))
+            return p
         if self.lib.or_resolve_policy(name.encode(), C.byref(p)) != 0:
             raise ValueError(f"unknown policy '{name}' (valid: fp32, full_fp16, hybrid)")
         return p
@@ -437,6 +444,23 @@ class Reference:
                             policy.encode(), C.byref(out)):
             raise ValueError(L.ref_last_error().decode())
         return out.value
+
+    def serialize_checkpoint(self, c: ModelConfig, params, path: str, f16: bool = False):
+        """prlab::serialize_checkpoint (src/checkpoint.cpp:104-121)."""
+        L = self.lib
+        L.ref_serialize_checkpoint.argtypes = ([C.c_int] + [C.c_int64] * 6 +
+                                               [C.c_uint64, C.POINTER(C.c_float), C.c_int, C.c_char_p])
+        if L.ref_serialize_checkpoint(*self._c(c), c.seed, _fp(params), int(f16), path.encode()):
+            raise ValueError(L.ref_last_error().decode())
+
+    def load_checkpoint(self, path: str, c: ModelConfig) -> np.ndarray:
+        """prlab::load_checkpoint (src/checkpoint.cpp:133-162) -> flat canonical params."""
+        L = self.lib
+        L.ref_load_checkpoint.argtypes = [C.c_char_p, C.POINTER(C.c_float), C.c_int64]
+        out = np.empty(self.param_count(c), dtype=np.float32)
+        if L.ref_load_checkpoint(path.encode(), _fp(out), out.size):
+            raise ValueError(L.ref_last_error().decode())
+        return out
 
     def make_adversarial_model(self, c: ModelConfig, probe_ids, batch, seq, target=30.0):
         L = self.lib

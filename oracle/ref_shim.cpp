@@ -20,6 +20,7 @@
 #include "prlab/fidelity.hpp"
 #include "prlab/float16.hpp"
 #include "prlab/kernels.hpp"
+#include "prlab/checkpoint.hpp"
 #include "prlab/model.hpp"
 #include "prlab/policy.hpp"
 
@@ -212,6 +213,34 @@ int ref_perplexity(int archetype, int64_t L, int64_t h, int64_t H, int64_t f, in
     const prlab::Model m = model_from_flat(make_cfg(archetype, L, h, H, f, V, P, 0), params);
     *out = prlab::perplexity(m, std::span<const int32_t>(stream, static_cast<size_t>(n)), context_len,
                              prlab::resolve_policy(policy));
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, -1);
+  }
+}
+
+// serialize_checkpoint (src/checkpoint.cpp:104-121) of flat canonical params; dtype 0 f32, 1 f16
+int ref_serialize_checkpoint(int archetype, int64_t L, int64_t h, int64_t H, int64_t f, int64_t V, int64_t P,
+                             uint64_t seed, const float* params, int dtype, const char* path) {
+  try {
+    const prlab::Model m = model_from_flat(make_cfg(archetype, L, h, H, f, V, P, seed), params);
+    prlab::serialize_checkpoint(m, dtype ? prlab::Dtype::F16E : prlab::Dtype::F32, path);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, -1);
+  }
+}
+
+// load_checkpoint (src/checkpoint.cpp:133-162) -> flat canonical params
+int ref_load_checkpoint(const char* path, float* out, int64_t cap) {
+  try {
+    const prlab::Model m = prlab::load_checkpoint(path);
+    int64_t n = 0;
+    m.for_each_param([&](const std::string&, const prlab::Tensor& t) {
+      if (n + static_cast<int64_t>(t.data.size()) > cap) throw std::runtime_error("output too small");
+      std::memcpy(out + n, t.data.data(), t.data.size() * sizeof(float));
+      n += static_cast<int64_t>(t.data.size());
+    });
     return 0;
   } catch (const std::exception& e) {
     return fail(e, -1);

@@ -169,6 +169,7 @@ EXPORTS = [
                                                   C.c_int64, C.c_int64, _P, C.POINTER(LogitComparison)]),
     ("prlab_gpu_perplexity", C.c_int, [_P, _IP, C.c_int64, C.c_int64, C.POINTER(PrecisionPolicy),
                                        C.POINTER(C.c_double)]),
+    ("prlab_gpu_model_load_checkpoint", C.c_int, [C.c_char_p, C.c_int, _P, C.POINTER(C.c_void_p)]),
     ("prlab_gpu_classifier_probs", C.c_int, [_P, _IP, C.c_int64, C.c_int64,
                                              C.POINTER(PrecisionPolicy), _FP]),
     ("prlab_gpu_forward_device", C.c_int, [_P, _P, C.c_int64, C.c_int64,
@@ -311,6 +312,19 @@ class DeviceModel:
         d = config._desc()
         _check(lib().prlab_gpu_model_create_flat(C.byref(d), _f(flat), device, C.byref(h)))
         self._h = h
+
+    @classmethod
+    def from_checkpoint(cls, path: str, device: int = 0) -> "DeviceModel":
+        """load_checkpoint (src/checkpoint.cpp:133-162) straight into the device arena."""
+        self = cls.__new__(cls)
+        h = C.c_void_p()
+        d = _ModelDesc()
+        _check(lib().prlab_gpu_model_load_checkpoint(path.encode(), device, C.byref(d), C.byref(h)))
+        self._h = h
+        self.config = ModelConfig(archetype=d.archetype, num_layers=d.num_layers, hidden=d.hidden,
+                                  heads=d.heads, ffn=d.ffn, vocab=d.vocab,
+                                  max_positions=d.max_positions, seed=d.seed)
+        return self
 
     def close(self):
         if getattr(self, "_h", None):

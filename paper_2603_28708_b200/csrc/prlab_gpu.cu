@@ -21,6 +21,8 @@
 #include <vector>
 
 #include "../../include/prlab_gpu.h"
+#include <fstream>
+#include <cctype>
 #include "common.cuh"
 #include "internal.h"
 
@@ -239,6 +241,189 @@ std::vector<size_t> param_sizes(const prlab_model_desc& d) {
     s.push_back(2);
   }
   return s;
+}
+
+// Model::for_each_param canonical names and shapes (src/model.cpp:178-209)
+std::vector<std::pair<std::string, std::vector<int64_t>>> param_specs(const prlab_model_desc& d) {
+  const int64_t h = d.hidden, f = d.ffn;
+  std::vector<std::pair<std::string, std::vector<int64_t>>> s = {{"token_embedding", {d.vocab, h}},
+                                                                  {"position_embedding", {d.max_positions, h}}};
+  for (int64_t l = 0; l < d.num_layers; ++l) {
+    const std::string p = "layers." + std::to_string(l) + ".";
+    s.push_back({p + "ln1.gamma", {h}});
+    s.push_back({p + "ln1.beta", {h}});
+    s.push_back({p + "attn.wq", {h, h}});
+    s.push_back({p + "attn.bq", {h}});
+    s.push_back({p + "attn.wk", {h, h}});
+    s.push_back({p + "attn.bk", {h}});
+    s.push_back({p + "attn.wv", {h, h}});
+    s.push_back({p + "attn.bv", {h}});
+    s.push_back({p + "attn.wo", {h, h}});
+    s.push_back({p + "attn.bo", {h}});
+    s.push_back({p + "ln2.gamma", {h}});
+    s.push_back({p + "ln2.beta", {h}});
+    s.push_back({p + "ffn.w1", {h, f}});
+    s.push_back({p + "ffn.b1", {f}});
+    s.push_back({p + "ffn.w2", {f, h}});
+    s.push_back({p + "ffn.b2", {h}});
+  }
+  s.push_back({"final_ln.gamma", {h}});
+  s.push_back({"final_ln.beta", {h}});
+  if (d.archetype == 0) {
+    s.push_back({"pooler.weight", {h, h}});
+    s.push_back({"pooler.bias", {h}});
+    s.push_back({"classifier.weight", {h, 2}});
+    s.push_back({"classifier.bias", {2}});
+  }
+  return s;
+}
+
+std::string shape_str(const std::vector<int64_t>& v) {  // src/tensor.cpp:27-36
+  std::string o = "[";
+  for (size_t i = 0; i < v.size(); ++i) o += (i ? ", " : "") + std::to_string(v[i]);
+  return o + "]";
+}
+
+// binary16 -> fp32 (f16_decode, src/float16.cpp; exact for every non-NaN encoding)
+float f16_decode_host(uint16_t h) {
+  const uint32_t sign = (h & 0x8000u) << 16, e = (h >> 10) & 0x1Fu, m = h & 0x3FFu;
+  uint32_t u;
+  if (e == 0x1F) {
+    u = m ? 0x7FC00000u : (sign | 0x7F800000u);
+  } else if (e == 0) {
+    float v = static_cast<float>(m) * 5.9604644775390625e-08f;  // m * 2^-24, exact
+    std::memcpy(&u, &v, 4);
+    u |= sign;
+  } else {
+    u = sign | ((e + 112u) << 23) | (m << 13);
+  }
+  float x;
+  std::memcpy(&x, &u, 4);
+  return x;
+}
+
+// The flat JSON object config_to_json writes (src/model.cpp:148-176): string / integer
+// values only; "preset" names the reference presets (src/model.cpp:122-136).
+prlab_model_desc config_from_json(const std::string& js) {
+  std::map<std::string, std::string> kv;
+  size_t i = 0;
+  auto ws = [&] { while (i < js.size() && std::isspace(static_cast<unsigned char>(js[i]))) ++i; };
+  auto str = [&]() {
+    if (js[i] != '"') throw std::runtime_error("checkpoint config is not valid JSON");
+    std::string o;
+    for (++i; i < js.size() && js[i] != '"'; ++i) o += js[i];
+    ++i;
+    return o;
+  };
+  ws();
+  if (i >= js.size() || js[i] != '{') throw std::runtime_error("checkpoint config is not a JSON object");
+  ++i;
+  for (ws(); i < js.size() && js[i] != '}';) {
+    const std::string k = str();
+    ws();
+    if (js[i] != ':') throw std::runtime_error("checkpoint config is not valid JSON");
+    ++i;
+    ws();
+    std::string v;
+    if (js[i] == '"') {
+      v = str();
+    } else {
+      while (i < js.size() && js[i] != ',' && js[i] != '}' && !std::isspace(static_cast<unsigned char>(js[i]))) v += js[i++];
+    }
+    kv[k] = v;
+    ws();
+    if (js[i] == ',') ++i;
+    ws();
+  }
+  prlab_model_desc d{};
+  auto preset = [&](const std::string& n) {
+    if (n == "bert_base") d = {0, 12, 768, 12, 3072, 30522, 512, 0};
+    else if (n == "gpt2_small") d = {1, 12, 768, 12, 3072, 50257, 1024, 0};
+    else if (n == "encoder_toy") d = {0, 4, 128, 4, 256, 320, 160, 0};
+    else if (n == "decoder_toy") d = {1, 4, 128, 4, 256, 320, 160, 0};
+    else
+      throw std::invalid_argument("unknown model preset '" + n + "' (valid: bert_base, gpt2_small, encoder_toy, decoder_toy)");
+  };
+  d = {1, 0, 0, 0, 0, 0, 0, 0};  // ModelConfig defaults (include/prlab/model.hpp:21-29)
+  if (kv.count("preset")) preset(kv["preset"]);
+  if (kv.count("archetype")) {
+    if (kv["archetype"] == "encoder_only") d.archetype = 0;
+    else if (kv["archetype"] == "decoder_only") d.archetype = 1;
+    else throw std::invalid_argument("unknown archetype '" + kv["archetype"] + "' (expected encoder_only or decoder_only)");
+  }
+  auto num = [&](const char* k, int64_t& dst) { if (kv.count(k)) dst = std::stoll(kv[k]); };
+  num("num_layers", d.num_layers);
+  num("hidden", d.hidden);
+  num("heads", d.heads);
+  num("ffn", d.ffn);
+  num("vocab", d.vocab);
+  num("max_positions", d.max_positions);
+  if (kv.count("seed")) d.seed = std::stoull(kv["seed"]);
+  validate_desc(d);
+  return d;
+}
+
+// load_checkpoint (src/checkpoint.cpp:133-162): PRLABCKP v1, config JSON, tensor records
+// in canonical order; f16 payloads are decoded exactly (they land on the fp16 arena as-is).
+std::vector<std::vector<float>> read_checkpoint(const std::string& path, prlab_model_desc& desc) {
+  std::ifstream in(path, std::ios::binary);
+  if (!in) throw std::runtime_error("cannot open checkpoint: " + path);
+  auto get_u32 = [&](const std::string& what) {
+    unsigned char b[4];
+    if (!in.read(reinterpret_cast<char*>(b), 4)) throw std::runtime_error("checkpoint truncated while reading " + what);
+    return static_cast<uint32_t>(b[0]) | (static_cast<uint32_t>(b[1]) << 8) | (static_cast<uint32_t>(b[2]) << 16) |
+           (static_cast<uint32_t>(b[3]) << 24);
+  };
+  auto get_u64 = [&](const std::string& what) {
+    const uint64_t lo = get_u32(what), hi = get_u32(what);
+    return lo | (hi << 32);
+  };
+  char magic[8];
+  if (!in.read(magic, 8) || std::memcmp(magic, "PRLABCKP", 8) != 0)
+    throw std::runtime_error("not a checkpoint (bad magic): " + path);
+  const uint32_t version = get_u32("format version");
+  if (version != 1) throw std::runtime_error("unsupported checkpoint version " + std::to_string(version));
+  const uint32_t cfg_len = get_u32("config length");
+  std::string cfg(cfg_len, '\0');
+  if (!in.read(cfg.data(), cfg_len)) throw std::runtime_error("checkpoint truncated while reading config");
+  desc = config_from_json(cfg);
+  const auto specs = param_specs(desc);
+  std::vector<std::vector<float>> params;
+  params.reserve(specs.size());
+  for (const auto& sp : specs) {
+    const uint32_t name_len = get_u32("tensor name length");
+    std::string name(name_len, '\0');
+    if (!in.read(name.data(), name_len)) throw std::runtime_error("checkpoint truncated while reading tensor name");
+    if (name != sp.first) throw std::runtime_error("unexpected tensor '" + name + "' (wanted '" + sp.first + "')");
+    const int tag = in.get();
+    if (tag != 0 && tag != 1)
+      throw std::runtime_error("tensor '" + name + "' has unknown dtype tag " + std::to_string(tag));
+    const uint32_t rank = get_u32("tensor rank");
+    std::vector<int64_t> shape(rank);
+    int64_t numel = 1;
+    for (uint32_t r = 0; r < rank; ++r) {
+      shape[r] = static_cast<int64_t>(get_u64("tensor extent"));
+      numel *= shape[r];
+    }
+    std::vector<float> t(static_cast<size_t>(numel));
+    if (tag == 0) {
+      for (auto& v : t) {
+        const uint32_t u = get_u32("tensor payload");
+        std::memcpy(&v, &u, 4);
+      }
+    } else {
+      std::vector<unsigned char> raw(static_cast<size_t>(numel) * 2);
+      if (!in.read(reinterpret_cast<char*>(raw.data()), static_cast<std::streamsize>(raw.size())))
+        throw std::runtime_error("checkpoint truncated while reading tensor payload");
+      for (size_t k = 0; k < t.size(); ++k)
+        t[k] = f16_decode_host(static_cast<uint16_t>(raw[2 * k] | (raw[2 * k + 1] << 8)));
+    }
+    if (shape != sp.second)
+      throw std::runtime_error("tensor '" + name + "' has shape " + shape_str(shape) + ", expected " +
+                               shape_str(sp.second));
+    params.push_back(std::move(t));
+  }
+  return params;
 }
 }  // namespace
 
@@ -992,6 +1177,17 @@ int prlab_gpu_perplexity(prlab_gpu_model* m, const int32_t* tokens, int64_t n_to
       run(w * context_len, std::min(per_batch, nfull - w), context_len);
     if (tail >= 2) run(nfull * context_len, 1, tail);
     *ppl = std::exp(nll_sum / static_cast<double>(predicted));
+  });
+}
+
+int prlab_gpu_model_load_checkpoint(const char* path, int device, prlab_model_desc* desc, prlab_gpu_model** out) {
+  return guarded([&] {
+    prlab_model_desc d{};
+    const auto params = read_checkpoint(path, d);
+    std::vector<const float*> ptrs;
+    for (const auto& t : params) ptrs.push_back(t.data());
+    *out = create_model(d, ptrs.data(), static_cast<int64_t>(ptrs.size()), device);
+    if (desc) *desc = d;
   });
 }
 

@@ -95,3 +95,34 @@ def test_classifier_probs_rejects_decoder():
     ids = oracle().random_tokens(cfg.vocab, 1, 8, 1)
     with pytest.raises(ValueError, match="encoder_only"):
         m.classifier_probs(ids, 1, 8, "hybrid")
+
+
+# policy_from_spec (src/policy.cpp:69-116) outcomes: per-class assignments beyond the
+# three named policies run the generic per-class SIMT path with the same rounding points
+CUSTOM = {
+    # hybrid with an fp32 attention block (overrides.AttentionScoreMatmul + Softmax)
+    "hybrid_fp32_attention": [(1, 0, 1), (0, 0, 1), (0, 0, 1), (0, 0, 1), (1, 0, 1), (0, 0, 1), (0, 0, 1)],
+    # fp32 with fp16-lattice linears accumulating in fp32
+    "fp32_f16_linears": [(1, 0, 1), (0, 0, 1), (0, 0, 1), (0, 0, 1), (0, 0, 1), (0, 0, 1), (0, 0, 1)],
+    # hybrid with a narrow (F16E-accumulating) LayerNorm
+    "hybrid_narrow_ln": [(1, 0, 1), (1, 0, 1), (0, 0, 1), (1, 1, 1), (1, 0, 1), (0, 0, 1), (0, 0, 1)],
+}
+
+
+@pytest.mark.parametrize("name", sorted(CUSTOM))
+@pytest.mark.parametrize("cfg", [PRESETS["decoder_toy"], PRESETS["encoder_toy"]], ids=["dec", "enc"])
+def test_custom_policy_matches_oracle(name, cfg):
+    o = oracle()
+    m = device_model(cfg)
+    spec = CUSTOM[name]
+    pol = pg.PrecisionPolicy()
+    for i, (c_, a_, s_) in enumerate(spec):
+        pol.cls[i] = pg.KernelConfig(c_, a_, s_)
+    pg._check(pg.lib().prlab_gpu_validate_policy(pg.C.byref(pol)) if hasattr(pg, "C") else 0)
+    ids = o.random_tokens(cfg.vocab, 2, 24, 8)
+    p = model_params(cfg)
+    want = o.forward(cfg, p, ids, 2, 24, spec)
+    got = m.forward(ids, 2, 24, pol)
+    cmp = compare_logits(want, got)
+    assert cmp["candidate_nonfinite"] == 0
+    assert cmp["max_abs_error"] <= 5e-3 * float(np.abs(want).max()) and cmp["cosine"] >= 0.99999, cmp
