@@ -377,6 +377,17 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
       "l"(reinterpret_cast<uint64_t>(m)), "r"(to_leader(smem_u32(bar))), "r"(c0), "r"(c1)
       : "memory");
 }
+// Pair TMA load multicast to the CTAs in `mask` (cluster-relative ranks): each
+// destination receives the box at the same shared offset and the transaction bytes
+// complete on the mbarrier of its pair's leader (same offset).
+__device__ __forceinline__ void tma_load_2d_pair_mc(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1,
+                                                    uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+      "[%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(to_leader(smem_u32(bar))), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
 // arrive on a barrier of another CTA of the cluster (shared::cluster address).
 // Default (CTA-scope release) semantics: the data these arrivals announce is either
 // tracked by TMA transaction bytes or ordered by tcgen05 fences, so no cluster-scope
@@ -405,12 +416,12 @@ __device__ __forceinline__ void umma_f16_ss_pair(uint32_t d_tmem, uint64_t a_des
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-// commit to the same-offset mbarrier in both CTAs of the pair
-__device__ __forceinline__ void umma_commit_pair(uint64_t* bar) {
+// commit to the same-offset mbarrier in the CTAs of `mask` (cluster-relative ranks;
+// default: both CTAs of a pair in a 2-CTA cluster)
+__device__ __forceinline__ void umma_commit_pair(uint64_t* bar, uint16_t mask = 3) {
   asm volatile(
-      "{\n\t.reg .b16 m;\n\tmov.b16 m, 3;\n\t"
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], m;\n\t}" ::"r"(
-          smem_u32(bar))
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)), "h"(mask)
       : "memory");
 }
 

@@ -808,7 +808,11 @@ struct Cfg2 {
   static constexpr size_t SMEM = 1024 + BIAS_OFF + BIAS_BYTES;
 };
 
-template <int BN, int EPI>
+// MC: clusters of 4 = two CTA pairs on adjacent m-pairs of the same n-block; each CTA
+// loads a quarter of the weight tile and multicasts it to the matching CTA of the other
+// pair, so the per-CTA weight traffic from L2 halves (the main loop is L2-feed bound:
+// scripts/gemm_probe.py).  Stage release (empty) then needs both pairs' MMA commits.
+template <int BN, int EPI, bool MC = false>
 __global__ void __launch_bounds__(Cfg2<BN, EPI>::THREADS, 1)
     gemm_tc2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     const __grid_constant__ CUtensorMap tmC, const GemmArgs g) {
@@ -825,12 +829,20 @@ __global__ void __launch_bounds__(Cfg2<BN, EPI>::THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const uint32_t warp = warp_id(), lane = lane_id();
-  const uint32_t rank = cluster_ctarank();
+  const uint32_t crank = cluster_ctarank();
+  const uint32_t rank = crank & 1;           // rank inside the pair
+  const uint32_t pp = MC ? (crank >> 1) : 0; // pair inside the cluster
   const bool leader = rank == 0;
-  // work unit = (pair of m-blocks, n-block); pairs stride by the number of clusters
-  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  // work unit = (pair of m-blocks, n-block) -- with MC (quad of m-blocks, n-block), the
+  // cluster's two pairs taking the two m-pairs; units stride by the number of clusters
+  const int csize = MC ? 4 : 2;
+  const int pair = blockIdx.x / csize, npairs = gridDim.x / csize;
   const int m_pairs = (g.num_m_blocks + 1) / 2;
-  const int total_units = m_pairs * g.num_n_blocks;
+  const int m_units = MC ? (m_pairs + 1) / 2 : m_pairs;
+  const int total_units = m_units * g.num_n_blocks;
+  const uint16_t pair_mask = static_cast<uint16_t>(3u << (2 * pp));
+  const uint16_t all_mask = MC ? 0xF : 3;
+  const uint16_t mc_mask = static_cast<uint16_t>((1u << rank) | (1u << (2 + rank)));
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
@@ -838,7 +850,7 @@ __global__ void __launch_bounds__(Cfg2<BN, EPI>::THREADS, 1)
     if (g.tma_store) tma_prefetch_desc(&tmC);
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 2);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], MC ? 2 : 1);  // MC: both pairs' MMAs read this stage's weights
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&tfull[s], 1);
@@ -858,14 +870,23 @@ __global__ void __launch_bounds__(Cfg2<BN, EPI>::THREADS, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   auto coords = [&](int unit, int& mp, int& n_blk) {
-    // bands of group_m/2 m-pairs; n-blocks advance slowest inside a band
-    const int GROUP = g.group_m >> 1;
+    // bands of group_m/2 m-pairs (group_m/4 m-quads); n-blocks advance slowest inside a band
+    const int GROUP = MC ? max(1, g.group_m >> 2) : (g.group_m >> 1);
     const int band = unit / (GROUP * g.num_n_blocks);
     const int m0 = band * GROUP;
-    const int rows = min(GROUP, m_pairs - m0);
+    const int rows = min(GROUP, m_units - m0);
     const int local = unit - band * GROUP * g.num_n_blocks;
     n_blk = local / rows;
     mp = m0 + local % rows;
+    if (MC) mp = 2 * mp + static_cast<int>(pp);
+  };
+  // this CTA's weight rows: its half of the pair's tile (MC: a quarter, multicast)
+  auto load_b = [&](int stage, int kb, int n_blk) {
+    if (MC)
+      tma_load_2d_pair_mc(sB + stage * C::B_BYTES + pp * (C::B_BYTES / 2), &tmB, &full[stage], kb * BK,
+                          n_blk * BN + rank * (BN / 2) + pp * (BN / 4), mc_mask);
+    else
+      tma_load_2d_pair(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, n_blk * BN + rank * (BN / 2));
   };
 
   if (warp == 0) {
@@ -878,7 +899,7 @@ __global__ void __launch_bounds__(Cfg2<BN, EPI>::THREADS, 1)
         pre = min(C::STAGES, g.num_k_blocks);
         for (int i = 0; i < pre; ++i) {  // weight halves first (independent of the upstream kernel)
           if (leader) mbar_expect_tx(&full[i], 2 * C::STAGE_BYTES);
-          tma_load_2d_pair(sB + i * C::B_BYTES, &tmB, &full[i], i * BK, n_blk * BN + rank * (BN / 2));
+          load_b(i, i, n_blk);
         }
       }
       pdl_wait();
@@ -899,13 +920,12 @@ __global__ void __launch_bounds__(Cfg2<BN, EPI>::THREADS, 1)
               else mbar_arrive(&full[stage]);
             }
             if (!(g.dbg_noload & 1)) tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
-            if (!(g.dbg_noload & 2))
-              tma_load_2d_pair(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, n_blk * BN + rank * (BN / 2));
+            if (!(g.dbg_noload & 2)) load_b(stage, kb, n_blk);
           } else {
             mbar_wait(&empty[stage], phase ^ 1);
             if (leader) mbar_expect_tx(&full[stage], 2 * C::STAGE_BYTES);
             tma_load_2d_pair(sA + stage * C::A_BYTES, &tmA, &full[stage], kb * BK, m_blk * BM);
-            tma_load_2d_pair(sB + stage * C::B_BYTES, &tmB, &full[stage], kb * BK, n_blk * BN + rank * (BN / 2));
+            load_b(stage, kb, n_blk);
           }
           if (!leader) mbar_arrive_cluster(to_leader(smem_u32(&full[stage])));
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
@@ -934,12 +954,12 @@ __global__ void __launch_bounds__(Cfg2<BN, EPI>::THREADS, 1)
             for (int k = 0; k < BK / 16; ++k)
               umma_f16_ss_pair(d_tmem, sw128_desc(a0 + k * 32, 0, 1024), sw128_desc(b0 + k * 32, 0, 1024), idesc,
                                (kb > 0 || k > 0) ? 1u : 0u);
-            umma_commit_pair(&empty[stage]);
+            umma_commit_pair(&empty[stage], all_mask);
           }
           __syncwarp();
           if (++stage == C::STAGES) { stage = 0; phase ^= 1; }
         }
-        if (lane == 0) umma_commit_pair(&tfull[acc]);
+        if (lane == 0) umma_commit_pair(&tfull[acc], pair_mask);
         __syncwarp();
       }
       // the peer's last tempty arrivals must land before the leader retires
@@ -1032,9 +1052,10 @@ __global__ void __launch_bounds__(Cfg2<BN, EPI>::THREADS, 1)
 
 template <int BN, int EPI>
 void configure_pair_one() {
-  auto k = gemm_tc2_kernel<BN, EPI>;
-  PRLAB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(Cfg2<BN, EPI>::SMEM)));
+  for (auto k : {gemm_tc2_kernel<BN, EPI, false>, gemm_tc2_kernel<BN, EPI, true>}) {
+    PRLAB_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(Cfg2<BN, EPI>::SMEM)));
+  }
 }
 
 template <int BN>
@@ -1054,14 +1075,17 @@ void launch_pair_one(const GemmPlan& p, const GemmArgs& g, cudaStream_t st) {
   cfg.stream = st;
   cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.x = p.pair_mc ? 4 : 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
   attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 2;
-  PRLAB_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<BN, EPI>, p.tmA, p.tmB, p.tmC, g));
+  if (p.pair_mc)
+    PRLAB_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<BN, EPI, true>, p.tmA, p.tmB, p.tmC, g));
+  else
+    PRLAB_CUDA(cudaLaunchKernelEx(&cfg, gemm_tc2_kernel<BN, EPI, false>, p.tmA, p.tmB, p.tmC, g));
 }
 
 template <int BN>
@@ -1123,6 +1147,28 @@ SplitScratch& global_split_scratch() {
     PRLAB_CUDA(cudaMemset(s.tickets, 0, s.n_tickets * sizeof(int)));
   }
   return s;
+}
+
+// co-resident 4-CTA clusters of the ~200 KB pair kernel (GPC packing leaves SMs idle)
+int max_active_clusters4() {
+  static int n = 0;
+  if (n == 0) {
+    configure_gemm_tc();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(4 * 64);
+    cfg.blockDim = dim3(Cfg2<256, EPI_BIAS_F16>::THREADS);
+    cfg.dynamicSmemBytes = Cfg2<256, EPI_BIAS_F16>::SMEM;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 4;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    PRLAB_CUDA(cudaOccupancyMaxActiveClusters(&n, gemm_tc2_kernel<256, EPI_BIAS_F16, true>, &cfg));
+    n = std::max(n, 1);
+  }
+  return n;
 }
 
 GemmPlan plan_gemm_tc(const void* A, int64_t lda, const void* Wt, int64_t ldw, const float* bias,
@@ -1216,9 +1262,21 @@ GemmPlan plan_gemm_tc(const void* A, int64_t lda, const void* Wt, int64_t ldw, c
     if (!p.tma_store) p.pair = false;  // the pair kernel only has the TMA-store epilogue
   }
   if (p.pair) {
-    const int pair_units = ((mb + 1) / 2) * ((N + bn - 1) / bn);
-    p.grid = 2 * std::min(pair_units, sms / 2);
-    p.tmB = make_tmap_f16_2d(Wt, N, K, ldw, bn / 2, BK);
+    // two pairs per cluster sharing the weight tile (multicast) once there are >= 2 m-pairs
+    const int m_pairs = (mb + 1) / 2;
+    // Off by default: 4-CTA clusters only tile 132 of the 148 SMs (33 co-resident
+    // clusters, scripts/ubench/cluster_occ.cu), which costs more than the halved weight
+    // traffic saves (profiles/r01/gemm_probe_mc.jsonl).  PRLAB_GEMM_MC=1 enables it.
+    p.pair_mc = m_pairs >= 2 && std::getenv("PRLAB_GEMM_MC") != nullptr;
+    if (p.pair_mc) {
+      const int units = ((m_pairs + 1) / 2) * ((N + bn - 1) / bn);
+      p.grid = 4 * std::min(units, max_active_clusters4());
+      p.tmB = make_tmap_f16_2d(Wt, N, K, ldw, bn / 4, BK);
+    } else {
+      const int pair_units = m_pairs * ((N + bn - 1) / bn);
+      p.grid = 2 * std::min(pair_units, sms / 2);
+      p.tmB = make_tmap_f16_2d(Wt, N, K, ldw, bn / 2, BK);
+    }
   } else {
     p.tmB = make_tmap_f16_2d(Wt, N, K, ldw, bn, BK);
   }

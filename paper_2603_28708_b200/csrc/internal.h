@@ -73,6 +73,7 @@ struct GemmPlan {
   bool lean;
   bool cluster;  // split-K reduced through DSMEM inside a thread-block cluster
   bool pair;     // CTA-pair (cta_group::2) kernel, 256-row tiles
+  bool pair_mc;  // pair kernel in 4-CTA clusters: weight tile multicast to both pairs
   const float* bias;
   void* out;
   int64_t ldo;
