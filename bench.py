@@ -192,9 +192,9 @@ def run_reference_arm(args, wl):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
-def kernel_profile(pg, torch, cfg, B, S, stream, reps=20):
-    """Per-kernel device times of one forward's kernels, each timed standalone
-    with CUDA events on the launching stream (inputs resident)."""
+def kernel_profile(pg, torch, cfg, B, S, stream, reps=20, causal=1):
+    """Per-kernel device times of one forward's kernels (inputs resident): each kernel
+    replayed `reps` times from a CUDA graph, CUDA events on the stream it runs on."""
     M, h, f, V, H, hd = B * S, cfg.hidden, cfg.ffn, cfg.vocab, cfg.heads, cfg.hidden // cfg.heads
     dev = "cuda"
     g = torch.Generator(device=dev).manual_seed(0)
@@ -209,35 +209,57 @@ def kernel_profile(pg, torch, cfg, B, S, stream, reps=20):
     ld_head = (V + 7) // 8 * 8
     items = {
         # name: (launch fn, launches per forward, algorithmic bytes, flops)
-        "gemm_qkv": (lambda: pg.linear_f16_device(A, W, bias, out16, M, 3 * h, h, 3 * h, 0, stream),
+        "gemm_qkv": (lambda st: pg.linear_f16_device(A, W, bias, out16, M, 3 * h, h, 3 * h, 0, st),
                      L, 2 * (M * h + 3 * h * h + M * 3 * h), 2 * M * 3 * h * h),
-        "gemm_wo": (lambda: pg.linear_f16_device(A, W, bias, out32, M, h, h, h, 2, stream),
+        "gemm_wo": (lambda st: pg.linear_f16_device(A, W, bias, out32, M, h, h, h, 2, st),
                     L, 2 * (M * h + h * h) + 8 * M * h, 2 * M * h * h),
-        "gemm_ffn1": (lambda: pg.linear_f16_device(A, W, bias, out16, M, f, h, f, 1, stream),
+        "gemm_ffn1": (lambda st: pg.linear_f16_device(A, W, bias, out16, M, f, h, f, 1, st),
                       L, 2 * (M * h + h * f + M * f), 2 * M * h * f),
-        "gemm_ffn2": (lambda: pg.linear_f16_device(A, W, bias, out32, M, h, f, h, 2, stream),
+        "gemm_ffn2": (lambda st: pg.linear_f16_device(A, W, bias, out32, M, h, f, h, 2, st),
                       L, 2 * (M * f + h * f) + 8 * M * h, 2 * M * h * f),
-        "gemm_head": (lambda: pg.linear_f16_device(A, W, None, out16, M, V, h, ld_head, 3, stream),
+        "gemm_head": (lambda st: pg.linear_f16_device(A, W, None, out16, M, V, h, ld_head, 3, st),
                       1, 2 * (M * h + V * h + M * V), 2 * M * h * V),
-        "attention": (lambda: pg.attention_f16_device(qkv, ctx, B, S, H, hd, 1, stream),
+        "attention": (lambda st: pg.attention_f16_device(qkv, ctx, B, S, H, hd, causal, st),
                       L, 2 * (M * 3 * h + M * h), 4 * B * S * S * h),
     }
     res = {}
-    s = torch.cuda.current_stream()
+    # each kernel is replayed `reps` times from one CUDA graph (as in the forward: PDL-chained,
+    # no host launch gaps), timed with CUDA events on the stream the kernels run on
+    side = torch.cuda.Stream()
     for name, (fn, count, nbytes, flops) in items.items():
-        for _ in range(3):
-            fn()
-        torch.cuda.synchronize()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(s)
-        for _ in range(reps):
-            fn()
-        e1.record(s)
-        torch.cuda.synchronize()
+        with torch.cuda.stream(side):
+            sp = side.cuda_stream
+            for _ in range(3):
+                fn(sp)
+            side.synchronize()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, stream=side):
+                for _ in range(reps):
+                    fn(torch.cuda.current_stream().cuda_stream)
+            g.replay()
+            side.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(side)
+            g.replay()
+            e1.record(side)
+            side.synchronize()
         t = e0.elapsed_time(e1) / reps / 1000.0
         res[name] = {"us": t * 1e6, "per_forward": count, "bytes": nbytes, "flops": flops,
                      "share_us": t * 1e6 * count}
     return res
+
+
+def ncu_traffic(wl, kernel):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` at workload `wl`
+    (committed ncu capture summary), or None."""
+    path = os.path.join(ROOT, "profiles", "r01", "traffic.json")
+    try:
+        with open(path) as f:
+            t = json.load(f)
+        e = t[wl][kernel]
+        return {"dram_bytes": float(e["dram_bytes"]), "source": f"profiles/r01/traffic.json ({e['kernel']})"}
+    except Exception:
+        return None
 
 
 def run_ours(args, wl):
@@ -333,7 +355,8 @@ def run_ours(args, wl):
 
     # ---- roofline of the dominant kernel (standalone CUDA-event timing) ----
     pk = peaks()
-    prof = kernel_profile(pg, torch, cfg, B, S, sp) if not args.no_profile else {}
+    prof = (kernel_profile(pg, torch, cfg, B, S, sp, causal=int(cfg.archetype == 1))
+            if not args.no_profile else {})
     roof = None
     if prof:
         dom = max(prof, key=lambda k: prof[k]["share_us"])
@@ -352,6 +375,13 @@ def run_ours(args, wl):
                     "unit": "TFLOP/s", "frac": ach / pk["tflops"], "traffic": None,
                     "algorithmic_flops": d["flops"], "launch_us": d["us"]}
         roof["peak_source"] = pk["source"]
+        # DRAM bytes per launch of the same kernel from one `ncu --set full` capture of this
+        # workload (scripts/gpu_ncu_full.sh -> scripts/ncu_traffic.py -> profiles/r01/traffic.json)
+        tr = ncu_traffic(wl, dom)
+        if tr is not None:
+            roof["traffic"] = tr["dram_bytes"]
+            roof["traffic_source"] = tr["source"]
+            roof["traffic_over_algorithmic"] = tr["dram_bytes"] / d["bytes"]
         roof["breakdown_us_per_forward"] = {k: round(v["share_us"], 2) for k, v in prof.items()}
 
     # ---- CPU baseline: the reference on this host (rank 0, N=1 only) ----
