@@ -235,6 +235,8 @@ int prlab_gpu_attention_f16_device_dbg(const void* qkv, void* ctx, int64_t batch
 /* Debug: GEMM launches after this call write %globaltimer phase stamps ([grid][8] int64,
  * device memory) into dbg (NULL switches the stamps off). */
 int prlab_gpu_debug_gemm_stamps(long long* dbg);
+/* Debug: per-stage %globaltimer stamps of the batch-1 persistent forward, [stage][grid][2]. */
+int prlab_gpu_debug_small_stamps(long long* dbg);
 
 #ifdef __cplusplus
 }

@@ -1,0 +1,693 @@
+// Batch-1 forward as ONE persistent kernel (hybrid policy, M = B*S <= 128 rows,
+// S <= 128 keys): the 85 dependent steps of a GPT-2/BERT forward_hidden
+// (src/model.cpp:350-452) run as stages of a cooperative grid (one CTA per SM)
+// separated by grid-wide barriers, instead of 85 kernel launches whose fixed
+// launch/drain cost (~2.9 us each) dominates batch-1 latency.
+//
+// Per layer (tasks are spread over the CTAs; every stage reads only what the previous
+// stages wrote, so one barrier between stages is the whole synchronisation):
+//   QKV   xn16 . Wqkv^T     tcgen05 M=128 N=32 tiles, K split in 2 -> fp32 partials
+//   ATTN  per (batch, head, 16 queries): q/k/v = round16(round16(p0 + p1) + b) from the
+//         partials, scores round16(fp32 dot * 0.125), causal -inf, exact two-pass
+//         softmax, p = round16(e / sum), o = round16(sum_j p_j v_j) -> ctx16 (SIMT fp32;
+//         products of fp16 values are exact in fp32, kernels.cpp:85-168)
+//   WO    ctx16 . Wo^T      N=32 tiles x K/128 splits -> fp32 partials
+//   RLN2  per row: x += round16(round16(sum of partials) + bo); xn16 = round16(LN2(x))
+//   FFN1  xn16 . W1^T       N=32 tiles, full K, epilogue round16(gelu(round16(acc+b1)))
+//   FFN2  ff16 . W2^T       N=32 tiles x F/512 splits -> fp32 partials
+//   RLN1  per row: x += round16(round16(sum) + b2); xn16 = round16(LN(x)) with the next
+//         layer's LN1 (or the final LN) -- embed + LN1 of layer 0 is stage 0
+// The tied head stays a separate (PDL-chained) GEMM launch on xn16.
+// Rounding points are those of the multi-kernel path; the only
+// difference is the fp32 summation order (split-K partials, SIMT attention dots).
+#include <cstdlib>
+#include <cstring>
+#include <stdexcept>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace prlab_gpu {
+
+namespace {
+
+constexpr int kThreads = 256;            // warps 0-3: epilogue / TMEM quadrants; 4: TMA; 5: MMA
+constexpr int kTileN = 32;               // GEMM output columns per task
+constexpr int kStages = 8;               // A ring (the attention scratch aliases it)
+constexpr uint32_t kABytes = 128 * 64 * 2;         // 16 KB
+constexpr uint32_t kBBox = kTileN * 64 * 2;        // 4 KB per 64-wide k-block
+constexpr int kMaxKB = 16;                         // B for one task: <= 16 k-blocks (1024 of K)
+constexpr int kQB = 16;                            // queries per attention task
+
+constexpr int kKS = 68, kVS = 64;  // fp32 row strides of the staged K (16B-aligned, conflict-free LDS.128) and V
+struct SmemL {
+  static constexpr uint32_t A = 0;
+  static constexpr uint32_t B = A + kStages * kABytes;             // 64 KB
+  static constexpr uint32_t ATT = A;                               // attention scratch: the A ring is idle then
+  static constexpr uint32_t ATT_BYTES = (128 * kKS + 128 * kVS + 8 * 128) * 4;
+  static constexpr uint32_t BAR = B + kMaxKB * kBBox;
+};
+
+struct LayerW {
+  const float *ln1g, *ln1b, *ln2g, *ln2b;  // fp32 [h]
+  const float *bqkv, *bo, *b1, *b2;        // pre-rounded fp32
+  const __half *wqkv, *wo, *w1, *w2;       // fp16 K-major weights (L2 prefetch of the next layer)
+};
+
+constexpr int kMaxLayers = 48;
+// Everything the stages dereference lives in the (32 KB) kernel parameter space: the
+// tensor maps (TMA descriptors are fetched from param space) and the per-layer
+// parameter pointers, so no stage starts with a dependent global load.
+struct SmallArgs {
+  CUtensorMap maps[3 + 4 * kMaxLayers];  // xn16, ctx16, ff16, then per layer Wqkv, Wo, W1, W2
+  LayerW lw[kMaxLayers];
+  int M, B, S, h, f, H, L, V, causal;
+  int split_qkv, split_wo, split_ffn2;
+  const float *tok, *pos, *lnfg, *lnfb;
+  const int32_t* ids;
+  int* err;
+  float* x;
+  __half *xn16, *ctx16, *ff16;
+  float *qkvp, *part;            // partial sums [split][M][3h], [split][M][h]
+  unsigned* gbar;                // grid barrier counter (zeroed before each launch)
+  long long* dbg;                // optional [stage][grid][2] globaltimer (arrive, release)
+};
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// all CTAs are co-resident (cooperative launch, one CTA per SM).  Arrive = one
+// red.release.gpu (cumulative over the CTA's writes ordered by the bar.sync before it),
+// wait = ld.acquire.gpu polling by one thread.
+__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned& target, long long* dbg = nullptr) {
+  asm volatile("fence.proxy.async;" ::: "memory");  // generic writes (global, smem) before later async-proxy (TMA) accesses
+  __syncthreads();
+  const unsigned stage = target / gridDim.x;
+  target += gridDim.x;
+  if (threadIdx.x == 0) {
+    if (dbg) dbg[(static_cast<int64_t>(stage) * gridDim.x + blockIdx.x) * 2] = globaltimer();
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar) : "memory");
+    const long long t0 = clock64();
+    while (ld_acquire(bar) < target) {
+      if (clock64() - t0 > (1ll << 32)) {  // watchdog (~2 s): a protocol bug must trap, not hang
+        printf("prlab_gpu watchdog: grid barrier timeout block %d target %u seen %u\n", blockIdx.x, target,
+               ld_acquire(bar));
+        __trap();
+      }
+    }
+    if (dbg) dbg[(static_cast<int64_t>(stage) * gridDim.x + blockIdx.x) * 2 + 1] = globaltimer();
+  }
+  __syncthreads();
+}
+
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
+// Pull this layer's small fp32 vectors (LN gamma/beta, biases) into L2 -- spread over
+// the CTAs, one 128-byte line per thread -- so the row stages do not start with DRAM
+// misses on parameters the previous forward evicted.
+__device__ void prefetch_layer_params(const SmallArgs& a, const LayerW& w) {
+  const int h = a.h, f = a.f;
+  const float* vec[8] = {w.ln1g, w.ln1b, w.ln2g, w.ln2b, w.bqkv, w.bo, w.b1, w.b2};
+  const int len[8] = {h, h, h, h, 3 * h, h, f, h};
+  int idx = static_cast<int>(blockIdx.x * blockDim.x + threadIdx.x);
+  for (int v = 0; v < 8; ++v) {
+    const int lines = (len[v] + 31) / 32;
+    if (idx < lines) prefetch_l2(vec[v] + idx * 32);
+    idx -= lines;
+  }
+}
+// ... and the layer's fp16 weights (3h*h + h*h + 2*h*f halves, 14 MB for GPT-2), one
+// 128-byte line per prefetch, spread over the whole grid: the next layer streams from
+// HBM while this one computes, so its TMA weight loads hit L2
+__device__ void prefetch_layer_weights(const SmallArgs& a, const LayerW& w) {
+  const int64_t h = a.h, f = a.f;
+  const __half* mat[4] = {w.wqkv, w.wo, w.w1, w.w2};
+  const int64_t n[4] = {3 * h * h, h * h, f * h, h * f};
+  const int64_t nthr = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t tid = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (int m = 0; m < 4; ++m)
+    for (int64_t line = tid; line < n[m] / 64; line += nthr) prefetch_l2(mat[m] + line * 64);
+}
+
+__device__ __forceinline__ float block_sum(float v, float* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  float s = 0.0f;
+#pragma unroll
+  for (int w = 0; w < kThreads / 32; ++w) s += red[w];  // fixed order
+  return s;
+}
+
+// x (fp32 row, already final) -> round16(LN(x)) into xn16.  Two-pass fp32 statistics
+// like layernorm_lastdim (src/kernels.cpp:170-219): mean, population variance,
+// inv = 1/sqrt(var + eps), y = gamma*((x - mean)*inv) + beta.
+__device__ void ln_row(const float* xv, int nper, int h, const float* __restrict__ g, const float* __restrict__ b,
+                       __half* __restrict__ out, float* red) {
+  float gv[4], bv[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)  // parameter loads first: their latency overlaps the reductions
+    if (i < nper) {
+      gv[i] = g[threadIdx.x + i * kThreads];
+      bv[i] = b[threadIdx.x + i * kThreads];
+    }
+  float s = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (i < nper) s += xv[i];
+  const float mean = __fdiv_rn(block_sum(s, red), static_cast<float>(h));
+  float q = 0.0f;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (i < nper) {
+      const float d = __fsub_rn(xv[i], mean);
+      q = __fmaf_rn(d, d, q);
+    }
+  const float var = __fdiv_rn(block_sum(q, red), static_cast<float>(h));
+  const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, 1e-5f)));
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+    if (i < nper)
+      out[threadIdx.x + i * kThreads] =
+          __float2half_rn(__fadd_rn(__fmul_rn(gv[i], __fmul_rn(__fsub_rn(xv[i], mean), inv)), bv[i]));
+}
+
+struct Ctl {
+  uint64_t *full, *empty, *bfull, *accfull, *accempty;
+  uint32_t tmem;
+  uint32_t kc, tc;   // running k-block and task counters (barrier phases)
+  int bpref;         // the next task's weights were already requested (prefetch)
+};
+
+// Weights (B) of one task into smem: issued by the producer thread as soon as the
+// previous task's MMAs have consumed sB -- at the end of the previous stage, so the
+// DRAM latency of the weights hides under the grid barrier.
+template <int NT>
+__device__ void load_b(Ctl& c, uint8_t* smem, const CUtensorMap* mB, int n0, int k0, int nkb) {
+  if (threadIdx.x == 4 * 32) {
+    mbar_wait(c.accempty, (c.tc & 1) ^ 1);  // previous task's MMAs done reading sB
+    mbar_expect_tx(c.bfull, static_cast<uint32_t>(nkb) * NT * 128);
+    for (int kb = 0; kb < nkb; ++kb) tma_load_2d(smem + SmemL::B + kb * kBBox, mB, c.bfull, k0 + kb * 64, n0);
+  }
+  c.bpref = 1;
+}
+
+// One GEMM task: D[128 x NT] = A[:, k0:k0+64*nkb] . B[n0:n0+NT, same]^T, then `EPI`.
+// EPI 0: fp32 partial -> out32 (row pitch ld32); 1: round16(gelu(round16(round16(acc) + b)))
+// -> out16; 2: round16(round16(acc) + b) -> out16.
+template <int NT, int EPI>
+__device__ void gemm_task(const SmallArgs& a, uint8_t* smem, Ctl& c, const CUtensorMap* mA, const CUtensorMap* mB,
+                          int n0, int k0, int nkb, float* out32, int64_t ld32, const float* bias, __half* out16,
+                          int64_t ld16) {
+  const uint32_t warp = warp_id(), lane = lane_id();
+  uint8_t* sA = smem + SmemL::A;
+  uint8_t* sB = smem + SmemL::B;
+  if (!c.bpref) load_b<NT>(c, smem, mB, n0, k0, nkb);
+  c.bpref = 0;
+  if (warp == 4) {
+    if (lane == 0) {
+      for (int kb = 0; kb < nkb; ++kb) {
+        const uint32_t k = c.kc + kb, st = k % kStages;
+        mbar_wait(&c.empty[st], ((k / kStages) & 1) ^ 1);
+        mbar_expect_tx(&c.full[st], kABytes);
+        tma_load_2d(sA + st * kABytes, mA, &c.full[st], k0 + kb * 64, 0);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 5) {
+    if (lane == 0) {
+      long long* gs = (a.dbg && blockIdx.x == 0 && c.tc < 64) ? a.dbg + 220000 + c.tc * 8 : nullptr;
+      if (gs) gs[0] = globaltimer();
+      constexpr uint32_t idesc = idesc_f16_f32(128, NT, 0, 0);
+      mbar_wait(c.accempty, (c.tc & 1) ^ 1);  // epilogue of the previous task read TMEM
+      mbar_wait(c.bfull, c.tc & 1);
+      if (gs) gs[1] = globaltimer();
+      tc_fence_after();
+      for (int kb = 0; kb < nkb; ++kb) {
+        const uint32_t k = c.kc + kb, st = k % kStages;
+        mbar_wait(&c.full[st], (k / kStages) & 1);
+        if (gs && kb == 0) gs[2] = globaltimer();
+        tc_fence_after();
+        const uint32_t a0 = smem_u32(sA + st * kABytes), b0 = smem_u32(sB + kb * kBBox);
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          umma_f16_ss(c.tmem, sw128_desc(a0 + kk * 32, 0, 1024), sw128_desc(b0 + kk * 32, 0, 1024), idesc,
+                      (kb | kk) != 0);
+        umma_commit(&c.empty[st]);
+      }
+      umma_commit(c.accfull);
+      if (gs) gs[3] = globaltimer();
+    }
+    __syncwarp();
+  } else if (warp < 4) {
+    float bv[NT];
+    if (EPI != 0) {  // this tile's biases before the accumulator wait (their latency hides under the MMAs)
+#pragma unroll
+      for (int i = 0; i < NT / 4; ++i) {
+        const float4 b4 = reinterpret_cast<const float4*>(bias + n0)[i];
+        bv[4 * i] = b4.x;
+        bv[4 * i + 1] = b4.y;
+        bv[4 * i + 2] = b4.z;
+        bv[4 * i + 3] = b4.w;
+      }
+    }
+    mbar_wait(c.accfull, c.tc & 1);
+    if (a.dbg && blockIdx.x == 0 && c.tc < 64 && threadIdx.x == 0) a.dbg[220000 + c.tc * 8 + 4] = globaltimer();
+    tc_fence_after();
+    uint32_t u[NT];
+    if constexpr (NT == 32) {
+      tmem_ld32(c.tmem + ((warp * 32) << 16), u);
+    } else {
+      tmem_ld16(c.tmem + ((warp * 32) << 16), u);
+    }
+    tmem_wait_ld();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(c.accempty);
+    const int row = static_cast<int>(warp * 32 + lane);
+    if (row < a.M) {
+      if (EPI == 0) {
+        float4* o = reinterpret_cast<float4*>(out32 + static_cast<int64_t>(row) * ld32 + n0);
+#pragma unroll
+        for (int i = 0; i < NT / 4; ++i)
+          o[i] = make_float4(__uint_as_float(u[4 * i]), __uint_as_float(u[4 * i + 1]), __uint_as_float(u[4 * i + 2]),
+                             __uint_as_float(u[4 * i + 3]));
+      } else {
+        uint32_t pk[NT / 2];
+#pragma unroll
+        for (int i = 0; i < NT / 2; ++i) {
+          uint32_t hh = h2_add_rn(h2_pack_rn(__uint_as_float(u[2 * i]), __uint_as_float(u[2 * i + 1])),
+                                  h2_pack_rn(bv[2 * i], bv[2 * i + 1]));
+          if (EPI == 1) {
+            float x0, x1;
+            h2_unpack(hh, x0, x1);
+            gelu2_fast(x0, x1);
+            hh = h2_pack_rn(x0, x1);
+          }
+          pk[i] = hh;
+        }
+        uint4* o = reinterpret_cast<uint4*>(out16 + static_cast<int64_t>(row) * ld16 + n0);
+#pragma unroll
+        for (int i = 0; i < NT / 8; ++i) o[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+      }
+    }
+  }
+  if (a.dbg && blockIdx.x == 0 && c.tc < 64 && threadIdx.x == 0) a.dbg[220000 + c.tc * 8 + 5] = globaltimer();
+  c.kc += nkb;
+  c.tc += 1;
+}
+
+__device__ __forceinline__ float h2f_lo(uint32_t v) { return __half2float(__ushort_as_half(static_cast<unsigned short>(v & 0xFFFFu))); }
+__device__ __forceinline__ float h2f_hi(uint32_t v) { return __half2float(__ushort_as_half(static_cast<unsigned short>(v >> 16))); }
+
+// x[r] += round16(round16(sum_s part[s][r]) + bias); xn16[r] = round16(LN(x[r]))
+__device__ void residual_ln_row(const SmallArgs& a, int r, int nsplit, const float* bias, const float* g,
+                                const float* b, float* red, long long* ts = nullptr) {
+  const int h = a.h, nper = h / kThreads;
+  if (ts && threadIdx.x == 0) ts[0] = globaltimer();
+  float xv[4], pv[4][8], xo[4], bs[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {  // every load of the row in flight before the ordered sums
+    if (i < nper) {
+      const int cc = threadIdx.x + i * kThreads;
+#pragma unroll
+      for (int sp = 0; sp < 8; ++sp) pv[i][sp] = sp < nsplit ? a.part[(static_cast<int64_t>(sp) * a.M + r) * h + cc] : 0.0f;
+      xo[i] = a.x[static_cast<int64_t>(r) * h + cc];
+      bs[i] = bias[cc];
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    if (i < nper) {
+      float sum = 0.0f;
+#pragma unroll
+      for (int sp = 0; sp < 8; ++sp)
+        if (sp < nsplit) sum = __fadd_rn(sum, pv[i][sp]);
+      xv[i] = __fadd_rn(xo[i], r16(__fadd_rn(r16(sum), bs[i])));
+      a.x[static_cast<int64_t>(r) * h + threadIdx.x + i * kThreads] = xv[i];
+    }
+  }
+  if (ts && threadIdx.x == 0) ts[1] = globaltimer();
+  ln_row(xv, nper, h, g, b, a.xn16 + static_cast<int64_t>(r) * h, red);
+  if (ts && threadIdx.x == 0) ts[2] = globaltimer();
+}
+
+__global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_constant__ SmallArgs a) {
+  // no static shared memory in this kernel: the dynamic window starts 1024-aligned, and
+  // indexing it directly keeps every access in the shared state space (LDS/STS)
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int h = a.h, f = a.f, M = a.M, S = a.S, H = a.H;
+  const uint32_t warp = warp_id(), lane = lane_id();
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SmemL::BAR);
+  float* red = reinterpret_cast<float*>(bars + 16);  // [8]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(red + 8);
+  float* sk = reinterpret_cast<float*>(smem + SmemL::ATT);  // [128][68]
+  float* sv = sk + 128 * kKS;                                // [128][64]
+  float* sp_ = sv + 128 * kVS;                               // [8 warps][128] probabilities
+  Ctl c;
+  c.full = bars;
+  c.empty = bars + kStages;
+  c.bfull = bars + 2 * kStages;
+  c.accfull = bars + 2 * kStages + 1;
+  c.accempty = bars + 2 * kStages + 2;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kStages; ++i) {
+      mbar_init(&c.full[i], 1);
+      mbar_init(&c.empty[i], 1);
+    }
+    mbar_init(c.bfull, 1);
+    mbar_init(c.accfull, 1);
+    mbar_init(c.accempty, 4);
+    fence_barrier_init();
+  }
+  if (warp == 5) {
+    tmem_alloc(tslot, 32);
+    tmem_relinquish();
+  }
+  if (warp == 6)
+    for (int i = lane; i < 3 + 4 * a.L; i += 32) tma_prefetch_desc(&a.maps[i]);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  c.tmem = *tslot;
+  c.kc = 0;
+  c.tc = 0;
+  c.bpref = 0;
+  unsigned target = 0;
+  const CUtensorMap* mXn = a.maps + 0;
+  const CUtensorMap* mCtx = a.maps + 1;
+  const CUtensorMap* mFf = a.maps + 2;
+  const int nper = h / kThreads;  // columns per thread in row tasks (h % 256 == 0)
+  // task geometry (same on every CTA)
+  const int t_qkv = 3 * h / 16;                    // N=16 tiles, full K -> fp16 q/k/v
+  const int t_wo = (h / kTileN) * a.split_wo;      // N=32 tiles x K splits -> partials
+  const int t_ffn1 = f / kTileN;                   // N=32 tiles, full K, GELU
+  const int t_ffn2 = (h / kTileN) * a.split_ffn2;  // N=32 tiles x K splits -> partials
+  const int kb_wo = h / 64 / a.split_wo, kb_ffn2 = f / 64 / a.split_ffn2;
+  auto pre_qkv = [&](int l) {
+    if (static_cast<int>(blockIdx.x) < t_qkv) load_b<16>(c, smem, a.maps + 3 + 4 * l + 0, blockIdx.x * 16, 0, h / 64);
+  };
+  auto pre_wo = [&](int l) {
+    const int t = blockIdx.x;
+    if (t < t_wo)
+      load_b<kTileN>(c, smem, a.maps + 3 + 4 * l + 1, (t / a.split_wo) * kTileN, (t % a.split_wo) * kb_wo * 64, kb_wo);
+  };
+  auto pre_ffn1 = [&](int l) {
+    if (static_cast<int>(blockIdx.x) < t_ffn1) load_b<kTileN>(c, smem, a.maps + 3 + 4 * l + 2, blockIdx.x * kTileN, 0, h / 64);
+  };
+  auto pre_ffn2 = [&](int l) {
+    const int t = blockIdx.x;
+    if (t < t_ffn2)
+      load_b<kTileN>(c, smem, a.maps + 3 + 4 * l + 3, (t / a.split_ffn2) * kTileN, (t % a.split_ffn2) * kb_ffn2 * 64,
+                     kb_ffn2);
+  };
+
+  // ---- stage 0: embedding gather (bit-exact fp32 tok + pos) + LN1 of layer 0
+  pre_qkv(0);
+  prefetch_layer_params(a, a.lw[0]);
+  prefetch_layer_weights(a, a.lw[0]);
+  for (int r = blockIdx.x; r < M; r += gridDim.x) {
+    const int id = a.ids[r];
+    const bool ok = id >= 0 && id < a.V;
+    if (!ok && threadIdx.x == 0) atomicExch(a.err, 1);
+    const int t = r % S;
+    float xv[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (i < nper) {
+        const int cc = threadIdx.x + i * kThreads;
+        xv[i] = __fadd_rn(ok ? a.tok[static_cast<int64_t>(id) * h + cc] : 0.0f, a.pos[static_cast<int64_t>(t) * h + cc]);
+      }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (i < nper) a.x[static_cast<int64_t>(r) * h + threadIdx.x + i * kThreads] = xv[i];
+    ln_row(xv, nper, h, a.lw[0].ln1g, a.lw[0].ln1b, a.xn16 + static_cast<int64_t>(r) * h, red);
+  }
+  grid_sync(a.gbar, target, a.dbg);
+
+  for (int l = 0; l < a.L; ++l) {
+    const LayerW& w = a.lw[l];
+    const CUtensorMap* mW = a.maps + 3 + 4 * l;
+    if (l + 1 < a.L) {
+      prefetch_layer_params(a, a.lw[l + 1]);
+      prefetch_layer_weights(a, a.lw[l + 1]);
+    }
+    // ---- QKV: N=16 tiles, full K, round16(round16(acc) + b) -> fp16 q|k|v (ff16 buffer)
+    for (int t = blockIdx.x; t < t_qkv; t += gridDim.x)
+      gemm_task<16, 2>(a, smem, c, mXn, mW + 0, t * 16, 0, h / 64, nullptr, 0, w.bqkv, a.ff16, 3 * h);
+    pre_wo(l);
+    grid_sync(a.gbar, target, a.dbg);
+    // ---- attention: (batch, head, 16-query block), SIMT fp32 on the fp16 q/k/v
+    {
+      const __half* qkv = a.ff16;
+      const int nqb = (S + kQB - 1) / kQB;
+      // causal: the later query blocks see more keys -- split the last nqb/2 blocks in two
+      // 8-query tasks when the grid has room, so no single task dominates the stage
+      const int nsplit = (a.causal && a.B * H * (nqb + nqb / 2) <= static_cast<int>(gridDim.x)) ? nqb / 2 : 0;
+      const int per_bh = nqb + nsplit;
+      float* pw = sp_ + warp * 128;
+      for (int t = blockIdx.x; t < a.B * H * per_bh; t += gridDim.x) {
+        const int sub = t % per_bh, hd_ = (t / per_bh) % H, b = t / (per_bh * H);
+        const int nfull = nqb - nsplit;
+        const int q0 = sub < nfull ? sub * kQB : (nfull + (sub - nfull) / 2) * kQB + ((sub - nfull) & 1) * (kQB / 2);
+        const int qcount = sub < nfull ? kQB : kQB / 2;
+        __syncthreads();  // previous task's readers are done with sk / sv
+        {
+          // k and v rows of this (batch, head): 8 fp16 (16 bytes) per load, all loads first
+          constexpr int PER = 128 * 8 / kThreads;  // 4 chunks of 8 per thread, per tensor
+          uint4 kc[PER], vc[PER];
+#pragma unroll
+          for (int u = 0; u < PER; ++u) {
+            const int e = threadIdx.x + u * kThreads, j = e >> 3, d8 = (e & 7) * 8;
+            if (j < S) {
+              const __half* rowp = qkv + (static_cast<int64_t>(b) * S + j) * 3 * h + hd_ * 64 + d8;
+              kc[u] = *reinterpret_cast<const uint4*>(rowp + h);
+              vc[u] = *reinterpret_cast<const uint4*>(rowp + 2 * h);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < PER; ++u) {
+            const int e = threadIdx.x + u * kThreads, j = e >> 3, d8 = (e & 7) * 8;
+            if (j < S) {
+              const uint32_t kw[4] = {kc[u].x, kc[u].y, kc[u].z, kc[u].w};
+              const uint32_t vw[4] = {vc[u].x, vc[u].y, vc[u].z, vc[u].w};
+              float4* kd = reinterpret_cast<float4*>(sk + j * kKS + d8);
+              float4* vd = reinterpret_cast<float4*>(sv + j * kVS + d8);
+              kd[0] = make_float4(h2f_lo(kw[0]), h2f_hi(kw[0]), h2f_lo(kw[1]), h2f_hi(kw[1]));
+              kd[1] = make_float4(h2f_lo(kw[2]), h2f_hi(kw[2]), h2f_lo(kw[3]), h2f_hi(kw[3]));
+              vd[0] = make_float4(h2f_lo(vw[0]), h2f_hi(vw[0]), h2f_lo(vw[1]), h2f_hi(vw[1]));
+              vd[1] = make_float4(h2f_lo(vw[2]), h2f_hi(vw[2]), h2f_lo(vw[3]), h2f_hi(vw[3]));
+            }
+          }
+        }
+        __syncthreads();
+        long long* ats = (a.dbg && blockIdx.x == 0 && threadIdx.x == 0) ? a.dbg + 210000 + l * 8 : nullptr;
+        if (ats) ats[0] = globaltimer();
+        for (int qi = warp; qi < qcount; qi += kThreads / 32) {
+          const int i = q0 + qi;  // query position
+          if (i >= S) break;
+          const int64_t row = static_cast<int64_t>(b) * S + i;
+          float q[64];
+          {
+            const uint4* qp = reinterpret_cast<const uint4*>(qkv + row * 3 * h + hd_ * 64);
+            uint4 qc[8];
+#pragma unroll
+            for (int v4 = 0; v4 < 8; ++v4) qc[v4] = qp[v4];
+#pragma unroll
+            for (int v4 = 0; v4 < 8; ++v4) {
+              const uint32_t w4[4] = {qc[v4].x, qc[v4].y, qc[v4].z, qc[v4].w};
+#pragma unroll
+              for (int k2 = 0; k2 < 4; ++k2) {
+                q[v4 * 8 + 2 * k2] = h2f_lo(w4[k2]);
+                q[v4 * 8 + 2 * k2 + 1] = h2f_hi(w4[k2]);
+              }
+            }
+          }
+          float sc[4];
+          float mx = __int_as_float(0xff800000);
+#pragma unroll
+          for (int cidx = 0; cidx < 4; ++cidx) {
+            const int j = cidx * 32 + lane;
+            float acc = 0.0f;
+            if (j < S) {
+              const float4* kr = reinterpret_cast<const float4*>(sk + j * kKS);
+#pragma unroll
+              for (int d4 = 0; d4 < 16; ++d4) {  // ascending d
+                const float4 kv = kr[d4];
+                acc = __fmaf_rn(q[4 * d4], kv.x, acc);
+                acc = __fmaf_rn(q[4 * d4 + 1], kv.y, acc);
+                acc = __fmaf_rn(q[4 * d4 + 2], kv.z, acc);
+                acc = __fmaf_rn(q[4 * d4 + 3], kv.w, acc);
+              }
+            }
+            const bool valid = j < S && (!a.causal || j <= i);
+            sc[cidx] = valid ? r16(__fmul_rn(acc, 0.125f)) : __int_as_float(0xff800000);
+            mx = fmaxf(mx, sc[cidx]);
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+          constexpr float LOG2E = 1.4426950408889634f;
+          const float mxl = __fmul_rn(mx, LOG2E);
+          float e[4], sum = 0.0f;
+#pragma unroll
+          for (int cidx = 0; cidx < 4; ++cidx) {
+            e[cidx] = ex2_approx(__fmaf_rn(sc[cidx], LOG2E, -mxl));  // exp(-inf) = 0 for masked keys
+            sum = __fadd_rn(sum, e[cidx]);
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) sum = __fadd_rn(sum, __shfl_xor_sync(0xffffffffu, sum, o));
+          const float inv = __frcp_rn(sum);
+#pragma unroll
+          for (int cidx = 0; cidx < 4; ++cidx) pw[cidx * 32 + lane] = r16(__fmul_rn(e[cidx], inv));
+          __syncwarp();
+          // o[d] for d = 2*lane, 2*lane + 1
+          // four interleaved partial sums (key j mod 4) break the FMA dependency chain
+          float oa[4] = {0.0f, 0.0f, 0.0f, 0.0f}, ob[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+          const int jmax = a.causal ? min(S, i + 1) : S;
+          int j = 0;
+          for (; j + 4 <= jmax; j += 4) {
+            const float4 p4 = *reinterpret_cast<const float4*>(pw + j);
+            const float pj[4] = {p4.x, p4.y, p4.z, p4.w};
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+              const float2 vv = *reinterpret_cast<const float2*>(sv + (j + u) * kVS + 2 * lane);
+              oa[u] = __fmaf_rn(pj[u], vv.x, oa[u]);
+              ob[u] = __fmaf_rn(pj[u], vv.y, ob[u]);
+            }
+          }
+          for (; j < jmax; ++j) {
+            const float pj = pw[j];
+            const float2 vv = *reinterpret_cast<const float2*>(sv + j * kVS + 2 * lane);
+            oa[0] = __fmaf_rn(pj, vv.x, oa[0]);
+            ob[0] = __fmaf_rn(pj, vv.y, ob[0]);
+          }
+          const float o0 = __fadd_rn(__fadd_rn(oa[0], oa[1]), __fadd_rn(oa[2], oa[3]));
+          const float o1 = __fadd_rn(__fadd_rn(ob[0], ob[1]), __fadd_rn(ob[2], ob[3]));
+          *reinterpret_cast<__half2*>(a.ctx16 + row * h + hd_ * 64 + 2 * lane) = __floats2half2_rn(o0, o1);
+          __syncwarp();  // pw is rewritten by this warp's next query
+        }
+        if (ats) ats[1] = globaltimer();
+      }
+    }
+    grid_sync(a.gbar, target, a.dbg);
+    // ---- Wo: partials over K splits
+    for (int t = blockIdx.x; t < t_wo; t += gridDim.x)
+      gemm_task<kTileN, 0>(a, smem, c, mCtx, mW + 1, (t / a.split_wo) * kTileN, (t % a.split_wo) * kb_wo * 64, kb_wo,
+                           a.part + static_cast<int64_t>(t % a.split_wo) * M * h, h, nullptr, nullptr, 0);
+    pre_ffn1(l);
+    grid_sync(a.gbar, target, a.dbg);
+    // ---- residual + LN2
+    for (int r = blockIdx.x; r < M; r += gridDim.x)
+      residual_ln_row(a, r, a.split_wo, w.bo, w.ln2g, w.ln2b, red,
+                      (a.dbg && blockIdx.x == 0) ? a.dbg + 200000 + l * 8 : nullptr);
+    grid_sync(a.gbar, target, a.dbg);
+    // ---- FFN1 + GELU, full K
+    for (int t = blockIdx.x; t < t_ffn1; t += gridDim.x)
+      gemm_task<kTileN, 1>(a, smem, c, mXn, mW + 2, t * kTileN, 0, h / 64, nullptr, 0, w.b1, a.ff16, f);
+    pre_ffn2(l);
+    grid_sync(a.gbar, target, a.dbg);
+    // ---- FFN2: partials over K splits
+    for (int t = blockIdx.x; t < t_ffn2; t += gridDim.x)
+      gemm_task<kTileN, 0>(a, smem, c, mFf, mW + 3, (t / a.split_ffn2) * kTileN, (t % a.split_ffn2) * kb_ffn2 * 64,
+                           kb_ffn2, a.part + static_cast<int64_t>(t % a.split_ffn2) * M * h, h, nullptr, nullptr, 0);
+    if (l + 1 < a.L) pre_qkv(l + 1);
+    grid_sync(a.gbar, target, a.dbg);
+    // ---- residual + LN1 of the next layer (or the final LN)
+    {
+      const float* g = l + 1 < a.L ? a.lw[l + 1].ln1g : a.lnfg;
+      const float* bb = l + 1 < a.L ? a.lw[l + 1].ln1b : a.lnfb;
+      for (int r = blockIdx.x; r < M; r += gridDim.x) residual_ln_row(a, r, a.split_ffn2, w.b2, g, bb, red);
+    }
+    if (l + 1 < a.L) grid_sync(a.gbar, target, a.dbg);
+  }
+  pdl_trigger();
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) {
+    tc_fence_after();
+    tmem_dealloc(c.tmem, 32);
+  }
+}
+
+constexpr size_t kSmem = SmemL::BAR + 16 * 8 + 8 * 4 + 16;
+static_assert(kSmem <= 227 * 1024, "fwd_small smem");
+
+
+}  // namespace
+
+long long*& small_debug_stamps() {
+  static long long* p = nullptr;
+  return p;
+}
+
+bool fwd_small_supported(int64_t M, int64_t S, int64_t h, int64_t f, int64_t hd, int64_t L) {
+  if (std::getenv("PRLAB_NO_FWD_SMALL")) return false;
+  return L <= kMaxLayers && M >= 1 && M <= 128 && S <= 128 && hd == 64 && L >= 1 && h % 256 == 0 && h <= 1024 && f % 512 == 0 &&
+         h / 64 <= kMaxKB && (f / 512) <= 8 && (f / 512) * 64 <= kMaxKB * 64;
+}
+
+size_t fwd_small_workspace_floats(int64_t M, int64_t h, int64_t f) {
+  (void)f;
+  const int64_t sp_wo = h / 128, sp_ffn2 = f / 512;
+  return static_cast<size_t>(std::max<int64_t>(std::max(sp_wo, sp_ffn2) * M * h, 2 * M * 3 * h) + 64);
+}
+
+void launch_fwd_small(const FwdSmallPlan& p, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    PRLAB_CUDA(cudaFuncSetAttribute(fwd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kSmem)));
+    configured = true;
+  }
+  static SmallArgs a;  // 28 KB: not on the host stack
+  a = SmallArgs{};
+  a.M = p.M;
+  a.B = p.B;
+  a.S = p.S;
+  a.h = p.h;
+  a.f = p.f;
+  a.H = p.H;
+  a.L = p.L;
+  a.V = p.V;
+  a.causal = p.causal;
+  a.split_qkv = 1;
+  a.split_wo = p.h / 128;
+  a.split_ffn2 = p.f / 512;
+  if (p.L > kMaxLayers) throw std::invalid_argument("fwd_small: too many layers");
+  std::memcpy(a.maps, p.host_maps, sizeof(CUtensorMap) * (3 + 4 * p.L));
+  std::memcpy(a.lw, p.host_lw, sizeof(LayerW) * p.L);
+  a.tok = p.tok;
+  a.pos = p.pos;
+  a.lnfg = p.lnfg;
+  a.lnfb = p.lnfb;
+  a.ids = p.ids;
+  a.err = p.err;
+  a.x = p.x;
+  a.xn16 = p.xn16;
+  a.ctx16 = p.ctx16;
+  a.ff16 = p.ff16;
+  a.qkvp = nullptr;
+  a.part = p.scratch;
+  a.gbar = p.gbar;
+  a.dbg = small_debug_stamps();
+  PRLAB_CUDA(cudaMemsetAsync(p.gbar, 0, sizeof(unsigned), st));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(num_sms());
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = kSmem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeCooperative;
+  attr[0].val.cooperative = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  PRLAB_CUDA(cudaLaunchKernelEx(&cfg, fwd_small_kernel, a));
+}
+
+}  // namespace prlab_gpu

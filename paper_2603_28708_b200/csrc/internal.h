@@ -99,6 +99,24 @@ GemmPlan plan_gemm_tc(const void* A, int64_t lda, const void* Wt, int64_t ldw, c
 void launch_gemm_tc(const GemmPlan& p, cudaStream_t st);
 void configure_gemm_tc();
 
+// --- batch-1 forward_hidden as one cooperative persistent kernel (fwd_small.cu) ---
+struct FwdSmallPlan {
+  int M, B, S, h, f, H, L, V, causal;
+  const void* host_lw;              // host array of per-layer LN / bias device pointers (8 per layer)
+  const CUtensorMap* host_maps;     // host array: xn16, ctx16, ff16, then Wqkv, Wo, W1, W2 per layer
+  const float *tok, *pos, *lnfg, *lnfb;
+  const int32_t* ids;
+  int* err;
+  float* x;
+  __half *xn16, *ctx16, *ff16;
+  float* scratch;            // fwd_small_workspace_floats()
+  unsigned* gbar;
+};
+bool fwd_small_supported(int64_t M, int64_t S, int64_t h, int64_t f, int64_t hd, int64_t L);
+size_t fwd_small_workspace_floats(int64_t M, int64_t h, int64_t f);
+void launch_fwd_small(const FwdSmallPlan& p, cudaStream_t st);
+long long*& small_debug_stamps();  // [stage][grid][2] globaltimer stamps target (debug; null = off)
+
 // --- fused tensor-core attention (hybrid, head_dim 64, seq <= 512) ---
 struct AttnPlan {
   CUtensorMap tmQKV;

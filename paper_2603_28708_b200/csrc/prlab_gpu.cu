@@ -484,6 +484,12 @@ struct prlab_gpu_model {
     int64_t ld16 = 0;
     std::vector<GemmPlan> gemms;  // fast path: 4 per layer + head
     AttnPlan attn{};
+    // batch-1 shapes: forward_hidden as one cooperative persistent kernel (fwd_small.cu)
+    bool small = false;
+    FwdSmallPlan sp{};
+    DeviceBuffer small_buf;  // ctx16 + scratch + barrier counter
+    std::vector<CUtensorMap> small_maps;
+    std::vector<std::array<const void*, 12>> small_lw;
     std::map<std::tuple<const void*, void*, int, int64_t>, cudaGraphExec_t> graphs;
     std::map<std::tuple<void*, int64_t>, GemmPlan> head_plans;
   };
@@ -645,6 +651,58 @@ void ensure_f32(prlab_gpu_model& m) {
   m.have32 = true;
 }
 
+// Batch-1 plan: tensor maps (activations box 128 x 64, weights box 32 x 64) and the
+// per-layer parameter pointers live in one device buffer next to ctx16 / the fp32
+// split-K partials / the grid-barrier counter.
+void plan_small(prlab_gpu_model& m, prlab_gpu_model::Plan& p, int64_t B, int64_t S) {
+  const int64_t M = B * S, h = m.h, f = m.f, L = m.L;
+  ArenaPlan ap;
+  const int s_ctx = ap.add(static_cast<size_t>(M * h) * 2);
+  const int s_scr = ap.add(fwd_small_workspace_floats(M, h, f) * 4);
+  const int s_bar = ap.add(64);
+  p.small_buf.alloc(ap.total);
+  char* base = static_cast<char*>(p.small_buf.p);
+  __half* ctx16 = reinterpret_cast<__half*>(base + ap.offs[s_ctx]);
+  auto& maps = p.small_maps;
+  maps.clear();
+  maps.push_back(make_tmap_f16_2d(p.xn16, M, h, h, 128, 64));
+  maps.push_back(make_tmap_f16_2d(ctx16, M, h, h, 128, 64));
+  maps.push_back(make_tmap_f16_2d(p.big16, M, f, f, 128, 64));  // ff16 reuses the qkv/ff buffer
+  p.small_lw.assign(static_cast<size_t>(L), {});
+  for (int64_t l = 0; l < L; ++l) {
+    const auto& w = m.l16[l];
+    maps.push_back(make_tmap_f16_2d(w.wqkv, 3 * h, h, h, 16, 64));  // QKV tasks: N = 16
+    maps.push_back(make_tmap_f16_2d(w.wo, h, h, h, 32, 64));
+    maps.push_back(make_tmap_f16_2d(w.w1, f, h, h, 32, 64));
+    maps.push_back(make_tmap_f16_2d(w.w2, h, f, f, 32, 64));
+    p.small_lw[l] = {w.ln1g, w.ln1b, w.ln2g, w.ln2b, w.bqkv, w.bo, w.b1, w.b2, w.wqkv, w.wo, w.w1, w.w2};
+  }
+  FwdSmallPlan& sp = p.sp;
+  sp.M = static_cast<int>(M);
+  sp.B = static_cast<int>(B);
+  sp.S = static_cast<int>(S);
+  sp.h = static_cast<int>(h);
+  sp.f = static_cast<int>(f);
+  sp.H = static_cast<int>(m.H);
+  sp.L = static_cast<int>(L);
+  sp.V = static_cast<int>(m.V);
+  sp.causal = m.d.archetype == 1;
+  sp.host_lw = p.small_lw.data();
+  sp.host_maps = maps.data();
+  sp.tok = m.tok;
+  sp.pos = m.pos;
+  sp.lnfg = m.lnfg;
+  sp.lnfb = m.lnfb;
+  sp.err = m.err.at<int>(0);
+  sp.x = p.x;
+  sp.xn16 = p.xn16;
+  sp.ctx16 = ctx16;
+  sp.ff16 = p.big16;
+  sp.scratch = reinterpret_cast<float*>(base + ap.offs[s_scr]);
+  sp.gbar = reinterpret_cast<unsigned*>(base + ap.offs[s_bar]);
+  p.small = true;
+}
+
 prlab_gpu_model::Plan& get_plan(prlab_gpu_model& m, int64_t B, int64_t S, const prlab_policy& pol) {
   const auto key = std::make_tuple(B, S, policy_key(pol));
   auto it = m.plans.find(key);
@@ -704,6 +762,7 @@ prlab_gpu_model::Plan& get_plan(prlab_gpu_model& m, int64_t B, int64_t S, const 
                                    static_cast<int>(V), hi, EPI_F16, &m.scratch));
     p.attn = plan_attn_tc(p.big16, 3 * h, p.xn16, h, static_cast<int>(B), static_cast<int>(S),
                           static_cast<int>(m.H), static_cast<int>(m.hd), m.d.archetype == 1);
+    if (fwd_small_supported(M, S, h, f, m.hd, m.L)) plan_small(m, p, B, S);
   } else {
     p.xn32 = m.ws.at<float>(at(s_a));
     p.qkv32 = m.ws.at<float>(at(s_b));
@@ -750,7 +809,13 @@ int64_t enqueue_forward(prlab_gpu_model& m, prlab_gpu_model::Plan& p, const int3
     ++n;
   };
   const int64_t tap_stride = B * m.H * S * S;
-  if (p.fast) {
+  if (p.fast && p.small && !o.tap && !o.timing) {
+    // batch-1 shapes: embed .. final LN as one cooperative kernel (fwd_small.cu)
+    FwdSmallPlan sp = p.sp;
+    sp.ids = ids;
+    launch_fwd_small(sp, st);
+    n += 1;
+  } else if (p.fast) {
     T(PRLAB_EMBEDDING, [&] { embed_f32(m.tok, V, m.pos, hi, ids, Bi, Si, p.x, err, st); });
     for (int64_t l = 0; l < L; ++l) {
       const auto& w = m.l16[l];
@@ -764,6 +829,8 @@ int64_t enqueue_forward(prlab_gpu_model& m, prlab_gpu_model::Plan& p, const int3
       T(PRLAB_LINEAR, [&] { launch_gemm_tc(p.gemms[4 * l + 3], st); });                          // FFN2 + residual
     }
     T(PRLAB_LAYERNORM, [&] { ln_f32_to_f16(p.x, Mi, hi, m.lnfg, m.lnfb, 1e-5f, p.xn16, st); });
+  }
+  if (p.fast) {
     if (o.hidden_only) return n;  // forward_hidden: r16(final LN) in xn16 (the Linear lattice)
     if (out_dtype == PRLAB_OUT_F16) {
       if (ld % 8 != 0) throw std::invalid_argument("fp16 logits need a row pitch that is a multiple of 8");
@@ -1391,7 +1458,8 @@ int prlab_gpu_forward_kernel_count(prlab_gpu_model* m, int64_t B, int64_t S, con
     check_forward_args(*m, B, S);
     const bool fast = fast_eligible(*m, S, *policy);
     const int64_t L = m->L;
-    *count = fast ? 1 + 7 * L + 1 + 1 : 1 + 7 * L + (L > 0 ? 2 : 1);
+    const bool small = fast && fwd_small_supported(B * S, S, m->h, m->f, m->hd, L);
+    *count = small ? 2 : (fast ? 1 + 7 * L + 1 + 1 : 1 + 7 * L + (L > 0 ? 2 : 1));
   });
 }
 
@@ -1525,6 +1593,10 @@ int prlab_gpu_linear_f16_device_ex(const void* A, const void* Wt, const float* b
                                     static_cast<int>(K_), epi, &global_split_scratch(), bn, splits, lean);
     launch_gemm_tc(p, static_cast<cudaStream_t>(stream));
   });
+}
+
+int prlab_gpu_debug_small_stamps(long long* dbg) {
+  return guarded([&] { small_debug_stamps() = dbg; });
 }
 
 int prlab_gpu_debug_gemm_stamps(long long* dbg) {

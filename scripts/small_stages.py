@@ -1,0 +1,87 @@
+#!/usr/bin/env python3
+"""Per-stage timeline of the batch-1 persistent forward (fwd_small.cu): for every stage,
+the stage's work time (last CTA arriving at the barrier minus the previous release) and
+the barrier latency (release minus last arrival), from %globaltimer stamps."""
+import ctypes as C
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2603_28708_b200 as pg  # noqa: E402
+
+NAMES = ["qkv", "attn", "wo", "rln2", "ffn1", "ffn2", "rln1"]
+
+
+def main():
+    cfg = pg.ModelConfig.preset(sys.argv[1] if len(sys.argv) > 1 else "gpt2_small")
+    B, S = 1, 128
+    m = pg.DeviceModel(cfg, pg.build_model(cfg))
+    ids = torch.from_numpy(pg.random_tokens(cfg.vocab, B, S, 3)).cuda()
+    V = cfg.vocab
+    ld = (V + 7) // 8 * 8
+    out = torch.empty(B * S, ld, device="cuda", dtype=torch.float16)
+    st = torch.cuda.current_stream().cuda_stream
+    for _ in range(3):
+        m.forward_device(ids.data_ptr(), B, S, "hybrid", out.data_ptr(), pg.OUT_F16, ld, st, False)
+    torch.cuda.synchronize()
+    nst = 1 + 7 * cfg.num_layers
+    dbg = torch.zeros(300000, dtype=torch.int64, device="cuda")
+    pg._check(pg.lib().prlab_gpu_debug_small_stamps(C.c_void_p(dbg.data_ptr())))
+    m.forward_device(ids.data_ptr(), B, S, "hybrid", out.data_ptr(), pg.OUT_F16, ld, st, False)
+    torch.cuda.synchronize()
+    pg._check(pg.lib().prlab_gpu_debug_small_stamps(None))
+    raw = dbg.cpu().numpy().astype(np.float64)
+    d = raw[: nst * 148 * 2].reshape(nst, 148, 2)
+    rl = raw[200000:200000 + 8 * cfg.num_layers].reshape(cfg.num_layers, 8)
+    arrive_max = d[:, :, 0].max(1)
+    release_min = np.where(d[:, :, 1] > 0, d[:, :, 1], np.inf).min(1)
+    release_max = d[:, :, 1].max(1)
+    t0 = d[0, :, 0].min()
+    prev_release = t0
+    rows = []
+    for k in range(nst - 1):
+        name = "embed+ln1" if k == 0 else NAMES[(k - 1) % 7]
+        rows.append({"stage": k, "name": name, "work_us": round((arrive_max[k] - prev_release) / 1e3, 2),
+                     "barrier_us": round((release_max[k] - arrive_max[k]) / 1e3, 2)})
+        prev_release = release_max[k]
+    agg = {}
+    for r in rows:
+        a = agg.setdefault(r["name"], [0.0, 0.0, 0])
+        a[0] += r["work_us"]
+        a[1] += r["barrier_us"]
+        a[2] += 1
+    print(json.dumps({"total_us": round((release_max[nst - 2] - t0) / 1e3, 1),
+                      "per_stage_type": {k: {"n": v[2], "work_us_avg": round(v[0] / v[2], 2),
+                                             "barrier_us_avg": round(v[1] / v[2], 2)} for k, v in agg.items()}}))
+    for r in rows[:9]:
+        print(json.dumps(r))
+    at = raw[210000:210000 + 8 * cfg.num_layers].reshape(cfg.num_layers, 8)
+    for l in range(min(3, cfg.num_layers)):
+        k = 1 + 7 * l + 1  # attention stage index
+        print(json.dumps({"layer": l, "attn_cta0": {"staging_us": round((at[l, 0] - d[k - 1, 0, 1]) / 1e3, 2),
+                                                    "queries_us": round((at[l, 1] - at[l, 0]) / 1e3, 2),
+                                                    "to_arrive_us": round((d[k, 0, 0] - at[l, 1]) / 1e3, 2)}}))
+    gt = raw[220000:220000 + 64 * 8].reshape(64, 8)
+    names = ["qkv", "wo", "ffn1", "ffn2"]
+    for t in range(8):
+        g = gt[t]
+        if g[0] == 0:
+            break
+        print(json.dumps({"gemm_task_cta0": names[t % 4], "b_ready_us": round((g[1] - g[0]) / 1e3, 2),
+                          "first_a_us": round((g[2] - g[0]) / 1e3, 2), "mma_issued_us": round((g[3] - g[0]) / 1e3, 2),
+                          "acc_ready_us": round((g[4] - g[0]) / 1e3, 2), "epilogue_done_us": round((g[5] - g[0]) / 1e3, 2)}))
+    # CTA 0 inside RLN2 of each layer: release -> start, loads+residual, LN
+    for l in range(min(3, cfg.num_layers)):
+        k = 1 + 7 * l + 3  # the RLN2 stage index
+        print(json.dumps({"layer": l, "rln2_cta0": {"start_after_release_us": round((rl[l, 0] - d[k - 1, 0, 1]) / 1e3, 2),
+                                                    "loads_us": round((rl[l, 1] - rl[l, 0]) / 1e3, 2),
+                                                    "ln_us": round((rl[l, 2] - rl[l, 1]) / 1e3, 2),
+                                                    "to_arrive_us": round((d[k, 0, 0] - rl[l, 2]) / 1e3, 2)}}))
+
+
+if __name__ == "__main__":
+    main()

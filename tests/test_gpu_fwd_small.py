@@ -1,0 +1,54 @@
+"""The batch-1 persistent forward (fwd_small.cu: forward_hidden as one cooperative
+kernel with grid barriers, used for B*S <= 128) against the multi-kernel tensor-core
+path and the CPU oracle, decoder (causal) and encoder shapes, including ragged M."""
+import os
+
+import numpy as np
+import pytest
+
+import paper_2603_28708_b200 as pg
+from oracle.oracle import ModelConfig, compare_logits
+from prlab_testutil import model_params, oracle
+
+pytestmark = pytest.mark.gpu
+
+GPT2_SMALLV = ModelConfig(archetype=1, num_layers=2, hidden=768, heads=12, ffn=3072, vocab=4096,
+                          max_positions=512, seed=0)
+BERT_SMALLV = GPT2_SMALLV.replace(archetype=0, seed=1)
+
+
+@pytest.mark.parametrize("cfg", [GPT2_SMALLV, BERT_SMALLV], ids=["gpt2", "bert"])
+@pytest.mark.parametrize("B,S", [(1, 128), (1, 1), (1, 37), (2, 64), (4, 32), (3, 17)])
+def test_fwd_small_matches_multikernel_and_oracle(cfg, B, S, monkeypatch):
+    o = oracle()
+    p = model_params(cfg)
+    ids = o.random_tokens(cfg.vocab, B, S, 5 + B + S)
+    small = pg.DeviceModel(pg.ModelConfig(**cfg.__dict__), p)
+    assert small.kernel_count(B, S, "hybrid") == 2  # the cooperative kernel + the LM head
+    got = small.forward(ids, B, S, "hybrid")
+    monkeypatch.setenv("PRLAB_NO_FWD_SMALL", "1")
+    multi = pg.DeviceModel(pg.ModelConfig(**cfg.__dict__), p)
+    assert multi.kernel_count(B, S, "hybrid") > 2
+    ref = multi.forward(ids, B, S, "hybrid")
+    monkeypatch.delenv("PRLAB_NO_FWD_SMALL")
+    r = compare_logits(ref, got)
+    assert r["candidate_nonfinite"] == 0 and r["cosine"] >= 0.99999, r
+    cpu32 = o.forward(cfg, p, ids, B, S, "fp32")
+    r32 = compare_logits(cpu32, got)
+    assert r32["cosine"] >= 0.9998, r32
+    small.close()
+    multi.close()
+
+
+def test_fwd_small_bad_token_reported():
+    cfg = GPT2_SMALLV
+    m = pg.DeviceModel(pg.ModelConfig(**cfg.__dict__), model_params(cfg))
+    import torch
+    ids = torch.zeros(64, dtype=torch.int32, device="cuda")
+    ids[5] = cfg.vocab + 3
+    out = torch.empty(64, (cfg.vocab + 7) // 8 * 8, dtype=torch.float16, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    m.forward_device(ids.data_ptr(), 1, 64, "hybrid", out.data_ptr(), pg.OUT_F16, out.shape[1], st, True)
+    with pytest.raises(IndexError):
+        m.sync_status(st)
+    m.close()
