@@ -21,7 +21,8 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libprlab_gpu.so")
+# PRLAB_GPU_LIB: an alternative build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("PRLAB_GPU_LIB") or os.path.join(_HERE, "_lib", "libprlab_gpu.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "prlab_gpu.h")
 
 F32, F16E = 0, 1

@@ -388,6 +388,24 @@ __device__ __forceinline__ void tma_load_2d_pair_mc(void* dst, const CUtensorMap
       "l"(reinterpret_cast<uint64_t>(m)), "r"(to_leader(smem_u32(bar))), "r"(c0), "r"(c1), "h"(mask)
       : "memory");
 }
+// Plain (cta_group::1) TMA load multicast to the CTAs in `mask`: each destination CTA
+// receives the box at the same shared offset and the bytes complete on ITS mbarrier
+// at the same offset.
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1,
+                                               uint16_t mask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster "
+      "[%0], [%1, {%3, %4}], [%2], %5;" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "h"(mask)
+      : "memory");
+}
+// cta_group::1 commit arriving on the same-offset mbarrier of every CTA in `mask`
+__device__ __forceinline__ void umma_commit_mc(uint64_t* bar, uint16_t mask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          smem_u32(bar)), "h"(mask)
+      : "memory");
+}
 // arrive on a barrier of another CTA of the cluster (shared::cluster address).
 // Default (CTA-scope release) semantics: the data these arrivals announce is either
 // tracked by TMA transaction bytes or ordered by tcgen05 fences, so no cluster-scope

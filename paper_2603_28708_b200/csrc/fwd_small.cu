@@ -33,8 +33,13 @@ namespace {
 
 constexpr int kThreads = 256;            // warps 0-3: epilogue / TMEM quadrants; 4: TMA; 5: MMA
 constexpr int kTileN = 32;               // GEMM output columns per task
-constexpr int kStages = 8;               // A ring (the attention scratch aliases it)
-constexpr uint32_t kABytes = 128 * 64 * 2;         // 16 KB
+// Operand loads are 3D tensor maps over a K-major matrix viewed as [K/64][rows][64]: one
+// TMA request moves several 64-wide k-blocks.  Measured (scripts/ubench/ubench_tma2d.cu,
+// profiles/r01/ubench_tma2d.jsonl): a 2D 128-row SW128 box (16 KB) streams at 26.6 B/clk
+// per SM, a 3D box of 2 k-blocks (32 KB) at 91.5 B/clk -- the per-request cost dominates.
+constexpr int kKPR = 2;                  // k-blocks per A request / ring stage
+constexpr int kStages = 4;               // A ring of 4 x 32 KB (the attention scratch aliases it)
+constexpr uint32_t kABytes = 128 * 64 * 2;         // 16 KB per k-block
 constexpr uint32_t kBBox = kTileN * 64 * 2;        // 4 KB per 64-wide k-block
 constexpr int kMaxKB = 16;                         // B for one task: <= 16 k-blocks (1024 of K)
 constexpr int kQB = 16;                            // queries per attention task
@@ -42,7 +47,7 @@ constexpr int kQB = 16;                            // queries per attention task
 constexpr int kKS = 68, kVS = 64;  // fp32 row strides of the staged K (16B-aligned, conflict-free LDS.128) and V
 struct SmemL {
   static constexpr uint32_t A = 0;
-  static constexpr uint32_t B = A + kStages * kABytes;             // 64 KB
+  static constexpr uint32_t B = A + kStages * kKPR * kABytes;      // 128 KB
   static constexpr uint32_t ATT = A;                               // attention scratch: the A ring is idle then
   static constexpr uint32_t ATT_BYTES = (128 * kKS + 128 * kVS + 8 * 128) * 4;
   static constexpr uint32_t BAR = B + kMaxKB * kBBox;
@@ -193,7 +198,7 @@ __device__ void load_b(Ctl& c, uint8_t* smem, const CUtensorMap* mB, int n0, int
   if (threadIdx.x == 4 * 32) {
     mbar_wait(c.accempty, (c.tc & 1) ^ 1);  // previous task's MMAs done reading sB
     mbar_expect_tx(c.bfull, static_cast<uint32_t>(nkb) * NT * 128);
-    for (int kb = 0; kb < nkb; ++kb) tma_load_2d(smem + SmemL::B + kb * kBBox, mB, c.bfull, k0 + kb * 64, n0);
+    tma_load_3d(smem + SmemL::B, mB, c.bfull, 0, n0, k0 / 64);  // the task's whole B: one request
   }
   c.bpref = 1;
 }
@@ -212,11 +217,11 @@ __device__ void gemm_task(const SmallArgs& a, uint8_t* smem, Ctl& c, const CUten
   c.bpref = 0;
   if (warp == 4) {
     if (lane == 0) {
-      for (int kb = 0; kb < nkb; ++kb) {
-        const uint32_t k = c.kc + kb, st = k % kStages;
-        mbar_wait(&c.empty[st], ((k / kStages) & 1) ^ 1);
-        mbar_expect_tx(&c.full[st], kABytes);
-        tma_load_2d(sA + st * kABytes, mA, &c.full[st], k0 + kb * 64, 0);
+      for (int kb = 0; kb < nkb; kb += kKPR) {
+        const uint32_t u = (c.kc + kb) / kKPR, st = u % kStages;
+        mbar_wait(&c.empty[st], ((u / kStages) & 1) ^ 1);
+        mbar_expect_tx(&c.full[st], kKPR * kABytes);
+        tma_load_3d(sA + st * kKPR * kABytes, mA, &c.full[st], 0, 0, k0 / 64 + kb);
       }
     }
     __syncwarp();
@@ -229,16 +234,19 @@ __device__ void gemm_task(const SmallArgs& a, uint8_t* smem, Ctl& c, const CUten
       mbar_wait(c.bfull, c.tc & 1);
       if (gs) gs[1] = globaltimer();
       tc_fence_after();
-      for (int kb = 0; kb < nkb; ++kb) {
-        const uint32_t k = c.kc + kb, st = k % kStages;
-        mbar_wait(&c.full[st], (k / kStages) & 1);
+      for (int kb = 0; kb < nkb; kb += kKPR) {
+        const uint32_t u = (c.kc + kb) / kKPR, st = u % kStages;
+        mbar_wait(&c.full[st], (u / kStages) & 1);
         if (gs && kb == 0) gs[2] = globaltimer();
         tc_fence_after();
-        const uint32_t a0 = smem_u32(sA + st * kABytes), b0 = smem_u32(sB + kb * kBBox);
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          umma_f16_ss(c.tmem, sw128_desc(a0 + kk * 32, 0, 1024), sw128_desc(b0 + kk * 32, 0, 1024), idesc,
-                      (kb | kk) != 0);
+        for (int j = 0; j < kKPR; ++j) {
+          const uint32_t a0 = smem_u32(sA + (st * kKPR + j) * kABytes), b0 = smem_u32(sB + (kb + j) * (NT * 128));  // the 3D box packs k-blocks at NT rows
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            umma_f16_ss(c.tmem, sw128_desc(a0 + kk * 32, 0, 1024), sw128_desc(b0 + kk * 32, 0, 1024), idesc,
+                        (kb | j | kk) != 0);
+        }
         umma_commit(&c.empty[st]);
       }
       umma_commit(c.accfull);

@@ -665,16 +665,22 @@ void plan_small(prlab_gpu_model& m, prlab_gpu_model::Plan& p, int64_t B, int64_t
   __half* ctx16 = reinterpret_cast<__half*>(base + ap.offs[s_ctx]);
   auto& maps = p.small_maps;
   maps.clear();
-  maps.push_back(make_tmap_f16_2d(p.xn16, M, h, h, 128, 64));
-  maps.push_back(make_tmap_f16_2d(ctx16, M, h, h, 128, 64));
-  maps.push_back(make_tmap_f16_2d(p.big16, M, f, f, 128, 64));  // ff16 reuses the qkv/ff buffer
+  // K-major matrices viewed as [K/64 k-blocks][rows][64]: a box spans several k-blocks
+  // (one TMA request per 2 k-blocks of A, one per task for B -- fwd_small.cu)
+  auto kblk = [](const void* base, int64_t rows, int64_t K, uint32_t box_rows, uint32_t box_kb) {
+    return make_tmap_f16_3d(base, 64, rows, K / 64, K, 64, 64, box_rows, box_kb);
+  };
+  maps.push_back(kblk(p.xn16, M, h, 128, 2));
+  maps.push_back(kblk(ctx16, M, h, 128, 2));
+  maps.push_back(kblk(p.big16, M, f, 128, 2));  // ff16 reuses the qkv/ff buffer
   p.small_lw.assign(static_cast<size_t>(L), {});
+  const int64_t kb_wo = h / 64 / (h / 128), kb_ffn2 = f / 64 / (f / 512);  // split-K depths (launch_fwd_small)
   for (int64_t l = 0; l < L; ++l) {
     const auto& w = m.l16[l];
-    maps.push_back(make_tmap_f16_2d(w.wqkv, 3 * h, h, h, 16, 64));  // QKV tasks: N = 16
-    maps.push_back(make_tmap_f16_2d(w.wo, h, h, h, 32, 64));
-    maps.push_back(make_tmap_f16_2d(w.w1, f, h, h, 32, 64));
-    maps.push_back(make_tmap_f16_2d(w.w2, h, f, f, 32, 64));
+    maps.push_back(kblk(w.wqkv, 3 * h, h, 16, static_cast<uint32_t>(h / 64)));  // QKV tasks: N = 16, full K
+    maps.push_back(kblk(w.wo, h, h, 32, static_cast<uint32_t>(kb_wo)));
+    maps.push_back(kblk(w.w1, f, h, 32, static_cast<uint32_t>(h / 64)));
+    maps.push_back(kblk(w.w2, h, f, 32, static_cast<uint32_t>(kb_ffn2)));
     p.small_lw[l] = {w.ln1g, w.ln1b, w.ln2g, w.ln2b, w.bqkv, w.bo, w.b1, w.b2, w.wqkv, w.wo, w.w1, w.w2};
   }
   FwdSmallPlan& sp = p.sp;

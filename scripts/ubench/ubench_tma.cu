@@ -17,7 +17,7 @@ __device__ __forceinline__ void bulk(void* dst, const void* src, uint32_t n, uin
 }
 
 template <int STAGES, int CHUNK>
-__global__ void k(const uint8_t* src, size_t span, int iters, unsigned long long* out) {
+__global__ void k(const uint8_t* src, size_t span, int iters, unsigned long long* out, int order) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + STAGES * CHUNK);
   if (threadIdx.x == 0) {
@@ -27,7 +27,9 @@ __global__ void k(const uint8_t* src, size_t span, int iters, unsigned long long
   __syncthreads();
   if (threadIdx.x != 0) return;
   const size_t nchunks = span / CHUNK;
-  size_t c = (size_t)blockIdx.x * 97;
+  // order 0: CTAs start at scattered chunks; 1: all CTAs read the same chunks in the same
+  // order (every SM streams one small activation matrix); 2: same chunks, rotated start
+  size_t c = order == 0 ? (size_t)blockIdx.x * 97 : order == 1 ? 0 : (size_t)blockIdx.x;
   long long t0 = clock64();
   for (int i = 0; i < STAGES; ++i) {
     expect_tx(&bars[i], CHUNK);
@@ -48,11 +50,11 @@ __global__ void k(const uint8_t* src, size_t span, int iters, unsigned long long
 }
 
 template <int STAGES, int CHUNK>
-void run(const uint8_t* d, size_t span, int grid, unsigned long long* d_out, const char* tag) {
+void run(const uint8_t* d, size_t span, int grid, unsigned long long* d_out, const char* tag, int order = 0) {
   const int iters = 2000;
   size_t smem = STAGES * CHUNK + 1024;
   cudaFuncSetAttribute(k<STAGES, CHUNK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  for (int rep = 0; rep < 2; ++rep) k<STAGES, CHUNK><<<grid, 32, smem>>>(d, span, iters, d_out);
+  for (int rep = 0; rep < 2; ++rep) k<STAGES, CHUNK><<<grid, 32, smem>>>(d, span, iters, d_out, order);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); return; }
   unsigned long long h[1024];
@@ -82,5 +84,9 @@ int main() {
   run<3, 65536>(d, 32u << 20, sms, d_out, "L2 32MB");
   run<6, 32768>(d, 1ull << 30, sms, d_out, "DRAM 1GB");
   run<6, 32768>(d, 4u << 20, sms, d_out, "L2 4MB");
+  run<8, 16384>(d, 196608, sms, d_out, "hot 196KB same order", 1);
+  run<8, 16384>(d, 196608, sms, d_out, "hot 196KB rotated", 2);
+  run<8, 16384>(d, 196608, 1, d_out, "hot 196KB one SM", 1);
+  run<8, 16384>(d, 32u << 20, sms, d_out, "L2 32MB 8x16KB");
   return 0;
 }
