@@ -78,6 +78,13 @@ struct SmallArgs {
   long long* dbg;                // optional [stage][grid][2] globaltimer (arrive, release)
 };
 
+// Generic-proxy global writes of one stage (epilogue / row-stage stores) are read by
+// TMA (async proxy) in a later stage on other CTAs: after the barrier's release/acquire,
+// the TMA-issuing thread fences its generic view against the async proxy before its
+// loads.  (The unqualified fence.proxy.async by every thread costs a MEMBAR.ALL.GPU each
+// -- ~10% of all warp stall samples in ncu, profiles/r01.)
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
 __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -88,7 +95,6 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
 // red.release.gpu (cumulative over the CTA's writes ordered by the bar.sync before it),
 // wait = ld.acquire.gpu polling by one thread.
 __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned& target, long long* dbg = nullptr) {
-  asm volatile("fence.proxy.async;" ::: "memory");  // generic writes (global, smem) before later async-proxy (TMA) accesses
   __syncthreads();
   const unsigned stage = target / gridDim.x;
   target += gridDim.x;
@@ -217,6 +223,7 @@ __device__ void gemm_task(const SmallArgs& a, uint8_t* smem, Ctl& c, const CUten
   c.bpref = 0;
   if (warp == 4) {
     if (lane == 0) {
+      fence_proxy_async_global();  // A was written by generic stores of the previous stage
       for (int kb = 0; kb < nkb; kb += kKPR) {
         const uint32_t u = (c.kc + kb) / kKPR, st = u % kStages;
         mbar_wait(&c.empty[st], ((u / kStages) & 1) ^ 1);
@@ -582,6 +589,8 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
         }
         if (ats) ats[1] = globaltimer();
       }
+      // sk / sv (generic smem writes) alias the A ring the next GEMM stage fills by TMA
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     grid_sync(a.gbar, target, a.dbg);
     // ---- Wo: partials over K splits

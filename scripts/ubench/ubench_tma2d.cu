@@ -37,9 +37,10 @@ __device__ __forceinline__ void load3d(void* dst, const CUtensorMap* m, uint64_t
 // mode 0: 2D, `sub` requests of (64 cols x 128/sub rows) per k-block; mode 1: 3D, one
 // request of `kpr` k-blocks.  Stage = kpr k-blocks (kpr * 16 KB).
 __global__ void k(const __grid_constant__ CUtensorMap m, int mode, int sub, int kpr, int stages, int nkb, int iters,
-                  unsigned long long* out) {
+                  unsigned long long* out, int br, int nrb) {
   extern __shared__ __align__(1024) uint8_t sm[];
-  const uint32_t stage_bytes = kpr * 16384;
+  const uint32_t kb_bytes = br * 128, stage_bytes = kpr * kb_bytes;
+  const int row0 = (blockIdx.x % nrb) * br;
   uint64_t* bars = reinterpret_cast<uint64_t*>(sm + stages * stage_bytes);
   if (threadIdx.x == 0) {
     for (int i = 0; i < stages; ++i) mbar_init(&bars[i], 1);
@@ -55,9 +56,9 @@ __global__ void k(const __grid_constant__ CUtensorMap m, int mode, int sub, int 
     if (mode == 0) {
       for (int j = 0; j < kpr; ++j)
         for (int r = 0; r < sub; ++r)
-          load2d(dst + j * 16384 + r * (16384 / sub), &m, &bars[s], (kb0 + j) * 64, r * (128 / sub));
+          load2d(dst + j * kb_bytes + r * (kb_bytes / sub), &m, &bars[s], (kb0 + j) * 64, row0 + r * (br / sub));
     } else {
-      load3d(dst, &m, &bars[s], 0, 0, kb0);
+      load3d(dst, &m, &bars[s], 0, row0, kb0);
     }
   };
   long long t0 = clock64();
@@ -88,48 +89,48 @@ int main() {
   EncodeFn enc = (EncodeFn)fnp;
   unsigned long long* d_out;
   cudaMalloc(&d_out, 1024 * 8);
-  for (int K : {64, 768}) {
+  struct Shape { int R, K, br; const char* what; };
+  Shape shapes[] = {{128, 768, 128, "hot A 128x768 (batch-1)"}, {4096, 768, 128, "A 4096x768, 128-row boxes"},
+                    {2304, 768, 256, "W 2304x768, 256-row boxes"}, {4096, 768, 64, "A 4096x768, 64-row boxes"}};
+  for (auto& sh : shapes) {
+    const int K = sh.K, br = sh.br, nrb = sh.R / br;
     void* a;
-    cudaMalloc(&a, 128 * K * 2);
-    cudaMemset(a, 0, 128 * K * 2);
-    const int nkb = K / 64;  // K = 64: the whole matrix is one contiguous box
-    struct Cfg { int mode, sub, kpr, stages; const char* tag; CUtensorMapL2promotion promo; };
-    Cfg cfgs[] = {{0, 1, 1, 8, "2d 128-row box (16KB)", CU_TENSOR_MAP_L2_PROMOTION_L2_256B},
-                  {0, 1, 1, 8, "2d 128-row box, promo none", CU_TENSOR_MAP_L2_PROMOTION_NONE},
-                  {0, 1, 1, 8, "2d 128-row box, promo 128", CU_TENSOR_MAP_L2_PROMOTION_L2_128B},
-                  {0, 2, 1, 8, "2d 64-row boxes (8KB)", CU_TENSOR_MAP_L2_PROMOTION_L2_256B},
-                  {1, 1, 1, 8, "3d box 1 kblock (16KB)", CU_TENSOR_MAP_L2_PROMOTION_L2_256B},
-                  {1, 1, 1, 8, "3d box 1 kblock, promo none", CU_TENSOR_MAP_L2_PROMOTION_NONE},
-                  {1, 1, 2, 4, "3d box 2 kblocks (32KB)", CU_TENSOR_MAP_L2_PROMOTION_L2_256B},
-                  {1, 1, 2, 4, "3d box 2 kblocks, promo none", CU_TENSOR_MAP_L2_PROMOTION_NONE},
-                  {1, 1, 4, 2, "3d box 4 kblocks (64KB)", CU_TENSOR_MAP_L2_PROMOTION_L2_256B}};
+    cudaMalloc(&a, (size_t)sh.R * K * 2);
+    cudaMemset(a, 0, (size_t)sh.R * K * 2);
+    const int nkb = K / 64;
+    struct Cfg { int mode, kpr, stages; const char* tag; };
+    const int kbk = br * 128 / 1024;  // KB per k-block
+    Cfg cfgs[] = {{0, 1, 128 / kbk, "2d, 1 k-block per request"}, {0, 2, 64 / kbk, "2d x2 requests per stage"},
+                  {1, 1, 128 / kbk, "3d, 1 k-block per request"}, {1, 2, 64 / kbk, "3d, 2 k-blocks per request"},
+                  {1, 4, 32 / kbk > 0 ? 32 / kbk : 1, "3d, 4 k-blocks per request"}};
     for (auto& c : cfgs) {
       CUtensorMap m;
       CUresult r;
       if (c.mode == 0) {
-        cuuint64_t dims[2] = {(cuuint64_t)K, 128};
+        cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)sh.R};
         cuuint64_t strides[1] = {(cuuint64_t)K * 2};
-        cuuint32_t box[2] = {64, (cuuint32_t)(128 / c.sub)};
+        cuuint32_t box[2] = {64, (cuuint32_t)br};
         cuuint32_t es[2] = {1, 1};
         r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, a, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                CU_TENSOR_MAP_SWIZZLE_128B, c.promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       } else {
-        cuuint64_t dims[3] = {64, 128, (cuuint64_t)nkb};
+        cuuint64_t dims[3] = {64, (cuuint64_t)sh.R, (cuuint64_t)nkb};
         cuuint64_t strides[2] = {(cuuint64_t)K * 2, 128};
-        cuuint32_t box[3] = {64, 128, (cuuint32_t)c.kpr};
+        cuuint32_t box[3] = {64, (cuuint32_t)br, (cuuint32_t)c.kpr};
         cuuint32_t es[3] = {1, 1, 1};
         r = enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 3, a, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                CU_TENSOR_MAP_SWIZZLE_128B, c.promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
       }
       if (r != CUDA_SUCCESS) {
-        printf("{\"tag\": \"%s\", \"K\": %d, \"encode_error\": %d}\n", c.tag, K, (int)r);
+        printf("{\"shape\": \"%s\", \"tag\": \"%s\", \"encode_error\": %d}\n", sh.what, c.tag, (int)r);
         continue;
       }
-      const size_t smem = (size_t)c.stages * c.kpr * 16384 + 1024;
+      const size_t smem = (size_t)c.stages * c.kpr * br * 128 + 1024;
       cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       const int iters = 3000 / c.kpr;
       for (int grid : {1, sms}) {
-        for (int rep = 0; rep < 2; ++rep) k<<<grid, 32, smem>>>(m, c.mode, c.sub, c.kpr, c.stages, nkb, iters, d_out);
+        for (int rep = 0; rep < 2; ++rep)
+          k<<<grid, 32, smem>>>(m, c.mode, 1, c.kpr, c.stages, nkb, iters, d_out, br, nrb);
         cudaError_t e = cudaDeviceSynchronize();
         if (e != cudaSuccess) {
           printf("{\"tag\": \"%s\", \"err\": \"%s\"}\n", c.tag, cudaGetErrorString(e));
@@ -143,9 +144,9 @@ int main() {
           mx = h[i] > mx ? h[i] : mx;
         }
         cyc /= grid;
-        const double bytes = (double)(iters + c.stages) * c.kpr * 16384;
-        printf("{\"tag\": \"%s\", \"K\": %d, \"grid\": %d, \"B_per_clk_per_sm\": %.1f, \"chip_B_per_clk\": %.0f}\n", c.tag,
-               K, grid, bytes / cyc, bytes / mx * grid);
+        const double bytes = (double)(iters + c.stages) * c.kpr * br * 128;
+        printf("{\"shape\": \"%s\", \"tag\": \"%s\", \"in_flight_kb\": %d, \"grid\": %d, \"B_per_clk_per_sm\": %.1f, \"chip_B_per_clk\": %.0f}\n",
+               sh.what, c.tag, (int)(c.stages * c.kpr * kbk), grid, bytes / cyc, bytes / mx * grid);
       }
     }
     cudaFree(a);

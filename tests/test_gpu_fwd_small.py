@@ -52,3 +52,27 @@ def test_fwd_small_bad_token_reported():
     with pytest.raises(IndexError):
         m.sync_status(st)
     m.close()
+
+
+def test_fwd_small_repeatable_under_back_to_back_launches():
+    """Race detector for the grid-barrier protocol (release/acquire + the TMA thread's
+    proxy fence): 200 back-to-back forwards of a 12-layer model on one stream must give
+    bit-identical logits -- a stale operand read in any of the ~85 stages would not."""
+    import torch
+    cfg = GPT2_SMALLV.replace(num_layers=12)
+    o = oracle()
+    m = pg.DeviceModel(pg.ModelConfig(**cfg.__dict__), model_params(cfg))
+    B, S = 1, 128
+    ids = torch.as_tensor(o.random_tokens(cfg.vocab, B, S, 11).reshape(-1), dtype=torch.int32, device="cuda")
+    width = (cfg.vocab + 7) // 8 * 8
+    outs = torch.empty(200, B * S, width, dtype=torch.float16, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    for i in range(outs.shape[0]):
+        m.forward_device(ids.data_ptr(), B, S, "hybrid", outs[i].data_ptr(), pg.OUT_F16, width, st, True)
+    torch.cuda.synchronize()
+    m.sync_status(st)
+    ref = outs[0]
+    assert torch.isfinite(ref.float()).all()
+    bad = [(i) for i in range(1, outs.shape[0]) if not torch.equal(outs[i], ref)]
+    assert not bad, f"{len(bad)} of {outs.shape[0] - 1} repeats differ (first {bad[:5]})"
+    m.close()
