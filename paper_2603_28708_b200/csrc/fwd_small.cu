@@ -37,8 +37,8 @@ constexpr int kTileN = 32;               // GEMM output columns per task
 // TMA request moves several 64-wide k-blocks.  Measured (scripts/ubench/ubench_tma2d.cu,
 // profiles/r01/ubench_tma2d.jsonl): a 2D 128-row SW128 box (16 KB) streams at 26.6 B/clk
 // per SM, a 3D box of 2 k-blocks (32 KB) at 91.5 B/clk -- the per-request cost dominates.
-constexpr int kKPR = 2;                  // k-blocks per A request / ring stage
-constexpr int kStages = 4;               // A ring of 4 x 32 KB (the attention scratch aliases it)
+constexpr int kKPR = 4;                  // max k-blocks per A request (one ring slot)
+constexpr int kStages = 2;               // A ring of 2 x 64 KB (the attention scratch aliases it)
 constexpr uint32_t kABytes = 128 * 64 * 2;         // 16 KB per k-block
 constexpr uint32_t kBBox = kTileN * 64 * 2;        // 4 KB per 64-wide k-block
 constexpr int kMaxKB = 16;                         // B for one task: <= 16 k-blocks (1024 of K)
@@ -212,7 +212,7 @@ __device__ void load_b(Ctl& c, uint8_t* smem, const CUtensorMap* mB, int n0, int
 // One GEMM task: D[128 x NT] = A[:, k0:k0+64*nkb] . B[n0:n0+NT, same]^T, then `EPI`.
 // EPI 0: fp32 partial -> out32 (row pitch ld32); 1: round16(gelu(round16(round16(acc) + b)))
 // -> out16; 2: round16(round16(acc) + b) -> out16.
-template <int NT, int EPI>
+template <int NT, int EPI, int KP>
 __device__ void gemm_task(const SmallArgs& a, uint8_t* smem, Ctl& c, const CUtensorMap* mA, const CUtensorMap* mB,
                           int n0, int k0, int nkb, float* out32, int64_t ld32, const float* bias, __half* out16,
                           int64_t ld16) {
@@ -224,10 +224,10 @@ __device__ void gemm_task(const SmallArgs& a, uint8_t* smem, Ctl& c, const CUten
   if (warp == 4) {
     if (lane == 0) {
       fence_proxy_async_global();  // A was written by generic stores of the previous stage
-      for (int kb = 0; kb < nkb; kb += kKPR) {
-        const uint32_t u = (c.kc + kb) / kKPR, st = u % kStages;
+      for (int kb = 0; kb < nkb; kb += KP) {  // one request of KP k-blocks per ring slot
+        const uint32_t u = c.kc + kb / KP, st = u % kStages;
         mbar_wait(&c.empty[st], ((u / kStages) & 1) ^ 1);
-        mbar_expect_tx(&c.full[st], kKPR * kABytes);
+        mbar_expect_tx(&c.full[st], KP * kABytes);
         tma_load_3d(sA + st * kKPR * kABytes, mA, &c.full[st], 0, 0, k0 / 64 + kb);
       }
     }
@@ -241,13 +241,13 @@ __device__ void gemm_task(const SmallArgs& a, uint8_t* smem, Ctl& c, const CUten
       mbar_wait(c.bfull, c.tc & 1);
       if (gs) gs[1] = globaltimer();
       tc_fence_after();
-      for (int kb = 0; kb < nkb; kb += kKPR) {
-        const uint32_t u = (c.kc + kb) / kKPR, st = u % kStages;
+      for (int kb = 0; kb < nkb; kb += KP) {
+        const uint32_t u = c.kc + kb / KP, st = u % kStages;
         mbar_wait(&c.full[st], (u / kStages) & 1);
         if (gs && kb == 0) gs[2] = globaltimer();
         tc_fence_after();
 #pragma unroll
-        for (int j = 0; j < kKPR; ++j) {
+        for (int j = 0; j < KP; ++j) {
           const uint32_t a0 = smem_u32(sA + (st * kKPR + j) * kABytes), b0 = smem_u32(sB + (kb + j) * (NT * 128));  // the 3D box packs k-blocks at NT rows
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
@@ -314,7 +314,7 @@ __device__ void gemm_task(const SmallArgs& a, uint8_t* smem, Ctl& c, const CUten
     }
   }
   if (a.dbg && blockIdx.x == 0 && c.tc < 64 && threadIdx.x == 0) a.dbg[220000 + c.tc * 8 + 5] = globaltimer();
-  c.kc += nkb;
+  c.kc += nkb / KP;  // ring slots used
   c.tc += 1;
 }
 
@@ -455,7 +455,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
     }
     // ---- QKV: N=16 tiles, full K, round16(round16(acc) + b) -> fp16 q|k|v (ff16 buffer)
     for (int t = blockIdx.x; t < t_qkv; t += gridDim.x)
-      gemm_task<16, 2>(a, smem, c, mXn, mW + 0, t * 16, 0, h / 64, nullptr, 0, w.bqkv, a.ff16, 3 * h);
+      gemm_task<16, 2, 4>(a, smem, c, mXn, mW + 0, t * 16, 0, h / 64, nullptr, 0, w.bqkv, a.ff16, 3 * h);
     pre_wo(l);
     grid_sync(a.gbar, target, a.dbg);
     // ---- attention: (batch, head, 16-query block), SIMT fp32 on the fp16 q/k/v
@@ -595,7 +595,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
     grid_sync(a.gbar, target, a.dbg);
     // ---- Wo: partials over K splits
     for (int t = blockIdx.x; t < t_wo; t += gridDim.x)
-      gemm_task<kTileN, 0>(a, smem, c, mCtx, mW + 1, (t / a.split_wo) * kTileN, (t % a.split_wo) * kb_wo * 64, kb_wo,
+      gemm_task<kTileN, 0, 2>(a, smem, c, mCtx, mW + 1, (t / a.split_wo) * kTileN, (t % a.split_wo) * kb_wo * 64, kb_wo,
                            a.part + static_cast<int64_t>(t % a.split_wo) * M * h, h, nullptr, nullptr, 0);
     pre_ffn1(l);
     grid_sync(a.gbar, target, a.dbg);
@@ -606,12 +606,12 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
     grid_sync(a.gbar, target, a.dbg);
     // ---- FFN1 + GELU, full K
     for (int t = blockIdx.x; t < t_ffn1; t += gridDim.x)
-      gemm_task<kTileN, 1>(a, smem, c, mXn, mW + 2, t * kTileN, 0, h / 64, nullptr, 0, w.b1, a.ff16, f);
+      gemm_task<kTileN, 1, 4>(a, smem, c, mXn, mW + 2, t * kTileN, 0, h / 64, nullptr, 0, w.b1, a.ff16, f);
     pre_ffn2(l);
     grid_sync(a.gbar, target, a.dbg);
     // ---- FFN2: partials over K splits
     for (int t = blockIdx.x; t < t_ffn2; t += gridDim.x)
-      gemm_task<kTileN, 0>(a, smem, c, mFf, mW + 3, (t / a.split_ffn2) * kTileN, (t % a.split_ffn2) * kb_ffn2 * 64,
+      gemm_task<kTileN, 0, 4>(a, smem, c, mFf, mW + 3, (t / a.split_ffn2) * kTileN, (t % a.split_ffn2) * kb_ffn2 * 64,
                            kb_ffn2, a.part + static_cast<int64_t>(t % a.split_ffn2) * M * h, h, nullptr, nullptr, 0);
     if (l + 1 < a.L) pre_qkv(l + 1);
     grid_sync(a.gbar, target, a.dbg);

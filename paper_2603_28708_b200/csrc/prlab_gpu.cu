@@ -666,13 +666,13 @@ void plan_small(prlab_gpu_model& m, prlab_gpu_model::Plan& p, int64_t B, int64_t
   auto& maps = p.small_maps;
   maps.clear();
   // K-major matrices viewed as [K/64 k-blocks][rows][64]: a box spans several k-blocks
-  // (one TMA request per 2 k-blocks of A, one per task for B -- fwd_small.cu)
+  // (one TMA request per 2-4 k-blocks of A, one per task for B -- fwd_small.cu)
   auto kblk = [](const void* base, int64_t rows, int64_t K, uint32_t box_rows, uint32_t box_kb) {
     return make_tmap_f16_3d(base, 64, rows, K / 64, K, 64, 64, box_rows, box_kb);
   };
-  maps.push_back(kblk(p.xn16, M, h, 128, 2));
-  maps.push_back(kblk(ctx16, M, h, 128, 2));
-  maps.push_back(kblk(p.big16, M, f, 128, 2));  // ff16 reuses the qkv/ff buffer
+  maps.push_back(kblk(p.xn16, M, h, 128, 4));    // QKV / FFN1 A: 4 k-blocks per request
+  maps.push_back(kblk(ctx16, M, h, 128, 2));     // Wo A: the split depth is 2 k-blocks
+  maps.push_back(kblk(p.big16, M, f, 128, 4));   // FFN2 A (ff16 reuses the qkv/ff buffer)
   p.small_lw.assign(static_cast<size_t>(L), {});
   const int64_t kb_wo = h / 64 / (h / 128), kb_ffn2 = f / 64 / (f / 512);  // split-K depths (launch_fwd_small)
   for (int64_t l = 0; l < L; ++l) {
