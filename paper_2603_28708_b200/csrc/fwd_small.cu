@@ -1,25 +1,25 @@
 // Batch-1 forward as ONE persistent kernel (hybrid policy, M = B*S <= 128 rows,
-// S <= 128 keys): the 85 dependent steps of a GPT-2/BERT forward_hidden
+// S <= 128 keys): the 73 dependent steps of a GPT-2/BERT forward_hidden
 // (src/model.cpp:350-452) run as stages of a cooperative grid (one CTA per SM)
-// separated by grid-wide barriers, instead of 85 kernel launches whose fixed
+// separated by grid-wide barriers, instead of ~85 kernel launches whose fixed
 // launch/drain cost (~2.9 us each) dominates batch-1 latency.
 //
 // Per layer (tasks are spread over the CTAs; every stage reads only what the previous
 // stages wrote, so one barrier between stages is the whole synchronisation):
-//   QKV   xn16 . Wqkv^T     tcgen05 M=128 N=32 tiles, K split in 2 -> fp32 partials
-//   ATTN  per (batch, head, 16 queries): q/k/v = round16(round16(p0 + p1) + b) from the
-//         partials, scores round16(fp32 dot * 0.125), causal -inf, exact two-pass
-//         softmax, p = round16(e / sum), o = round16(sum_j p_j v_j) -> ctx16 (SIMT fp32;
-//         products of fp16 values are exact in fp32, kernels.cpp:85-168)
-//   WO    ctx16 . Wo^T      N=32 tiles x K/128 splits -> fp32 partials
-//   RLN2  per row: x += round16(round16(sum of partials) + bo); xn16 = round16(LN2(x))
-//   FFN1  xn16 . W1^T       N=32 tiles, full K, epilogue round16(gelu(round16(acc+b1)))
-//   FFN2  ff16 . W2^T       N=32 tiles x F/512 splits -> fp32 partials
-//   RLN1  per row: x += round16(round16(sum) + b2); xn16 = round16(LN(x)) with the next
-//         layer's LN1 (or the final LN) -- embed + LN1 of layer 0 is stage 0
+//   QKV     xn16 . Wqkv^T   tcgen05 M=128 N=16 tiles, full K, epilogue round16(round16(acc) + b)
+//                           -> fp16 q|k|v
+//   ATTN+WO per (batch, head, 16 queries), warp-level tensor-core tiles (mma.sync): scores
+//           round16(q.k * 0.125), causal -inf, exact two-pass softmax, p = round16(e / sum),
+//           ctx = round16(p . v), then the head's share of the output projection
+//           ctx_h . Wo[:, head cols]^T -> fp32 partial per head (model.cpp:372-392)
+//   RLN2    per row: x += round16(round16(sum of the head partials) + bo); xn16 = round16(LN2(x))
+//   FFN1    xn16 . W1^T     N=32 tiles, full K, epilogue round16(gelu(round16(acc+b1)))
+//   FFN2    ff16 . W2^T     N=32 tiles x F/512 splits -> fp32 partials
+//   RLN1    per row: x += round16(round16(sum) + b2); xn16 = round16(LN(x)) with the next
+//           layer's LN1 (or the final LN) -- embed + LN1 of layer 0 is stage 0
 // The tied head stays a separate (PDL-chained) GEMM launch on xn16.
 // Rounding points are those of the multi-kernel path; the only
-// difference is the fp32 summation order (split-K partials, SIMT attention dots).
+// difference is the fp32 summation order (split-K / per-head partials, mma.sync tiles).
 #include <cstdlib>
 #include <cstring>
 #include <stdexcept>
@@ -42,16 +42,23 @@ constexpr int kStages = 2;               // A ring of 2 x 64 KB (the attention s
 constexpr uint32_t kABytes = 128 * 64 * 2;         // 16 KB per k-block
 constexpr uint32_t kBBox = kTileN * 64 * 2;        // 4 KB per 64-wide k-block
 constexpr int kMaxKB = 16;                         // B for one task: <= 16 k-blocks (1024 of K)
-constexpr int kQB = 16;                            // queries per attention task
+constexpr int kQB = 16;                            // queries per attention task (one m16 MMA row block)
 
-constexpr int kKS = 68, kVS = 64;  // fp32 row strides of the staged K (16B-aligned, conflict-free LDS.128) and V
 struct SmemL {
   static constexpr uint32_t A = 0;
   static constexpr uint32_t B = A + kStages * kKPR * kABytes;      // 128 KB
-  static constexpr uint32_t ATT = A;                               // attention scratch: the A ring is idle then
-  static constexpr uint32_t ATT_BYTES = (128 * kKS + 128 * kVS + 8 * 128) * 4;
-  static constexpr uint32_t BAR = B + kMaxKB * kBBox;
+  static constexpr uint32_t BAR = B + kMaxKB * kBBox;              // 192 KB
 };
+// Attention + Wo stage scratch (the A ring and the B region are idle then): the head's
+// Wo column slice [h rows][64] (TMA, 128B-swizzled), then K, V, Q, scores, P, ctx with
+// padded rows (conflict-free ldmatrix).
+constexpr int kRowH = 72;    // fp16 row stride (halves) of K / V / Q / ctx
+constexpr int kRowP = 136;   // fp16 row stride of P
+constexpr int kRowS = 132;   // fp32 row stride of the scores
+__host__ __device__ constexpr uint32_t att_bytes(int h) {
+  return static_cast<uint32_t>(h) * 128 + (2 * 128 + 2 * kQB) * kRowH * 2 + kQB * kRowS * 4 + kQB * kRowP * 2;
+}
+static_assert(att_bytes(1024) <= SmemL::BAR, "attention scratch");
 
 struct LayerW {
   const float *ln1g, *ln1b, *ln2g, *ln2b;  // fp32 [h]
@@ -64,16 +71,16 @@ constexpr int kMaxLayers = 48;
 // tensor maps (TMA descriptors are fetched from param space) and the per-layer
 // parameter pointers, so no stage starts with a dependent global load.
 struct SmallArgs {
-  CUtensorMap maps[3 + 4 * kMaxLayers];  // xn16, ctx16, ff16, then per layer Wqkv, Wo, W1, W2
+  CUtensorMap maps[2 + 4 * kMaxLayers];  // xn16, ff16, then per layer Wqkv, Wo (2D, 256-row box), W1, W2
   LayerW lw[kMaxLayers];
   int M, B, S, h, f, H, L, V, causal;
-  int split_qkv, split_wo, split_ffn2;
+  int split_ffn2;
   const float *tok, *pos, *lnfg, *lnfb;
   const int32_t* ids;
   int* err;
   float* x;
-  __half *xn16, *ctx16, *ff16;
-  float *qkvp, *part;            // partial sums [split][M][3h], [split][M][h]
+  __half *xn16, *ff16;
+  float* part;                   // fp32 partial sums [split][M][h] (split = head for Wo, K split for FFN2)
   unsigned* gbar;                // grid barrier counter (zeroed before each launch)
   long long* dbg;                // optional [stage][grid][2] globaltimer (arrive, release)
 };
@@ -318,21 +325,186 @@ __device__ void gemm_task(const SmallArgs& a, uint8_t* smem, Ctl& c, const CUten
   c.tc += 1;
 }
 
+// ---- warp-level tensor-core fragments (mma.sync m16n8k16, fp16 x fp16 -> fp32) for the
+// attention tiles: 16 queries x <= 128 keys x 64 dims is far below one tcgen05 tile.
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t (&r)[4]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0, %1, %2, %3}, [%4];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x2_trans(uint32_t addr, uint32_t (&r)[2]) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x2.trans.shared.b16 {%0, %1}, [%2];" : "=r"(r[0]), "=r"(r[1]) : "r"(addr));
+}
+__device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
+}
+
+// One (batch, head, 16-query block) of attention fused with its slice of the output
+// projection (model.cpp:372-392 + the Wo Linear): scores round16(q.k * 0.125) (causal
+// -inf), exact two-pass softmax p = round16(e / sum), ctx = round16(p . v), then the
+// head's Wo partial ctx_h . Wo[:, head cols]^T -> part[head][rows] in fp32; the RLN2
+// stage sums the heads' partials in head order.  q/k/v come from the QKV stage's fp16
+// output (pitch 3h).
+__device__ void attn_wo_task(const SmallArgs& a, uint8_t* smem, const CUtensorMap* mWo, uint64_t* wo_bar,
+                             uint32_t wo_phase, int b, int hh, int q0) {
+  const int h = a.h, S = a.S;
+  const uint32_t warp = warp_id(), lane = lane_id();
+  uint8_t* sWo = smem;
+  __half* sK = reinterpret_cast<__half*>(smem + h * 128);
+  __half* sV = sK + 128 * kRowH;
+  __half* sQ = sV + 128 * kRowH;
+  __half* sC = sQ + kQB * kRowH;
+  float* sS = reinterpret_cast<float*>(sC + kQB * kRowH);
+  __half* sP = reinterpret_cast<__half*>(sS + kQB * kRowS);
+  const int kv = a.causal ? min(S, q0 + kQB) : S;  // keys this block can see
+  const int kvp = (kv + 15) & ~15;
+  __syncthreads();  // the previous task's readers are done with the scratch
+  if (threadIdx.x == 0) {  // the head's Wo column slice: h rows x 64 (128 B), 256-row boxes
+    mbar_expect_tx(wo_bar, static_cast<uint32_t>(h) * 128);
+    for (int r = 0; r < h; r += 256) tma_load_2d(sWo + r * 128, mWo, wo_bar, hh * 64, r);
+  }
+  {
+    const __half* base = a.ff16 + static_cast<int64_t>(b) * S * 3 * h + hh * 64;
+    const uint4 z = make_uint4(0, 0, 0, 0);
+    for (int e = threadIdx.x; e < kvp * 8; e += kThreads) {
+      const int j = e >> 3, c8 = (e & 7) * 8;
+      uint4 kk = z, vv = z;
+      if (j < kv) {
+        kk = *reinterpret_cast<const uint4*>(base + static_cast<int64_t>(j) * 3 * h + h + c8);
+        vv = *reinterpret_cast<const uint4*>(base + static_cast<int64_t>(j) * 3 * h + 2 * h + c8);
+      }
+      *reinterpret_cast<uint4*>(sK + j * kRowH + c8) = kk;
+      *reinterpret_cast<uint4*>(sV + j * kRowH + c8) = vv;
+    }
+    if (threadIdx.x < kQB * 8) {
+      const int i = threadIdx.x >> 3, c8 = (threadIdx.x & 7) * 8;
+      uint4 qq = z;
+      if (q0 + i < S) qq = *reinterpret_cast<const uint4*>(base + static_cast<int64_t>(q0 + i) * 3 * h + c8);
+      *reinterpret_cast<uint4*>(sQ + i * kRowH + c8) = qq;
+    }
+  }
+  __syncthreads();
+  const int g = lane >> 2, t4 = lane & 3;
+  // scores: warp w -> keys [16w, 16w + 16)
+  if (static_cast<int>(warp) * 16 < kvp) {
+    float acc[2][4] = {};
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) {
+      uint32_t af[4], bf[4];
+      ldsm_x4(smem_u32(sQ + (lane & 15) * kRowH + ks * 16 + (lane >> 4) * 8), af);
+      ldsm_x4(smem_u32(sK + (warp * 16 + (lane & 7) + (lane >> 4) * 8) * kRowH + ks * 16 + ((lane >> 3) & 1) * 8), bf);
+      mma16816(acc[0], af, bf[0], bf[1]);
+      mma16816(acc[1], af, bf[2], bf[3]);
+    }
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const int r = g + (e >> 1) * 8, j = warp * 16 + nt * 8 + 2 * t4 + (e & 1);
+        const bool valid = j < kv && (!a.causal || j <= q0 + r);
+        sS[r * kRowS + j] = valid ? r16(__fmul_rn(acc[nt][e], 0.125f)) : __int_as_float(0xff800000);
+      }
+  }
+  __syncthreads();
+  // softmax: warp w -> rows 2w, 2w + 1; lane -> keys lane + 32c
+#pragma unroll
+  for (int rr = 0; rr < 2; ++rr) {
+    const int r = warp * 2 + rr;
+    float sc[4];
+    float mx = __int_as_float(0xff800000);
+#pragma unroll
+    for (int c4 = 0; c4 < 4; ++c4) {
+      const int j = c4 * 32 + lane;
+      sc[c4] = j < kvp ? sS[r * kRowS + j] : __int_as_float(0xff800000);
+      mx = fmaxf(mx, sc[c4]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    constexpr float LOG2E = 1.4426950408889634f;
+    const float mxl = __fmul_rn(mx, LOG2E);
+    float e[4], sum = 0.0f;
+#pragma unroll
+    for (int c4 = 0; c4 < 4; ++c4) {
+      e[c4] = ex2_approx(__fmaf_rn(sc[c4], LOG2E, -mxl));  // exp(-inf) = 0 for masked keys
+      sum = __fadd_rn(sum, e[c4]);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum = __fadd_rn(sum, __shfl_xor_sync(0xffffffffu, sum, o));
+    const float inv = __frcp_rn(sum);
+#pragma unroll
+    for (int c4 = 0; c4 < 4; ++c4) {
+      const int j = c4 * 32 + lane;
+      if (j < kvp) sP[r * kRowP + j] = __float2half_rn(__fmul_rn(e[c4], inv));
+    }
+  }
+  __syncthreads();
+  // ctx = round16(P . V): warp w -> dims [8w, 8w + 8)
+  {
+    float o[4] = {};
+    for (int ks = 0; ks < kvp / 16; ++ks) {
+      uint32_t af[4], bf[2];
+      ldsm_x4(smem_u32(sP + (lane & 15) * kRowP + ks * 16 + (lane >> 4) * 8), af);
+      ldsm_x2_trans(smem_u32(sV + (ks * 16 + (lane & 15)) * kRowH + warp * 8), bf);
+      mma16816(o, af, bf[0], bf[1]);
+    }
+    *reinterpret_cast<__half2*>(sC + g * kRowH + warp * 8 + 2 * t4) = __floats2half2_rn(o[0], o[1]);
+    *reinterpret_cast<__half2*>(sC + (g + 8) * kRowH + warp * 8 + 2 * t4) = __floats2half2_rn(o[2], o[3]);
+  }
+  __syncthreads();
+  // Wo partial: out[16][h] = ctx . WoSlice^T; warp w -> n-tiles [w * h/64, (w+1) * h/64) (pairs)
+  {
+    uint32_t af[4][4];
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks) ldsm_x4(smem_u32(sC + (lane & 15) * kRowH + ks * 16 + (lane >> 4) * 8), af[ks]);
+    mbar_wait(wo_bar, wo_phase);
+    const int per_warp = h / 64;  // n-tiles of 8 columns per warp (h / 8 tiles over 8 warps)
+    float* outp = a.part + static_cast<int64_t>(hh) * a.M * h;
+    const int row0 = b * S + q0;
+    for (int p2 = 0; p2 < per_warp; p2 += 2) {
+      const int n0 = (warp * per_warp + p2) * 8;
+      float d[2][4] = {};
+      const int n = n0 + (lane & 7) + (lane >> 4) * 8;
+#pragma unroll
+      for (int ks = 0; ks < 4; ++ks) {
+        uint32_t bf[4];
+        const int chunk = ks * 2 + ((lane >> 3) & 1);
+        ldsm_x4(smem_u32(sWo + n * 128 + ((chunk ^ (n & 7)) << 4)), bf);
+        mma16816(d[0], af[ks], bf[0], bf[1]);
+        mma16816(d[1], af[ks], bf[2], bf[3]);
+      }
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt) {
+        const int col = n0 + nt * 8 + 2 * t4;
+        if (q0 + g < S)
+          *reinterpret_cast<float2*>(outp + static_cast<int64_t>(row0 + g) * h + col) = make_float2(d[nt][0], d[nt][1]);
+        if (q0 + g + 8 < S)
+          *reinterpret_cast<float2*>(outp + static_cast<int64_t>(row0 + g + 8) * h + col) =
+              make_float2(d[nt][2], d[nt][3]);
+      }
+    }
+  }
+}
+
 __device__ __forceinline__ float h2f_lo(uint32_t v) { return __half2float(__ushort_as_half(static_cast<unsigned short>(v & 0xFFFFu))); }
 __device__ __forceinline__ float h2f_hi(uint32_t v) { return __half2float(__ushort_as_half(static_cast<unsigned short>(v >> 16))); }
 
 // x[r] += round16(round16(sum_s part[s][r]) + bias); xn16[r] = round16(LN(x[r]))
+template <int MAXSP>
 __device__ void residual_ln_row(const SmallArgs& a, int r, int nsplit, const float* bias, const float* g,
                                 const float* b, float* red, long long* ts = nullptr) {
   const int h = a.h, nper = h / kThreads;
   if (ts && threadIdx.x == 0) ts[0] = globaltimer();
-  float xv[4], pv[4][8], xo[4], bs[4];
+  float xv[4], pv[4][MAXSP], xo[4], bs[4];
 #pragma unroll
   for (int i = 0; i < 4; ++i) {  // every load of the row in flight before the ordered sums
     if (i < nper) {
       const int cc = threadIdx.x + i * kThreads;
 #pragma unroll
-      for (int sp = 0; sp < 8; ++sp) pv[i][sp] = sp < nsplit ? a.part[(static_cast<int64_t>(sp) * a.M + r) * h + cc] : 0.0f;
+      for (int sp = 0; sp < MAXSP; ++sp) pv[i][sp] = sp < nsplit ? a.part[(static_cast<int64_t>(sp) * a.M + r) * h + cc] : 0.0f;
       xo[i] = a.x[static_cast<int64_t>(r) * h + cc];
       bs[i] = bias[cc];
     }
@@ -342,7 +514,7 @@ __device__ void residual_ln_row(const SmallArgs& a, int r, int nsplit, const flo
     if (i < nper) {
       float sum = 0.0f;
 #pragma unroll
-      for (int sp = 0; sp < 8; ++sp)
+      for (int sp = 0; sp < MAXSP; ++sp)
         if (sp < nsplit) sum = __fadd_rn(sum, pv[i][sp]);
       xv[i] = __fadd_rn(xo[i], r16(__fadd_rn(r16(sum), bs[i])));
       a.x[static_cast<int64_t>(r) * h + threadIdx.x + i * kThreads] = xv[i];
@@ -362,15 +534,14 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SmemL::BAR);
   float* red = reinterpret_cast<float*>(bars + 16);  // [8]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(red + 8);
-  float* sk = reinterpret_cast<float*>(smem + SmemL::ATT);  // [128][68]
-  float* sv = sk + 128 * kKS;                                // [128][64]
-  float* sp_ = sv + 128 * kVS;                               // [8 warps][128] probabilities
   Ctl c;
   c.full = bars;
   c.empty = bars + kStages;
   c.bfull = bars + 2 * kStages;
   c.accfull = bars + 2 * kStages + 1;
   c.accempty = bars + 2 * kStages + 2;
+  uint64_t* wo_bar = bars + 2 * kStages + 3;  // the attention task's Wo slice (TMA)
+  uint32_t n_att = 0;                         // attention tasks run by this CTA (wo_bar phase)
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {
       mbar_init(&c.full[i], 1);
@@ -379,6 +550,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
     mbar_init(c.bfull, 1);
     mbar_init(c.accfull, 1);
     mbar_init(c.accempty, 4);
+    mbar_init(wo_bar, 1);
     fence_barrier_init();
   }
   if (warp == 5) {
@@ -386,7 +558,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
     tmem_relinquish();
   }
   if (warp == 6)
-    for (int i = lane; i < 3 + 4 * a.L; i += 32) tma_prefetch_desc(&a.maps[i]);
+    for (int i = lane; i < 2 + 4 * a.L; i += 32) tma_prefetch_desc(&a.maps[i]);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -396,30 +568,23 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
   c.bpref = 0;
   unsigned target = 0;
   const CUtensorMap* mXn = a.maps + 0;
-  const CUtensorMap* mCtx = a.maps + 1;
-  const CUtensorMap* mFf = a.maps + 2;
+  const CUtensorMap* mFf = a.maps + 1;
   const int nper = h / kThreads;  // columns per thread in row tasks (h % 256 == 0)
   // task geometry (same on every CTA)
   const int t_qkv = 3 * h / 16;                    // N=16 tiles, full K -> fp16 q/k/v
-  const int t_wo = (h / kTileN) * a.split_wo;      // N=32 tiles x K splits -> partials
   const int t_ffn1 = f / kTileN;                   // N=32 tiles, full K, GELU
   const int t_ffn2 = (h / kTileN) * a.split_ffn2;  // N=32 tiles x K splits -> partials
-  const int kb_wo = h / 64 / a.split_wo, kb_ffn2 = f / 64 / a.split_ffn2;
+  const int kb_ffn2 = f / 64 / a.split_ffn2;
   auto pre_qkv = [&](int l) {
-    if (static_cast<int>(blockIdx.x) < t_qkv) load_b<16>(c, smem, a.maps + 3 + 4 * l + 0, blockIdx.x * 16, 0, h / 64);
-  };
-  auto pre_wo = [&](int l) {
-    const int t = blockIdx.x;
-    if (t < t_wo)
-      load_b<kTileN>(c, smem, a.maps + 3 + 4 * l + 1, (t / a.split_wo) * kTileN, (t % a.split_wo) * kb_wo * 64, kb_wo);
+    if (static_cast<int>(blockIdx.x) < t_qkv) load_b<16>(c, smem, a.maps + 2 + 4 * l + 0, blockIdx.x * 16, 0, h / 64);
   };
   auto pre_ffn1 = [&](int l) {
-    if (static_cast<int>(blockIdx.x) < t_ffn1) load_b<kTileN>(c, smem, a.maps + 3 + 4 * l + 2, blockIdx.x * kTileN, 0, h / 64);
+    if (static_cast<int>(blockIdx.x) < t_ffn1) load_b<kTileN>(c, smem, a.maps + 2 + 4 * l + 2, blockIdx.x * kTileN, 0, h / 64);
   };
   auto pre_ffn2 = [&](int l) {
     const int t = blockIdx.x;
     if (t < t_ffn2)
-      load_b<kTileN>(c, smem, a.maps + 3 + 4 * l + 3, (t / a.split_ffn2) * kTileN, (t % a.split_ffn2) * kb_ffn2 * 64,
+      load_b<kTileN>(c, smem, a.maps + 2 + 4 * l + 3, (t / a.split_ffn2) * kTileN, (t % a.split_ffn2) * kb_ffn2 * 64,
                      kb_ffn2);
   };
 
@@ -448,7 +613,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
 
   for (int l = 0; l < a.L; ++l) {
     const LayerW& w = a.lw[l];
-    const CUtensorMap* mW = a.maps + 3 + 4 * l;
+    const CUtensorMap* mW = a.maps + 2 + 4 * l;
     if (l + 1 < a.L) {
       prefetch_layer_params(a, a.lw[l + 1]);
       prefetch_layer_weights(a, a.lw[l + 1]);
@@ -456,153 +621,30 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
     // ---- QKV: N=16 tiles, full K, round16(round16(acc) + b) -> fp16 q|k|v (ff16 buffer)
     for (int t = blockIdx.x; t < t_qkv; t += gridDim.x)
       gemm_task<16, 2, 4>(a, smem, c, mXn, mW + 0, t * 16, 0, h / 64, nullptr, 0, w.bqkv, a.ff16, 3 * h);
-    pre_wo(l);
     grid_sync(a.gbar, target, a.dbg);
-    // ---- attention: (batch, head, 16-query block), SIMT fp32 on the fp16 q/k/v
+    // ---- attention + Wo: (batch, head, 16-query block) tasks, head partials -> part[head]
     {
-      const __half* qkv = a.ff16;
       const int nqb = (S + kQB - 1) / kQB;
-      // causal: the later query blocks see more keys -- split the last nqb/2 blocks in two
-      // 8-query tasks when the grid has room, so no single task dominates the stage
-      const int nsplit = (a.causal && a.B * H * (nqb + nqb / 2) <= static_cast<int>(gridDim.x)) ? nqb / 2 : 0;
-      const int per_bh = nqb + nsplit;
-      float* pw = sp_ + warp * 128;
-      for (int t = blockIdx.x; t < a.B * H * per_bh; t += gridDim.x) {
-        const int sub = t % per_bh, hd_ = (t / per_bh) % H, b = t / (per_bh * H);
-        const int nfull = nqb - nsplit;
-        const int q0 = sub < nfull ? sub * kQB : (nfull + (sub - nfull) / 2) * kQB + ((sub - nfull) & 1) * (kQB / 2);
-        const int qcount = sub < nfull ? kQB : kQB / 2;
-        __syncthreads();  // previous task's readers are done with sk / sv
-        {
-          // k and v rows of this (batch, head): 8 fp16 (16 bytes) per load, all loads first
-          constexpr int PER = 128 * 8 / kThreads;  // 4 chunks of 8 per thread, per tensor
-          uint4 kc[PER], vc[PER];
-#pragma unroll
-          for (int u = 0; u < PER; ++u) {
-            const int e = threadIdx.x + u * kThreads, j = e >> 3, d8 = (e & 7) * 8;
-            if (j < S) {
-              const __half* rowp = qkv + (static_cast<int64_t>(b) * S + j) * 3 * h + hd_ * 64 + d8;
-              kc[u] = *reinterpret_cast<const uint4*>(rowp + h);
-              vc[u] = *reinterpret_cast<const uint4*>(rowp + 2 * h);
-            }
-          }
-#pragma unroll
-          for (int u = 0; u < PER; ++u) {
-            const int e = threadIdx.x + u * kThreads, j = e >> 3, d8 = (e & 7) * 8;
-            if (j < S) {
-              const uint32_t kw[4] = {kc[u].x, kc[u].y, kc[u].z, kc[u].w};
-              const uint32_t vw[4] = {vc[u].x, vc[u].y, vc[u].z, vc[u].w};
-              float4* kd = reinterpret_cast<float4*>(sk + j * kKS + d8);
-              float4* vd = reinterpret_cast<float4*>(sv + j * kVS + d8);
-              kd[0] = make_float4(h2f_lo(kw[0]), h2f_hi(kw[0]), h2f_lo(kw[1]), h2f_hi(kw[1]));
-              kd[1] = make_float4(h2f_lo(kw[2]), h2f_hi(kw[2]), h2f_lo(kw[3]), h2f_hi(kw[3]));
-              vd[0] = make_float4(h2f_lo(vw[0]), h2f_hi(vw[0]), h2f_lo(vw[1]), h2f_hi(vw[1]));
-              vd[1] = make_float4(h2f_lo(vw[2]), h2f_hi(vw[2]), h2f_lo(vw[3]), h2f_hi(vw[3]));
-            }
-          }
-        }
-        __syncthreads();
-        long long* ats = (a.dbg && blockIdx.x == 0 && threadIdx.x == 0) ? a.dbg + 210000 + l * 8 : nullptr;
-        if (ats) ats[0] = globaltimer();
-        for (int qi = warp; qi < qcount; qi += kThreads / 32) {
-          const int i = q0 + qi;  // query position
-          if (i >= S) break;
-          const int64_t row = static_cast<int64_t>(b) * S + i;
-          float q[64];
-          {
-            const uint4* qp = reinterpret_cast<const uint4*>(qkv + row * 3 * h + hd_ * 64);
-            uint4 qc[8];
-#pragma unroll
-            for (int v4 = 0; v4 < 8; ++v4) qc[v4] = qp[v4];
-#pragma unroll
-            for (int v4 = 0; v4 < 8; ++v4) {
-              const uint32_t w4[4] = {qc[v4].x, qc[v4].y, qc[v4].z, qc[v4].w};
-#pragma unroll
-              for (int k2 = 0; k2 < 4; ++k2) {
-                q[v4 * 8 + 2 * k2] = h2f_lo(w4[k2]);
-                q[v4 * 8 + 2 * k2 + 1] = h2f_hi(w4[k2]);
-              }
-            }
-          }
-          float sc[4];
-          float mx = __int_as_float(0xff800000);
-#pragma unroll
-          for (int cidx = 0; cidx < 4; ++cidx) {
-            const int j = cidx * 32 + lane;
-            float acc = 0.0f;
-            if (j < S) {
-              const float4* kr = reinterpret_cast<const float4*>(sk + j * kKS);
-#pragma unroll
-              for (int d4 = 0; d4 < 16; ++d4) {  // ascending d
-                const float4 kv = kr[d4];
-                acc = __fmaf_rn(q[4 * d4], kv.x, acc);
-                acc = __fmaf_rn(q[4 * d4 + 1], kv.y, acc);
-                acc = __fmaf_rn(q[4 * d4 + 2], kv.z, acc);
-                acc = __fmaf_rn(q[4 * d4 + 3], kv.w, acc);
-              }
-            }
-            const bool valid = j < S && (!a.causal || j <= i);
-            sc[cidx] = valid ? r16(__fmul_rn(acc, 0.125f)) : __int_as_float(0xff800000);
-            mx = fmaxf(mx, sc[cidx]);
-          }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-          constexpr float LOG2E = 1.4426950408889634f;
-          const float mxl = __fmul_rn(mx, LOG2E);
-          float e[4], sum = 0.0f;
-#pragma unroll
-          for (int cidx = 0; cidx < 4; ++cidx) {
-            e[cidx] = ex2_approx(__fmaf_rn(sc[cidx], LOG2E, -mxl));  // exp(-inf) = 0 for masked keys
-            sum = __fadd_rn(sum, e[cidx]);
-          }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) sum = __fadd_rn(sum, __shfl_xor_sync(0xffffffffu, sum, o));
-          const float inv = __frcp_rn(sum);
-#pragma unroll
-          for (int cidx = 0; cidx < 4; ++cidx) pw[cidx * 32 + lane] = r16(__fmul_rn(e[cidx], inv));
-          __syncwarp();
-          // o[d] for d = 2*lane, 2*lane + 1
-          // four interleaved partial sums (key j mod 4) break the FMA dependency chain
-          float oa[4] = {0.0f, 0.0f, 0.0f, 0.0f}, ob[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-          const int jmax = a.causal ? min(S, i + 1) : S;
-          int j = 0;
-          for (; j + 4 <= jmax; j += 4) {
-            const float4 p4 = *reinterpret_cast<const float4*>(pw + j);
-            const float pj[4] = {p4.x, p4.y, p4.z, p4.w};
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const float2 vv = *reinterpret_cast<const float2*>(sv + (j + u) * kVS + 2 * lane);
-              oa[u] = __fmaf_rn(pj[u], vv.x, oa[u]);
-              ob[u] = __fmaf_rn(pj[u], vv.y, ob[u]);
-            }
-          }
-          for (; j < jmax; ++j) {
-            const float pj = pw[j];
-            const float2 vv = *reinterpret_cast<const float2*>(sv + j * kVS + 2 * lane);
-            oa[0] = __fmaf_rn(pj, vv.x, oa[0]);
-            ob[0] = __fmaf_rn(pj, vv.y, ob[0]);
-          }
-          const float o0 = __fadd_rn(__fadd_rn(oa[0], oa[1]), __fadd_rn(oa[2], oa[3]));
-          const float o1 = __fadd_rn(__fadd_rn(ob[0], ob[1]), __fadd_rn(ob[2], ob[3]));
-          *reinterpret_cast<__half2*>(a.ctx16 + row * h + hd_ * 64 + 2 * lane) = __floats2half2_rn(o0, o1);
-          __syncwarp();  // pw is rewritten by this warp's next query
-        }
-        if (ats) ats[1] = globaltimer();
+      long long* ats = (a.dbg && blockIdx.x == 0 && threadIdx.x == 0) ? a.dbg + 210000 + l * 8 : nullptr;
+      if (ats) ats[0] = globaltimer();
+      for (int t = blockIdx.x; t < a.B * H * nqb; t += gridDim.x) {
+        const int qb = t % nqb, hh = (t / nqb) % H, b = t / (nqb * H);
+        // generic reads of the previous task's Wo slice before this task's TMA rewrites it
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        attn_wo_task(a, smem, mW + 1, wo_bar, n_att & 1, b, hh, qb * kQB);
+        ++n_att;
       }
-      // sk / sv (generic smem writes) alias the A ring the next GEMM stage fills by TMA
+      if (ats) ats[1] = globaltimer();
+      // the scratch (generic writes) overlaps the B region the FFN1 weights are fetched into
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      pre_ffn1(l);
     }
     grid_sync(a.gbar, target, a.dbg);
-    // ---- Wo: partials over K splits
-    for (int t = blockIdx.x; t < t_wo; t += gridDim.x)
-      gemm_task<kTileN, 0, 2>(a, smem, c, mCtx, mW + 1, (t / a.split_wo) * kTileN, (t % a.split_wo) * kb_wo * 64, kb_wo,
-                           a.part + static_cast<int64_t>(t % a.split_wo) * M * h, h, nullptr, nullptr, 0);
-    pre_ffn1(l);
-    grid_sync(a.gbar, target, a.dbg);
-    // ---- residual + LN2
+    // ---- residual + LN2: x += round16(round16(sum over heads of the Wo partials) + bo)
     for (int r = blockIdx.x; r < M; r += gridDim.x)
-      residual_ln_row(a, r, a.split_wo, w.bo, w.ln2g, w.ln2b, red,
-                      (a.dbg && blockIdx.x == 0) ? a.dbg + 200000 + l * 8 : nullptr);
+      residual_ln_row<16>(a, r, H, w.bo, w.ln2g, w.ln2b, red,
+                          (a.dbg && blockIdx.x == 0) ? a.dbg + 200000 + l * 8 : nullptr);
     grid_sync(a.gbar, target, a.dbg);
     // ---- FFN1 + GELU, full K
     for (int t = blockIdx.x; t < t_ffn1; t += gridDim.x)
@@ -619,7 +661,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
     {
       const float* g = l + 1 < a.L ? a.lw[l + 1].ln1g : a.lnfg;
       const float* bb = l + 1 < a.L ? a.lw[l + 1].ln1b : a.lnfb;
-      for (int r = blockIdx.x; r < M; r += gridDim.x) residual_ln_row(a, r, a.split_ffn2, w.b2, g, bb, red);
+      for (int r = blockIdx.x; r < M; r += gridDim.x) residual_ln_row<8>(a, r, a.split_ffn2, w.b2, g, bb, red);
     }
     if (l + 1 < a.L) grid_sync(a.gbar, target, a.dbg);
   }
@@ -650,9 +692,8 @@ bool fwd_small_supported(int64_t M, int64_t S, int64_t h, int64_t f, int64_t hd,
 }
 
 size_t fwd_small_workspace_floats(int64_t M, int64_t h, int64_t f) {
-  (void)f;
-  const int64_t sp_wo = h / 128, sp_ffn2 = f / 512;
-  return static_cast<size_t>(std::max<int64_t>(std::max(sp_wo, sp_ffn2) * M * h, 2 * M * 3 * h) + 64);
+  const int64_t heads = h / 64, sp_ffn2 = f / 512;  // Wo partials per head, FFN2 K splits
+  return static_cast<size_t>(std::max(heads, sp_ffn2) * M * h + 64);
 }
 
 void launch_fwd_small(const FwdSmallPlan& p, cudaStream_t st) {
@@ -673,11 +714,9 @@ void launch_fwd_small(const FwdSmallPlan& p, cudaStream_t st) {
   a.L = p.L;
   a.V = p.V;
   a.causal = p.causal;
-  a.split_qkv = 1;
-  a.split_wo = p.h / 128;
   a.split_ffn2 = p.f / 512;
   if (p.L > kMaxLayers) throw std::invalid_argument("fwd_small: too many layers");
-  std::memcpy(a.maps, p.host_maps, sizeof(CUtensorMap) * (3 + 4 * p.L));
+  std::memcpy(a.maps, p.host_maps, sizeof(CUtensorMap) * (2 + 4 * p.L));
   std::memcpy(a.lw, p.host_lw, sizeof(LayerW) * p.L);
   a.tok = p.tok;
   a.pos = p.pos;
@@ -687,9 +726,7 @@ void launch_fwd_small(const FwdSmallPlan& p, cudaStream_t st) {
   a.err = p.err;
   a.x = p.x;
   a.xn16 = p.xn16;
-  a.ctx16 = p.ctx16;
   a.ff16 = p.ff16;
-  a.qkvp = nullptr;
   a.part = p.scratch;
   a.gbar = p.gbar;
   a.dbg = small_debug_stamps();

@@ -103,12 +103,12 @@ void configure_gemm_tc();
 struct FwdSmallPlan {
   int M, B, S, h, f, H, L, V, causal;
   const void* host_lw;              // host array of per-layer LN / bias device pointers (8 per layer)
-  const CUtensorMap* host_maps;     // host array: xn16, ctx16, ff16, then Wqkv, Wo, W1, W2 per layer
+  const CUtensorMap* host_maps;     // host array: xn16, ff16, then Wqkv, Wo, W1, W2 per layer
   const float *tok, *pos, *lnfg, *lnfb;
   const int32_t* ids;
   int* err;
   float* x;
-  __half *xn16, *ctx16, *ff16;
+  __half *xn16, *ff16;
   float* scratch;            // fwd_small_workspace_floats()
   unsigned* gbar;
 };

@@ -652,17 +652,15 @@ void ensure_f32(prlab_gpu_model& m) {
 }
 
 // Batch-1 plan: tensor maps (activations box 128 x 64, weights box 32 x 64) and the
-// per-layer parameter pointers live in one device buffer next to ctx16 / the fp32
-// split-K partials / the grid-barrier counter.
+// the fp32 partials (per-head Wo, FFN2 K splits) and the grid-barrier counter live in
+// one device buffer.
 void plan_small(prlab_gpu_model& m, prlab_gpu_model::Plan& p, int64_t B, int64_t S) {
   const int64_t M = B * S, h = m.h, f = m.f, L = m.L;
   ArenaPlan ap;
-  const int s_ctx = ap.add(static_cast<size_t>(M * h) * 2);
   const int s_scr = ap.add(fwd_small_workspace_floats(M, h, f) * 4);
   const int s_bar = ap.add(64);
   p.small_buf.alloc(ap.total);
   char* base = static_cast<char*>(p.small_buf.p);
-  __half* ctx16 = reinterpret_cast<__half*>(base + ap.offs[s_ctx]);
   auto& maps = p.small_maps;
   maps.clear();
   // K-major matrices viewed as [K/64 k-blocks][rows][64]: a box spans several k-blocks
@@ -671,14 +669,13 @@ void plan_small(prlab_gpu_model& m, prlab_gpu_model::Plan& p, int64_t B, int64_t
     return make_tmap_f16_3d(base, 64, rows, K / 64, K, 64, 64, box_rows, box_kb);
   };
   maps.push_back(kblk(p.xn16, M, h, 128, 4));    // QKV / FFN1 A: 4 k-blocks per request
-  maps.push_back(kblk(ctx16, M, h, 128, 2));     // Wo A: the split depth is 2 k-blocks
   maps.push_back(kblk(p.big16, M, f, 128, 4));   // FFN2 A (ff16 reuses the qkv/ff buffer)
   p.small_lw.assign(static_cast<size_t>(L), {});
-  const int64_t kb_wo = h / 64 / (h / 128), kb_ffn2 = f / 64 / (f / 512);  // split-K depths (launch_fwd_small)
+  const int64_t kb_ffn2 = f / 64 / (f / 512);  // FFN2 split-K depth (launch_fwd_small)
   for (int64_t l = 0; l < L; ++l) {
     const auto& w = m.l16[l];
     maps.push_back(kblk(w.wqkv, 3 * h, h, 16, static_cast<uint32_t>(h / 64)));  // QKV tasks: N = 16, full K
-    maps.push_back(kblk(w.wo, h, h, 32, static_cast<uint32_t>(kb_wo)));
+    maps.push_back(make_tmap_f16_2d(w.wo, h, h, h, 256, 64));  // a head's Wo column slice, 256 rows per box
     maps.push_back(kblk(w.w1, f, h, 32, static_cast<uint32_t>(h / 64)));
     maps.push_back(kblk(w.w2, h, f, 32, static_cast<uint32_t>(kb_ffn2)));
     p.small_lw[l] = {w.ln1g, w.ln1b, w.ln2g, w.ln2b, w.bqkv, w.bo, w.b1, w.b2, w.wqkv, w.wo, w.w1, w.w2};
@@ -702,7 +699,6 @@ void plan_small(prlab_gpu_model& m, prlab_gpu_model::Plan& p, int64_t B, int64_t
   sp.err = m.err.at<int>(0);
   sp.x = p.x;
   sp.xn16 = p.xn16;
-  sp.ctx16 = ctx16;
   sp.ff16 = p.big16;
   sp.scratch = reinterpret_cast<float*>(base + ap.offs[s_scr]);
   sp.gbar = reinterpret_cast<unsigned*>(base + ap.offs[s_bar]);

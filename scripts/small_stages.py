@@ -13,7 +13,8 @@ import torch
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2603_28708_b200 as pg  # noqa: E402
 
-NAMES = ["qkv", "attn", "wo", "rln2", "ffn1", "ffn2", "rln1"]
+NAMES = ["qkv", "attn+wo", "rln2", "ffn1", "ffn2", "rln1"]
+PER = len(NAMES)  # stages per layer
 
 
 def main():
@@ -28,7 +29,7 @@ def main():
     for _ in range(3):
         m.forward_device(ids.data_ptr(), B, S, "hybrid", out.data_ptr(), pg.OUT_F16, ld, st, False)
     torch.cuda.synchronize()
-    nst = 1 + 7 * cfg.num_layers
+    nst = 1 + PER * cfg.num_layers
     dbg = torch.zeros(300000, dtype=torch.int64, device="cuda")
     pg._check(pg.lib().prlab_gpu_debug_small_stamps(C.c_void_p(dbg.data_ptr())))
     m.forward_device(ids.data_ptr(), B, S, "hybrid", out.data_ptr(), pg.OUT_F16, ld, st, False)
@@ -44,7 +45,7 @@ def main():
     prev_release = t0
     rows = []
     for k in range(nst - 1):
-        name = "embed+ln1" if k == 0 else NAMES[(k - 1) % 7]
+        name = "embed+ln1" if k == 0 else NAMES[(k - 1) % PER]
         rows.append({"stage": k, "name": name, "work_us": round((arrive_max[k] - prev_release) / 1e3, 2),
                      "barrier_us": round((release_max[k] - arrive_max[k]) / 1e3, 2)})
         prev_release = release_max[k]
@@ -61,22 +62,22 @@ def main():
         print(json.dumps(r))
     at = raw[210000:210000 + 8 * cfg.num_layers].reshape(cfg.num_layers, 8)
     for l in range(min(3, cfg.num_layers)):
-        k = 1 + 7 * l + 1  # attention stage index
-        print(json.dumps({"layer": l, "attn_cta0": {"staging_us": round((at[l, 0] - d[k - 1, 0, 1]) / 1e3, 2),
-                                                    "queries_us": round((at[l, 1] - at[l, 0]) / 1e3, 2),
+        k = 1 + PER * l + 1  # attention stage index
+        print(json.dumps({"layer": l, "attn_cta0": {"start_us": round((at[l, 0] - d[k - 1, 0, 1]) / 1e3, 2),
+                                                    "tasks_us": round((at[l, 1] - at[l, 0]) / 1e3, 2),
                                                     "to_arrive_us": round((d[k, 0, 0] - at[l, 1]) / 1e3, 2)}}))
     gt = raw[220000:220000 + 64 * 8].reshape(64, 8)
-    names = ["qkv", "wo", "ffn1", "ffn2"]
-    for t in range(8):
+    names = ["qkv", "ffn1", "ffn2"]
+    for t in range(6):
         g = gt[t]
         if g[0] == 0:
             break
-        print(json.dumps({"gemm_task_cta0": names[t % 4], "b_ready_us": round((g[1] - g[0]) / 1e3, 2),
+        print(json.dumps({"gemm_task_cta0": names[t % 3], "b_ready_us": round((g[1] - g[0]) / 1e3, 2),
                           "first_a_us": round((g[2] - g[0]) / 1e3, 2), "mma_issued_us": round((g[3] - g[0]) / 1e3, 2),
                           "acc_ready_us": round((g[4] - g[0]) / 1e3, 2), "epilogue_done_us": round((g[5] - g[0]) / 1e3, 2)}))
     # CTA 0 inside RLN2 of each layer: release -> start, loads+residual, LN
     for l in range(min(3, cfg.num_layers)):
-        k = 1 + 7 * l + 3  # the RLN2 stage index
+        k = 1 + PER * l + 2  # the RLN2 stage index
         print(json.dumps({"layer": l, "rln2_cta0": {"start_after_release_us": round((rl[l, 0] - d[k - 1, 0, 1]) / 1e3, 2),
                                                     "loads_us": round((rl[l, 1] - rl[l, 0]) / 1e3, 2),
                                                     "ln_us": round((rl[l, 2] - rl[l, 1]) / 1e3, 2),
