@@ -350,7 +350,9 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], 
 // stage sums the heads' partials in head order.  q/k/v come from the QKV stage's fp16
 // output (pitch 3h).
 __device__ void attn_wo_task(const SmallArgs& a, uint8_t* smem, const CUtensorMap* mWo, uint64_t* wo_bar,
-                             uint32_t wo_phase, int b, int hh, int q0) {
+                             uint32_t wo_phase, int b, int hh, int q0, long long* ts) {
+  // ts (debug, thread 0 only): [0] start [1] q/k/v staged [2] scores [3] softmax [4] ctx [5] Wo landed [6] done
+  if (ts) ts[0] = globaltimer();
   const int h = a.h, S = a.S;
   const uint32_t warp = warp_id(), lane = lane_id();
   uint8_t* sWo = smem;
@@ -370,24 +372,34 @@ __device__ void attn_wo_task(const SmallArgs& a, uint8_t* smem, const CUtensorMa
   {
     const __half* base = a.ff16 + static_cast<int64_t>(b) * S * 3 * h + hh * 64;
     const uint4 z = make_uint4(0, 0, 0, 0);
-    for (int e = threadIdx.x; e < kvp * 8; e += kThreads) {
-      const int j = e >> 3, c8 = (e & 7) * 8;
-      uint4 kk = z, vv = z;
+    // every load in flight before the first smem store: one L2 round trip, not four
+    constexpr int PER = 128 * 8 / kThreads;  // 16-byte chunks per thread per tensor (<= 128 keys)
+    uint4 kk[PER], vv[PER], qq = z;
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = threadIdx.x + u * kThreads, j = e >> 3, c8 = (e & 7) * 8;
+      kk[u] = z;
+      vv[u] = z;
       if (j < kv) {
-        kk = *reinterpret_cast<const uint4*>(base + static_cast<int64_t>(j) * 3 * h + h + c8);
-        vv = *reinterpret_cast<const uint4*>(base + static_cast<int64_t>(j) * 3 * h + 2 * h + c8);
+        kk[u] = *reinterpret_cast<const uint4*>(base + static_cast<int64_t>(j) * 3 * h + h + c8);
+        vv[u] = *reinterpret_cast<const uint4*>(base + static_cast<int64_t>(j) * 3 * h + 2 * h + c8);
       }
-      *reinterpret_cast<uint4*>(sK + j * kRowH + c8) = kk;
-      *reinterpret_cast<uint4*>(sV + j * kRowH + c8) = vv;
     }
-    if (threadIdx.x < kQB * 8) {
-      const int i = threadIdx.x >> 3, c8 = (threadIdx.x & 7) * 8;
-      uint4 qq = z;
-      if (q0 + i < S) qq = *reinterpret_cast<const uint4*>(base + static_cast<int64_t>(q0 + i) * 3 * h + c8);
-      *reinterpret_cast<uint4*>(sQ + i * kRowH + c8) = qq;
+    const int qi = threadIdx.x >> 3, qc8 = (threadIdx.x & 7) * 8;
+    if (threadIdx.x < kQB * 8 && q0 + qi < S)
+      qq = *reinterpret_cast<const uint4*>(base + static_cast<int64_t>(q0 + qi) * 3 * h + qc8);
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = threadIdx.x + u * kThreads, j = e >> 3, c8 = (e & 7) * 8;
+      if (j < kvp) {
+        *reinterpret_cast<uint4*>(sK + j * kRowH + c8) = kk[u];
+        *reinterpret_cast<uint4*>(sV + j * kRowH + c8) = vv[u];
+      }
     }
+    if (threadIdx.x < kQB * 8) *reinterpret_cast<uint4*>(sQ + qi * kRowH + qc8) = qq;
   }
   __syncthreads();
+  if (ts) ts[1] = globaltimer();
   const int g = lane >> 2, t4 = lane & 3;
   // scores: warp w -> keys [16w, 16w + 16)
   if (static_cast<int>(warp) * 16 < kvp) {
@@ -410,38 +422,51 @@ __device__ void attn_wo_task(const SmallArgs& a, uint8_t* smem, const CUtensorMa
       }
   }
   __syncthreads();
-  // softmax: warp w -> rows 2w, 2w + 1; lane -> keys lane + 32c
+  if (ts) ts[2] = globaltimer();
+  // softmax: warp w -> rows 2w, 2w + 1 (interleaved); lane -> keys lane + 32c
+  {
+    float sc[2][4], mx[2], sum[2], e[2][4];
 #pragma unroll
-  for (int rr = 0; rr < 2; ++rr) {
-    const int r = warp * 2 + rr;
-    float sc[4];
-    float mx = __int_as_float(0xff800000);
+    for (int rr = 0; rr < 2; ++rr) {
+      mx[rr] = __int_as_float(0xff800000);
 #pragma unroll
-    for (int c4 = 0; c4 < 4; ++c4) {
-      const int j = c4 * 32 + lane;
-      sc[c4] = j < kvp ? sS[r * kRowS + j] : __int_as_float(0xff800000);
-      mx = fmaxf(mx, sc[c4]);
+      for (int c4 = 0; c4 < 4; ++c4) {
+        const int j = c4 * 32 + lane;
+        sc[rr][c4] = j < kvp ? sS[(warp * 2 + rr) * kRowS + j] : __int_as_float(0xff800000);
+        mx[rr] = fmaxf(mx[rr], sc[rr][c4]);
+      }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+      for (int rr = 0; rr < 2; ++rr) mx[rr] = fmaxf(mx[rr], __shfl_xor_sync(0xffffffffu, mx[rr], o));
     constexpr float LOG2E = 1.4426950408889634f;
-    const float mxl = __fmul_rn(mx, LOG2E);
-    float e[4], sum = 0.0f;
 #pragma unroll
-    for (int c4 = 0; c4 < 4; ++c4) {
-      e[c4] = ex2_approx(__fmaf_rn(sc[c4], LOG2E, -mxl));  // exp(-inf) = 0 for masked keys
-      sum = __fadd_rn(sum, e[c4]);
+    for (int rr = 0; rr < 2; ++rr) {
+      const float mxl = __fmul_rn(mx[rr], LOG2E);
+      sum[rr] = 0.0f;
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4) {
+        e[rr][c4] = ex2_approx(__fmaf_rn(sc[rr][c4], LOG2E, -mxl));  // exp(-inf) = 0 for masked keys
+        sum[rr] = __fadd_rn(sum[rr], e[rr][c4]);
+      }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum = __fadd_rn(sum, __shfl_xor_sync(0xffffffffu, sum, o));
-    const float inv = __frcp_rn(sum);
+    for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-    for (int c4 = 0; c4 < 4; ++c4) {
-      const int j = c4 * 32 + lane;
-      if (j < kvp) sP[r * kRowP + j] = __float2half_rn(__fmul_rn(e[c4], inv));
+      for (int rr = 0; rr < 2; ++rr) sum[rr] = __fadd_rn(sum[rr], __shfl_xor_sync(0xffffffffu, sum[rr], o));
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const float inv = __frcp_rn(sum[rr]);
+#pragma unroll
+      for (int c4 = 0; c4 < 4; ++c4) {
+        const int j = c4 * 32 + lane;
+        if (j < kvp) sP[(warp * 2 + rr) * kRowP + j] = __float2half_rn(__fmul_rn(e[rr][c4], inv));
+      }
     }
   }
   __syncthreads();
+  if (ts) ts[3] = globaltimer();
   // ctx = round16(P . V): warp w -> dims [8w, 8w + 8)
   {
     float o[4] = {};
@@ -455,15 +480,18 @@ __device__ void attn_wo_task(const SmallArgs& a, uint8_t* smem, const CUtensorMa
     *reinterpret_cast<__half2*>(sC + (g + 8) * kRowH + warp * 8 + 2 * t4) = __floats2half2_rn(o[2], o[3]);
   }
   __syncthreads();
+  if (ts) ts[4] = globaltimer();
   // Wo partial: out[16][h] = ctx . WoSlice^T; warp w -> n-tiles [w * h/64, (w+1) * h/64) (pairs)
   {
     uint32_t af[4][4];
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks) ldsm_x4(smem_u32(sC + (lane & 15) * kRowH + ks * 16 + (lane >> 4) * 8), af[ks]);
     mbar_wait(wo_bar, wo_phase);
+    if (ts) ts[5] = globaltimer();
     const int per_warp = h / 64;  // n-tiles of 8 columns per warp (h / 8 tiles over 8 warps)
     float* outp = a.part + static_cast<int64_t>(hh) * a.M * h;
     const int row0 = b * S + q0;
+#pragma unroll 2
     for (int p2 = 0; p2 < per_warp; p2 += 2) {
       const int n0 = (warp * per_warp + p2) * 8;
       float d[2][4] = {};
@@ -487,6 +515,7 @@ __device__ void attn_wo_task(const SmallArgs& a, uint8_t* smem, const CUtensorMa
       }
     }
   }
+  if (ts) ts[6] = globaltimer();  // thread 0's warp (lane 0 issues the stamp after its own stores)
 }
 
 __device__ __forceinline__ float h2f_lo(uint32_t v) { return __half2float(__ushort_as_half(static_cast<unsigned short>(v & 0xFFFFu))); }
@@ -631,7 +660,9 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
         const int qb = t % nqb, hh = (t / nqb) % H, b = t / (nqb * H);
         // generic reads of the previous task's Wo slice before this task's TMA rewrites it
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        attn_wo_task(a, smem, mW + 1, wo_bar, n_att & 1, b, hh, qb * kQB);
+        // debug stamps: the heaviest causal task of head 0 (last query block)
+        long long* ts = (a.dbg && qb == nqb - 1 && hh == 0 && b == 0 && threadIdx.x == 0) ? a.dbg + 230000 + l * 8 : nullptr;
+        attn_wo_task(a, smem, mW + 1, wo_bar, n_att & 1, b, hh, qb * kQB, ts);
         ++n_att;
       }
       if (ats) ats[1] = globaltimer();

@@ -66,6 +66,17 @@ def main():
         print(json.dumps({"layer": l, "attn_cta0": {"start_us": round((at[l, 0] - d[k - 1, 0, 1]) / 1e3, 2),
                                                     "tasks_us": round((at[l, 1] - at[l, 0]) / 1e3, 2),
                                                     "to_arrive_us": round((d[k, 0, 0] - at[l, 1]) / 1e3, 2)}}))
+    ta = raw[230000:230000 + 8 * cfg.num_layers].reshape(cfg.num_layers, 8)
+    for l in range(min(3, cfg.num_layers)):
+        k = 1 + PER * l + 1
+        t = ta[l]
+        if t[0] == 0:
+            continue
+        print(json.dumps({"layer": l, "attn_task_last_qblock": {
+            "start_after_release_us": round((t[0] - d[k - 1, :, 1].max()) / 1e3, 2),
+            "stage_us": round((t[1] - t[0]) / 1e3, 2), "scores_us": round((t[2] - t[1]) / 1e3, 2),
+            "softmax_us": round((t[3] - t[2]) / 1e3, 2), "pv_us": round((t[4] - t[3]) / 1e3, 2),
+            "wo_wait_us": round((t[5] - t[4]) / 1e3, 2), "wo_mma_store_us": round((t[6] - t[5]) / 1e3, 2)}}))
     gt = raw[220000:220000 + 64 * 8].reshape(64, 8)
     names = ["qkv", "ffn1", "ffn2"]
     for t in range(6):
