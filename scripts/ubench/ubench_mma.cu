@@ -11,7 +11,7 @@ __device__ __forceinline__ void umma_ts(uint32_t d, uint32_t a, uint64_t b, uint
                "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d), "r"(a), "l"(b), "r"(idesc), "r"(acc) : "memory");
 }
 
-template <int N, bool TS, bool BMN>
+template <int N, bool TS, bool BMN, int M = 128>
 __global__ void __launch_bounds__(128, 1) k(int iters, unsigned long long* out) {
   extern __shared__ __align__(1024) uint8_t sm[];
   uint8_t* s = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(sm) + 1023) & ~uintptr_t(1023));
@@ -27,7 +27,7 @@ __global__ void __launch_bounds__(128, 1) k(int iters, unsigned long long* out) 
   tc_fence_after();
   const uint32_t tmem = slot;
   if (threadIdx.x == 0) {
-    constexpr uint32_t idesc = idesc_f16_f32(128, N, 0, BMN ? 1 : 0);
+    constexpr uint32_t idesc = idesc_f16_f32(M, N, 0, BMN ? 1 : 0);
     const uint32_t a0 = smem_u32(s), b0 = smem_u32(s + 32768);
     long long t0 = clock64();
     for (int it = 0; it < iters; ++it) {
@@ -47,12 +47,12 @@ __global__ void __launch_bounds__(128, 1) k(int iters, unsigned long long* out) 
   if (warp == 0) { tc_fence_after(); tmem_dealloc(tmem, 512); }
 }
 
-template <int N, bool TS, bool BMN>
+template <int N, bool TS, bool BMN, int M = 128>
 void run(int sms, unsigned long long* d_out, const char* tag) {
   const int iters = 256;
   const size_t smem = 65536 + 1024;
-  cudaFuncSetAttribute(k<N, TS, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  for (int rep = 0; rep < 3; ++rep) k<N, TS, BMN><<<sms, 128, smem>>>(iters, d_out);
+  cudaFuncSetAttribute(k<N, TS, BMN, M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  for (int rep = 0; rep < 3; ++rep) k<N, TS, BMN, M><<<sms, 128, smem>>>(iters, d_out);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { printf("{\"err\": \"%s\"}\n", cudaGetErrorString(e)); return; }
   unsigned long long h[1024];
@@ -60,7 +60,8 @@ void run(int sms, unsigned long long* d_out, const char* tag) {
   double cyc = 0;
   for (int i = 0; i < sms; ++i) cyc += h[i];
   cyc /= sms;
-  printf("{\"mma\": \"%s\", \"N\": %d, \"cycles_per_mma\": %.1f, \"ideal\": %.1f}\n", tag, N, cyc / iters, 128.0 * N / 256.0);
+  printf("{\"mma\": \"%s\", \"M\": %d, \"N\": %d, \"cycles_per_mma\": %.1f, \"ideal\": %.1f}\n", tag, M, N, cyc / iters,
+         M * N / 256.0);
 }
 
 int main() {
@@ -75,5 +76,12 @@ int main() {
   run<128, false, false>(sms, d_out, "ss B K-major");
   run<128, true, true>(sms, d_out, "ts B MN-major");
   run<256, false, false>(sms, d_out, "ss B K-major");
+  // narrow tiles (batch-1 forward kernel: 128 token rows x 16/32 weight rows)
+  run<16, false, false>(sms, d_out, "ss B K-major");
+  run<32, false, false>(sms, d_out, "ss B K-major");
+  run<32, false, false>(1, d_out, "ss B K-major, one SM");
+  // transposed batch-1 tiles: M = 64/128 weight rows x N = 128 tokens
+  run<128, false, false, 64>(sms, d_out, "ss B K-major");
+  run<64, false, false, 64>(sms, d_out, "ss B K-major");
   return 0;
 }
