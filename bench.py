@@ -348,10 +348,15 @@ def run_ours(args, wl):
             t = torch.tensor([el], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
+        # under hybrid the library moves the (round16'd) logits as fp16 rows and widens them
+        # to fp32 on host threads (host_widen.cpp): the PCIe bytes are half the fp32 result
+        widened = policy == "hybrid" and not os.environ.get("PRLAB_NO_HOST_WIDEN")
         e2e = {"value": world * B * e2e_steps / el, "unit": "seq/s",
-               "h2d_bytes_per_step": int(ids_np.nbytes), "d2h_bytes_per_step": int(log_np.nbytes),
+               "h2d_bytes_per_step": int(ids_np.nbytes),
+               "d2h_bytes_per_step": int(log_np.nbytes // 2 if widened else log_np.nbytes),
                "ms_per_step": 1000 * el / e2e_steps,
-               "api": "prlab_gpu_forward (host int32 ids -> host fp32 logits, pinned buffers)"}
+               "api": "prlab_gpu_forward (host int32 ids -> host fp32 logits, pinned buffers)"
+                      + ("; logits cross PCIe as fp16 rows, widened exactly on host" if widened else "")}
 
     # ---- roofline of the dominant kernel (standalone CUDA-event timing) ----
     pk = peaks()

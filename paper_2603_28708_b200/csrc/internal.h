@@ -174,6 +174,11 @@ void simt_pool_mean(const float* x32, const __half* x16, int B, int S, int h, Kc
                     cudaStream_t st);
 void simt_round_copy(const float* x, int64_t n, int f16, float* out, cudaStream_t st);
 // fp16 padded [M, ld16] -> fp32 dense [M, N]
+// Device fp16 rows (pitch ld_src halves) -> host fp32 rows (pitch ld_dst), copied in
+// row chunks and widened on host threads as each chunk lands (host_widen.cpp).  Exact;
+// returns once every row is in h_dst.
+void d2h_widen_f16(const void* d_src, int64_t ld_src, float* h_dst, int64_t ld_dst, int64_t rows, int64_t cols,
+                   cudaStream_t st);
 void convert_f16_to_f32(const __half* in, int64_t ld_in, float* out, int64_t ld_out, int M, int N,
                         cudaStream_t st);
 void f32_to_f16(const float* in, __half* out, int64_t n, cudaStream_t st);

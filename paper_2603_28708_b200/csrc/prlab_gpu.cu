@@ -1312,9 +1312,17 @@ int prlab_gpu_forward(prlab_gpu_model* m, const int32_t* ids, int64_t B, int64_t
     const int64_t w = m->L > 0 ? m->V : m->h;
     cudaStream_t st = m->stream;
     PRLAB_CUDA(cudaMemcpyAsync(p.ids, ids, B * S * 4, cudaMemcpyHostToDevice, st));
-    run_forward(*m, p, p.ids, p.out32, PRLAB_OUT_F32, w, st, !std::getenv("PRLAB_NO_GRAPH"));
-    PRLAB_CUDA(cudaMemcpyAsync(logits, p.out32, B * S * w * 4, cudaMemcpyDeviceToHost, st));
-    PRLAB_CUDA(cudaStreamSynchronize(st));
+    const bool graph = !std::getenv("PRLAB_NO_GRAPH");
+    if (p.fast && m->L > 0 && !std::getenv("PRLAB_NO_HOST_WIDEN")) {
+      // hybrid: the head's logits are round16'd, so the fp16 rows widened on the host are
+      // the fp32 logits bit for bit -- half the PCIe bytes (host_widen.cpp)
+      run_forward(*m, p, p.ids, p.logit16, PRLAB_OUT_F16, p.ld16, st, graph);
+      d2h_widen_f16(p.logit16, p.ld16, logits, w, B * S, w, st);
+    } else {
+      run_forward(*m, p, p.ids, p.out32, PRLAB_OUT_F32, w, st, graph);
+      PRLAB_CUDA(cudaMemcpyAsync(logits, p.out32, B * S * w * 4, cudaMemcpyDeviceToHost, st));
+      PRLAB_CUDA(cudaStreamSynchronize(st));
+    }
     if (trace) fill_calls(*m, B, *policy, trace);
   });
 }

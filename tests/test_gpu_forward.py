@@ -136,6 +136,23 @@ def test_device_forward_graph_matches_host_forward():
         assert np.array_equal(got, host), "device fp16 logits differ from the host path"
 
 
+def test_host_widened_logits_equal_device_fp32_copy(monkeypatch):
+    """prlab_gpu_forward under hybrid copies fp16 logits and widens them on host threads
+    (host_widen.cpp); the fp32 copy of the same forward must agree bit for bit, for
+    odd vocab widths and row counts that do not split evenly into copy chunks."""
+    cfg = PRESETS["gpt2_small"].replace(num_layers=2, vocab=5003)
+    o = oracle()
+    m = device_model(cfg)
+    for B, S in ((1, 128), (3, 37), (1, 1)):
+        ids = o.random_tokens(cfg.vocab, B, S, 9)
+        widened = m.forward(ids, B, S, "hybrid")
+        monkeypatch.setenv("PRLAB_NO_HOST_WIDEN", "1")
+        plain = m.forward(ids, B, S, "hybrid")
+        monkeypatch.delenv("PRLAB_NO_HOST_WIDEN")
+        assert widened.dtype == np.float32 and widened.shape == (B, S, cfg.vocab)
+        assert np.array_equal(widened.view(np.uint32), plain.view(np.uint32))
+
+
 def test_forward_errors_match_reference():
     cfg = PRESETS["decoder_toy"]
     m = device_model(cfg)
