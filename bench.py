@@ -348,9 +348,10 @@ def run_ours(args, wl):
             t = torch.tensor([el], device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
-        # under hybrid the library moves the (round16'd) logits as fp16 rows and widens them
-        # to fp32 on host threads (host_widen.cpp): the PCIe bytes are half the fp32 result
-        widened = policy == "hybrid" and not os.environ.get("PRLAB_NO_HOST_WIDEN")
+        # under hybrid the library may move the (round16'd) logits as fp16 rows and widen them
+        # to fp32 on host threads (host_widen.cpp; chosen by timing on the first call): the
+        # PCIe bytes are then half the fp32 result
+        widened = model.host_copy_mode(B, S, policy) == 1
         e2e = {"value": world * B * e2e_steps / el, "unit": "seq/s",
                "h2d_bytes_per_step": int(ids_np.nbytes),
                "d2h_bytes_per_step": int(log_np.nbytes // 2 if widened else log_np.nbytes),

@@ -188,6 +188,12 @@ int prlab_gpu_sync_status(prlab_gpu_model* m, void* stream);
 int prlab_gpu_forward_kernel_count(prlab_gpu_model* m, int64_t batch, int64_t seq,
                                    const prlab_policy* policy, int64_t* count);
 
+/* How prlab_gpu_forward moves this key's logits to the host (after its first call):
+ * 0 = not decided yet, 1 = fp16 rows widened exactly on host threads (hybrid: the
+ * logits are round16'd), 2 = fp32 device->host copy.  For bench accounting. */
+int prlab_gpu_host_copy_mode(prlab_gpu_model* m, int64_t batch, int64_t seq, const prlab_policy* policy,
+                             int32_t* mode);
+
 /* ---- per-operator entry points mirroring include/prlab/kernels.hpp:30-70.
  * Host fp32 buffers in/out (the reference's Tensor storage), synchronous. */
 int prlab_gpu_matmul(const float* a, const float* b, int64_t m, int64_t k, int64_t n,

@@ -180,6 +180,8 @@ EXPORTS = [
     ("prlab_gpu_forward_kernel_count", C.c_int, [_P, C.c_int64, C.c_int64,
                                                  C.POINTER(PrecisionPolicy),
                                                  C.POINTER(C.c_int64)]),
+    ("prlab_gpu_host_copy_mode", C.c_int, [_P, C.c_int64, C.c_int64, C.POINTER(PrecisionPolicy),
+                                           C.POINTER(C.c_int32)]),
     ("prlab_gpu_matmul", C.c_int, [_FP, _FP, C.c_int64, C.c_int64, C.c_int64, KernelConfig, _FP]),
     ("prlab_gpu_attention_scores", C.c_int, [_FP, _FP, C.c_int64, C.c_int64, C.c_int64, C.c_float,
                                              KernelConfig, _FP, _FP]),
@@ -402,6 +404,13 @@ class DeviceModel:
 
     def sync_status(self, stream: int = 0):
         _check(lib().prlab_gpu_sync_status(self._h, C.c_void_p(stream)))
+
+    def host_copy_mode(self, batch, seq, policy="hybrid") -> int:
+        """How forward() moves this key's logits to the host: 0 undecided, 1 fp16 rows
+        widened on host threads, 2 fp32 copy (decided by timing on the first call)."""
+        mode = C.c_int32()
+        _check(lib().prlab_gpu_host_copy_mode(self._h, batch, seq, C.byref(_policy(policy)), C.byref(mode)))
+        return int(mode.value)
 
     def kernel_count(self, batch, seq, policy="hybrid") -> int:
         n = C.c_int64()

@@ -160,6 +160,15 @@ int env_int(const char* name, int dflt) {
   return v ? std::max(1, std::atoi(v)) : dflt;
 }
 
+// 0: cudaEventSynchronize spin, 1: blocking-sync events, 2: cudaEventQuery + yield
+int wait_mode() {
+  static const int m = [] {
+    const char* v = std::getenv("PRLAB_WIDEN_WAIT");
+    return v ? std::atoi(v) : 0;
+  }();
+  return m;
+}
+
 struct Widener {
   std::mutex mu;  // one call at a time (the staging buffer and events are shared)
   // pool threads (+ the caller); PRLAB_WIDEN_THREADS overrides (tuning)
@@ -207,7 +216,8 @@ void d2h_widen_f16(const void* d_src, int64_t ld_src, float* h_dst, int64_t ld_d
   const int nch = static_cast<int>((rows + per - 1) / per);
   while (static_cast<int>(w.ev.size()) < nch) {
     cudaEvent_t e;
-    check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+    check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming | (wait_mode() == 1 ? cudaEventBlockingSync : 0)),
+          "cudaEventCreate");
     w.ev.push_back(e);
   }
   uint16_t* stg = static_cast<uint16_t*>(w.staging);
@@ -221,7 +231,13 @@ void d2h_widen_f16(const void* d_src, int64_t ld_src, float* h_dst, int64_t ld_d
   w.pool.run(nch, [&](int c) {
     const int64_t r0 = c * per, nr = std::min(per, rows - r0);
     check(cudaSetDevice(dev), "cudaSetDevice");
-    check(cudaEventSynchronize(w.ev[c]), "cudaEventSynchronize");
+    if (wait_mode() == 2) {  // poll + yield: waiting threads leave the cores to the converting ones
+      cudaError_t q;
+      while ((q = cudaEventQuery(w.ev[c])) == cudaErrorNotReady) std::this_thread::yield();
+      check(q, "cudaEventQuery");
+    } else {
+      check(cudaEventSynchronize(w.ev[c]), "cudaEventSynchronize");
+    }
     widen_rows(stg + r0 * cols, cols, h_dst + r0 * ld_dst, ld_dst, nr, cols);
   });
 }

@@ -8,6 +8,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <chrono>
 #include <array>
 #include <cmath>
 #include <cstdlib>
@@ -482,6 +483,8 @@ struct prlab_gpu_model {
     int32_t* ids = nullptr;
     float* out32 = nullptr;
     int64_t ld16 = 0;
+    // host forward copy-out: 0 = not calibrated, 1 = fp16 rows widened on host, 2 = fp32 copy
+    int copy_mode = 0;
     std::vector<GemmPlan> gemms;  // fast path: 4 per layer + head
     AttnPlan attn{};
     // batch-1 shapes: forward_hidden as one cooperative persistent kernel (fwd_small.cu)
@@ -1315,9 +1318,36 @@ int prlab_gpu_forward(prlab_gpu_model* m, const int32_t* ids, int64_t B, int64_t
     const bool graph = !std::getenv("PRLAB_NO_GRAPH");
     if (p.fast && m->L > 0 && !std::getenv("PRLAB_NO_HOST_WIDEN")) {
       // hybrid: the head's logits are round16'd, so the fp16 rows widened on the host are
-      // the fp32 logits bit for bit -- half the PCIe bytes (host_widen.cpp)
+      // the fp32 logits bit for bit -- half the PCIe bytes (host_widen.cpp), but host-thread
+      // work whose speed depends on the host; the first call of a plan times both copy-outs
+      // of the same logits and keeps the faster one
       run_forward(*m, p, p.ids, p.logit16, PRLAB_OUT_F16, p.ld16, st, graph);
-      d2h_widen_f16(p.logit16, p.ld16, logits, w, B * S, w, st);
+      if (const char* force = std::getenv("PRLAB_HOST_COPY"))  // "widen" / "fp32": skip the timing
+        p.copy_mode = std::strcmp(force, "widen") == 0 ? 1 : 2;
+      if (p.copy_mode == 0) {
+        using clk = std::chrono::steady_clock;
+        double t_w = 1e30, t_f = 1e30;
+        for (int r = 0; r < 3; ++r) {
+          const auto t0 = clk::now();
+          d2h_widen_f16(p.logit16, p.ld16, logits, w, B * S, w, st);
+          t_w = std::min(t_w, std::chrono::duration<double>(clk::now() - t0).count());
+        }
+        convert_f16_to_f32(p.logit16, p.ld16, p.out32, w, static_cast<int>(B * S), static_cast<int>(w), st);
+        PRLAB_CUDA(cudaStreamSynchronize(st));
+        for (int r = 0; r < 3; ++r) {
+          const auto t0 = clk::now();
+          PRLAB_CUDA(cudaMemcpyAsync(logits, p.out32, B * S * w * 4, cudaMemcpyDeviceToHost, st));
+          PRLAB_CUDA(cudaStreamSynchronize(st));
+          t_f = std::min(t_f, std::chrono::duration<double>(clk::now() - t0).count());
+        }
+        p.copy_mode = t_w < t_f ? 1 : 2;
+      } else if (p.copy_mode == 1) {
+        d2h_widen_f16(p.logit16, p.ld16, logits, w, B * S, w, st);
+      } else {
+        convert_f16_to_f32(p.logit16, p.ld16, p.out32, w, static_cast<int>(B * S), static_cast<int>(w), st);
+        PRLAB_CUDA(cudaMemcpyAsync(logits, p.out32, B * S * w * 4, cudaMemcpyDeviceToHost, st));
+        PRLAB_CUDA(cudaStreamSynchronize(st));
+      }
     } else {
       run_forward(*m, p, p.ids, p.out32, PRLAB_OUT_F32, w, st, graph);
       PRLAB_CUDA(cudaMemcpyAsync(logits, p.out32, B * S * w * 4, cudaMemcpyDeviceToHost, st));
@@ -1470,6 +1500,16 @@ int prlab_gpu_forward_kernel_count(prlab_gpu_model* m, int64_t B, int64_t S, con
     const int64_t L = m->L;
     const bool small = fast && fwd_small_supported(B * S, S, m->h, m->f, m->hd, L);
     *count = small ? 2 : (fast ? 1 + 7 * L + 1 + 1 : 1 + 7 * L + (L > 0 ? 2 : 1));
+  });
+}
+
+int prlab_gpu_host_copy_mode(prlab_gpu_model* m, int64_t B, int64_t S, const prlab_policy* policy,
+                             int32_t* mode) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(m->mu);
+    check_forward_args(*m, B, S);
+    auto it = m->plans.find(std::make_tuple(B, S, policy_key(*policy)));
+    *mode = it == m->plans.end() ? 0 : (it->second->fast && m->L > 0 ? it->second->copy_mode : 2);
   });
 }
 

@@ -137,18 +137,25 @@ def test_device_forward_graph_matches_host_forward():
 
 
 def test_host_widened_logits_equal_device_fp32_copy(monkeypatch):
-    """prlab_gpu_forward under hybrid copies fp16 logits and widens them on host threads
-    (host_widen.cpp); the fp32 copy of the same forward must agree bit for bit, for
-    odd vocab widths and row counts that do not split evenly into copy chunks."""
+    """prlab_gpu_forward under hybrid may copy fp16 logits and widen them on host threads
+    (host_widen.cpp; chosen by timing on a plan's first call); the fp32 copy of the same
+    forward must agree bit for bit, for odd vocab widths and row counts that do not split
+    evenly into copy chunks."""
     cfg = PRESETS["gpt2_small"].replace(num_layers=2, vocab=5003)
     o = oracle()
     m = device_model(cfg)
     for B, S in ((1, 128), (3, 37), (1, 1)):
         ids = o.random_tokens(cfg.vocab, B, S, 9)
+        first = m.forward(ids, B, S, "hybrid")  # times both copy-outs, keeps the faster
+        assert m.host_copy_mode(B, S, "hybrid") in (1, 2)
+        monkeypatch.setenv("PRLAB_HOST_COPY", "widen")
         widened = m.forward(ids, B, S, "hybrid")
-        monkeypatch.setenv("PRLAB_NO_HOST_WIDEN", "1")
+        assert m.host_copy_mode(B, S, "hybrid") == 1
+        monkeypatch.setenv("PRLAB_HOST_COPY", "fp32")
         plain = m.forward(ids, B, S, "hybrid")
-        monkeypatch.delenv("PRLAB_NO_HOST_WIDEN")
+        assert m.host_copy_mode(B, S, "hybrid") == 2
+        monkeypatch.delenv("PRLAB_HOST_COPY")
+        assert np.array_equal(first.view(np.uint32), plain.view(np.uint32))
         assert widened.dtype == np.float32 and widened.shape == (B, S, cfg.vocab)
         assert np.array_equal(widened.view(np.uint32), plain.view(np.uint32))
 
