@@ -192,9 +192,11 @@ def run_reference_arm(args, wl):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
-def kernel_profile(pg, torch, cfg, B, S, stream, reps=20, causal=1):
+def kernel_profile(pg, torch, cfg, B, S, stream, reps=20, causal=1, model=None, d_ids=None, policy="hybrid"):
     """Per-kernel device times of one forward's kernels (inputs resident): each kernel
-    replayed `reps` times from a CUDA graph, CUDA events on the stream it runs on."""
+    replayed `reps` times from a CUDA graph, CUDA events on the stream it runs on.
+    With `model` given and a batch-1 shape (forward = the persistent trunk kernel + the
+    LM head), the items are exactly those two kernels."""
     M, h, f, V, H, hd = B * S, cfg.hidden, cfg.ffn, cfg.vocab, cfg.heads, cfg.hidden // cfg.heads
     dev = "cuda"
     g = torch.Generator(device=dev).manual_seed(0)
@@ -207,8 +209,15 @@ def kernel_profile(pg, torch, cfg, B, S, stream, reps=20, causal=1):
     ctx = torch.empty(M, h, device=dev, dtype=torch.float16)
     L = cfg.num_layers
     ld_head = (V + 7) // 8 * 8
+    small = model is not None and model.kernel_count(B, S, policy) == 2
+    fl = pg.flop_count(cfg, B, S)
+    # trunk: every layer's fp16 weights streamed from HBM once (they exceed L2 across the
+    # 12 layers), the embedding rows gathered, the final hidden rows written
+    trunk_bytes = L * 2 * (4 * h * h + 2 * h * f) + 2 * 4 * M * h + 2 * M * h
     items = {
         # name: (launch fn, launches per forward, algorithmic bytes, flops)
+        "fwd_small": (lambda st: model.forward_trunk_device(d_ids.data_ptr(), B, S, policy, st),
+                      1, trunk_bytes, fl["linear"] + fl["attention"]),
         "gemm_qkv": (lambda st: pg.linear_f16_device(A, W, bias, out16, M, 3 * h, h, 3 * h, 0, st),
                      L, 2 * (M * h + 3 * h * h + M * 3 * h), 2 * M * 3 * h * h),
         "gemm_wo": (lambda st: pg.linear_f16_device(A, W, bias, out32, M, h, h, h, 2, st),
@@ -222,6 +231,10 @@ def kernel_profile(pg, torch, cfg, B, S, stream, reps=20, causal=1):
         "attention": (lambda st: pg.attention_f16_device(qkv, ctx, B, S, H, hd, causal, st),
                       L, 2 * (M * 3 * h + M * h), 4 * B * S * S * h),
     }
+    if small:  # the two kernels of the measured step
+        items = {k: items[k] for k in ("fwd_small", "gemm_head")}
+    else:
+        del items["fwd_small"]
     res = {}
     # each kernel is replayed `reps` times from one CUDA graph (as in the forward: PDL-chained,
     # no host launch gaps), timed with CUDA events on the stream the kernels run on
@@ -361,7 +374,8 @@ def run_ours(args, wl):
 
     # ---- roofline of the dominant kernel (standalone CUDA-event timing) ----
     pk = peaks()
-    prof = (kernel_profile(pg, torch, cfg, B, S, sp, causal=int(cfg.archetype == 1))
+    prof = (kernel_profile(pg, torch, cfg, B, S, sp, causal=int(cfg.archetype == 1), model=model,
+                           d_ids=d_ids, policy=policy)
             if not args.no_profile else {})
     roof = None
     if prof:

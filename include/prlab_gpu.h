@@ -182,6 +182,14 @@ int prlab_gpu_classifier_probs(prlab_gpu_model* m, const int32_t* ids, int64_t b
 int prlab_gpu_forward_device(prlab_gpu_model* m, const int32_t* d_ids, int64_t batch,
                              int64_t seq, const prlab_policy* policy, void* d_out,
                              int32_t out_dtype, int64_t ld, void* stream, int32_t use_graph);
+/* The shared trunk alone (embeddings .. final LayerNorm, src/model.cpp:350-452
+ * forward_hidden, which forward() and classifier_probs() build on), enqueued on
+ * `stream` without a graph; the hidden states stay in the model's workspace.  For
+ * timing the trunk's kernels (batch-1 shapes: the single persistent kernel).
+ * *kernels (optional) receives the number of kernels launched. */
+int prlab_gpu_forward_trunk_device(prlab_gpu_model* m, const int32_t* d_ids, int64_t batch,
+                                   int64_t seq, const prlab_policy* policy, void* stream,
+                                   int64_t* kernels);
 /* Synchronizes the stream and reports deferred device-side errors (bad ids). */
 int prlab_gpu_sync_status(prlab_gpu_model* m, void* stream);
 /* Number of kernels one forward_device launch issues for this key (for bench accounting). */

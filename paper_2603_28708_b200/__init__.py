@@ -176,6 +176,8 @@ EXPORTS = [
     ("prlab_gpu_forward_device", C.c_int, [_P, _P, C.c_int64, C.c_int64,
                                            C.POINTER(PrecisionPolicy), _P, C.c_int32, C.c_int64,
                                            _P, C.c_int32]),
+    ("prlab_gpu_forward_trunk_device", C.c_int, [_P, _P, C.c_int64, C.c_int64,
+                                                 C.POINTER(PrecisionPolicy), _P, C.POINTER(C.c_int64)]),
     ("prlab_gpu_sync_status", C.c_int, [_P, _P]),
     ("prlab_gpu_forward_kernel_count", C.c_int, [_P, C.c_int64, C.c_int64,
                                                  C.POINTER(PrecisionPolicy),
@@ -401,6 +403,15 @@ class DeviceModel:
         _check(lib().prlab_gpu_forward_device(self._h, C.c_void_p(d_ids), batch, seq,
                                               C.byref(pol), C.c_void_p(d_out), out_dtype, ld,
                                               C.c_void_p(stream), int(use_graph)))
+
+    def forward_trunk_device(self, d_ids: int, batch: int, seq: int, policy="hybrid", stream: int = 0) -> int:
+        """The trunk alone (embeddings .. final LN, model.cpp:350 forward_hidden) on
+        `stream`; returns the number of kernels launched (timing helper)."""
+        n = C.c_int64()
+        _check(lib().prlab_gpu_forward_trunk_device(self._h, C.c_void_p(d_ids), batch, seq,
+                                                    C.byref(_policy(policy)), C.c_void_p(stream),
+                                                    C.byref(n)))
+        return int(n.value)
 
     def sync_status(self, stream: int = 0):
         _check(lib().prlab_gpu_sync_status(self._h, C.c_void_p(stream)))

@@ -1479,6 +1479,21 @@ int prlab_gpu_forward_device(prlab_gpu_model* m, const int32_t* d_ids, int64_t B
   });
 }
 
+int prlab_gpu_forward_trunk_device(prlab_gpu_model* m, const int32_t* d_ids, int64_t B, int64_t S,
+                                   const prlab_policy* policy, void* stream, int64_t* kernels) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(m->mu);
+    validate_policy(*policy);
+    check_forward_args(*m, B, S);
+    PRLAB_CUDA(cudaSetDevice(m->device));
+    auto& p = get_plan(*m, B, S, *policy);
+    FwdOpts o;
+    o.hidden_only = true;
+    const int64_t n = enqueue_forward(*m, p, d_ids, nullptr, PRLAB_OUT_F32, 0, static_cast<cudaStream_t>(stream), o);
+    if (kernels) *kernels = n;
+  });
+}
+
 int prlab_gpu_sync_status(prlab_gpu_model* m, void* stream) {
   return guarded([&] {
     PRLAB_CUDA(cudaSetDevice(m->device));

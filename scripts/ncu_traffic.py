@@ -31,8 +31,17 @@ def dram_bytes(path):
 
 def main(out_path, *pairs):
     table = {}
-    for spec in pairs:  # workload=layer.ncu-rep,head.ncu-rep
+    try:  # keep the entries of workloads not re-captured this time
+        with open(out_path) as f:
+            table = json.load(f)
+    except (OSError, ValueError):
+        pass
+    for spec in pairs:  # workload=layer.ncu-rep,head.ncu-rep  or  workload=small:trunk.ncu-rep,head.ncu-rep
         wl, files = spec.split("=")
+        if files.startswith("small:"):  # batch-1 path: the persistent trunk kernel + the LM head
+            trunk, head = files[len("small:"):].split(",")
+            table[wl] = {"fwd_small": dram_bytes(trunk)[0], "gemm_head": dram_bytes(head)[0]}
+            continue
         layer, head = files.split(",")
         rows = dram_bytes(layer)
         entry = {name: rows[i] for i, name in enumerate(LAYER_ORDER) if i < len(rows)}
