@@ -5,7 +5,8 @@
 // fp16 logits widened.  Moving the fp16 rows over PCIe and widening them on the host
 // halves the device->host bytes of the call (25.7 MB -> 12.9 MB for GPT-2 at seq 128),
 // which is what bounds the end-to-end call (bench.py e2e).  The copy is chunked by rows:
-// chunk c is widened by a pool thread as soon as its copy lands (CUDA event), while the
+// the calling thread waits on each chunk's CUDA event in order and publishes it; the pool
+// threads widen their share of the chunk's columns as soon as it is published, while the
 // next chunks are still in flight.  Widening is exact (F16C / bit-exact scalar path).
 #include <cuda_runtime.h>
 #include <immintrin.h>
@@ -101,7 +102,10 @@ class Pool {
     cv_.notify_all();
     for (auto& t : th_) t.join();
   }
-  void run(int n, const std::function<void(int)>& f) {
+  int size() const { return static_cast<int>(th_.size()); }
+  // start(n, f): the workers begin executing f(0..n-1); finish(): the caller joins the
+  // remaining items, waits for the workers and rethrows the first error.
+  void start(int n, const std::function<void(int)>& f) {
     {
       std::lock_guard<std::mutex> lk(mu_);
       job_ = &f;
@@ -112,6 +116,8 @@ class Pool {
       ++gen_;
     }
     cv_.notify_all();
+  }
+  void finish() {
     work();
     std::unique_lock<std::mutex> lk(mu_);
     done_.wait(lk, [&] { return pending_ == 0; });
@@ -160,22 +166,14 @@ int env_int(const char* name, int dflt) {
   return v ? std::max(1, std::atoi(v)) : dflt;
 }
 
-// 0: cudaEventSynchronize spin, 1: blocking-sync events, 2: cudaEventQuery + yield
-int wait_mode() {
-  static const int m = [] {
-    const char* v = std::getenv("PRLAB_WIDEN_WAIT");
-    return v ? std::atoi(v) : 0;
-  }();
-  return m;
-}
-
 struct Widener {
   std::mutex mu;  // one call at a time (the staging buffer and events are shared)
   // pool threads (+ the caller); PRLAB_WIDEN_THREADS overrides (tuning)
-  // 4 threads measured best on the 16-core B200 host (scripts/e2e_sweep.py): more threads
-  // spinning on chunk events slow the copy-out down
+  // half the host's hardware threads, at most 8: on the 16-core B200 host the copy-out
+  // of GPT-2's 128 x 50257 logits takes 0.33 ms at 8 threads vs 0.42 at 4 and 0.50 for
+  // the fp32 copy (scripts/e2e_sweep.py)
   Pool pool{env_int("PRLAB_WIDEN_THREADS",
-                    std::max(1, std::min(4, static_cast<int>(std::thread::hardware_concurrency()) / 2))) - 1};
+                    std::max(1, std::min(8, static_cast<int>(std::thread::hardware_concurrency()) / 2))) - 1};
   void* staging = nullptr;
   size_t cap = 0;
   std::vector<cudaEvent_t> ev;
@@ -216,8 +214,7 @@ void d2h_widen_f16(const void* d_src, int64_t ld_src, float* h_dst, int64_t ld_d
   const int nch = static_cast<int>((rows + per - 1) / per);
   while (static_cast<int>(w.ev.size()) < nch) {
     cudaEvent_t e;
-    check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming | (wait_mode() == 1 ? cudaEventBlockingSync : 0)),
-          "cudaEventCreate");
+    check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
     w.ev.push_back(e);
   }
   uint16_t* stg = static_cast<uint16_t*>(w.staging);
@@ -228,18 +225,35 @@ void d2h_widen_f16(const void* d_src, int64_t ld_src, float* h_dst, int64_t ld_d
           "cudaMemcpy2DAsync(logits)");
     check(cudaEventRecord(w.ev[c], st), "cudaEventRecord");
   }
-  w.pool.run(nch, [&](int c) {
-    const int64_t r0 = c * per, nr = std::min(per, rows - r0);
-    check(cudaSetDevice(dev), "cudaSetDevice");
-    if (wait_mode() == 2) {  // poll + yield: waiting threads leave the cores to the converting ones
-      cudaError_t q;
-      while ((q = cudaEventQuery(w.ev[c])) == cudaErrorNotReady) std::this_thread::yield();
-      check(q, "cudaEventQuery");
-    } else {
-      check(cudaEventSynchronize(w.ev[c]), "cudaEventSynchronize");
+  // Only the caller talks to CUDA (waiting on the chunk events in order and publishing
+  // `ready`); the pool threads spin on that counter and widen 1/P of every chunk's
+  // columns each -- CUDA calls from several threads contend on driver locks
+  // (measured: spinning cudaEventSynchronize in 8+ threads was slower than 4).
+  const int P = w.pool.size() + 1;
+  std::atomic<int> ready{0};
+  std::atomic<bool> failed{false};
+  const std::function<void(int)> job = [&](int i) {
+    const int c = i / P, q = i % P;
+    while (ready.load(std::memory_order_acquire) <= c) {
+      if (failed.load(std::memory_order_relaxed)) return;
+      _mm_pause();
     }
-    widen_rows(stg + r0 * cols, cols, h_dst + r0 * ld_dst, ld_dst, nr, cols);
-  });
+    const int64_t r0 = c * per, nr = std::min(per, rows - r0);
+    const int64_t c0 = (cols * q / P) & ~int64_t(7), c1 = q + 1 == P ? cols : (cols * (q + 1) / P) & ~int64_t(7);
+    if (c1 > c0) widen_rows(stg + r0 * cols + c0, cols, h_dst + r0 * ld_dst + c0, ld_dst, nr, c1 - c0);
+  };
+  w.pool.start(nch * P, job);
+  try {
+    for (int c = 0; c < nch; ++c) {
+      check(cudaEventSynchronize(w.ev[c]), "cudaEventSynchronize");
+      ready.store(c + 1, std::memory_order_release);
+    }
+  } catch (...) {
+    failed.store(true);
+    w.pool.finish();
+    throw;
+  }
+  w.pool.finish();
 }
 
 }  // namespace prlab_gpu

@@ -60,6 +60,20 @@ def main():
                                              "barrier_us_avg": round(v[1] / v[2], 2)} for k, v in agg.items()}}))
     for r in rows[:9]:
         print(json.dumps(r))
+    # per-CTA arrival spread inside each stage type (layers 1..L-1: warm L2), relative to
+    # the previous barrier's last release: who is late, and by how much
+    spread = {}
+    for k in range(1 + PER, nst - 1):
+        name = NAMES[(k - 1) % PER]
+        arr = (d[k, :, 0] - release_max[k - 1]) / 1e3
+        active = arr[arr > -1e3]
+        spread.setdefault(name, []).append((np.percentile(active, 10), np.median(active), active.max(),
+                                            int(np.argmax(arr))))
+    print(json.dumps({"arrival_spread_us": {n: {"p10": round(float(np.mean([v[0] for v in vs])), 2),
+                                                "median": round(float(np.mean([v[1] for v in vs])), 2),
+                                                "max": round(float(np.mean([v[2] for v in vs])), 2),
+                                                "latest_cta": [v[3] for v in vs][:6]}
+                                            for n, vs in spread.items()}}))
     at = raw[210000:210000 + 8 * cfg.num_layers].reshape(cfg.num_layers, 8)
     for l in range(min(3, cfg.num_layers)):
         k = 1 + PER * l + 1  # attention stage index
