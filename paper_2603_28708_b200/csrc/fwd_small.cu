@@ -31,7 +31,7 @@ namespace prlab_gpu {
 
 namespace {
 
-constexpr int kThreads = 256;            // warps 0-3: epilogue / TMEM quadrants; 4: TMA; 5: MMA
+constexpr int kThreads = 256;            // GEMM tasks: warp 4 TMA, warp 5 MMA, all 8 warps epilogue
 constexpr int kTileN = 32;               // GEMM output columns per task
 // Operand loads are 3D tensor maps over a K-major matrix viewed as [K/64][rows][64]: one
 // TMA request moves several 64-wide k-blocks.  Measured (scripts/ubench/ubench_tma2d.cu,
@@ -165,35 +165,37 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 
 // x (fp32 row, already final) -> round16(LN(x)) into xn16.  Two-pass fp32 statistics
 // like layernorm_lastdim (src/kernels.cpp:170-219): mean, population variance,
-// inv = 1/sqrt(var + eps), y = gamma*((x - mean)*inv) + beta.
-__device__ void ln_row(const float* xv, int nper, int h, const float* __restrict__ g, const float* __restrict__ b,
-                       __half* __restrict__ out, float* red) {
-  float gv[4], bv[4];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)  // parameter loads first: their latency overlaps the reductions
-    if (i < nper) {
-      gv[i] = g[threadIdx.x + i * kThreads];
-      bv[i] = b[threadIdx.x + i * kThreads];
-    }
-  float s = 0.0f;
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-    if (i < nper) s += xv[i];
+// inv = 1/sqrt(var + eps), y = gamma*((x - mean)*inv) + beta.  Row stages map thread t
+// to columns [4t, 4t + 4) (h <= 1024): one 16-byte access per operand and split.
+__device__ void ln_row(const float (&xv)[4], bool act, int h, const float* __restrict__ g,
+                       const float* __restrict__ b, __half* __restrict__ out, float* red) {
+  const int c = 4 * threadIdx.x;
+  float4 gv = make_float4(0.f, 0.f, 0.f, 0.f), bv = gv;
+  if (act) {  // parameter loads first: their latency overlaps the reductions
+    gv = *reinterpret_cast<const float4*>(g + c);
+    bv = *reinterpret_cast<const float4*>(b + c);
+  }
+  const float s = act ? __fadd_rn(__fadd_rn(__fadd_rn(xv[0], xv[1]), xv[2]), xv[3]) : 0.0f;
   const float mean = __fdiv_rn(block_sum(s, red), static_cast<float>(h));
   float q = 0.0f;
+  if (act)
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
-    if (i < nper) {
+    for (int i = 0; i < 4; ++i) {
       const float d = __fsub_rn(xv[i], mean);
       q = __fmaf_rn(d, d, q);
     }
   const float var = __fdiv_rn(block_sum(q, red), static_cast<float>(h));
   const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, 1e-5f)));
+  if (act) {
+    const float ga[4] = {gv.x, gv.y, gv.z, gv.w}, ba[4] = {bv.x, bv.y, bv.z, bv.w};
+    uint32_t pk[2];
 #pragma unroll
-  for (int i = 0; i < 4; ++i)
-    if (i < nper)
-      out[threadIdx.x + i * kThreads] =
-          __float2half_rn(__fadd_rn(__fmul_rn(gv[i], __fmul_rn(__fsub_rn(xv[i], mean), inv)), bv[i]));
+    for (int i = 0; i < 2; ++i)
+      pk[i] = h2_pack_rn(__fadd_rn(__fmul_rn(ga[2 * i], __fmul_rn(__fsub_rn(xv[2 * i], mean), inv)), ba[2 * i]),
+                         __fadd_rn(__fmul_rn(ga[2 * i + 1], __fmul_rn(__fsub_rn(xv[2 * i + 1], mean), inv)),
+                                   ba[2 * i + 1]));
+    *reinterpret_cast<uint2*>(out + c) = make_uint2(pk[0], pk[1]);
+  }
 }
 
 struct Ctl {
@@ -267,12 +269,18 @@ __device__ void gemm_task(const SmallArgs& a, uint8_t* smem, Ctl& c, const CUten
       if (gs) gs[3] = globaltimer();
     }
     __syncwarp();
-  } else if (warp < 4) {
-    float bv[NT];
-    if (EPI != 0) {  // this tile's biases before the accumulator wait (their latency hides under the MMAs)
+  }
+  // epilogue on all 8 warps (the TMA and MMA warps join once their loops are issued):
+  // warp w reads TMEM lane quadrant w % 4 (rows 32(w%4) ..), column half w / 4
+  {
+    constexpr int NH = NT / 2;
+    const uint32_t quad = warp & 3, half = warp >> 2;
+    const int c0 = n0 + static_cast<int>(half) * NH;
+    float bv[NH];
+    if (EPI != 0) {  // this half's biases before the accumulator wait (latency hidden under the MMAs)
 #pragma unroll
-      for (int i = 0; i < NT / 4; ++i) {
-        const float4 b4 = reinterpret_cast<const float4*>(bias + n0)[i];
+      for (int i = 0; i < NH / 4; ++i) {
+        const float4 b4 = reinterpret_cast<const float4*>(bias + c0)[i];
         bv[4 * i] = b4.x;
         bv[4 * i + 1] = b4.y;
         bv[4 * i + 2] = b4.z;
@@ -282,28 +290,31 @@ __device__ void gemm_task(const SmallArgs& a, uint8_t* smem, Ctl& c, const CUten
     mbar_wait(c.accfull, c.tc & 1);
     if (a.dbg && blockIdx.x == 0 && c.tc < 64 && threadIdx.x == 0) a.dbg[220000 + c.tc * 8 + 4] = globaltimer();
     tc_fence_after();
-    uint32_t u[NT];
-    if constexpr (NT == 32) {
-      tmem_ld32(c.tmem + ((warp * 32) << 16), u);
+    uint32_t u[NH];
+    const uint32_t taddr = c.tmem + ((quad * 32) << 16) + half * NH;
+    if constexpr (NH == 8) {
+      tmem_ld8(taddr, u);
+    } else if constexpr (NH == 16) {
+      tmem_ld16(taddr, u);
     } else {
-      tmem_ld16(c.tmem + ((warp * 32) << 16), u);
+      tmem_ld32(taddr, u);
     }
     tmem_wait_ld();
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(c.accempty);
-    const int row = static_cast<int>(warp * 32 + lane);
+    const int row = static_cast<int>(quad * 32 + lane);
     if (row < a.M) {
       if (EPI == 0) {
-        float4* o = reinterpret_cast<float4*>(out32 + static_cast<int64_t>(row) * ld32 + n0);
+        float4* o = reinterpret_cast<float4*>(out32 + static_cast<int64_t>(row) * ld32 + c0);
 #pragma unroll
-        for (int i = 0; i < NT / 4; ++i)
+        for (int i = 0; i < NH / 4; ++i)
           o[i] = make_float4(__uint_as_float(u[4 * i]), __uint_as_float(u[4 * i + 1]), __uint_as_float(u[4 * i + 2]),
                              __uint_as_float(u[4 * i + 3]));
       } else {
-        uint32_t pk[NT / 2];
+        uint32_t pk[NH / 2];
 #pragma unroll
-        for (int i = 0; i < NT / 2; ++i) {
+        for (int i = 0; i < NH / 2; ++i) {
           uint32_t hh = h2_add_rn(h2_pack_rn(__uint_as_float(u[2 * i]), __uint_as_float(u[2 * i + 1])),
                                   h2_pack_rn(bv[2 * i], bv[2 * i + 1]));
           if (EPI == 1) {
@@ -314,9 +325,9 @@ __device__ void gemm_task(const SmallArgs& a, uint8_t* smem, Ctl& c, const CUten
           }
           pk[i] = hh;
         }
-        uint4* o = reinterpret_cast<uint4*>(out16 + static_cast<int64_t>(row) * ld16 + n0);
+        uint4* o = reinterpret_cast<uint4*>(out16 + static_cast<int64_t>(row) * ld16 + c0);
 #pragma unroll
-        for (int i = 0; i < NT / 8; ++i) o[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
+        for (int i = 0; i < NH / 8; ++i) o[i] = make_uint4(pk[4 * i], pk[4 * i + 1], pk[4 * i + 2], pk[4 * i + 3]);
       }
     }
   }
@@ -525,32 +536,34 @@ __device__ __forceinline__ float h2f_hi(uint32_t v) { return __half2float(__usho
 template <int MAXSP>
 __device__ void residual_ln_row(const SmallArgs& a, int r, int nsplit, const float* bias, const float* g,
                                 const float* b, float* red, long long* ts = nullptr) {
-  const int h = a.h, nper = h / kThreads;
+  const int h = a.h, c = 4 * threadIdx.x;
+  const bool act = c < h;
   if (ts && threadIdx.x == 0) ts[0] = globaltimer();
-  float xv[4], pv[4][MAXSP], xo[4], bs[4];
+  float xv[4];
+  if (act) {
+    float4 pv[MAXSP];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {  // every load of the row in flight before the ordered sums
-    if (i < nper) {
-      const int cc = threadIdx.x + i * kThreads;
+    for (int sp = 0; sp < MAXSP; ++sp)  // every load of the row in flight before the ordered sums
+      if (sp < nsplit) pv[sp] = *reinterpret_cast<const float4*>(a.part + (static_cast<int64_t>(sp) * a.M + r) * h + c);
+    float4* xp = reinterpret_cast<float4*>(a.x + static_cast<int64_t>(r) * h + c);
+    const float4 xo = *xp, bs = *reinterpret_cast<const float4*>(bias + c);
+    float sum[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-      for (int sp = 0; sp < MAXSP; ++sp) pv[i][sp] = sp < nsplit ? a.part[(static_cast<int64_t>(sp) * a.M + r) * h + cc] : 0.0f;
-      xo[i] = a.x[static_cast<int64_t>(r) * h + cc];
-      bs[i] = bias[cc];
-    }
-  }
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    if (i < nper) {
-      float sum = 0.0f;
-#pragma unroll
-      for (int sp = 0; sp < MAXSP; ++sp)
-        if (sp < nsplit) sum = __fadd_rn(sum, pv[i][sp]);
-      xv[i] = __fadd_rn(xo[i], r16(__fadd_rn(r16(sum), bs[i])));
-      a.x[static_cast<int64_t>(r) * h + threadIdx.x + i * kThreads] = xv[i];
-    }
+    for (int sp = 0; sp < MAXSP; ++sp)
+      if (sp < nsplit) {
+        sum[0] = __fadd_rn(sum[0], pv[sp].x);
+        sum[1] = __fadd_rn(sum[1], pv[sp].y);
+        sum[2] = __fadd_rn(sum[2], pv[sp].z);
+        sum[3] = __fadd_rn(sum[3], pv[sp].w);
+      }
+    xv[0] = __fadd_rn(xo.x, r16(__fadd_rn(r16(sum[0]), bs.x)));
+    xv[1] = __fadd_rn(xo.y, r16(__fadd_rn(r16(sum[1]), bs.y)));
+    xv[2] = __fadd_rn(xo.z, r16(__fadd_rn(r16(sum[2]), bs.z)));
+    xv[3] = __fadd_rn(xo.w, r16(__fadd_rn(r16(sum[3]), bs.w)));
+    *xp = make_float4(xv[0], xv[1], xv[2], xv[3]);
   }
   if (ts && threadIdx.x == 0) ts[1] = globaltimer();
-  ln_row(xv, nper, h, g, b, a.xn16 + static_cast<int64_t>(r) * h, red);
+  ln_row(xv, act, h, g, b, a.xn16 + static_cast<int64_t>(r) * h, red);
   if (ts && threadIdx.x == 0) ts[2] = globaltimer();
 }
 
@@ -578,7 +591,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
     }
     mbar_init(c.bfull, 1);
     mbar_init(c.accfull, 1);
-    mbar_init(c.accempty, 4);
+    mbar_init(c.accempty, 8);  // every warp reads its TMEM slice
     mbar_init(wo_bar, 1);
     fence_barrier_init();
   }
@@ -598,7 +611,6 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
   unsigned target = 0;
   const CUtensorMap* mXn = a.maps + 0;
   const CUtensorMap* mFf = a.maps + 1;
-  const int nper = h / kThreads;  // columns per thread in row tasks (h % 256 == 0)
   // task geometry (same on every CTA)
   const int t_qkv = 3 * h / 16;                    // N=16 tiles, full K -> fp16 q/k/v
   const int t_ffn1 = f / kTileN;                   // N=32 tiles, full K, GELU
@@ -625,18 +637,20 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
     const int id = a.ids[r];
     const bool ok = id >= 0 && id < a.V;
     if (!ok && threadIdx.x == 0) atomicExch(a.err, 1);
-    const int t = r % S;
-    float xv[4];
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (i < nper) {
-        const int cc = threadIdx.x + i * kThreads;
-        xv[i] = __fadd_rn(ok ? a.tok[static_cast<int64_t>(id) * h + cc] : 0.0f, a.pos[static_cast<int64_t>(t) * h + cc]);
-      }
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-      if (i < nper) a.x[static_cast<int64_t>(r) * h + threadIdx.x + i * kThreads] = xv[i];
-    ln_row(xv, nper, h, a.lw[0].ln1g, a.lw[0].ln1b, a.xn16 + static_cast<int64_t>(r) * h, red);
+    const int t = r % S, cc = 4 * threadIdx.x;
+    const bool act = cc < h;
+    float xv[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+    if (act) {
+      const float4 pe = *reinterpret_cast<const float4*>(a.pos + static_cast<int64_t>(t) * h + cc);
+      const float4 te = ok ? *reinterpret_cast<const float4*>(a.tok + static_cast<int64_t>(id) * h + cc)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+      xv[0] = __fadd_rn(te.x, pe.x);
+      xv[1] = __fadd_rn(te.y, pe.y);
+      xv[2] = __fadd_rn(te.z, pe.z);
+      xv[3] = __fadd_rn(te.w, pe.w);
+      *reinterpret_cast<float4*>(a.x + static_cast<int64_t>(r) * h + cc) = make_float4(xv[0], xv[1], xv[2], xv[3]);
+    }
+    ln_row(xv, act, h, a.lw[0].ln1g, a.lw[0].ln1b, a.xn16 + static_cast<int64_t>(r) * h, red);
   }
   grid_sync(a.gbar, target, a.dbg);
 
