@@ -209,7 +209,12 @@ void d2h_widen_f16(const void* d_src, int64_t ld_src, float* h_dst, int64_t ld_d
     check(cudaMallocHost(&w.staging, bytes), "cudaMallocHost(widen staging)");
     w.cap = bytes;
   }
-  static const int kChunks = env_int("PRLAB_WIDEN_CHUNKS", 16);
+  // 8 row chunks: each D2H copy costs ~3.5 us of setup (128 x 50257 fp16: 238 us as one
+  // copy, 293 us as 16 -- scripts/ubench/ubench_d2h.py), fewer chunks leave a longer widening
+  // tail; measured e2e 0.686 ms at 8 vs 0.697 at 12 and 0.703 at 6 (scripts/gpu_e2e_sweep.sh).
+  // Moving a slice of the rows as fp32 instead (device-widened) did not help: the host's
+  // DRAM bandwidth, shared by the DMA writes and the widening, is the bound.
+  static const int kChunks = env_int("PRLAB_WIDEN_CHUNKS", 8);
   const int64_t per = (rows + kChunks - 1) / kChunks;
   const int nch = static_cast<int>((rows + per - 1) / per);
   while (static_cast<int>(w.ev.size()) < nch) {
