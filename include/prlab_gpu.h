@@ -190,6 +190,19 @@ int prlab_gpu_forward_device(prlab_gpu_model* m, const int32_t* d_ids, int64_t b
 int prlab_gpu_forward_trunk_device(prlab_gpu_model* m, const int32_t* d_ids, int64_t batch,
                                    int64_t seq, const prlab_policy* policy, void* stream,
                                    int64_t* kernels);
+/* Forward with the tied head's log-softmax statistics fused into the head GEMM's
+ * epilogue (the reduction window_nll_sum, src/fidelity.cpp:213-240,
+ * and greedy argmax apply to the logits of src/model.cpp:469-480): per row b*seq + s,
+ * d_nll (double, may be NULL) = -log_softmax(logits row)[d_targets[row]] as
+ * prlab_gpu_row_nll_device defines it, d_argmax (may be NULL) = first column of the row
+ * maximum.  The [batch*seq, V] logits are never written to HBM.  Device pointers, async
+ * on `stream`, no graph.  The fused epilogue runs on the tensor-core path (hybrid policy)
+ * when the head is tiled by CTA pairs (batch*seq >= 512 rows); otherwise the logits go
+ * through a workspace buffer and prlab_gpu_row_nll_device's kernel -- *fused (may be
+ * NULL) tells which.  Bad ids: reported by prlab_gpu_sync_status(). */
+int prlab_gpu_forward_nll_device(prlab_gpu_model* m, const int32_t* d_ids, const int32_t* d_targets,
+                                 int64_t batch, int64_t seq, const prlab_policy* policy, double* d_nll,
+                                 int32_t* d_argmax, void* stream, int32_t* fused);
 /* Synchronizes the stream and reports deferred device-side errors (bad ids). */
 int prlab_gpu_sync_status(prlab_gpu_model* m, void* stream);
 /* Number of kernels one forward_device launch issues for this key (for bench accounting). */

@@ -178,6 +178,8 @@ EXPORTS = [
                                            _P, C.c_int32]),
     ("prlab_gpu_forward_trunk_device", C.c_int, [_P, _P, C.c_int64, C.c_int64,
                                                  C.POINTER(PrecisionPolicy), _P, C.POINTER(C.c_int64)]),
+    ("prlab_gpu_forward_nll_device", C.c_int, [_P, _P, _P, C.c_int64, C.c_int64, C.POINTER(PrecisionPolicy),
+                                               _P, _P, _P, C.POINTER(C.c_int32)]),
     ("prlab_gpu_sync_status", C.c_int, [_P, _P]),
     ("prlab_gpu_forward_kernel_count", C.c_int, [_P, C.c_int64, C.c_int64,
                                                  C.POINTER(PrecisionPolicy),
@@ -412,6 +414,18 @@ class DeviceModel:
                                                     C.byref(_policy(policy)), C.c_void_p(stream),
                                                     C.byref(n)))
         return int(n.value)
+
+    def forward_nll_device(self, d_ids: int, d_targets: int, batch: int, seq: int, policy, d_nll: int,
+                           d_argmax: int, stream: int = 0) -> bool:
+        """Per-row next-token NLL (double) and first argmax (int32) with the head's
+        log-softmax fused into its GEMM epilogue (no logits written); raw device pointers
+        (0 = NULL).  Returns True when the fused epilogue ran."""
+        fused = C.c_int32()
+        _check(lib().prlab_gpu_forward_nll_device(self._h, C.c_void_p(d_ids), C.c_void_p(d_targets or None),
+                                                  batch, seq, C.byref(_policy(policy)),
+                                                  C.c_void_p(d_nll or None), C.c_void_p(d_argmax or None),
+                                                  C.c_void_p(stream), C.byref(fused)))
+        return bool(fused.value)
 
     def sync_status(self, stream: int = 0):
         _check(lib().prlab_gpu_sync_status(self._h, C.c_void_p(stream)))

@@ -43,6 +43,8 @@ struct GemmArgs {
   int tma_store;  // epilogue through smem staging + TMA store / reduce-add
   int group_m;    // raster band height in m-blocks (A band kept L2-resident)
   int dbg_noload; // debug: after the first fill, skip the TMA loads (MMA/epilogue pacing probe)
+  const int32_t* targets;  // EPI_ROWSTAT: target column per row (< 0: none)
+  float* tval;             // EPI_ROWSTAT: round16 logit at the target column per row
   long long* dbg; // optional per-CTA %globaltimer stamps [grid][8] (debug), null = off
 };
 
@@ -847,7 +849,7 @@ __global__ void __launch_bounds__(Cfg2<BN, EPI>::THREADS, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tmA);
     tma_prefetch_desc(&tmB);
-    if (g.tma_store) tma_prefetch_desc(&tmC);
+    if (g.tma_store && EPI != EPI_ROWSTAT) tma_prefetch_desc(&tmC);
     for (int s = 0; s < C::STAGES; ++s) {
       mbar_init(&full[s], 2);
       mbar_init(&empty[s], MC ? 2 : 1);  // MC: both pairs' MMAs read this stage's weights
@@ -992,6 +994,55 @@ __global__ void __launch_bounds__(Cfg2<BN, EPI>::THREADS, 1)
       }
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
+      if constexpr (EPI == EPI_ROWSTAT) {
+        // Fused log-softmax statistics of this thread's row over the warp's columns
+        // (logits v = round16(acc), exactly the values EPI_F16 would store): running max
+        // with rescaled fp32 sum of expf(v - max) (expf like row_nll), the first column of
+        // the maximum (strict >, ascending columns), the target's value.
+        const int row = m_blk * BM + static_cast<int>(quad) * 32 + static_cast<int>(lane);
+        const int32_t tgt = (g.targets != nullptr && row < g.M) ? g.targets[row] : -1;
+        const float ninf = __int_as_float(0xff800000);
+        float mx = ninf, sum = 0.0f, best = ninf;
+        int bidx = 0x7fffffff;
+        bool bad = false;
+#pragma unroll 1
+        for (int c = cbase; c < cbase + C::COLS_PER_WARP; c += 32) {
+          uint32_t u[32];
+          tmem_ld32(tmem_base + ((quad * 32) << 16) + acc * BN + c, u);
+          tmem_wait_ld();
+          const int col0 = n_blk * BN + c;
+          float v[32];
+          float cm = ninf;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            v[j] = col0 + j < g.N ? __half2float(__float2half_rn(__uint_as_float(u[j]))) : ninf;
+            bad |= isnan(v[j]) || v[j] == __int_as_float(0x7f800000);
+            cm = fmaxf(cm, v[j]);
+            if (v[j] > best) {
+              best = v[j];
+              bidx = col0 + j;
+            }
+            if (col0 + j == tgt) g.tval[row] = v[j];
+          }
+          if (cm > mx) {
+            sum = mx == ninf ? 0.0f : sum * expf(mx - cm);
+            mx = cm;
+          }
+          if (mx != ninf) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) sum += expf(v[j] - mx);
+          }
+        }
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
+        if (row < g.M) {
+          const int slot = n_blk * (C::EPI_WARPS / 4) + ((static_cast<int>(warp) - 2) >> 2);
+          reinterpret_cast<float4*>(g.out)[static_cast<int64_t>(slot) * g.M + row] =
+              make_float4(mx, sum, __int_as_float(bidx), bad ? 1.0f : 0.0f);
+        }
+        continue;
+      }
 #pragma unroll 1
       for (int c = cbase; c < cbase + C::COLS_PER_WARP; c += SC, ++store_k) {
         uint8_t* buf = ebuf + (C::NBUF == 2 ? (store_k & 1) * 4096 : 0);
@@ -1064,6 +1115,7 @@ void configure_pair_bn() {
   configure_pair_one<BN, EPI_BIAS_GELU_F16>();
   configure_pair_one<BN, EPI_BIAS_RESID_F32>();
   configure_pair_one<BN, EPI_F16>();
+  configure_pair_one<BN, EPI_ROWSTAT>();
 }
 
 template <int BN, int EPI>
@@ -1095,6 +1147,7 @@ void launch_pair_bn(const GemmPlan& p, const GemmArgs& g, cudaStream_t st) {
     case EPI_BIAS_GELU_F16: launch_pair_one<BN, EPI_BIAS_GELU_F16>(p, g, st); break;
     case EPI_BIAS_RESID_F32: launch_pair_one<BN, EPI_BIAS_RESID_F32>(p, g, st); break;
     case EPI_F16: launch_pair_one<BN, EPI_F16>(p, g, st); break;
+    case EPI_ROWSTAT: launch_pair_one<BN, EPI_ROWSTAT>(p, g, st); break;
     default: throw std::invalid_argument("unknown gemm epilogue");
   }
 }
@@ -1254,7 +1307,10 @@ GemmPlan plan_gemm_tc(const void* A, int64_t lda, const void* Wt, int64_t ldw, c
   const int64_t row_bytes = ldo * (f32out ? 4 : 2);
   p.tma_store = !std::getenv("PRLAB_NO_TMA_STORE") && (row_bytes % 16 == 0) &&
                 (reinterpret_cast<uintptr_t>(out) % 16 == 0);
-  if (p.tma_store)
+  if (epi == EPI_ROWSTAT) {  // no output tile: the pair kernel writes row statistics
+    if (!p.pair) throw std::invalid_argument("tc gemm: row statistics need the CTA-pair kernel");
+    p.tma_store = true;
+  } else if (p.tma_store)
     p.tmC = f32out ? make_tmap_f32_2d(out, M, N, ldo, 32, 32) : make_tmap_f16_2d(out, M, N, ldo, 32, 64);
   const int units = tiles * p.splits;
   p.grid = p.cluster ? units : (units < sms ? units : sms);
@@ -1320,6 +1376,8 @@ void launch_gemm_tc(const GemmPlan& p, cudaStream_t st) {
   g.group_m = p.group_m;
   g.dbg_noload = std::getenv("PRLAB_DBG_GEMM_NOLOAD") ? std::atoi(std::getenv("PRLAB_DBG_GEMM_NOLOAD")) : 0;
   g.dbg = debug_stamps();
+  g.targets = p.targets;
+  g.tval = p.tval;
   if (p.pair) {
     if (p.bn == 256)
       launch_pair_bn<256>(p, g, st);

@@ -64,6 +64,11 @@ enum GemmEpi : int {
   EPI_BIAS_GELU_F16 = 1,  // round16(gelu(round16(round16(acc)+b))) -> fp16
   EPI_BIAS_RESID_F32 = 2, // x += round16(round16(acc) + b)          (fp32, in place)
   EPI_F16 = 3,            // round16(acc)                           -> fp16
+  // per-row statistics of round16(acc) instead of the values (the LM head's fused
+  // log-softmax / argmax): out = float4 [nslots][M] partials
+  // (max, sum exp(v - max), first argmax column, non-finite flag), one slot per
+  // (n-block, epilogue column group); tval[row] = v at targets[row].  Pair kernel only.
+  EPI_ROWSTAT = 4,
 };
 struct GemmPlan {
   CUtensorMap tmA, tmB, tmC;  // tmC: output map for the TMA-store epilogue
@@ -81,6 +86,9 @@ struct GemmPlan {
   int* tickets;
   int grid;
   int group_m;  // raster band height (m-blocks)
+  const int32_t* targets = nullptr;  // EPI_ROWSTAT
+  float* tval = nullptr;
+  int nslots = 0;
 };
 // Split-K scratch: fp32 partial tiles + per-tile tickets (zero between launches).
 // One per model: kernels of one forward run in stream order, so they share it.
@@ -165,6 +173,10 @@ void simt_add(const float* a, const float* b, int64_t n, Kcfg cfg, float* out, c
 void simt_tanh(const float* x, int64_t n, Kcfg cfg, float* out, cudaStream_t st);
 // device logits reductions (logits_reduce.cu): per row NLL of targets[row] (skipped
 // when < 0; double) and argmax; compare_logits partials [rows][7]
+// fold the EPI_ROWSTAT partials of the LM head: per row NLL of the target (as row_nll)
+// and the first argmax column
+void rowstat_combine(const void* stat, int nslots, int64_t rows, int64_t n, const int32_t* targets,
+                     const float* tval, double* nll, int32_t* amax, cudaStream_t st);
 void row_nll(const void* logits, int dtype, int64_t rows, int64_t n, int64_t ld, const int32_t* targets,
              double* nll, int32_t* amax, cudaStream_t st);
 void compare_rows(const void* base, int base_dtype, int64_t ldb, const void* cand, int cand_dtype, int64_t ldc,

@@ -152,7 +152,57 @@ __global__ void __launch_bounds__(kThreads) compare_rows_kernel(const TB* __rest
   if (threadIdx.x == 0) out[6] = static_cast<double>(bad);
 }
 
+// Fold of the LM head's fused row statistics (gemm_tc.cu EPI_ROWSTAT): one thread per
+// row walks its slots in column order -- slot-major layout, so a warp's loads cover 32
+// consecutive rows -- max M and the first column reaching it (strict >: lowest index on
+// ties, as row_nll), denominator sum_p s_p * exp(m_p - M) in double, then the NLL of the
+// target exactly as row_nll forms it (0 without a target, NaN for a non-finite row).
+__global__ void __launch_bounds__(kThreads) rowstat_combine_kernel(const float4* __restrict__ stat, int nslots,
+                                                                   int64_t rows, int64_t n,
+                                                                   const int32_t* __restrict__ targets,
+                                                                   const float* __restrict__ tval,
+                                                                   double* __restrict__ nll, int32_t* __restrict__ amax) {
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
+  if (r >= rows) return;
+  float mx = __int_as_float(0xff800000);
+  int idx = 0x7fffffff;
+  bool bad = false;
+  for (int p = 0; p < nslots; ++p) {
+    const float4 q = stat[static_cast<int64_t>(p) * rows + r];
+    bad |= q.w != 0.0f;
+    if (q.x > mx) {
+      mx = q.x;
+      idx = __float_as_int(q.z);
+    }
+  }
+  if (amax != nullptr) amax[r] = idx;
+  if (nll == nullptr) return;
+  const int32_t t = targets != nullptr ? targets[r] : -1;
+  if (t < 0 || t >= n) {
+    nll[r] = 0.0;
+    return;
+  }
+  if (!isfinite(mx) || bad) {
+    nll[r] = __longlong_as_double(0x7ff8000000000000ll);
+    return;
+  }
+  double den = 0.0;
+  for (int p = 0; p < nslots; ++p) {
+    const float4 q = stat[static_cast<int64_t>(p) * rows + r];
+    if (q.x != __int_as_float(0xff800000)) den += static_cast<double>(q.y) * exp(static_cast<double>(q.x) - mx);
+  }
+  nll[r] = -((static_cast<double>(tval[r]) - mx) - log(den));
+}
+
 }  // namespace
+
+void rowstat_combine(const void* stat, int nslots, int64_t rows, int64_t n, const int32_t* targets,
+                     const float* tval, double* nll, int32_t* amax, cudaStream_t st) {
+  if (rows <= 0) return;
+  rowstat_combine_kernel<<<static_cast<unsigned>((rows + kThreads - 1) / kThreads), kThreads, 0, st>>>(
+      static_cast<const float4*>(stat), nslots, rows, n, targets, tval, nll, amax);
+  PRLAB_CUDA(cudaGetLastError());
+}
 
 void row_nll(const void* logits, int dtype, int64_t rows, int64_t n, int64_t ld, const int32_t* targets,
              double* nll, int32_t* amax, cudaStream_t st) {

@@ -495,6 +495,10 @@ struct prlab_gpu_model {
     std::vector<std::array<const void*, 12>> small_lw;
     std::map<std::tuple<const void*, void*, int, int64_t>, cudaGraphExec_t> graphs;
     std::map<std::tuple<void*, int64_t>, GemmPlan> head_plans;
+    // fused head statistics (prlab_gpu_forward_nll_device): 0 = not planned, 1 = fused, 2 = unfused
+    int rs_state = 0;
+    GemmPlan rs_plan{};
+    DeviceBuffer rs_buf;  // float4 [nslots][M] partials + float [M] target logits
   };
   std::map<std::tuple<int64_t, int64_t, uint64_t>, std::unique_ptr<Plan>> plans;
 
@@ -1194,6 +1198,9 @@ int prlab_gpu_compare_logits_device(const void* d_base, int32_t base_dtype, int6
   });
 }
 
+void enqueue_nll(prlab_gpu_model& m, prlab_gpu_model::Plan& p, const int32_t* d_ids, const int32_t* d_targets,
+                 double* d_nll, int32_t* d_argmax, cudaStream_t st, int32_t* fused);
+
 int prlab_gpu_perplexity(prlab_gpu_model* m, const int32_t* tokens, int64_t n_tokens, int64_t context_len,
                          const prlab_policy* policy, double* ppl) {
   return guarded([&] {
@@ -1231,8 +1238,9 @@ int prlab_gpu_perplexity(prlab_gpu_model* m, const int32_t* tokens, int64_t n_to
       TmpDev dtg(rows * 4), dnll(rows * sizeof(double));
       PRLAB_CUDA(cudaMemcpyAsync(p.ids, tokens + off, rows * 4, cudaMemcpyHostToDevice, st));
       PRLAB_CUDA(cudaMemcpyAsync(dtg.p, tg.data(), rows * 4, cudaMemcpyHostToDevice, st));
-      enqueue_forward(*m, p, p.ids, p.out32, PRLAB_OUT_F32, V, st);  // logits stay on the device
-      row_nll(p.out32, 0, rows, V, V, static_cast<const int32_t*>(dtg.p), static_cast<double*>(dnll.p), nullptr, st);
+      // logits stay on the device; under hybrid on the tensor-core path the head's epilogue
+      // reduces them to per-row statistics and they are never written (enqueue_nll)
+      enqueue_nll(*m, p, p.ids, static_cast<const int32_t*>(dtg.p), static_cast<double*>(dnll.p), nullptr, st, nullptr);
       std::vector<double> h(static_cast<size_t>(rows));
       PRLAB_CUDA(cudaMemcpyAsync(h.data(), dnll.p, rows * sizeof(double), cudaMemcpyDeviceToHost, st));
       PRLAB_CUDA(cudaStreamSynchronize(st));
@@ -1491,6 +1499,62 @@ int prlab_gpu_forward_trunk_device(prlab_gpu_model* m, const int32_t* d_ids, int
     o.hidden_only = true;
     const int64_t n = enqueue_forward(*m, p, d_ids, nullptr, PRLAB_OUT_F32, 0, static_cast<cudaStream_t>(stream), o);
     if (kernels) *kernels = n;
+  });
+}
+
+// Forward + per-row NLL / argmax (prlab_gpu_forward_nll_device, perplexity): the tied
+// head's log-softmax statistics come out of the head GEMM's epilogue (EPI_ROWSTAT) when
+// the head runs on CTA pairs; otherwise logits -> workspace -> row_nll.
+void enqueue_nll(prlab_gpu_model& m, prlab_gpu_model::Plan& p, const int32_t* d_ids, const int32_t* d_targets,
+                 double* d_nll, int32_t* d_argmax, cudaStream_t st, int32_t* fused) {
+  const int64_t M = p.B * p.S, V = m.V;
+  if (p.rs_state == 0) {
+    p.rs_state = 2;
+    if (p.fast && !std::getenv("PRLAB_NO_FUSED_NLL")) {
+      // the head GEMM exactly as the logits path plans it, with the statistics epilogue
+      GemmPlan probe = plan_gemm_tc(p.xn16, m.h, m.emb16, m.h, nullptr, p.logit16, p.ld16, static_cast<int>(M),
+                                    static_cast<int>(V), static_cast<int>(m.h), EPI_F16, &m.scratch);
+      if (probe.pair) {
+        const int nslots = ((static_cast<int>(V) + probe.bn - 1) / probe.bn) * 2;  // 2 column groups per tile
+        p.rs_buf.alloc(static_cast<size_t>(nslots) * M * 16 + M * 4);
+        p.rs_plan = plan_gemm_tc(p.xn16, m.h, m.emb16, m.h, nullptr, p.rs_buf.p, 8, static_cast<int>(M),
+                                 static_cast<int>(V), static_cast<int>(m.h), EPI_ROWSTAT, &m.scratch, probe.bn);
+        p.rs_plan.nslots = nslots;
+        p.rs_plan.tval =
+            reinterpret_cast<float*>(static_cast<char*>(p.rs_buf.p) + static_cast<size_t>(nslots) * M * 16);
+        p.rs_state = p.rs_plan.pair ? 1 : 2;
+      }
+    }
+  }
+  if (fused) *fused = p.rs_state == 1 ? 1 : 0;
+  if (p.rs_state == 1) {
+    FwdOpts o;
+    o.hidden_only = true;  // forward_hidden: round16(final LN) in xn16
+    enqueue_forward(m, p, d_ids, nullptr, PRLAB_OUT_F32, 0, st, o);
+    GemmPlan hp = p.rs_plan;
+    hp.targets = d_targets;
+    launch_gemm_tc(hp, st);
+    rowstat_combine(p.rs_buf.p, hp.nslots, M, V, d_targets, hp.tval, d_nll, d_argmax, st);
+  } else if (p.fast) {  // unfused: logits into the workspace, then the row kernel
+    enqueue_forward(m, p, d_ids, p.logit16, PRLAB_OUT_F16, p.ld16, st);
+    row_nll(p.logit16, 1, M, V, p.ld16, d_targets, d_nll, d_argmax, st);
+  } else {
+    enqueue_forward(m, p, d_ids, p.out32, PRLAB_OUT_F32, V, st);
+    row_nll(p.out32, 0, M, V, V, d_targets, d_nll, d_argmax, st);
+  }
+}
+
+int prlab_gpu_forward_nll_device(prlab_gpu_model* m, const int32_t* d_ids, const int32_t* d_targets, int64_t B,
+                                 int64_t S, const prlab_policy* policy, double* d_nll, int32_t* d_argmax,
+                                 void* stream, int32_t* fused) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(m->mu);
+    validate_policy(*policy);
+    check_forward_args(*m, B, S);
+    if (m->L == 0) throw std::invalid_argument("forward_nll needs a model with a tied head (num_layers > 0)");
+    PRLAB_CUDA(cudaSetDevice(m->device));
+    auto& p = get_plan(*m, B, S, *policy);
+    enqueue_nll(*m, p, d_ids, d_targets, d_nll, d_argmax, static_cast<cudaStream_t>(stream), fused);
   });
 }
 

@@ -118,3 +118,45 @@ def test_window_nll_restatement_uniform():
     ppl = float(np.exp(nll.cpu().numpy()[:-1].sum() / (S - 1)))
     assert abs(ppl - V) <= 1e-9 * V
     assert abs(window_nll_sum(np.zeros((1, S, V), np.float32), np.arange(S)) / (S - 1) - np.log(V)) < 1e-12
+
+
+@pytest.mark.parametrize("B,S", [(4, 128), (3, 200), (1, 64)])
+def test_forward_nll_fused_head_matches_logits_path(B, S):
+    """forward_nll_device: the LM head's log-softmax statistics fused
+    into its GEMM epilogue (CTA-pair head, B*S >= 512 rows) give the same argmax as the
+    logits + row_nll path bit for bit and the same NLL within 2e-6 absolute (fp32 partial
+    sums of expf per 128 columns, folded in double); small shapes fall back to the logits
+    path (identical results).  Odd vocabulary tail, targets in the last partial tile, -1
+    targets (0 NLL)."""
+    cfg = PRESETS["gpt2_small"].replace(num_layers=1)
+    m = pg.DeviceModel(pg.ModelConfig(**cfg.__dict__), model_params(cfg))
+    o = oracle()
+    M, V = B * S, cfg.vocab
+    ids = torch.from_numpy(o.random_tokens(V, B, S, 5)).cuda()
+    rng = np.random.default_rng(7)
+    tg = rng.integers(0, V, M).astype(np.int32)
+    tg[::S] = -1
+    tg[1::17] = V - 1 - rng.integers(0, 80, tg[1::17].size)  # inside the last (partial) n-tile
+    tgd = torch.from_numpy(tg).cuda()
+    nll = torch.full((M,), -7.0, dtype=torch.float64, device="cuda")
+    am = torch.full((M,), -7, dtype=torch.int32, device="cuda")
+    fused = m.forward_nll_device(ids.data_ptr(), tgd.data_ptr(), B, S, "hybrid", nll.data_ptr(), am.data_ptr())
+    assert fused == (M >= 512)
+    ld = (V + 7) // 8 * 8
+    logits = torch.empty(M, ld, dtype=torch.float16, device="cuda")
+    m.forward_device(ids.data_ptr(), B, S, "hybrid", logits.data_ptr(), pg.OUT_F16, ld)
+    nll_ref = torch.empty(M, dtype=torch.float64, device="cuda")
+    am_ref = torch.empty(M, dtype=torch.int32, device="cuda")
+    pg.row_nll_device(logits, tgd, nll_ref, am_ref, rows=M, n=V, ld=ld)
+    torch.cuda.synchronize()
+    m.sync_status()
+    assert np.array_equal(am.cpu().numpy(), am_ref.cpu().numpy())
+    a, b = nll.cpu().numpy(), nll_ref.cpu().numpy()
+    assert np.all(a[tg < 0] == 0.0) and np.all(np.isfinite(a))
+    assert np.max(np.abs(a - b)) <= 2e-6, np.max(np.abs(a - b))
+    # argmax only (no NLL buffer, no targets)
+    am2 = torch.full((M,), -7, dtype=torch.int32, device="cuda")
+    m.forward_nll_device(ids.data_ptr(), 0, B, S, "hybrid", 0, am2.data_ptr())
+    torch.cuda.synchronize()
+    assert np.array_equal(am2.cpu().numpy(), am_ref.cpu().numpy())
+    m.close()
