@@ -9,9 +9,9 @@
 // the softmax is the reference's exact two-pass form (max, then exp/sum, then
 // normalise-then-round), not an online rescaling.
 //
-// Persistent CTAs (one per SM): CTA c owns the (batch, head) items c, c + grid, ...
-// and runs every 128-query tile of an item back to back (last tile first), so K and
-// V of the item are loaded into shared memory once and Q is double-buffered: the
+// Persistent CTAs (one per SM) over work units (unit_at below): a (batch, head) item
+// with every 128-query tile back to back (last tile first; non-causal), or one causal
+// tile.  K and V of a unit are loaded into shared memory once and Q is double-buffered: the
 // next tile's Q -- and, across items, the next item's K (after the last Q.K^T) and V
 // (after the last P.V) -- stream in under the current tile's softmax.
 // Warp roles:
@@ -33,6 +33,8 @@
 // column group g owns key block g and writes P_g into [128g, 128g+64); O lives in
 // [64, 128).  "narrow" mode (<= 2 key blocks): group g owns 32*nkb contiguous keys,
 // P goes to [256, 256 + 64*nkb), O to [384, 448).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -52,6 +54,7 @@ struct AttnArgs {
   __half* ctx;
   int64_t ld_ctx;
   long long* dbg;  // optional per-CTA stamps [grid][128] (clock64), null = off
+  int split_tiles;  // causal: one work unit per (batch, head, query tile) instead of per (batch, head)
 };
 
 struct Smem {
@@ -105,6 +108,40 @@ __device__ __forceinline__ int nkb_of(const AttnArgs& a, int qt) {
   return (a.causal && a.tap == nullptr) ? min(qt + 1, nkb_all) : nkb_all;
 }
 
+// Work units.  Non-causal (every tile costs the same): a unit is a whole (batch, head)
+// item, its tiles back to back so K/V are loaded once.  Causal: tile qt costs qt + 1 key
+// blocks, and whole items (1 + 2 + 3 + 4 = 10 blocks at S = 512) deal unevenly onto the
+// SMs (384 items on 148 SMs: 3 items = 30 blocks on the busiest SM for an average of 26),
+// so a unit is one tile, units ordered by cost (all last tiles first) and dealt in a
+// snake over the CTAs (max 27 blocks per SM); K/V of a unit are its key blocks only.
+struct Unit {
+  int b, head, qt0, ntile, kbn;  // tiles qt0, qt0 - 1, ... (ntile of them); K/V blocks [0, kbn)
+};
+__device__ __forceinline__ int unit_at(const AttnArgs& a, int k) {
+  const int n = a.B * a.H * (a.split_tiles ? a.nqt : 1);
+  const int g = static_cast<int>(gridDim.x), c = static_cast<int>(blockIdx.x);
+  const int u = k * g + ((k & 1) ? g - 1 - c : c);
+  return u < n ? u : -1;
+}
+__device__ __forceinline__ Unit unit_decode(const AttnArgs& a, int u) {
+  Unit x;
+  int bh;
+  if (a.split_tiles) {
+    const int items = a.B * a.H;
+    bh = u % items;
+    x.qt0 = a.nqt - 1 - u / items;
+    x.ntile = 1;
+  } else {
+    bh = u;
+    x.qt0 = tile_of(a, 0);
+    x.ntile = a.nqt;
+  }
+  x.head = bh % a.H;
+  x.b = bh / a.H;
+  x.kbn = nkb_of(a, x.qt0);  // the unit's first tile needs the most key blocks
+  return x;
+}
+
 __global__ void __launch_bounds__(kThreads, 1)
     attn_tc_kernel(const __grid_constant__ CUtensorMap tm, const AttnArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -115,8 +152,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + Smem::BAR);
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + B_COUNT);
 
-  const int items = a.B * a.H;
-  const int nkb_all = (a.S + 127) / 128;
   const uint32_t warp = warp_id(), lane = lane_id();
   long long* dbg = a.dbg ? a.dbg + static_cast<int64_t>(blockIdx.x) * 128 : nullptr;
   if (dbg && threadIdx.x == 0) dbg[0] = clock64();
@@ -141,23 +176,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ---------------- TMA producer ----------------
     if (lane == 0) {
       pdl_wait();  // q/k/v are written by the upstream QKV GEMM
-      uint32_t t = 0, it = 0;
-      for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
-        const int head = item % a.H, b = item / a.H;
+      uint32_t t = 0;
+      for (int it = 0, u; (u = unit_at(a, it)) >= 0; ++it) {
+        const Unit x = unit_decode(a, u);
+        const int head = x.head, b = x.b;
         if (it > 0) mbar_wait(&bars[B_KEMPTY], (it - 1) & 1);
-        for (int kb = 0; kb < nkb_all; ++kb) {
+        for (int kb = 0; kb < x.kbn; ++kb) {
           mbar_expect_tx(&bars[B_KFULL + kb], kTile);
           tma_load_3d(smem + Smem::K + kb * kTile, &tm, &bars[B_KFULL + kb], a.h + head * 64, kb * 128, b);
         }
-        for (int j = 0; j < a.nqt; ++j, ++t) {
-          const int qt = tile_of(a, j);
+        for (int j = 0; j < x.ntile; ++j, ++t) {
+          const int qt = x.qt0 - j;
           const uint32_t qb = t & 1;
           mbar_wait(&bars[B_QEMPTY + qb], ((t >> 1) & 1) ^ 1);
           mbar_expect_tx(&bars[B_QFULL + qb], kTile);
           tma_load_3d(smem + Smem::Q + qb * kTile, &tm, &bars[B_QFULL + qb], head * 64, qt * 128, b);
           if (j == 0) {  // V after the first Q: it is needed only once the first P exists
             if (it > 0) mbar_wait(&bars[B_VEMPTY], (it - 1) & 1);
-            for (int kb = 0; kb < nkb_all; ++kb) {
+            for (int kb = 0; kb < x.kbn; ++kb) {
               mbar_expect_tx(&bars[B_VFULL + kb], kTile);
               tma_load_3d(smem + Smem::V + kb * kTile, &tm, &bars[B_VFULL + kb], 2 * a.h + head * 64, kb * 128, b);
             }
@@ -171,10 +207,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       constexpr uint32_t idesc_s = idesc_f16_f32(128, 128, 0, 0);
       constexpr uint32_t idesc_o = idesc_f16_f32(128, 64, 0, 1);
-      uint32_t t = 0, it = 0;
-      for (int item = blockIdx.x; item < items; item += gridDim.x, ++it) {
-        for (int j = 0; j < a.nqt; ++j, ++t) {
-          const int qt = tile_of(a, j);
+      uint32_t t = 0, kvph = 0;  // kvph: parity bit per K/V block barrier
+      for (int it = 0, u; (u = unit_at(a, it)) >= 0; ++it) {
+        const Unit x = unit_decode(a, u);
+        for (int j = 0; j < x.ntile; ++j, ++t) {
+          const int qt = x.qt0 - j;
           const int nkb = nkb_of(a, qt);
           const bool wide = nkb > 2;
           const uint32_t o_col = wide ? 64u : 384u;
@@ -186,7 +223,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t q0 = smem_u32(smem + Smem::Q + qb * kTile);
           // ---- S = Q . K^T : M=128 queries, N=128 keys per block, K = 64 (4 x 16)
           for (int kb = 0; kb < nkb; ++kb) {
-            mbar_wait(&bars[B_KFULL + kb], it & 1);
+            mbar_wait(&bars[B_KFULL + kb], (kvph >> kb) & 1);
             tc_fence_after();
             const uint32_t k0 = smem_u32(smem + Smem::K + kb * kTile);
 #pragma unroll
@@ -196,12 +233,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             umma_commit(&bars[B_SFULL + kb]);
           }
           umma_commit(&bars[B_QEMPTY + qb]);
-          if (j == a.nqt - 1) umma_commit(&bars[B_KEMPTY]);
+          if (j == x.ntile - 1) umma_commit(&bars[B_KEMPTY]);
           // ---- O = P . V : M=128, N=64 (head dim, V MN-major in smem), K = keys, P in TMEM
           mbar_wait(&bars[B_PREADY], t & 1);
           tc_fence_after();
           for (int kb = 0; kb < nkb; ++kb) {
-            mbar_wait(&bars[B_VFULL + kb], it & 1);
+            mbar_wait(&bars[B_VFULL + kb], (kvph >> kb) & 1);
             tc_fence_after();
             const uint32_t v0 = smem_u32(smem + Smem::V + kb * kTile);
             const uint32_t pcol = wide ? 128u * kb : 256u + 64u * kb;
@@ -211,8 +248,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                           idesc_o, (kb | kk) != 0);
           }
           umma_commit(&bars[B_OFULL]);
-          if (j == a.nqt - 1) umma_commit(&bars[B_VEMPTY]);
+          if (j == x.ntile - 1) umma_commit(&bars[B_VEMPTY]);
         }
+        kvph ^= (1u << x.kbn) - 1;  // blocks [0, kbn) completed one phase in this unit
       }
     }
     __syncwarp();
@@ -226,10 +264,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float NEG_INF = __int_as_float(0xff800000);
     constexpr float LOG2E = 1.4426950408889634f;
     uint32_t t = 0, sph = 0;  // sph: parity bit per s_full barrier
-    for (int item = blockIdx.x; item < items; item += gridDim.x) {
-      const int head = item % a.H, b = item / a.H;
-      for (int j = 0; j < a.nqt; ++j, ++t) {
-        const int qt = tile_of(a, j);
+    for (int it = 0, u; (u = unit_at(a, it)) >= 0; ++it) {
+      const Unit x = unit_decode(a, u);
+      const int head = x.head, b = x.b;
+      for (int j = 0; j < x.ntile; ++j, ++t) {
+        const int qt = x.qt0 - j;
         const int nkb = nkb_of(a, qt);
         const bool wide = nkb > 2;
         const uint32_t o_col = wide ? 64u : 384u;
@@ -443,7 +482,12 @@ void launch_attn_tc(const AttnPlan& p, cudaStream_t st, float* tap) {
   a.ld_ctx = p.ld_ctx;
   a.dbg = p.dbg;
   a.tap = tap;
-  const int grid = std::min(p.B * p.H, num_sms());
+  static const bool split_env = [] {  // PRLAB_ATTN_SPLIT=0: whole (batch, head) units (A/B)
+    const char* e = std::getenv("PRLAB_ATTN_SPLIT");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  a.split_tiles = (split_env && p.causal && tap == nullptr && a.nqt > 1) ? 1 : 0;
+  const int grid = std::min(p.B * p.H * (a.split_tiles ? a.nqt : 1), num_sms());
   launch_pdl(attn_tc_kernel, dim3(grid), dim3(kThreads), kSmemBytes, st, p.tmQKV, a);
 }
 
