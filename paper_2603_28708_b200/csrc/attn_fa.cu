@@ -1,0 +1,375 @@
+// Hybrid attention, key-block streaming form (two CTAs per SM).
+//
+// Same scores and masking as attn_tc.cu (src/model.cpp:393-427, kernels.cpp:85-168):
+//   s_ij = round16(fp32dot(q_i, k_j) * 0.125), -inf above the causal diagonal,
+// but the softmax is computed online over 128-key blocks instead of over the resident
+// row: per row a running max m and sum l,
+//   e_ij = exp(s_ij - m_new),  P~_ij = round16(e_ij)  (fp16 A operand of P.V),
+//   O = O * exp(m_old - m_new) + P~ . V,   o_i = round16(O_i / l_i).
+// The reference normalises before rounding p (round16(e / sum), kernels.cpp:154-165);
+// here the fp16 rounding falls on e and the division on O -- the same number of
+// roundings of the same relative size (2^-11), in a different place.  Hybrid parity is
+// a cosine budget; tests/test_gpu_kernels.py holds both kernels to the
+// same bound against the fp32 restatement, and attn_tc.cu (exact two-pass form) remains
+// the kernel for the retain_scores tap and for PRLAB_ATTN_FA=0.
+//
+// Why: attn_tc.cu keeps a whole 128 x S score tile in TMEM (all 512 columns at S = 512),
+// so one CTA per SM alternates strictly between tensor-core and softmax phases.  Here a
+// CTA needs 192 TMEM columns (S block 128 fp32, O 64 fp32; P packed over consumed S
+// columns) and ~97 KB of shared memory, so two CTAs share an SM and one's softmax runs
+// under the other's MMAs.
+//
+// Per CTA: warp 0 TMA (Q ring 2, K ring 2, V ring 2), warp 1 tcgen05 issuer, warps 2..5
+// one query row per thread (TMEM lane = row).  Work units are (batch, head, 128-query
+// tile); causal units are ordered by key-block count and dealt in a snake over the CTAs.
+#include <cstdlib>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace prlab_gpu {
+
+namespace {
+
+constexpr int kThreads = 192;
+constexpr uint32_t kTile = 128 * 64 * 2;  // Q tile / one K or V block of 128 keys, 16 KB
+constexpr uint32_t kTmemCols = 256;
+constexpr uint32_t kColS = 0;    // S block [0, 128); P packed fp16 over [0, 64)
+constexpr uint32_t kColO = 128;  // O [128, 192)
+
+struct FaSmem {
+  static constexpr uint32_t Q = 0;               // 2 tiles
+  static constexpr uint32_t K = Q + 2 * kTile;   // 2 blocks
+  static constexpr uint32_t V = K + 2 * kTile;   // 2 blocks
+  static constexpr uint32_t BAR = V + 2 * kTile;
+  static constexpr uint32_t TOTAL = BAR + 256;
+};
+constexpr size_t kFaSmemBytes = 1024 + FaSmem::TOTAL;
+
+enum : int {
+  F_QFULL = 0,   // [2]
+  F_QEMPTY = 2,  // [2]
+  F_KFULL = 4,   // [2]
+  F_KEMPTY = 6,  // [2]
+  F_VFULL = 8,   // [2]
+  F_VEMPTY = 10, // [2]
+  F_SFULL = 12,  // S block in TMEM (and the previous P.V done)
+  F_PREADY = 13, // 4 softmax warps: P in TMEM, O rescaled
+  F_PVDONE = 14, // P.V of the block done (S/P columns free)
+  F_OFULL = 15,  // last P.V of the unit done
+  F_TFREE = 16,  // 4 softmax warps: O read by the epilogue
+  F_COUNT = 17
+};
+
+struct FaArgs {
+  int B, S, H, causal, nqt, h;
+  __half* ctx;
+  int64_t ld_ctx;
+};
+
+__device__ __forceinline__ void umma_f16_ts_fa(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                               uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+
+__device__ __forceinline__ float fmax3_fa(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+
+// unit u -> (b, head, qt); causal: all last tiles first (most key blocks), snake over CTAs
+__device__ __forceinline__ int fa_unit_at(const FaArgs& a, int k) {
+  const int n = a.B * a.H * a.nqt;
+  const int g = static_cast<int>(gridDim.x), c = static_cast<int>(blockIdx.x);
+  const int u = k * g + ((k & 1) ? g - 1 - c : c);
+  return u < n ? u : -1;
+}
+__device__ __forceinline__ void fa_decode(const FaArgs& a, int u, int& b, int& head, int& qt, int& nkb) {
+  const int items = a.B * a.H;
+  const int bh = u % items;
+  qt = a.nqt - 1 - u / items;
+  head = bh % a.H;
+  b = bh / a.H;
+  const int nkb_all = (a.S + 127) / 128;
+  nkb = a.causal ? min(qt + 1, nkb_all) : nkb_all;
+}
+
+__global__ void __launch_bounds__(kThreads, 2) attn_fa_kernel(const __grid_constant__ CUtensorMap tm, const FaArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + FaSmem::BAR);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + F_COUNT);
+  const uint32_t warp = warp_id(), lane = lane_id();
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm);
+    for (int i = 0; i < F_COUNT; ++i) mbar_init(&bars[i], (i == F_PREADY || i == F_TFREE) ? 4 : 1);
+    fence_barrier_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_slot, kTmemCols);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_trigger();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer: per unit Q, then K/V blocks in consumption order
+    if (lane == 0) {
+      pdl_wait();  // q/k/v are written by the upstream QKV GEMM
+      uint32_t qc = 0, kc = 0;
+      for (int it = 0, u; (u = fa_unit_at(a, it)) >= 0; ++it, ++qc) {
+        int b, head, qt, nkb;
+        fa_decode(a, u, b, head, qt, nkb);
+        const uint32_t qs = qc & 1;
+        mbar_wait(&bars[F_QEMPTY + qs], ((qc >> 1) & 1) ^ 1);
+        mbar_expect_tx(&bars[F_QFULL + qs], kTile);
+        tma_load_3d(smem + FaSmem::Q + qs * kTile, &tm, &bars[F_QFULL + qs], head * 64, qt * 128, b);
+        for (int kb = 0; kb < nkb; ++kb, ++kc) {
+          const uint32_t s = kc & 1, ph = ((kc >> 1) & 1) ^ 1;
+          mbar_wait(&bars[F_KEMPTY + s], ph);
+          mbar_expect_tx(&bars[F_KFULL + s], kTile);
+          tma_load_3d(smem + FaSmem::K + s * kTile, &tm, &bars[F_KFULL + s], a.h + head * 64, kb * 128, b);
+          mbar_wait(&bars[F_VEMPTY + s], ph);
+          mbar_expect_tx(&bars[F_VFULL + s], kTile);
+          tma_load_3d(smem + FaSmem::V + s * kTile, &tm, &bars[F_VFULL + s], 2 * a.h + head * 64, kb * 128, b);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ---------------- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = idesc_f16_f32(128, 128, 0, 0);
+      constexpr uint32_t idesc_o = idesc_f16_f32(128, 64, 0, 1);
+      uint32_t qc = 0, kc = 0, bc = 0;  // units, K/V blocks, blocks (single-slot barriers)
+      for (int it = 0, u; (u = fa_unit_at(a, it)) >= 0; ++it, ++qc) {
+        int b, head, qt, nkb;
+        fa_decode(a, u, b, head, qt, nkb);
+        const uint32_t qs = qc & 1;
+        mbar_wait(&bars[F_QFULL + qs], (qc >> 1) & 1);
+        const uint32_t q0 = smem_u32(smem + FaSmem::Q + qs * kTile);
+        for (int kb = 0; kb < nkb; ++kb, ++kc, ++bc) {
+          const uint32_t s = kc & 1, ph = (kc >> 1) & 1;
+          // S = Q . K^T (M = 128 queries, N = 128 keys, K = 64) once the previous P.V
+          // has read P (the S columns)
+          if (bc > 0) mbar_wait(&bars[F_PVDONE], (bc - 1) & 1);
+          mbar_wait(&bars[F_KFULL + s], ph);
+          tc_fence_after();
+          const uint32_t k0 = smem_u32(smem + FaSmem::K + s * kTile);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            umma_f16_ss(tmem + kColS, sw128_desc(q0 + k * 32, 0, 1024), sw128_desc(k0 + k * 32, 0, 1024), idesc_s,
+                        k != 0);
+          umma_commit(&bars[F_SFULL]);
+          umma_commit(&bars[F_KEMPTY + s]);
+          if (kb == nkb - 1) umma_commit(&bars[F_QEMPTY + qs]);
+          // O (+)= P~ . V once the softmax packed P and rescaled O; the unit's first P.V
+          // overwrites O, so the previous unit's epilogue must have read it
+          mbar_wait(&bars[F_PREADY], bc & 1);
+          if (kb == 0 && qc > 0) mbar_wait(&bars[F_TFREE], (qc - 1) & 1);
+          mbar_wait(&bars[F_VFULL + s], ph);
+          tc_fence_after();
+          const uint32_t v0 = smem_u32(smem + FaSmem::V + s * kTile);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)  // 16 keys per MMA = 8 packed TMEM columns of P
+            umma_f16_ts_fa(tmem + kColO, tmem + kColS + 8 * kk, sw128_desc(v0 + kk * 2048, 128 * 128, 1024), idesc_o,
+                           (kb | kk) != 0);
+          umma_commit(&bars[F_PVDONE]);
+          umma_commit(&bars[F_VEMPTY + s]);
+          if (kb == nkb - 1) umma_commit(&bars[F_OFULL]);
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- softmax + epilogue: thread = query row (TMEM lane)
+    const uint32_t quad = warp & 3;
+    const int r = static_cast<int>(quad * 32 + lane);
+    const uint32_t lane_addr = tmem + ((quad * 32) << 16);
+    const float NEG_INF = __int_as_float(0xff800000);
+    constexpr float LOG2E = 1.4426950408889634f;
+    const uint64_t k8 = f2_pack(0.125f, 0.125f), kl = f2_pack(LOG2E, LOG2E);
+    uint32_t qc = 0, bc = 0;
+    for (int it = 0, u; (u = fa_unit_at(a, it)) >= 0; ++it, ++qc) {
+      int b, head, qt, nkb;
+      fa_decode(a, u, b, head, qt, nkb);
+      const int qrow = qt * 128 + r;
+      const int row_lo = qt * 128 + static_cast<int>(quad) * 32, row_hi = row_lo + 31;  // this warp's rows
+      float m = NEG_INF, l = 0.0f;
+      for (int kb = 0; kb < nkb; ++kb, ++bc) {
+        mbar_wait(&bars[F_SFULL], bc & 1);
+        tc_fence_after();
+        const int key0 = kb * 128;
+        auto chunk_full = [&](int c) { return key0 + c + 32 <= a.S && (!a.causal || key0 + c + 31 <= row_lo); };
+        auto chunk_dead = [&](int c) { return key0 + c >= a.S || (a.causal && key0 + c > row_hi); };
+        // pass 1: block max of the raw accumulators (round16(x * 0.125) is monotone)
+        float m0 = NEG_INF, m1 = NEG_INF;
+#pragma unroll 1
+        for (int c = 0; c < 128; c += 32) {
+          if (chunk_dead(c)) continue;
+          uint32_t v[32];
+          tmem_ld32(lane_addr + kColS + c, v);
+          tmem_wait_ld();
+          if (chunk_full(c)) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              m0 = fmax3_fa(m0, __uint_as_float(v[i]), __uint_as_float(v[i + 1]));
+              m1 = fmax3_fa(m1, __uint_as_float(v[i + 2]), __uint_as_float(v[i + 3]));
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < 32; ++i) {
+              const int j = key0 + c + i;
+              const bool valid = j < a.S && (!a.causal || j <= qrow);
+              m0 = fmaxf(m0, valid ? __uint_as_float(v[i]) : NEG_INF);
+            }
+          }
+        }
+        const float mraw = fmaxf(m0, m1);
+        const float mblk = mraw == NEG_INF ? NEG_INF : r16(__fmul_rn(mraw, 0.125f));
+        const float mnew = fmaxf(m, mblk);
+        // rescale O (the previous blocks' P.V are complete: S of this block was issued after
+        // them).  tcgen05.ld/st are warp-collective: the whole warp rescales when any row's
+        // max moved (sc = 2^0 = 1 exactly for the others)
+        if (kb > 0 && __any_sync(0xffffffffu, mnew > m)) {
+          const float sc = ex2_approx(__fmul_rn(__fsub_rn(m, mnew), LOG2E));
+          l = __fmul_rn(l, sc);
+          const uint64_t sc2 = f2_pack(sc, sc);
+#pragma unroll
+          for (int h0 = 0; h0 < 64; h0 += 32) {
+            uint32_t o[32];
+            tmem_ld32(lane_addr + kColO + h0, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              float x0, x1;
+              f2_unpack(f2_mul(f2_pack(__uint_as_float(o[i]), __uint_as_float(o[i + 1])), sc2), x0, x1);
+              o[i] = __float_as_uint(x0);
+              o[i + 1] = __float_as_uint(x1);
+            }
+            tmem_st32(lane_addr + kColO + h0, o);
+          }
+        }
+        m = mnew;
+        // pass 2: e = exp(s - m), P~ = round16(e) packed over the consumed S columns
+        const float ml = __fmul_rn(m, LOG2E);
+        const uint64_t nm = f2_pack(-ml, -ml);
+        uint64_t sum2 = f2_pack(0.0f, 0.0f);
+#pragma unroll 1
+        for (int c = 0; c < 128; c += 32) {
+          uint32_t pk[16];
+          if (chunk_dead(c)) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) pk[i] = 0u;
+          } else {
+            uint32_t v[32];
+            tmem_ld32(lane_addr + kColS + c, v);
+            tmem_wait_ld();  // the chunk is in registers before P overwrites S columns
+            const bool full = chunk_full(c);
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              float s0, s1;
+              f2_unpack(f2_mul(f2_pack(__uint_as_float(v[i]), __uint_as_float(v[i + 1])), k8), s0, s1);
+              h2_unpack(h2_pack_rn(s0, s1), s0, s1);  // s = round16(acc * 0.125)
+              float x0, x1;
+              f2_unpack(f2_fma(f2_pack(s0, s1), kl, nm), x0, x1);
+              float e0 = ex2_approx(x0), e1 = ex2_approx(x1);
+              if (!full) {
+                const int j = key0 + c + i;
+                e0 = (j < a.S && (!a.causal || j <= qrow)) ? e0 : 0.0f;
+                e1 = (j + 1 < a.S && (!a.causal || j + 1 <= qrow)) ? e1 : 0.0f;
+              }
+              sum2 = f2_add(sum2, f2_pack(e0, e1));
+              pk[i / 2] = h2_pack_rn(e0, e1);
+            }
+          }
+          tmem_st16(lane_addr + kColS + c / 2, pk);
+        }
+        float sa, sb;
+        f2_unpack(sum2, sa, sb);
+        l = __fadd_rn(l, __fadd_rn(sa, sb));
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars[F_PREADY]);
+      }
+      // epilogue: o = round16(O / l) -> ctx
+      mbar_wait(&bars[F_OFULL], qc & 1);
+      tc_fence_after();
+      uint32_t o[64];
+      tmem_ld32(lane_addr + kColO, *reinterpret_cast<uint32_t(*)[32]>(o));
+      tmem_ld32(lane_addr + kColO + 32, *reinterpret_cast<uint32_t(*)[32]>(o + 32));
+      tmem_wait_ld();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[F_TFREE]);
+      if (qrow < a.S) {
+        const float inv = __frcp_rn(l);
+        const uint64_t inv2 = f2_pack(inv, inv);
+        uint4* dst = reinterpret_cast<uint4*>(a.ctx + (static_cast<int64_t>(b) * a.S + qrow) * a.ld_ctx + head * 64);
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          uint32_t pk[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            float x0, x1;
+            f2_unpack(f2_mul(f2_pack(__uint_as_float(o[8 * q + 2 * i]), __uint_as_float(o[8 * q + 2 * i + 1])), inv2),
+                      x0, x1);
+            pk[i] = h2_pack_rn(x0, x1);
+          }
+          dst[q] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, kTmemCols);
+  }
+}
+
+}  // namespace
+
+bool attn_fa_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("PRLAB_ATTN_FA");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
+void launch_attn_fa(const AttnPlan& p, cudaStream_t st) {
+  static bool configured = false;
+  if (!configured) {
+    PRLAB_CUDA(cudaFuncSetAttribute(attn_fa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kFaSmemBytes)));
+    configured = true;
+  }
+  FaArgs a;
+  a.B = p.B;
+  a.S = p.S;
+  a.H = p.H;
+  a.causal = p.causal;
+  a.nqt = (p.S + 127) / 128;
+  a.h = p.H * p.hd;
+  a.ctx = reinterpret_cast<__half*>(p.ctx);
+  a.ld_ctx = p.ld_ctx;
+  const int units = p.B * p.H * a.nqt;
+  const int grid = std::min(units, 2 * num_sms());
+  launch_pdl(attn_fa_kernel, dim3(grid), dim3(kThreads), kFaSmemBytes, st, p.tmQKV, a);
+}
+
+}  // namespace prlab_gpu

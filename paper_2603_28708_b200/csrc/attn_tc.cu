@@ -469,6 +469,10 @@ void configure_attn_tc() {
 }
 
 void launch_attn_tc(const AttnPlan& p, cudaStream_t st, float* tap) {
+  if (tap == nullptr && attn_fa_enabled()) {
+    launch_attn_fa(p, st);
+    return;
+  }
   configure_attn_tc();
   AttnArgs a;
   a.B = p.B;

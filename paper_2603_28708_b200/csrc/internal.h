@@ -139,6 +139,10 @@ AttnPlan plan_attn_tc(const void* qkv, int64_t ld_qkv, void* ctx, int64_t ld_ctx
 // tap (optional): [B][H][S][S] fp32 pre-mask scores (the reference's retain_scores capture)
 void launch_attn_tc(const AttnPlan& p, cudaStream_t st, float* tap = nullptr);
 void configure_attn_tc();
+// key-block streaming variant (attn_fa.cu: online softmax, two CTAs per SM); launch_attn_tc
+// dispatches to it when no tap is requested unless PRLAB_ATTN_FA=0
+bool attn_fa_enabled();
+void launch_attn_fa(const AttnPlan& p, cudaStream_t st);
 
 // --- SIMT kernels (any shape, any policy; fp32 storage) ---
 struct Kcfg {
