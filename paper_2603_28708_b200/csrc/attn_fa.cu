@@ -31,17 +31,22 @@ namespace prlab_gpu {
 
 namespace {
 
-constexpr int kThreads = 192;
+constexpr int kSoftmaxWarps = 8;  // 2 per TMEM lane quadrant, each half of the 128 key columns
+constexpr int kThreads = 64 + 32 * kSoftmaxWarps;
 constexpr uint32_t kTile = 128 * 64 * 2;  // Q tile / one K or V block of 128 keys, 16 KB
 constexpr uint32_t kTmemCols = 256;
-constexpr uint32_t kColS = 0;    // S block [0, 128); P packed fp16 over [0, 64)
+constexpr uint32_t kColS = 0;    // S block [0, 128)
 constexpr uint32_t kColO = 128;  // O [128, 192)
+constexpr uint32_t kColP = 192;  // P~ packed fp16 [192, 256): S of the next block can land while P.V reads P
 
 struct FaSmem {
   static constexpr uint32_t Q = 0;               // 2 tiles
   static constexpr uint32_t K = Q + 2 * kTile;   // 2 blocks
   static constexpr uint32_t V = K + 2 * kTile;   // 2 blocks
-  static constexpr uint32_t BAR = V + 2 * kTile;
+  // float [3][2][128]: partial row max per half (double-buffered by block parity: a fast
+  // warp may write the next block's before a slow one read this one's), partial row sums
+  static constexpr uint32_t RED = V + 2 * kTile;
+  static constexpr uint32_t BAR = RED + 3 * 256 * 4;
   static constexpr uint32_t TOTAL = BAR + 256;
 };
 constexpr size_t kFaSmemBytes = 1024 + FaSmem::TOTAL;
@@ -53,12 +58,11 @@ enum : int {
   F_KEMPTY = 6,  // [2]
   F_VFULL = 8,   // [2]
   F_VEMPTY = 10, // [2]
-  F_SFULL = 12,  // S block in TMEM (and the previous P.V done)
-  F_PREADY = 13, // 4 softmax warps: P in TMEM, O rescaled
-  F_PVDONE = 14, // P.V of the block done (S/P columns free)
-  F_OFULL = 15,  // last P.V of the unit done
-  F_TFREE = 16,  // 4 softmax warps: O read by the epilogue
-  F_COUNT = 17
+  F_SFULL = 12,  // S block in TMEM (every earlier MMA, so the previous P.V, complete)
+  F_PREADY = 13, // softmax warps: S read, P in TMEM, O rescaled
+  F_OFULL = 14,  // last P.V of the unit done
+  F_TFREE = 15,  // softmax warps: O read by the epilogue
+  F_COUNT = 16
 };
 
 struct FaArgs {
@@ -110,7 +114,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fa_kernel(const __grid_const
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm);
-    for (int i = 0; i < F_COUNT; ++i) mbar_init(&bars[i], (i == F_PREADY || i == F_TFREE) ? 4 : 1);
+    for (int i = 0; i < F_COUNT; ++i) mbar_init(&bars[i], (i == F_PREADY || i == F_TFREE) ? kSoftmaxWarps : 1);
     fence_barrier_init();
   }
   if (warp == 1) {
@@ -148,32 +152,38 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fa_kernel(const __grid_const
     }
     __syncwarp();
   } else if (warp == 1) {
-    // ---------------- MMA issuer
+    // ---------------- MMA issuer.  Per block: S_kb, then (after the softmax) P.V_kb
+    // immediately followed by S_kb+1 -- the SFULL commit of S_kb+1 therefore also
+    // covers P.V_kb, which is what the softmax needs before it rescales O and rewrites P.
     if (lane == 0) {
       constexpr uint32_t idesc_s = idesc_f16_f32(128, 128, 0, 0);
       constexpr uint32_t idesc_o = idesc_f16_f32(128, 64, 0, 1);
       uint32_t qc = 0, kc = 0, bc = 0;  // units, K/V blocks, blocks (single-slot barriers)
+      auto issue_s = [&](uint32_t q0, uint32_t kcount, bool last_of_unit, uint32_t qs) {
+        const uint32_t s = kcount & 1;
+        mbar_wait(&bars[F_KFULL + s], (kcount >> 1) & 1);
+        tc_fence_after();
+        const uint32_t k0 = smem_u32(smem + FaSmem::K + s * kTile);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          umma_f16_ss(tmem + kColS, sw128_desc(q0 + k * 32, 0, 1024), sw128_desc(k0 + k * 32, 0, 1024), idesc_s,
+                      k != 0);
+        umma_commit(&bars[F_SFULL]);
+        umma_commit(&bars[F_KEMPTY + s]);
+        if (last_of_unit) umma_commit(&bars[F_QEMPTY + qs]);
+      };
       for (int it = 0, u; (u = fa_unit_at(a, it)) >= 0; ++it, ++qc) {
         int b, head, qt, nkb;
         fa_decode(a, u, b, head, qt, nkb);
         const uint32_t qs = qc & 1;
         mbar_wait(&bars[F_QFULL + qs], (qc >> 1) & 1);
         const uint32_t q0 = smem_u32(smem + FaSmem::Q + qs * kTile);
+        // S of the unit's first block: the S columns are free once the softmax of the
+        // previous block (previous unit) signalled PREADY
+        if (bc > 0) mbar_wait(&bars[F_PREADY], (bc - 1) & 1);
+        issue_s(q0, kc, nkb == 1, qs);
         for (int kb = 0; kb < nkb; ++kb, ++kc, ++bc) {
           const uint32_t s = kc & 1, ph = (kc >> 1) & 1;
-          // S = Q . K^T (M = 128 queries, N = 128 keys, K = 64) once the previous P.V
-          // has read P (the S columns)
-          if (bc > 0) mbar_wait(&bars[F_PVDONE], (bc - 1) & 1);
-          mbar_wait(&bars[F_KFULL + s], ph);
-          tc_fence_after();
-          const uint32_t k0 = smem_u32(smem + FaSmem::K + s * kTile);
-#pragma unroll
-          for (int k = 0; k < 4; ++k)
-            umma_f16_ss(tmem + kColS, sw128_desc(q0 + k * 32, 0, 1024), sw128_desc(k0 + k * 32, 0, 1024), idesc_s,
-                        k != 0);
-          umma_commit(&bars[F_SFULL]);
-          umma_commit(&bars[F_KEMPTY + s]);
-          if (kb == nkb - 1) umma_commit(&bars[F_QEMPTY + qs]);
           // O (+)= P~ . V once the softmax packed P and rescaled O; the unit's first P.V
           // overwrites O, so the previous unit's epilogue must have read it
           mbar_wait(&bars[F_PREADY], bc & 1);
@@ -183,43 +193,48 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fa_kernel(const __grid_const
           const uint32_t v0 = smem_u32(smem + FaSmem::V + s * kTile);
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)  // 16 keys per MMA = 8 packed TMEM columns of P
-            umma_f16_ts_fa(tmem + kColO, tmem + kColS + 8 * kk, sw128_desc(v0 + kk * 2048, 128 * 128, 1024), idesc_o,
+            umma_f16_ts_fa(tmem + kColO, tmem + kColP + 8 * kk, sw128_desc(v0 + kk * 2048, 128 * 128, 1024), idesc_o,
                            (kb | kk) != 0);
-          umma_commit(&bars[F_PVDONE]);
           umma_commit(&bars[F_VEMPTY + s]);
           if (kb == nkb - 1) umma_commit(&bars[F_OFULL]);
+          if (kb + 1 < nkb) issue_s(q0, kc + 1, kb + 2 == nkb, qs);
         }
       }
     }
     __syncwarp();
   } else {
-    // ---------------- softmax + epilogue: thread = query row (TMEM lane)
-    const uint32_t quad = warp & 3;
+    // ---------------- softmax + epilogue: thread = query row (TMEM lane) x half of the
+    // key columns (warps 2..5 the first 64, warps 6..9 the second 64)
+    const uint32_t quad = warp & 3, half = (warp - 2) >> 2;
     const int r = static_cast<int>(quad * 32 + lane);
     const uint32_t lane_addr = tmem + ((quad * 32) << 16);
+    float* red = reinterpret_cast<float*>(smem + FaSmem::RED);
     const float NEG_INF = __int_as_float(0xff800000);
     constexpr float LOG2E = 1.4426950408889634f;
     const uint64_t k8 = f2_pack(0.125f, 0.125f), kl = f2_pack(LOG2E, LOG2E);
+    const int cb = static_cast<int>(half) * 64;  // this thread's first key column of a block
     uint32_t qc = 0, bc = 0;
     for (int it = 0, u; (u = fa_unit_at(a, it)) >= 0; ++it, ++qc) {
       int b, head, qt, nkb;
       fa_decode(a, u, b, head, qt, nkb);
       const int qrow = qt * 128 + r;
       const int row_lo = qt * 128 + static_cast<int>(quad) * 32, row_hi = row_lo + 31;  // this warp's rows
-      float m = NEG_INF, l = 0.0f;
+      float m = NEG_INF, l = 0.0f;  // l: this half's share of the row sum
       for (int kb = 0; kb < nkb; ++kb, ++bc) {
         mbar_wait(&bars[F_SFULL], bc & 1);
         tc_fence_after();
-        const int key0 = kb * 128;
+        const int key0 = kb * 128 + cb;
         auto chunk_full = [&](int c) { return key0 + c + 32 <= a.S && (!a.causal || key0 + c + 31 <= row_lo); };
         auto chunk_dead = [&](int c) { return key0 + c >= a.S || (a.causal && key0 + c > row_hi); };
-        // pass 1: block max of the raw accumulators (round16(x * 0.125) is monotone)
+        const bool dead0 = chunk_dead(0), dead1 = chunk_dead(32);
+        // block max over both halves of the raw accumulators (round16(x * 0.125) is monotone)
         float m0 = NEG_INF, m1 = NEG_INF;
-#pragma unroll 1
-        for (int c = 0; c < 128; c += 32) {
-          if (chunk_dead(c)) continue;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = 32 * h;
+          if (h == 0 ? dead0 : dead1) continue;
           uint32_t v[32];
-          tmem_ld32(lane_addr + kColS + c, v);
+          tmem_ld32(lane_addr + kColS + cb + c, v);
           tmem_wait_ld();
           if (chunk_full(c)) {
 #pragma unroll
@@ -236,51 +251,33 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fa_kernel(const __grid_const
             }
           }
         }
-        const float mraw = fmaxf(m0, m1);
+        float* rmax = red + (bc & 1) * 256;
+        rmax[half * 128 + r] = fmaxf(m0, m1);
+        named_bar_sync(1, 32 * kSoftmaxWarps);
+        const float mraw = fmaxf(rmax[r], rmax[128 + r]);
         const float mblk = mraw == NEG_INF ? NEG_INF : r16(__fmul_rn(mraw, 0.125f));
         const float mnew = fmaxf(m, mblk);
-        // rescale O (the previous blocks' P.V are complete: S of this block was issued after
-        // them).  tcgen05.ld/st are warp-collective: the whole warp rescales when any row's
-        // max moved (sc = 2^0 = 1 exactly for the others)
-        if (kb > 0 && __any_sync(0xffffffffu, mnew > m)) {
-          const float sc = ex2_approx(__fmul_rn(__fsub_rn(m, mnew), LOG2E));
-          l = __fmul_rn(l, sc);
-          const uint64_t sc2 = f2_pack(sc, sc);
-#pragma unroll
-          for (int h0 = 0; h0 < 64; h0 += 32) {
-            uint32_t o[32];
-            tmem_ld32(lane_addr + kColO + h0, o);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 32; i += 2) {
-              float x0, x1;
-              f2_unpack(f2_mul(f2_pack(__uint_as_float(o[i]), __uint_as_float(o[i + 1])), sc2), x0, x1);
-              o[i] = __float_as_uint(x0);
-              o[i + 1] = __float_as_uint(x1);
-            }
-            tmem_st32(lane_addr + kColO + h0, o);
-          }
-        }
-        m = mnew;
-        // pass 2: e = exp(s - m), P~ = round16(e) packed over the consumed S columns
-        const float ml = __fmul_rn(m, LOG2E);
+        // e = exp(s - m_new), P~ = round16(e) -> TMEM (the previous P.V is complete: SFULL
+        // of this block was committed after it)
+        const float ml = __fmul_rn(mnew, LOG2E);
         const uint64_t nm = f2_pack(-ml, -ml);
         uint64_t sum2 = f2_pack(0.0f, 0.0f);
-#pragma unroll 1
-        for (int c = 0; c < 128; c += 32) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int c = 32 * h;
           uint32_t pk[16];
-          if (chunk_dead(c)) {
+          if (h == 0 ? dead0 : dead1) {
 #pragma unroll
             for (int i = 0; i < 16; ++i) pk[i] = 0u;
           } else {
-            uint32_t v[32];
-            tmem_ld32(lane_addr + kColS + c, v);
-            tmem_wait_ld();  // the chunk is in registers before P overwrites S columns
+            uint32_t w[32];  // reloaded: keeping both chunks live across the barrier spills
+            tmem_ld32(lane_addr + kColS + cb + c, w);
+            tmem_wait_ld();
             const bool full = chunk_full(c);
 #pragma unroll
             for (int i = 0; i < 32; i += 2) {
               float s0, s1;
-              f2_unpack(f2_mul(f2_pack(__uint_as_float(v[i]), __uint_as_float(v[i + 1])), k8), s0, s1);
+              f2_unpack(f2_mul(f2_pack(__uint_as_float(w[i]), __uint_as_float(w[i + 1])), k8), s0, s1);
               h2_unpack(h2_pack_rn(s0, s1), s0, s1);  // s = round16(acc * 0.125)
               float x0, x1;
               f2_unpack(f2_fma(f2_pack(s0, s1), kl, nm), x0, x1);
@@ -294,32 +291,57 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fa_kernel(const __grid_const
               pk[i / 2] = h2_pack_rn(e0, e1);
             }
           }
-          tmem_st16(lane_addr + kColS + c / 2, pk);
+          tmem_st16(lane_addr + kColP + (cb + c) / 2, pk);
         }
         float sa, sb;
         f2_unpack(sum2, sa, sb);
+        // rescale this half's 32 columns of O (warp-collective TMEM access: the whole warp
+        // rescales when any row's max moved; sc = 2^0 = 1 exactly for the others)
+        if (kb > 0 && __any_sync(0xffffffffu, mnew > m)) {
+          const float sc = ex2_approx(__fmul_rn(__fsub_rn(m, mnew), LOG2E));
+          l = __fmul_rn(l, sc);
+          const uint64_t sc2 = f2_pack(sc, sc);
+          uint32_t o[32];
+          tmem_ld32(lane_addr + kColO + half * 32, o);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) {
+            float x0, x1;
+            f2_unpack(f2_mul(f2_pack(__uint_as_float(o[i]), __uint_as_float(o[i + 1])), sc2), x0, x1);
+            o[i] = __float_as_uint(x0);
+            o[i + 1] = __float_as_uint(x1);
+          }
+          tmem_st32(lane_addr + kColO + half * 32, o);
+        }
         l = __fadd_rn(l, __fadd_rn(sa, sb));
+        m = mnew;
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars[F_PREADY]);
       }
-      // epilogue: o = round16(O / l) -> ctx
+      // epilogue: o = round16(O / l) -> ctx, this half's 32 columns; l = both halves' sums
+      float* rsum = red + 512;
+      rsum[half * 128 + r] = l;
       mbar_wait(&bars[F_OFULL], qc & 1);
       tc_fence_after();
-      uint32_t o[64];
-      tmem_ld32(lane_addr + kColO, *reinterpret_cast<uint32_t(*)[32]>(o));
-      tmem_ld32(lane_addr + kColO + 32, *reinterpret_cast<uint32_t(*)[32]>(o + 32));
+      uint32_t o[32];
+      tmem_ld32(lane_addr + kColO + half * 32, o);
       tmem_wait_ld();
       tc_fence_before();
+      // both partial sums visible (the next write of rsum is a unit later, behind at least
+      // one block barrier that this warp reaches only after its read)
+      named_bar_sync(1, 32 * kSoftmaxWarps);
+      const float lt = __fadd_rn(rsum[r], rsum[128 + r]);
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[F_TFREE]);
       if (qrow < a.S) {
-        const float inv = __frcp_rn(l);
+        const float inv = __frcp_rn(lt);
         const uint64_t inv2 = f2_pack(inv, inv);
-        uint4* dst = reinterpret_cast<uint4*>(a.ctx + (static_cast<int64_t>(b) * a.S + qrow) * a.ld_ctx + head * 64);
+        uint4* dst = reinterpret_cast<uint4*>(a.ctx + (static_cast<int64_t>(b) * a.S + qrow) * a.ld_ctx + head * 64 +
+                                              half * 32);
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < 4; ++q) {
           uint32_t pk[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
