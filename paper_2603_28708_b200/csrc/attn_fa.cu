@@ -4,8 +4,9 @@
 //   s_ij = round16(fp32dot(q_i, k_j) * 0.125), -inf above the causal diagonal,
 // but the softmax is computed online over 128-key blocks instead of over the resident
 // row: per row a running max m and sum l,
-//   e_ij = exp(s_ij - m_new),  P~_ij = round16(e_ij)  (fp16 A operand of P.V),
-//   O = O * exp(m_old - m_new) + P~ . V,   o_i = round16(O_i / l_i).
+//   e_ij = exp(s_ij - m),  P~_ij = round16(e_ij)  (fp16 A operand of P.V),
+//   O = O * exp(m_old - m) + P~ . V,   o_i = round16(O_i / l_i),
+// where m follows the running max lazily (moved only when it grew by > 5).
 // The reference normalises before rounding p (round16(e / sum), kernels.cpp:154-165);
 // here the fp16 rounding falls on e and the division on O -- the same number of
 // roundings of the same relative size (2^-11), in a different place.  Hybrid parity is
@@ -257,9 +258,17 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fa_kernel(const __grid_const
         const float mraw = fmaxf(rmax[r], rmax[128 + r]);
         const float mblk = mraw == NEG_INF ? NEG_INF : r16(__fmul_rn(mraw, 0.125f));
         const float mnew = fmaxf(m, mblk);
-        // e = exp(s - m_new), P~ = round16(e) -> TMEM (the previous P.V is complete: SFULL
+        // Lazy rescaling: O and l are rescaled (and m moved) only when some row of the
+        // warp saw its max grow by more than kLazy; otherwise this block's exponentials use
+        // the stale max, e <= e^kLazy, well inside fp16 -- and fp16 rounding is relative, so
+        // P~ keeps its precision.  Saves the O round trip through TMEM on most blocks.
+        constexpr float kLazy = 5.0f;
+        const bool rescale = kb > 0 && __any_sync(0xffffffffu, mnew > m + kLazy);
+        const float mold = m;
+        if (kb == 0 || rescale) m = mnew;
+        // e = exp(s - m), P~ = round16(e) -> TMEM (the previous P.V is complete: SFULL
         // of this block was committed after it)
-        const float ml = __fmul_rn(mnew, LOG2E);
+        const float ml = __fmul_rn(m, LOG2E);
         const uint64_t nm = f2_pack(-ml, -ml);
         uint64_t sum2 = f2_pack(0.0f, 0.0f);
 #pragma unroll
@@ -295,10 +304,11 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fa_kernel(const __grid_const
         }
         float sa, sb;
         f2_unpack(sum2, sa, sb);
-        // rescale this half's 32 columns of O (warp-collective TMEM access: the whole warp
-        // rescales when any row's max moved; sc = 2^0 = 1 exactly for the others)
-        if (kb > 0 && __any_sync(0xffffffffu, mnew > m)) {
-          const float sc = ex2_approx(__fmul_rn(__fsub_rn(m, mnew), LOG2E));
+        // rescale this half's 32 columns of O and the partial sum to the new max (the
+        // decision is warp-uniform: TMEM access is warp-collective; both halves of a row
+        // see the same maxima, so they decide alike)
+        if (rescale) {
+          const float sc = ex2_approx(__fmul_rn(__fsub_rn(mold, m), LOG2E));
           l = __fmul_rn(l, sc);
           const uint64_t sc2 = f2_pack(sc, sc);
           uint32_t o[32];
@@ -314,7 +324,6 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fa_kernel(const __grid_const
           tmem_st32(lane_addr + kColO + half * 32, o);
         }
         l = __fadd_rn(l, __fadd_rn(sa, sb));
-        m = mnew;
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();
