@@ -160,3 +160,22 @@ def test_forward_nll_fused_head_matches_logits_path(B, S):
     torch.cuda.synchronize()
     assert np.array_equal(am2.cpu().numpy(), am_ref.cpu().numpy())
     m.close()
+
+
+def test_perplexity_fused_head_matches_unfused(monkeypatch):
+    """perplexity (fidelity.cpp:248-279) with >= 512 rows per batch of windows runs the
+    head's fused log-softmax epilogue; the same stream through a model whose plans were
+    made with PRLAB_NO_FUSED_NLL=1 (logits + row kernel) agrees within 1e-6 relative."""
+    cfg = PRESETS["gpt2_small"].replace(num_layers=1)
+    p = model_params(cfg)
+    o = oracle()
+    stream = o.random_tokens(cfg.vocab, 1, 6 * 128 + 5, 23)
+    fused = pg.DeviceModel(pg.ModelConfig(**cfg.__dict__), p)
+    a = fused.perplexity(stream, 128, "hybrid")
+    monkeypatch.setenv("PRLAB_NO_FUSED_NLL", "1")
+    plain = pg.DeviceModel(pg.ModelConfig(**cfg.__dict__), p)
+    b = plain.perplexity(stream, 128, "hybrid")
+    monkeypatch.delenv("PRLAB_NO_FUSED_NLL")
+    assert np.isfinite(a) and abs(a - b) <= 1e-6 * b, (a, b)
+    fused.close()
+    plain.close()
