@@ -469,7 +469,12 @@ void configure_attn_tc() {
 }
 
 void launch_attn_tc(const AttnPlan& p, cudaStream_t st, float* tap) {
-  if (tap == nullptr && attn_fa_enabled()) {
+  // The streaming kernel wins once a sequence spans several key blocks or the (b, h)
+  // items fill the SMs; with S <= 128 and fewer items than SMs (one 128-key tile each) the
+  // resident-row kernel's 16 softmax warps per tile finish first (C3 sweep A/B,
+  // profiles/r01/ab_attn_c3_sweep.txt: B=8 S=32 0.557 vs 0.590 ms, B=16 S=32 0.698 vs 0.653).
+  const int nqt = (p.S + 127) / 128;
+  if (tap == nullptr && attn_fa_enabled() && (nqt > 1 || p.B * p.H > num_sms())) {
     launch_attn_fa(p, st);
     return;
   }
