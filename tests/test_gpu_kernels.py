@@ -89,9 +89,12 @@ def _attn_ref(qkv, B, S, H, hd, causal):
     return o.transpose(1, 2).reshape(B * S, h)
 
 
+# shapes on both attention kernels: the streaming one (S > 128, or B*H above the SM count:
+# (16, 1, 1), (13, 20, 1), (16, 3, 0)) and the resident-row one (the rest)
 @pytest.mark.parametrize("B,S,causal", [(1, 128, 0), (1, 128, 1), (2, 77, 0), (2, 77, 1),
                                          (1, 1, 1), (3, 200, 1), (2, 512, 0), (2, 512, 1),
-                                         (1, 384, 0), (4, 64, 1)])
+                                         (1, 384, 0), (4, 64, 1), (16, 1, 1), (13, 20, 1), (16, 3, 0),
+                                         (13, 128, 1)])
 def test_tc_attention_matches_fp32_reference(B, S, causal):
     H, hd = 12, 64
     g = torch.Generator(device="cuda").manual_seed(B * 1000 + S * 2 + causal)
