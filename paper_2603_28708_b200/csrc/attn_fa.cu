@@ -59,17 +59,19 @@ enum : int {
   F_KEMPTY = 6,  // [2]
   F_VFULL = 8,   // [2]
   F_VEMPTY = 10, // [2]
-  F_SFULL = 12,  // S block in TMEM (every earlier MMA, so the previous P.V, complete)
+  F_SFULL = 12,  // S block in TMEM
   F_PREADY = 13, // softmax warps: S read, P in TMEM, O rescaled
   F_OFULL = 14,  // last P.V of the unit done
   F_TFREE = 15,  // softmax warps: O read by the epilogue
-  F_COUNT = 16
+  F_PVDONE = 16, // P.V of a block done: P columns and O free for the next block's softmax
+  F_COUNT = 17
 };
 
 struct FaArgs {
   int B, S, H, causal, nqt, h;
   __half* ctx;
   int64_t ld_ctx;
+  long long* dbg;  // optional clock64 stamps of CTA 0, [block][8] (scripts/fa_phases.py), null = off
 };
 
 __device__ __forceinline__ void umma_f16_ts_fa(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
@@ -153,9 +155,9 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fa_kernel(const __grid_const
     }
     __syncwarp();
   } else if (warp == 1) {
-    // ---------------- MMA issuer.  Per block: S_kb, then (after the softmax) P.V_kb
-    // immediately followed by S_kb+1 -- the SFULL commit of S_kb+1 therefore also
-    // covers P.V_kb, which is what the softmax needs before it rescales O and rewrites P.
+    // ---------------- MMA issuer.  Per block, once the softmax released S_kb (PREADY):
+    // S_kb+1 first, then P.V_kb -- the next block's pass 1 (block max) runs while P.V_kb
+    // executes; the softmax waits PVDONE before it rewrites P or rescales O.
     if (lane == 0) {
       constexpr uint32_t idesc_s = idesc_f16_f32(128, 128, 0, 0);
       constexpr uint32_t idesc_o = idesc_f16_f32(128, 64, 0, 1);
@@ -188,6 +190,9 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fa_kernel(const __grid_const
           // O (+)= P~ . V once the softmax packed P and rescaled O; the unit's first P.V
           // overwrites O, so the previous unit's epilogue must have read it
           mbar_wait(&bars[F_PREADY], bc & 1);
+          long long* ms = (a.dbg && blockIdx.x == 0 && bc < 32) ? a.dbg + bc * 8 : nullptr;
+          if (ms) ms[4] = clock64();
+          if (kb + 1 < nkb) issue_s(q0, kc + 1, kb + 2 == nkb, qs);
           if (kb == 0 && qc > 0) mbar_wait(&bars[F_TFREE], (qc - 1) & 1);
           mbar_wait(&bars[F_VFULL + s], ph);
           tc_fence_after();
@@ -196,9 +201,10 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fa_kernel(const __grid_const
           for (int kk = 0; kk < 8; ++kk)  // 16 keys per MMA = 8 packed TMEM columns of P
             umma_f16_ts_fa(tmem + kColO, tmem + kColP + 8 * kk, sw128_desc(v0 + kk * 2048, 128 * 128, 1024), idesc_o,
                            (kb | kk) != 0);
+          umma_commit(&bars[F_PVDONE]);
           umma_commit(&bars[F_VEMPTY + s]);
           if (kb == nkb - 1) umma_commit(&bars[F_OFULL]);
-          if (kb + 1 < nkb) issue_s(q0, kc + 1, kb + 2 == nkb, qs);
+          if (ms) ms[5] = clock64();
         }
       }
     }
@@ -212,7 +218,6 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fa_kernel(const __grid_const
     float* red = reinterpret_cast<float*>(smem + FaSmem::RED);
     const float NEG_INF = __int_as_float(0xff800000);
     constexpr float LOG2E = 1.4426950408889634f;
-    const uint64_t k8 = f2_pack(0.125f, 0.125f), kl = f2_pack(LOG2E, LOG2E);
     const int cb = static_cast<int>(half) * 64;  // this thread's first key column of a block
     uint32_t qc = 0, bc = 0;
     for (int it = 0, u; (u = fa_unit_at(a, it)) >= 0; ++it, ++qc) {
@@ -223,6 +228,8 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fa_kernel(const __grid_const
       float m = NEG_INF, l = 0.0f;  // l: this half's share of the row sum
       for (int kb = 0; kb < nkb; ++kb, ++bc) {
         mbar_wait(&bars[F_SFULL], bc & 1);
+        long long* ts = (a.dbg && blockIdx.x == 0 && warp == 2 && lane == 0 && bc < 32) ? a.dbg + bc * 8 : nullptr;
+        if (ts) ts[0] = clock64();
         tc_fence_after();
         const int key0 = kb * 128 + cb;
         auto chunk_full = [&](int c) { return key0 + c + 32 <= a.S && (!a.causal || key0 + c + 31 <= row_lo); };
@@ -254,9 +261,11 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fa_kernel(const __grid_const
         }
         float* rmax = red + (bc & 1) * 256;
         rmax[half * 128 + r] = fmaxf(m0, m1);
+        if (ts) ts[1] = clock64();
         named_bar_sync(1, 32 * kSoftmaxWarps);
+        if (ts) ts[2] = clock64();
         const float mraw = fmaxf(rmax[r], rmax[128 + r]);
-        const float mblk = mraw == NEG_INF ? NEG_INF : r16(__fmul_rn(mraw, 0.125f));
+        const float mblk = mraw == NEG_INF ? NEG_INF : __fmul_rn(r16(mraw), 0.125f);
         const float mnew = fmaxf(m, mblk);
         // Lazy rescaling: O and l are rescaled (and m moved) only when some row of the
         // warp saw its max grow by more than kLazy; otherwise this block's exponentials use
@@ -266,10 +275,14 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fa_kernel(const __grid_const
         const bool rescale = kb > 0 && __any_sync(0xffffffffu, mnew > m + kLazy);
         const float mold = m;
         if (kb == 0 || rescale) m = mnew;
-        // e = exp(s - m), P~ = round16(e) -> TMEM (the previous P.V is complete: SFULL
-        // of this block was committed after it)
+        // e = exp(s - m), P~ = round16(e) -> TMEM
+        // P and O are free once the previous block's P.V completed (it was issued after
+        // this block's Q.K^T)
+        if (bc > 0) mbar_wait(&bars[F_PVDONE], (bc - 1) & 1);
+        tc_fence_after();
         const float ml = __fmul_rn(m, LOG2E);
         const uint64_t nm = f2_pack(-ml, -ml);
+        const uint64_t kl8 = f2_pack(0.125f * LOG2E, 0.125f * LOG2E);  // exact: 2^-3 scaling
         uint64_t sum2 = f2_pack(0.0f, 0.0f);
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
@@ -285,11 +298,12 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fa_kernel(const __grid_const
             const bool full = chunk_full(c);
 #pragma unroll
             for (int i = 0; i < 32; i += 2) {
+              // s = round16(acc) * 0.125 (= round16(acc * 0.125) outside the binary16
+              // subnormal range); the 2^-3 rides in the exponent FMA
               float s0, s1;
-              f2_unpack(f2_mul(f2_pack(__uint_as_float(w[i]), __uint_as_float(w[i + 1])), k8), s0, s1);
-              h2_unpack(h2_pack_rn(s0, s1), s0, s1);  // s = round16(acc * 0.125)
+              h2_unpack(h2_pack_rn(__uint_as_float(w[i]), __uint_as_float(w[i + 1])), s0, s1);
               float x0, x1;
-              f2_unpack(f2_fma(f2_pack(s0, s1), kl, nm), x0, x1);
+              f2_unpack(f2_fma(f2_pack(s0, s1), kl8, nm), x0, x1);
               float e0 = ex2_approx(x0), e1 = ex2_approx(x1);
               if (!full) {
                 const int j = key0 + c + i;
@@ -328,6 +342,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fa_kernel(const __grid_const
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&bars[F_PREADY]);
+        if (ts) ts[3] = clock64();
       }
       // epilogue: o = round16(O / l) -> ctx, this half's 32 columns; l = both halves' sums
       float* rsum = red + 512;
@@ -398,6 +413,7 @@ void launch_attn_fa(const AttnPlan& p, cudaStream_t st) {
   a.h = p.H * p.hd;
   a.ctx = reinterpret_cast<__half*>(p.ctx);
   a.ld_ctx = p.ld_ctx;
+  a.dbg = p.dbg;
   const int units = p.B * p.H * a.nqt;
   const int grid = std::min(units, 2 * num_sms());
   launch_pdl(attn_fa_kernel, dim3(grid), dim3(kThreads), kFaSmemBytes, st, p.tmQKV, a);
