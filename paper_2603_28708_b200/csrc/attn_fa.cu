@@ -84,6 +84,27 @@ __device__ __forceinline__ void umma_f16_ts_fa(uint32_t d_tmem, uint32_t a_tmem,
       : "memory");
 }
 
+// MMA-thread wait without the try_wait suspend: the issuer wakes as soon as the softmax
+// arrives (it is one thread; its polling costs one issue slot per iteration)
+__device__ __forceinline__ void mbar_wait_spin(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = smem_u32(bar);
+  uint32_t ok = 0;
+  const long long t0 = clock64();
+  while (!ok) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(addr), "r"(parity)
+        : "memory");
+    if (!ok && clock64() - t0 > (1ll << 31)) {
+      printf("prlab_gpu watchdog: mbarrier spin timeout block %d thread %d\n", blockIdx.x, threadIdx.x);
+      __trap();
+    }
+  }
+}
+
 __device__ __forceinline__ float fmax3_fa(float a, float b, float c) {
   float d;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
@@ -189,7 +210,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fa_kernel(const __grid_const
           const uint32_t s = kc & 1, ph = (kc >> 1) & 1;
           // O (+)= P~ . V once the softmax packed P and rescaled O; the unit's first P.V
           // overwrites O, so the previous unit's epilogue must have read it
-          mbar_wait(&bars[F_PREADY], bc & 1);
+          mbar_wait_spin(&bars[F_PREADY], bc & 1);
           long long* ms = (a.dbg && blockIdx.x == 0 && bc < 32) ? a.dbg + bc * 8 : nullptr;
           if (ms) ms[4] = clock64();
           if (kb + 1 < nkb) issue_s(q0, kc + 1, kb + 2 == nkb, qs);
