@@ -1,17 +1,23 @@
 #!/usr/bin/env python3
 """Benchmark of the B200-native prlab forward (BASELINE.json metric).
 
-Default workload (N=1, configs[1]): GPT-2 124M, hybrid precision, batch 1,
-seq 128, causal -- one "step" is one full forward (embedding -> 12 blocks ->
-final LN -> tied LM head, logits [1,128,50257] fp16-lattice) on device.
-`--workload c4` runs configs[3] (GPT-2 batch 32, seq 512) instead.
-Multi-GPU (torchrun, N>1): every rank runs an independent replica of the same
-workload on its own GPU (replicas only: the forward has no exchange step);
-value = sequences processed by all ranks / max-over-ranks device time.
+One GPU (default, configs[1]): C2 -- GPT-2 124M, hybrid precision, batch 1, seq 128,
+causal; one "step" is one full forward (embedding -> 12 blocks -> final LN -> tied LM
+head, logits [1,128,50257] fp16-lattice) on device.  The line also carries
+`c4_single_gpu`: the C4 replica step timed on this one GPU (the N=1 point of the
+scaling run).
+Several GPUs (torchrun, WORLD_SIZE > 1, configs[3]): C4 -- GPT-2 batch 32, seq 512 per
+replica, batch-sharded independent replicas (replicas only: the forward has no exchange
+step, src/model.cpp:397); the step is the forward with the tied head's log-softmax fused
+into its GEMM (per-row NLL + argmax; the 1.65 GB logits never written).  `--strong`
+shards a fixed global batch of 32 instead.  value = sequences processed by all ranks /
+max-over-ranks device time (paper_2603_28708_b200/replicas.py).
 
-Prints ONE JSON line on rank 0.  `--impl reference` times the reference's own
-CPU implementation (oracle/_ref/libprlab_ref.so, compiled from the unmodified
-reference sources) on the host cores instead.
+Prints ONE JSON line on rank 0.  `--impl reference` times the reference's own CPU
+implementation (oracle/_ref/libprlab_ref.so, compiled from the unmodified reference
+sources; the Model is built once by the reference's build_model, only prlab::forward is
+timed) on the host cores instead: all-core throughput as `value`, plus the single-thread
+p50 of the reference's own benchmark_forward (1 warm-up + 5 measured).
 """
 from __future__ import annotations
 
@@ -125,26 +131,43 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def model_desc(name):
-    import paper_2603_28708_b200 as pg
-    return pg.ModelConfig.preset(name)
-
-
 # ---------------------------------------------------------------------------
-# CPU reference (oracle/_ref = the unmodified reference sources, compiled here)
+# CPU reference (oracle/_ref = the unmodified reference sources, compiled here).
+# The reference Model is built ONCE by the reference's own build_model (seed 0),
+# outside the timed region; only prlab::forward is timed (src/bench.cpp:47-106).
+# Nothing here imports the product package.
 # ---------------------------------------------------------------------------
-def cpu_reference_run(cfg, params, S, policy, threads, n_seq, seed):
-    """n_seq independent batch-1 sequences over `threads` host threads through
-    the reference's prlab::forward; returns (wall seconds, sequences)."""
-    from oracle.oracle import ModelConfig as OC, Reference
+def ref_session(preset):
+    from oracle.oracle import PRESETS, Reference
     ref = Reference()
-    oc = OC(**cfg.__dict__)
-    import paper_2603_28708_b200 as pg
-    ids = pg.random_tokens(cfg.vocab, n_seq, S, seed)
-    width = cfg.vocab
-    t0 = time.perf_counter()
-    ref.forward(oc, params, ids, n_seq, S, policy, threads=threads)
-    return time.perf_counter() - t0, n_seq, width
+    oc = PRESETS[preset]
+    return ref, oc, ref.model_build(oc)
+
+
+def cpu_throughput(ref, oc, handle, S, policy, threads, seed):
+    """`threads` independent batch-1 seq-S forwards, one per host thread, over the prebuilt
+    reference Model; returns (seconds of the forwards only, sequences)."""
+    ids = ref.random_tokens(oc.vocab, threads, S, seed)
+    sec, _ = ref.forward_threads(handle, ids, threads, S, policy, threads)
+    return sec, threads
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model_name():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 def run_reference_arm(args, wl):
@@ -156,34 +179,43 @@ def run_reference_arm(args, wl):
     if not os.path.exists(REF_SO):
         print(json.dumps({"impl": "reference", "unavailable": f"{REF_SO} not built"}))
         return
-    import paper_2603_28708_b200 as pg
-    cfg = pg.ModelConfig.preset(preset)
-    params = pg.build_model(cfg)
-    ncores = os.cpu_count() or 1
-    threads = max(1, min(ncores, 32))
-    # bounded sample: each step runs `threads` batch-1 sequences concurrently
+    ref, oc, handle = ref_session(preset)
+    threads = max(1, min(host_cores(), 64))
+    # throughput: each step = `threads` concurrent batch-1 forwards (all host cores)
     steps = max(1, min(args.steps, 2))
     warm = 1 if args.warmup > 0 else 0
-    for _ in range(warm):
-        cpu_reference_run(cfg, params, S, policy, threads, threads, 7)
+    for i in range(warm):
+        cpu_throughput(ref, oc, handle, S, policy, threads, 7 + i)
     walls = []
     for i in range(steps):
-        w, n, _ = cpu_reference_run(cfg, params, S, policy, threads, threads, 100 + i)
+        w, _ = cpu_throughput(ref, oc, handle, S, policy, threads, 100 + i)
         walls.append(w)
     total = sum(walls)
     value = steps * threads / total
+    # latency: the reference's own benchmark_forward, one thread, 1 warm-up + 5 measured
+    # (src/bench.cpp:47-106 nearest-rank p50)
+    lat = None
+    if not args.no_cpu_latency:
+        ids1 = ref.random_tokens(oc.vocab, 1, S, 1234)
+        lat = ref.benchmark_forward(handle, ids1, 1, S, policy, 1, 5)
+    ref.model_free(handle)
     line = {
         "impl": "reference",
         "metric": f"sequences/sec ({desc})",
         "value": value, "unit": "seq/s", "n_gpus": args.gpus, "steps": steps, "warmup": warm,
-        "ms_per_step": 1000 * total / steps, "p50_latency_ms": 1000 * nearest_rank(walls, 0.5),
+        "ms_per_step": 1000 * total / steps,
+        "p50_latency_ms": 1000 * lat["p50_s"] if lat else None,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "f32 storage (binary16 emulated)", "data": "synthetic",
+        "dtype": "f32 storage (binary16 emulated)", "data": "synthetic: reference build_model(seed 0), random_tokens",
         "config": {"workload": desc, "model": preset, "global_batch": B, "seq_len": S,
-                   "parallelism": "host threads"},
+                   "parallelism": f"{threads} host threads", "policy": policy},
         "cpu_baseline": {"value": value, "unit": "seq/s", "cores": threads, "kind": "reference",
-                         "sample": f"{steps} steps x {threads} concurrent batch-1 seq{S} "
-                                   f"{policy} forwards (reference prlab::forward, 1 per thread)"},
+                         "cpu": cpu_model_name(),
+                         "sample": f"{steps} steps x {threads} concurrent batch-1 seq{S} {policy} forwards "
+                                   f"(reference prlab::forward on a Model built once, 1 per thread)",
+                         "latency_p50_ms_1thread": 1000 * lat["p50_s"] if lat else None,
+                         "latency_protocol": "prlab::benchmark_forward, 1 warm-up + 5 measured, 1 thread"
+                         if lat else None},
         "e2e": {"value": value, "unit": "seq/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -264,176 +296,242 @@ def kernel_profile(pg, torch, cfg, B, S, stream, reps=20, causal=1, model=None, 
 
 def ncu_traffic(wl, kernel):
     """dram__bytes_read.sum + dram__bytes_write.sum per launch of `kernel` at workload `wl`
-    (committed ncu capture summary), or None."""
-    path = os.path.join(ROOT, "profiles", "r01", "traffic.json")
-    try:
-        with open(path) as f:
-            t = json.load(f)
-        e = t[wl][kernel]
-        return {"dram_bytes": float(e["dram_bytes"]), "source": f"profiles/r01/traffic.json ({e['kernel']})"}
-    except Exception:
+    (committed ncu capture summary, latest round first), or None."""
+    for rnd in ("r02", "r01"):
+        path = os.path.join(ROOT, "profiles", rnd, "traffic.json")
+        try:
+            with open(path) as f:
+                t = json.load(f)
+            e = t[wl][kernel]
+            return {"dram_bytes": float(e["dram_bytes"]),
+                    "source": f"profiles/{rnd}/traffic.json ({e['kernel']})"}
+        except Exception:
+            continue
+    return None
+
+
+def roofline_of(prof, pk, wl):
+    if not prof:
         return None
+    dom = max(prof, key=lambda k: prof[k]["share_us"])
+    d = prof[dom]
+    t = d["us"] * 1e-6
+    ai = d["flops"] / d["bytes"]
+    ridge = pk["tflops"] * 1e12 / (pk["hbm_gbs"] * 1e9)
+    if ai < ridge:
+        ach = d["bytes"] / t / 1e9
+        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"],
+                "unit": "GB/s", "frac": ach / pk["hbm_gbs"], "traffic": None,
+                "algorithmic_bytes": d["bytes"], "launch_us": d["us"]}
+    else:
+        ach = d["flops"] / t / 1e12
+        roof = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": pk["tflops"],
+                "unit": "TFLOP/s", "frac": ach / pk["tflops"], "traffic": None,
+                "algorithmic_flops": d["flops"], "launch_us": d["us"]}
+    roof["peak_source"] = pk["source"]
+    # DRAM bytes per launch of the same kernel from one `ncu --set full` capture of this
+    # workload (scripts/gpu_ncu_full.sh -> scripts/ncu_traffic.py -> profiles/rNN/traffic.json)
+    tr = ncu_traffic(wl, dom)
+    if tr is not None:
+        roof["traffic"] = tr["dram_bytes"]
+        roof["traffic_source"] = tr["source"]
+        roof["traffic_over_algorithmic"] = tr["dram_bytes"] / d["bytes"]
+    roof["breakdown_us_per_forward"] = {k: round(v["share_us"], 2) for k, v in prof.items()}
+    return roof
+
+
+class DeviceWorkload:
+    """One replica's step on its GPU: a full forward of `count` sequences with ids resident
+    in HBM (device-timed `value`), plus the end-to-end drop-in call with host buffers."""
+
+    def __init__(self, args, wl, env, count, seed):
+        import torch
+        import paper_2603_28708_b200 as pg
+        self.torch, self.pg = torch, pg
+        preset, _, S, policy, desc = WORKLOADS[wl]
+        self.cfg = cfg = pg.ModelConfig.preset(preset)
+        self.params = pg.build_model(cfg)  # reference build_model stream (seed 0)
+        self.model = pg.DeviceModel(cfg, self.params, device=env.local)
+        self.B, self.S, self.policy, self.wl = count, S, policy, wl
+        V, M = cfg.vocab, count * S
+        self.ld = (V + 7) // 8 * 8
+        self.ids = pg.random_tokens(cfg.vocab, count, S, seed)
+        self.d_ids = torch.from_numpy(self.ids).cuda()
+        self.stream = torch.cuda.current_stream()
+        self.sp = self.stream.cuda_stream
+        # C4-sized logits (1.65 GB fp16) stay in the library workspace: the forward's head
+        # epilogue reduces them to the per-row NLL / argmax (the step's result)
+        self.nll_mode = M * V > 200_000_000
+        if self.nll_mode:
+            self.d_tg = torch.from_numpy(np.roll(self.ids, -1).astype(np.int32)).cuda()
+            self.d_nll = torch.empty(M, dtype=torch.float64, device="cuda")
+            self.d_am = torch.empty(M, dtype=torch.int32, device="cuda")
+        else:
+            self.out16 = torch.empty(M, self.ld, dtype=torch.float16, device="cuda")
+
+    def step(self):
+        m, B, S, pol = self.model, self.B, self.S, self.policy
+        if self.nll_mode:
+            m.forward_nll_device(self.d_ids.data_ptr(), self.d_tg.data_ptr(), B, S, pol,
+                                 self.d_nll.data_ptr(), self.d_am.data_ptr(), self.sp)
+        else:
+            m.forward_device(self.d_ids.data_ptr(), B, S, pol, self.out16.data_ptr(),
+                             self.pg.OUT_F16, self.ld, self.sp, True)
+
+    def kernels_per_step(self):
+        return self.model.kernel_count(self.B, self.S, self.policy) + (1 if self.nll_mode else 0)
+
+    def e2e(self, args, timer_dist, world):
+        """The public API a user calls, host buffers, copies inside the timed region."""
+        pg, B, S, pol, cfg = self.pg, self.B, self.S, self.policy, self.cfg
+        torch = self.torch
+        M, V = B * S, cfg.vocab
+        h_ids = torch.from_numpy(self.ids).pin_memory()
+        ids_np = h_ids.numpy()
+        if self.nll_mode:
+            # forward + fused next-token NLL / argmax; ids H2D, (nll, argmax) D2H per step
+            h_tg = torch.from_numpy(np.roll(self.ids, -1).astype(np.int32)).pin_memory()
+            h_nll = torch.empty(M, dtype=torch.float64).pin_memory()
+            h_am = torch.empty(M, dtype=torch.int32).pin_memory()
+
+            def call():
+                self.d_ids.copy_(h_ids, non_blocking=True)
+                self.d_tg.copy_(h_tg, non_blocking=True)
+                self.step()
+                h_nll.copy_(self.d_nll, non_blocking=True)
+                h_am.copy_(self.d_am, non_blocking=True)
+                self.stream.synchronize()
+            h2d, d2h = ids_np.nbytes + h_tg.numel() * 4, M * 12
+            api = ("prlab_gpu_forward_nll_device: host ids/targets -> host per-row NLL (f64) + argmax "
+                   "(i32), pinned, copies in the timed region")
+        else:
+            h_logits = torch.empty((B, S, V), dtype=torch.float32).pin_memory()
+            log_np = h_logits.numpy()
+
+            def call():
+                _fwd_into(pg, self.model, ids_np, B, S, pol, log_np)
+            h2d, d2h = ids_np.nbytes, None
+            api = "prlab_gpu_forward (host int32 ids -> host fp32 logits, pinned buffers)"
+        for _ in range(max(1, args.warmup)):
+            call()
+        n = max(3, min(args.steps, 20))
+        if timer_dist is not None:
+            timer_dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(n):
+            call()
+        el = time.perf_counter() - t0
+        from paper_2603_28708_b200 import replicas
+        el = replicas.max_over_ranks(el, timer_dist, "cuda" if timer_dist is not None else None)
+        gb = replicas.sum_over_ranks(B, timer_dist, "cuda" if timer_dist is not None else None)
+        if d2h is None:
+            # under hybrid the library may move the (round16'd) logits as fp16 rows and widen them
+            # to fp32 on host threads (host_widen.cpp; chosen by timing on the first call)
+            widened = self.model.host_copy_mode(B, S, pol) == 1
+            d2h = int(log_np.nbytes // 2 if widened else log_np.nbytes)
+            if widened:
+                api += "; logits cross PCIe as fp16 rows, widened exactly on host"
+        return {"value": gb * n / el, "unit": "seq/s", "h2d_bytes_per_step": int(h2d),
+                "d2h_bytes_per_step": int(d2h), "ms_per_step": 1000 * el / n, "api": api}
 
 
 def run_ours(args, wl):
+    from paper_2603_28708_b200 import replicas
+    env = replicas.ReplicaEnv.from_env()
+    if args.stub_device:
+        return run_stub(args, wl, env)
     import torch
     import paper_2603_28708_b200 as pg
 
-    rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
+    torch.cuda.set_device(env.local)
     dist = None
-    if world > 1:
+    if env.world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        dist.init_process_group("nccl", device_id=torch.device("cuda", env.local))
 
     preset, B, S, policy, desc = WORKLOADS[wl]
-    cfg = pg.ModelConfig.preset(preset)
-    params = pg.build_model(cfg)  # reference build_model stream (seed 0)
-    model = pg.DeviceModel(cfg, params, device=local)
-    V, M = cfg.vocab, B * S
-    ld = (V + 7) // 8 * 8
-    ids = pg.random_tokens(cfg.vocab, B, S, 1234 + rank)
-    d_ids = torch.from_numpy(ids).cuda()
-    out16 = torch.empty(M, ld, dtype=torch.float16, device="cuda")
-    stream = torch.cuda.current_stream()
-    sp = stream.cuda_stream
-
-    def step():
-        model.forward_device(d_ids.data_ptr(), B, S, policy, out16.data_ptr(), pg.OUT_F16, ld, sp,
-                             True)
-
-    for _ in range(max(3, args.warmup)):
-        step()
-    model.sync_status(sp)
-    kpf = model.kernel_count(B, S, policy)
-
-    def barrier():
-        if dist is not None:
-            dist.barrier()
-        torch.cuda.synchronize()
-
-    # ---- timed region: device-resident inputs; weights (0.25 GB) exceed L2 ----
-    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    start, count = replicas.rank_batch(B, env.world, env.rank, args.strong)
+    w = DeviceWorkload(args, wl, env, count, replicas.replica_token_seed(1234, env.rank))
+    w.step()
+    w.model.sync_status(w.sp)
+    kpf = w.kernels_per_step()
+    timer = replicas.CudaEventTimer(torch, w.stream)
 
     def busy():
         for _ in range(8):
-            step()
+            w.step()
         torch.cuda.synchronize()
 
-    with ClockSampler(local) as clk:
+    # ---- timed region: device-resident inputs; weights (0.25 GB) exceed L2 ----
+    with ClockSampler(env.local) as clk:
         # the sampler brackets the timed region: >= 2 samples under load before it and
         # one after it (a short timed region can fall between two 100 ms samples)
-        clk.wait_samples(2, busy=busy)
-        barrier()
-        evs[0].record(stream)
-        for i in range(args.steps):
-            step()
-            evs[i + 1].record(stream)
-        torch.cuda.synchronize()
-        barrier()
+        per_step, mine_ms, total_ms = replicas.timed_steps(
+            w.step, args.steps, max(3, args.warmup), timer, dist, "cuda",
+            before_timed=lambda: clk.wait_samples(2, busy=busy))
         clk.wait_samples(1, busy=busy)
-    per_step = [evs[i].elapsed_time(evs[i + 1]) for i in range(args.steps)]
-    total_ms = evs[0].elapsed_time(evs[-1])
-    model.sync_status(sp)
-    if dist is not None:
-        t = torch.tensor([total_ms], device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms = float(t.item())
-    value = world * B * args.steps / (total_ms / 1000.0)
+    w.model.sync_status(w.sp)
+    global_batch = int(replicas.sum_over_ranks(count, dist, "cuda"))
+    value = global_batch * args.steps / (total_ms / 1000.0)
 
-    # ---- e2e: the drop-in C-ABI call with HOST buffers (prlab_gpu_forward) ----
-    e2e = None
-    if not args.no_e2e:
-        h_ids = torch.from_numpy(ids).pin_memory()
-        h_logits = torch.empty((B, S, V), dtype=torch.float32).pin_memory()
-        ids_np, log_np = h_ids.numpy(), h_logits.numpy()
-        for _ in range(max(1, args.warmup)):  # warm the host-path graph and copy-out (W calls)
-            _fwd_into(pg, model, ids_np, B, S, policy, log_np)
-        e2e_steps = max(3, min(args.steps, 20 if M * V < 50_000_000 else 5))
-        barrier()
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            _fwd_into(pg, model, ids_np, B, S, policy, log_np)
-        t1 = time.perf_counter()
-        el = t1 - t0
-        if dist is not None:
-            t = torch.tensor([el], device="cuda")
-            dist.all_reduce(t, op=dist.ReduceOp.MAX)
-            el = float(t.item())
-        # under hybrid the library may move the (round16'd) logits as fp16 rows and widen them
-        # to fp32 on host threads (host_widen.cpp; chosen by timing on the first call): the
-        # PCIe bytes are then half the fp32 result
-        widened = model.host_copy_mode(B, S, policy) == 1
-        e2e = {"value": world * B * e2e_steps / el, "unit": "seq/s",
-               "h2d_bytes_per_step": int(ids_np.nbytes),
-               "d2h_bytes_per_step": int(log_np.nbytes // 2 if widened else log_np.nbytes),
-               "ms_per_step": 1000 * el / e2e_steps,
-               "api": "prlab_gpu_forward (host int32 ids -> host fp32 logits, pinned buffers)"
-                      + ("; logits cross PCIe as fp16 rows, widened exactly on host" if widened else "")}
+    e2e = None if args.no_e2e else w.e2e(args, dist, env.world)
 
-    # ---- roofline of the dominant kernel (standalone CUDA-event timing) ----
     pk = peaks()
-    prof = (kernel_profile(pg, torch, cfg, B, S, sp, causal=int(cfg.archetype == 1), model=model,
-                           d_ids=d_ids, policy=policy)
-            if not args.no_profile else {})
-    roof = None
-    if prof:
-        dom = max(prof, key=lambda k: prof[k]["share_us"])
-        d = prof[dom]
-        t = d["us"] * 1e-6
-        ai = d["flops"] / d["bytes"]
-        ridge = pk["tflops"] * 1e12 / (pk["hbm_gbs"] * 1e9)
-        if ai < ridge:
-            ach = d["bytes"] / t / 1e9
-            roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"],
-                    "unit": "GB/s", "frac": ach / pk["hbm_gbs"], "traffic": None,
-                    "algorithmic_bytes": d["bytes"], "launch_us": d["us"]}
-        else:
-            ach = d["flops"] / t / 1e12
-            roof = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": pk["tflops"],
-                    "unit": "TFLOP/s", "frac": ach / pk["tflops"], "traffic": None,
-                    "algorithmic_flops": d["flops"], "launch_us": d["us"]}
-        roof["peak_source"] = pk["source"]
-        # DRAM bytes per launch of the same kernel from one `ncu --set full` capture of this
-        # workload (scripts/gpu_ncu_full.sh -> scripts/ncu_traffic.py -> profiles/r01/traffic.json)
-        tr = ncu_traffic(wl, dom)
-        if tr is not None:
-            roof["traffic"] = tr["dram_bytes"]
-            roof["traffic_source"] = tr["source"]
-            roof["traffic_over_algorithmic"] = tr["dram_bytes"] / d["bytes"]
-        roof["breakdown_us_per_forward"] = {k: round(v["share_us"], 2) for k, v in prof.items()}
+    prof, roof, cpu, c4ref = {}, None, None, None
+    if env.rank == 0 and not args.no_profile:
+        prof = kernel_profile(pg, torch, w.cfg, count, S, w.sp, causal=int(w.cfg.archetype == 1),
+                              model=w.model, d_ids=w.d_ids, policy=policy)
+        roof = roofline_of(prof, pk, wl)
 
     # ---- CPU baseline: the reference on this host (rank 0, N=1 only) ----
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if env.rank == 0 and env.world == 1 and not args.no_cpu_baseline:
         try:
             from oracle.oracle import REF_SO
             if os.path.exists(REF_SO):
-                threads = max(1, min(os.cpu_count() or 1, 32))
-                wall, n, _ = cpu_reference_run(cfg, params, S, policy, threads, threads, 77)
+                threads = max(1, min(host_cores(), 64))
+                ref, oc, handle = ref_session(preset)
+                wall, n = cpu_throughput(ref, oc, handle, S, policy, threads, 77)
+                ref.model_free(handle)
                 cpu = {"value": n / wall, "unit": "seq/s", "cores": threads, "kind": "reference",
-                       "sample": f"{threads} concurrent batch-1 seq{S} {policy} forwards "
-                                 f"(one per thread) through the reference prlab::forward",
+                       "cpu": cpu_model_name(),
+                       "sample": f"{threads} concurrent batch-1 seq{S} {policy} forwards (one per thread) "
+                                 f"through the reference prlab::forward on a Model built once "
+                                 f"(forwards only timed)",
                        "latency_ms_per_seq": 1000 * wall}
         except Exception as e:  # reported, never silently replaced
             cpu = {"error": str(e)}
 
-    flops = pg.flop_count(cfg, B, S)["total"]
+    # ---- the replica workload (C4) on this one GPU, so the scaling run has its N=1 point ----
+    if env.world == 1 and wl == "c2" and not args.no_c4_ref:
+        del w
+        torch.cuda.synchronize()
+        w4 = DeviceWorkload(args, "c4", env, WORKLOADS["c4"][1], 1234)
+        n4 = max(3, min(args.steps, 10))
+        per4, _, tot4 = replicas.timed_steps(w4.step, n4, 3, replicas.CudaEventTimer(torch, w4.stream))
+        w4.model.sync_status(w4.sp)
+        c4ref = {"workload": WORKLOADS["c4"][4], "value": WORKLOADS["c4"][1] * n4 / (tot4 / 1000.0),
+                 "unit": "seq/s", "ms_per_step": tot4 / n4, "steps": n4,
+                 "note": "same step as `bench.py --gpus N` runs per replica for N > 1 (forward + fused "
+                         "next-token NLL/argmax head)"}
+        del w4
+
+    flops = pg.flop_count(pg.ModelConfig.preset(preset), 1, S)["total"]
     line = {
         "metric": f"sequences/sec ({desc})",
-        "value": value, "unit": "seq/s", "n_gpus": world, "steps": args.steps,
+        "value": value, "unit": "seq/s", "n_gpus": env.world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": total_ms / args.steps,
         "p50_latency_ms": nearest_rank(per_step, 0.5), "p95_latency_ms": nearest_rank(per_step, 0.95),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": True, "scaling": "strong" if args.strong else "weak", "vs_baseline": None,
         "dtype": "f16 operands / f32 accumulate (hybrid: fp32 LN, softmax, residual)",
         "data": "synthetic: reference build_model(seed 0) weights, random_tokens ids",
-        "config": {"workload": desc, "model": preset, "global_batch": world * B, "seq_len": S,
-                   "parallelism": f"replicas x{world} (no collective)", "policy": policy,
+        "config": {"workload": desc, "model": preset, "global_batch": global_batch, "seq_len": S,
+                   "per_replica_batch": count,
+                   "parallelism": f"replicas x{env.world} (batch-sharded, no collective)", "policy": policy,
                    "l2": "working set > L2 (0.25 GB fp16 weights streamed per step)",
-                   "graph": "one CUDA graph per forward"},
-        "model_tflops_per_s": flops * value / B / 1e12,
+                   "graph": "one CUDA graph per forward",
+                   "step": "forward + fused NLL/argmax head (logits never written)" if w_nll(wl)
+                   else "forward, fp16 logits in HBM"},
+        "model_tflops_per_s": flops * value / 1e12,
         "gpu_launches": kpf * args.steps,
         "kernels_per_step": kpf,
         "clocks": clk.summary(),
@@ -441,7 +539,50 @@ def run_ours(args, wl):
         "cpu_baseline": cpu,
         "e2e": e2e,
     }
-    if rank == 0:
+    if c4ref is not None:
+        line["c4_single_gpu"] = c4ref
+    if env.rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def w_nll(wl):
+    preset, B, S, _, _ = WORKLOADS[wl]
+    V = {"gpt2_small": 50257, "bert_base": 30522}[preset]
+    return B * S * V > 200_000_000
+
+
+def run_stub(args, wl, env):
+    """CPU stand-in for the device step (tests/test_replicas_gloo.py): the same replica
+    plumbing as run_ours -- gloo process group, rank_batch, timed_steps with a barrier on
+    both sides, max-over-ranks time, whole-job sequences -- around a numpy matmul."""
+    import torch.distributed as dist
+    from paper_2603_28708_b200 import replicas
+    if env.world > 1:
+        dist.init_process_group("gloo")
+    else:
+        dist = None
+    preset, B, S, policy, desc = WORKLOADS[wl]
+    start, count = replicas.rank_batch(B, env.world, env.rank, args.strong)
+    a = np.ones((64, 64), np.float32)
+    delay = 0.002 * (1 + env.rank)  # rank 1 is the slow one: the max must win
+
+    def step():
+        for _ in range(count):
+            a @ a
+        time.sleep(delay)
+
+    per, mine, total = replicas.timed_steps(step, args.steps, max(3, args.warmup), replicas.WallTimer(), dist)
+    gb = int(replicas.sum_over_ranks(count, dist))
+    line = {"metric": f"sequences/sec ({desc})", "value": gb * args.steps / (total / 1000.0), "unit": "seq/s",
+            "n_gpus": env.world, "steps": args.steps, "ms_per_step": total / args.steps,
+            "rank_ms": mine, "scaling": "strong" if args.strong else "weak",
+            "config": {"workload": desc, "global_batch": gb, "per_replica_batch": count, "seq_len": S,
+                       "shard_start": start},
+            "stub_device": True}
+    if env.rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
         dist.barrier()
@@ -461,15 +602,24 @@ def main():
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="c2")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default=None,
+                    help="default: c2 (configs[1]) on one GPU, c4 (configs[3], batch-sharded "
+                         "replicas) when WORLD_SIZE > 1")
+    ap.add_argument("--strong", action="store_true",
+                    help="strong scaling: the workload's batch is the GLOBAL batch, sharded over ranks")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cpu-latency", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-profile", action="store_true")
+    ap.add_argument("--no-c4-ref", action="store_true")
+    ap.add_argument("--stub-device", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    wl = args.workload or ("c4" if world > 1 else "c2")
     if args.impl == "reference":
-        run_reference_arm(args, args.workload)
+        run_reference_arm(args, wl)
     else:
-        run_ours(args, args.workload)
+        run_ours(args, wl)
 
 
 if __name__ == "__main__":

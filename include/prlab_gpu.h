@@ -9,6 +9,13 @@
  * include/prlab_gpu.hpp wraps this ABI back into the reference's C++ signatures
  * (same names, same exception types and messages).
  *
+ * Threading / streams: a model may be used from several host threads (calls on one model
+ * are serialised by its mutex) and from several CUDA streams: every call orders its work
+ * after the previous call's work on the same model (event wait when the stream differs),
+ * because all calls share the model's workspace.  Calls on distinct models run
+ * concurrently.  A stream that is being captured by the CALLER is not ordered (the
+ * caller's graph defines the order).
+ *
  * Errors: every function returns PRLAB_OK (0) or a status; the thread-local
  * message is available from prlab_gpu_last_error().  The status maps onto the
  * reference's exception types: PRLAB_EINVAL -> std::invalid_argument,
@@ -205,9 +212,12 @@ int prlab_gpu_forward_nll_device(prlab_gpu_model* m, const int32_t* d_ids, const
                                  int32_t* d_argmax, void* stream, int32_t* fused);
 /* Synchronizes the stream and reports deferred device-side errors (bad ids). */
 int prlab_gpu_sync_status(prlab_gpu_model* m, void* stream);
-/* Number of kernels one forward_device launch issues for this key (for bench accounting). */
+/* Number of kernels one forward_device launch with FP16 logits issues for this key (for
+ * bench accounting); _ex counts for either logits dtype (fp32 adds the widening kernel). */
 int prlab_gpu_forward_kernel_count(prlab_gpu_model* m, int64_t batch, int64_t seq,
                                    const prlab_policy* policy, int64_t* count);
+int prlab_gpu_forward_kernel_count_ex(prlab_gpu_model* m, int64_t batch, int64_t seq,
+                                      const prlab_policy* policy, int32_t out_dtype, int64_t* count);
 
 /* How prlab_gpu_forward moves this key's logits to the host (after its first call):
  * 0 = not decided yet, 1 = fp16 rows widened exactly on host threads (hybrid: the
@@ -262,6 +272,11 @@ int prlab_gpu_attention_f16_device_dbg(const void* qkv, void* ctx, int64_t batch
 /* Debug: GEMM launches after this call write %globaltimer phase stamps ([grid][8] int64,
  * device memory) into dbg (NULL switches the stamps off). */
 int prlab_gpu_debug_gemm_stamps(long long* dbg);
+/* Debug / parity: the hybrid hot path's embedding gather alone (embed(), src/kernels.cpp:256-294),
+ * d_out fp32 [B*S, h] on the device.  path 0 = the multi-kernel path's gather kernel
+ * (embed_f32_kernel), path 1 = stage 0 of the batch-1 persistent kernel (fwd_small).  Async. */
+int prlab_gpu_debug_embedding_device(prlab_gpu_model* m, const int32_t* d_ids, int64_t batch, int64_t seq,
+                                     int32_t path, float* d_out, void* stream);
 /* Debug: per-stage %globaltimer stamps of the batch-1 persistent forward, [stage][grid][2]. */
 int prlab_gpu_debug_small_stamps(long long* dbg);
 

@@ -403,6 +403,53 @@ class Reference:
             raise (IndexError if rc == -2 else ValueError)(msg)
         return (logits, calls.reshape(7, 2)) if want_calls else logits
 
+    # ---- prebuilt reference Model (built once, outside any timed region) ----
+    def model_build(self, c: ModelConfig):
+        """prlab::build_model(config) held on the C++ side (src/model.cpp:217-265); returns a handle."""
+        L = self.lib
+        L.ref_model_build.restype = C.c_void_p
+        L.ref_model_build.argtypes = [C.c_int] + [C.c_int64] * 6 + [C.c_uint64]
+        h = L.ref_model_build(*self._c(c), c.seed)
+        if not h:
+            raise ValueError(L.ref_last_error().decode())
+        return h
+
+    def model_free(self, h):
+        self.lib.ref_model_free.argtypes = [C.c_void_p]
+        self.lib.ref_model_free(h)
+
+    def benchmark_forward(self, h, ids, batch, seq, policy, warmup, measure):
+        """The reference's own prlab::benchmark_forward (src/bench.cpp:47-106), single thread:
+        dict(mean_s, p50_s, p95_s, throughput_sps, samples_s)."""
+        L = self.lib
+        L.ref_benchmark_forward.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.c_int64, C.c_int64,
+                                            C.c_char_p, C.c_int64, C.c_int64, C.POINTER(C.c_double),
+                                            C.POINTER(C.c_double)]
+        out = np.zeros(4, dtype=np.float64)
+        smp = np.zeros(max(1, measure), dtype=np.float64)
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        if L.ref_benchmark_forward(h, _ip(ids), batch, seq, policy.encode(), warmup, measure,
+                                   out.ctypes.data_as(C.POINTER(C.c_double)),
+                                   smp.ctypes.data_as(C.POINTER(C.c_double))):
+            raise ValueError(L.ref_last_error().decode())
+        return {"mean_s": out[0], "p50_s": out[1], "p95_s": out[2], "throughput_sps": out[3],
+                "samples_s": smp.tolist()}
+
+    def forward_threads(self, h, ids, batch, seq, policy, threads, want_logits=False, width=None):
+        """`batch` independent batch-1 prlab::forward calls on `threads` host threads over the
+        prebuilt Model; returns (seconds of the forwards only, logits or None)."""
+        L = self.lib
+        L.ref_forward_threads.argtypes = [C.c_void_p, C.POINTER(C.c_int32), C.c_int64, C.c_int64,
+                                          C.c_char_p, C.c_int, C.POINTER(C.c_float),
+                                          C.POINTER(C.c_double)]
+        ids = np.ascontiguousarray(ids, dtype=np.int32)
+        logits = np.empty((batch, seq, width), dtype=np.float32) if want_logits else None
+        sec = C.c_double(0.0)
+        if L.ref_forward_threads(h, _ip(ids), batch, seq, policy.encode(), threads, _fp(logits),
+                                 C.byref(sec)):
+            raise ValueError(L.ref_last_error().decode())
+        return sec.value, logits
+
     def forward_scores(self, c: ModelConfig, params, ids, batch, seq, policy):
         """prlab::forward(..., retain_scores=true): (logits, [L,B,H,S,S] fp32 taps)."""
         L = self.lib

@@ -15,8 +15,13 @@
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <atomic>
+#include <algorithm>
 #include <vector>
 
+#include <chrono>
+
+#include "prlab/bench.hpp"
 #include "prlab/fidelity.hpp"
 #include "prlab/float16.hpp"
 #include "prlab/kernels.hpp"
@@ -159,6 +164,93 @@ int ref_forward(int archetype, int64_t L, int64_t h, int64_t H, int64_t f, int64
     return fail(e, -2);
   } catch (const std::exception& e) {
     return fail(e, -3);
+  }
+}
+
+// ---- model handle: the reference Model built ONCE (prlab::build_model, src/model.cpp:217-265)
+// outside any timed region, as src/bench.cpp:47-106 run_benchmark / benchmark_forward expect.
+void* ref_model_build(int archetype, int64_t L, int64_t h, int64_t H, int64_t f, int64_t V, int64_t P,
+                      uint64_t seed) {
+  try {
+    return new prlab::Model(prlab::build_model(make_cfg(archetype, L, h, H, f, V, P, seed)));
+  } catch (const std::exception& e) {
+    fail(e, -1);
+    return nullptr;
+  }
+}
+
+void ref_model_free(void* m) { delete static_cast<prlab::Model*>(m); }
+
+// The reference's own benchmark of one forward configuration: prlab::benchmark_forward
+// (src/bench.cpp:102-106 -> run_benchmark :47-100) with BenchProtocol{warmup, measure},
+// single-threaded.  out: mean_s, p50_s, p95_s, throughput_sps; samples: measure doubles.
+int ref_benchmark_forward(void* m, const int32_t* ids, int64_t B, int64_t S, const char* policy,
+                          int64_t warmup, int64_t measure, double* out, double* samples) {
+  try {
+    prlab::TokenBatch tb;
+    tb.batch = B;
+    tb.seq = S;
+    tb.ids.assign(ids, ids + B * S);
+    prlab::BenchProtocol proto;
+    proto.warmup_iters = warmup;
+    proto.measure_iters = measure;
+    const prlab::BenchStats st =
+        prlab::benchmark_forward(*static_cast<prlab::Model*>(m), tb, prlab::resolve_policy(policy), proto);
+    out[0] = st.mean_s;
+    out[1] = st.p50_s;
+    out[2] = st.p95_s;
+    out[3] = st.throughput_sps;
+    for (size_t i = 0; i < st.samples_s.size(); ++i) samples[i] = st.samples_s[i];
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, -1);
+  }
+}
+
+// Throughput: B independent batch-1 prlab::forward calls of S tokens on `nthreads` host
+// threads over the prebuilt Model (batched and per-sequence logits are bit-identical,
+// SURVEY 8(d)); *seconds = steady_clock wall time of the forwards only (threads started
+// before the clock, released together).  logits may be NULL (discarded).
+int ref_forward_threads(void* mp, const int32_t* ids, int64_t B, int64_t S, const char* policy,
+                        int nthreads, float* logits, double* seconds) {
+  try {
+    const prlab::Model& m = *static_cast<prlab::Model*>(mp);
+    const prlab::PrecisionPolicy pol = prlab::resolve_policy(policy);
+    const int64_t out_w = m.config.num_layers > 0 ? m.config.vocab : m.config.hidden;
+    nthreads = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(nthreads, B)));
+    std::vector<std::thread> pool;
+    std::vector<std::string> errs(static_cast<size_t>(nthreads));
+    std::atomic<int> ready{0};
+    std::atomic<bool> go{false};
+    for (int t = 0; t < nthreads; ++t) {
+      pool.emplace_back([&, t] {
+        ready.fetch_add(1);
+        while (!go.load(std::memory_order_acquire)) std::this_thread::yield();
+        try {
+          for (int64_t b = t; b < B; b += nthreads) {
+            prlab::TokenBatch tb;
+            tb.batch = 1;
+            tb.seq = S;
+            tb.ids.assign(ids + b * S, ids + (b + 1) * S);
+            const prlab::ForwardTrace tr = prlab::forward(m, tb, pol);
+            if (logits)
+              std::memcpy(logits + b * S * out_w, tr.logits.data.data(), tr.logits.data.size() * sizeof(float));
+          }
+        } catch (const std::exception& e) {
+          errs[static_cast<size_t>(t)] = e.what();
+        }
+      });
+    }
+    while (ready.load() < nthreads) std::this_thread::yield();
+    const auto t0 = std::chrono::steady_clock::now();
+    go.store(true, std::memory_order_release);
+    for (auto& th : pool) th.join();
+    *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    for (const auto& e : errs)
+      if (!e.empty()) throw std::runtime_error(e);
+    return 0;
+  } catch (const std::exception& e) {
+    return fail(e, -1);
   }
 }
 

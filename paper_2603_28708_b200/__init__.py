@@ -184,6 +184,10 @@ EXPORTS = [
     ("prlab_gpu_forward_kernel_count", C.c_int, [_P, C.c_int64, C.c_int64,
                                                  C.POINTER(PrecisionPolicy),
                                                  C.POINTER(C.c_int64)]),
+    ("prlab_gpu_forward_kernel_count_ex", C.c_int, [_P, C.c_int64, C.c_int64,
+                                                    C.POINTER(PrecisionPolicy), C.c_int32,
+                                                    C.POINTER(C.c_int64)]),
+    ("prlab_gpu_debug_embedding_device", C.c_int, [_P, _P, C.c_int64, C.c_int64, C.c_int32, _P, _P]),
     ("prlab_gpu_host_copy_mode", C.c_int, [_P, C.c_int64, C.c_int64, C.POINTER(PrecisionPolicy),
                                            C.POINTER(C.c_int32)]),
     ("prlab_gpu_matmul", C.c_int, [_FP, _FP, C.c_int64, C.c_int64, C.c_int64, KernelConfig, _FP]),
@@ -307,6 +311,11 @@ def argmax_device(d_logits: int, dtype: int, rows: int, n: int, ld: int, d_token
                                          C.c_void_p(d_tokens), C.c_void_p(stream)))
 
 
+def _check_ids(ids: np.ndarray, batch: int, seq: int):
+    if batch < 0 or seq < 0 or ids.size != batch * seq:
+        raise ValueError(f"token batch holds {ids.size} ids, expected batch*seq = {batch}*{seq}")
+
+
 # ---------------------------------------------------------------------------
 # model + forward (src/model.cpp)
 # ---------------------------------------------------------------------------
@@ -316,6 +325,9 @@ class DeviceModel:
     def __init__(self, config: ModelConfig, params: np.ndarray, device: int = 0):
         self.config = config
         flat = _arr(params)
+        want = param_count(config)
+        if flat.size != want:  # the C entry point walks param_sizes(desc) over the pointer
+            raise ValueError(f"expected {want} parameters for this config, got {flat.size}")
         h = C.c_void_p()
         d = config._desc()
         _check(lib().prlab_gpu_model_create_flat(C.byref(d), _f(flat), device, C.byref(h)))
@@ -354,6 +366,7 @@ class DeviceModel:
         """Drop-in forward (src/model.cpp:456-482): host ids -> host fp32 logits [B,S,V]."""
         cfg = self.config
         ids = _arr(ids, np.int32)
+        _check_ids(ids, batch, seq)
         width = cfg.vocab if cfg.num_layers > 0 else cfg.hidden
         logits = np.empty((batch, seq, width), np.float32)
         tr = Trace()
@@ -368,6 +381,7 @@ class DeviceModel:
         layer_scores [L,B,H,S,S] fp32 pre-mask taps (ForwardTrace::layer_scores)."""
         cfg = self.config
         ids = _arr(ids, np.int32)
+        _check_ids(ids, batch, seq)
         width = cfg.vocab if cfg.num_layers > 0 else cfg.hidden
         logits = np.empty((batch, seq, width), np.float32)
         scores = (np.empty((cfg.num_layers, batch, cfg.heads, seq, seq), np.float32)
@@ -383,6 +397,7 @@ class DeviceModel:
     def classifier_probs(self, ids, batch: int, seq: int, policy="hybrid") -> np.ndarray:
         """classifier_probs (src/model.cpp:484-526): positive-class probability per row."""
         ids = _arr(ids, np.int32)
+        _check_ids(ids, batch, seq)
         out = np.empty(batch, np.float32)
         pol = _policy(policy)
         _check(lib().prlab_gpu_classifier_probs(self._h, ids.ctypes.data_as(_IP), batch, seq,
@@ -437,12 +452,21 @@ class DeviceModel:
         _check(lib().prlab_gpu_host_copy_mode(self._h, batch, seq, C.byref(_policy(policy)), C.byref(mode)))
         return int(mode.value)
 
-    def kernel_count(self, batch, seq, policy="hybrid") -> int:
+    def kernel_count(self, batch, seq, policy="hybrid", out_dtype=None) -> int:
+        """Kernels one forward_device launch issues (fp16 logits unless out_dtype given)."""
         n = C.c_int64()
         pol = _policy(policy)
-        _check(lib().prlab_gpu_forward_kernel_count(self._h, batch, seq, C.byref(pol),
-                                                    C.byref(n)))
+        _check(lib().prlab_gpu_forward_kernel_count_ex(self._h, batch, seq, C.byref(pol),
+                                                       OUT_F16 if out_dtype is None else out_dtype,
+                                                       C.byref(n)))
         return int(n.value)
+
+    def embedding_device(self, d_ids: int, batch: int, seq: int, path: int, d_out: int, stream: int = 0):
+        """Parity probe: the hot path's embedding gather alone into d_out fp32 [B*S, h]
+        (path 0 = embed_f32_kernel of the multi-kernel path, 1 = stage 0 of the batch-1
+        persistent kernel)."""
+        _check(lib().prlab_gpu_debug_embedding_device(self._h, C.c_void_p(d_ids), batch, seq, path,
+                                                      C.c_void_p(d_out), C.c_void_p(stream)))
 
 
 # ---------------------------------------------------------------------------

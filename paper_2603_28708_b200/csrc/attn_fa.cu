@@ -419,12 +419,12 @@ bool attn_fa_enabled() {
 }
 
 void launch_attn_fa(const AttnPlan& p, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
+  static std::mutex mu;
+  static uint64_t done = 0;
+  once_per_device(mu, done, [] {
     PRLAB_CUDA(cudaFuncSetAttribute(attn_fa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kFaSmemBytes)));
-    configured = true;
-  }
+  });
   FaArgs a;
   a.B = p.B;
   a.S = p.S;

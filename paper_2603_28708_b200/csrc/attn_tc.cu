@@ -461,11 +461,12 @@ AttnPlan plan_attn_tc(const void* qkv, int64_t ld_qkv, void* ctx, int64_t ld_ctx
 }
 
 void configure_attn_tc() {
-  static bool done = false;
-  if (done) return;
-  PRLAB_CUDA(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  static_cast<int>(kSmemBytes)));
-  done = true;
+  static std::mutex mu;
+  static uint64_t done = 0;
+  once_per_device(mu, done, [] {
+    PRLAB_CUDA(cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kSmemBytes)));
+  });
 }
 
 void launch_attn_tc(const AttnPlan& p, cudaStream_t st, float* tap) {

@@ -75,6 +75,7 @@ struct SmallArgs {
   LayerW lw[kMaxLayers];
   int M, B, S, h, f, H, L, V, causal;
   int split_ffn2;
+  int embed_only;                // debug: stop after stage 0 (x = the embedding gather)
   const float *tok, *pos, *lnfg, *lnfb;
   const int32_t* ids;
   int* err;
@@ -630,7 +631,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
   };
 
   // ---- stage 0: embedding gather (bit-exact fp32 tok + pos) + LN1 of layer 0
-  pre_qkv(0);
+  if (!a.embed_only) pre_qkv(0);  // (no TMA may be in flight when an embed-only launch exits)
   prefetch_layer_params(a, a.lw[0]);
   prefetch_layer_weights(a, a.lw[0]);
   for (int r = blockIdx.x; r < M; r += gridDim.x) {
@@ -654,7 +655,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
   }
   grid_sync(a.gbar, target, a.dbg);
 
-  for (int l = 0; l < a.L; ++l) {
+  for (int l = 0; l < (a.embed_only ? 0 : a.L); ++l) {
     const LayerW& w = a.lw[l];
     const CUtensorMap* mW = a.maps + 2 + 4 * l;
     if (l + 1 < a.L) {
@@ -742,13 +743,15 @@ size_t fwd_small_workspace_floats(int64_t M, int64_t h, int64_t f) {
 }
 
 void launch_fwd_small(const FwdSmallPlan& p, cudaStream_t st) {
-  static bool configured = false;
-  if (!configured) {
+  static std::mutex mu;
+  static uint64_t done = 0;
+  once_per_device(mu, done, [] {
     PRLAB_CUDA(cudaFuncSetAttribute(fwd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kSmem)));
-    configured = true;
-  }
-  static SmallArgs a;  // 28 KB: not on the host stack
+  });
+  // 28 KB of kernel parameters, copied at launch: one per host thread (models driven from
+  // several threads each launch with their own maps and weights), not on the stack
+  static thread_local SmallArgs a;
   a = SmallArgs{};
   a.M = p.M;
   a.B = p.B;
@@ -760,6 +763,7 @@ void launch_fwd_small(const FwdSmallPlan& p, cudaStream_t st) {
   a.V = p.V;
   a.causal = p.causal;
   a.split_ffn2 = p.f / 512;
+  a.embed_only = p.embed_only;
   if (p.L > kMaxLayers) throw std::invalid_argument("fwd_small: too many layers");
   std::memcpy(a.maps, p.host_maps, sizeof(CUtensorMap) * (2 + 4 * p.L));
   std::memcpy(a.lw, p.host_lw, sizeof(LayerW) * p.L);

@@ -1204,7 +1204,8 @@ SplitScratch& global_split_scratch() {
 
 // co-resident 4-CTA clusters of the ~200 KB pair kernel (GPC packing leaves SMs idle)
 int max_active_clusters4() {
-  static int n = 0;
+  static int n_dev[64] = {};
+  int& n = n_dev[current_device() & 63];
   if (n == 0) {
     configure_gemm_tc();
     cudaLaunchConfig_t cfg = {};
@@ -1340,19 +1341,20 @@ GemmPlan plan_gemm_tc(const void* A, int64_t lda, const void* Wt, int64_t ldw, c
 }
 
 void configure_gemm_tc() {
-  static bool done = false;  // per process; the library drives one device per process
-  if (done) return;
-  configure_bn<256, false>();
-  configure_bn<128, false>();
-  configure_bn<64, false>();
-  configure_bn<256, true>();
-  configure_bn<128, true>();
-  configure_bn<64, true>();
-  configure_cluster_bn<64>();
-  configure_cluster_bn<128>();
-  configure_pair_bn<128>();
-  configure_pair_bn<256>();
-  done = true;
+  static std::mutex mu;
+  static uint64_t done = 0;
+  once_per_device(mu, done, [] {
+    configure_bn<256, false>();
+    configure_bn<128, false>();
+    configure_bn<64, false>();
+    configure_bn<256, true>();
+    configure_bn<128, true>();
+    configure_bn<64, true>();
+    configure_cluster_bn<64>();
+    configure_cluster_bn<128>();
+    configure_pair_bn<128>();
+    configure_pair_bn<256>();
+  });
 }
 
 void launch_gemm_tc(const GemmPlan& p, cudaStream_t st) {

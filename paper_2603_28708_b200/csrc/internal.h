@@ -5,6 +5,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -24,8 +25,22 @@ struct cuda_error : std::runtime_error {
       throw ::prlab_gpu::cuda_error(std::string(#call) + ": " + cudaGetErrorString(e_));    \
   } while (0)
 
-int num_sms();
+int num_sms();  // of the current device (cached per device)
 bool pdl_enabled();
+int current_device();
+
+// Per-device one-time initialisation (cudaFuncSetAttribute, occupancy queries are per
+// device): runs f() the first time it is reached on the current device, under `mu`, so a
+// second model on another GPU -- or two threads racing on one -- never launches before
+// its device is configured.
+template <typename F>
+void once_per_device(std::mutex& mu, uint64_t& done_mask, F&& f) {
+  const int dev = current_device();
+  std::lock_guard<std::mutex> lk(mu);
+  if ((done_mask >> (dev & 63)) & 1u) return;
+  f();
+  done_mask |= 1ull << (dev & 63);
+}
 
 // Launch with programmatic stream serialization (PDL) so the kernel's prologue
 // overlaps the tail of the previous kernel in the stream / graph.
@@ -119,6 +134,7 @@ struct FwdSmallPlan {
   __half *xn16, *ff16;
   float* scratch;            // fwd_small_workspace_floats()
   unsigned* gbar;
+  int embed_only = 0;        // debug: stop after the embedding stage (x = tok + pos)
 };
 bool fwd_small_supported(int64_t M, int64_t S, int64_t h, int64_t f, int64_t hd, int64_t L);
 size_t fwd_small_workspace_floats(int64_t M, int64_t h, int64_t f);

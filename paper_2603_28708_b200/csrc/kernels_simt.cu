@@ -506,10 +506,12 @@ void simt_layernorm(const float* x, int rows, int n, const float* gamma, const f
 template <int VPT>
 void launch_ln(const float* x, int rows, const float* gamma, const float* beta, float eps, __half* out,
                cudaStream_t st) {
-  static int per_sm = 0;
+  static int per_sm_dev[64] = {};
+  int& per_sm = per_sm_dev[current_device() & 63];
   if (per_sm == 0) {
-    PRLAB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, ln_f16_kernel<VPT>, 256, 0));
-    per_sm = std::max(1, per_sm);
+    int v = 0;
+    PRLAB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, ln_f16_kernel<VPT>, 256, 0));
+    per_sm = std::max(1, v);
   }
   const int grid = std::min((rows + 7) / 8, num_sms() * per_sm);
   launch_pdl(ln_f16_kernel<VPT>, dim3(grid), dim3(256), 0, st, x, rows, gamma, beta, eps, out);
@@ -535,12 +537,17 @@ void simt_attention(const float* q, const float* k, const float* v, int64_t ld_i
                     Kcfg sm, float* tap, cudaStream_t st) {
   const int warps = 4;
   const size_t shmem = static_cast<size_t>(warps) * (S + hd) * sizeof(float);
-  static int configured_bytes = 48 * 1024;
-  if (shmem > static_cast<size_t>(configured_bytes)) {
-    PRLAB_CUDA(cudaFuncSetAttribute(simt_attention_kernel,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    static_cast<int>(shmem)));
-    configured_bytes = static_cast<int>(shmem);
+  {
+    static std::mutex mu;
+    static int configured_bytes[64] = {};
+    std::lock_guard<std::mutex> lk(mu);
+    int& cb = configured_bytes[current_device() & 63];
+    if (cb == 0) cb = 48 * 1024;
+    if (shmem > static_cast<size_t>(cb)) {
+      PRLAB_CUDA(cudaFuncSetAttribute(simt_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>(shmem)));
+      cb = static_cast<int>(shmem);
+    }
   }
   const int64_t rows = static_cast<int64_t>(B) * H * S;
   simt_attention_kernel<<<static_cast<int>((rows + warps - 1) / warps), warps * 32, shmem, st>>>(

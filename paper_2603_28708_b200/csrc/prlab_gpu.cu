@@ -61,14 +61,21 @@ void require_device() {
 }
 }  // namespace
 
+int current_device() {
+  int dev = 0;
+  PRLAB_CUDA(cudaGetDevice(&dev));
+  return dev;
+}
+
 int num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    PRLAB_CUDA(cudaGetDevice(&dev));
-    PRLAB_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev));
+  static int n[64] = {};
+  const int dev = current_device() & 63;
+  if (n[dev] == 0) {
+    int v = 0;
+    PRLAB_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+    n[dev] = v;
   }
-  return n;
+  return n[dev];
 }
 
 bool pdl_enabled() {
@@ -470,6 +477,12 @@ struct prlab_gpu_model {
   DeviceBuffer split_ws, split_tickets;
   SplitScratch scratch;
   cudaStream_t stream = nullptr;  // private stream of the host (drop-in) forward
+  // Every call shares the workspace below (activations, split-K scratch, the persistent
+  // kernel's grid-barrier counter, graphs): work queued on a stream other than the previous
+  // call's waits on this event, recorded after that call's work (see StreamOrder).
+  cudaEvent_t last_ev = nullptr;
+  cudaStream_t last_st = nullptr;
+  bool have_last = false;
 
   // activation workspace + per-key plans
   DeviceBuffer ws;
@@ -505,6 +518,7 @@ struct prlab_gpu_model {
   ~prlab_gpu_model() {
     drop_plans();
     if (stream) cudaStreamDestroy(stream);
+    if (last_ev) cudaEventDestroy(last_ev);
   }
   void drop_plans() {
     for (auto& kv : plans)
@@ -514,6 +528,28 @@ struct prlab_gpu_model {
 };
 
 namespace {
+
+// Stream ordering of one API call on the model's shared workspace (held under the model
+// mutex): before queuing on `st`, wait for the previous call's work if that was queued on
+// another stream; afterwards record the event on `st`.  Streams under the CALLER's graph
+// capture are left alone (the caller orders its graph).
+struct StreamOrder {
+  prlab_gpu_model& m;
+  cudaStream_t st;
+  bool active = true;
+  StreamOrder(prlab_gpu_model& mm, cudaStream_t s) : m(mm), st(s) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    PRLAB_CUDA(cudaStreamIsCapturing(st, &cs));
+    active = cs == cudaStreamCaptureStatusNone;
+    if (active && m.have_last && m.last_st != st) PRLAB_CUDA(cudaStreamWaitEvent(st, m.last_ev, 0));
+  }
+  ~StreamOrder() {
+    if (active && cudaEventRecord(m.last_ev, st) == cudaSuccess) {
+      m.last_st = st;
+      m.have_last = true;
+    }
+  }
+};
 
 // Fast (tensor-core) path eligibility: the hybrid policy and TMA-friendly extents.
 bool fast_eligible(const prlab_gpu_model& m, int64_t S, const prlab_policy& pol) {
@@ -1036,6 +1072,7 @@ prlab_gpu_model* create_model(const prlab_model_desc& desc, const float* const* 
   configure_gemm_tc();
   configure_attn_tc();
   PRLAB_CUDA(cudaStreamCreateWithFlags(&m->stream, cudaStreamNonBlocking));
+  PRLAB_CUDA(cudaEventCreateWithFlags(&m->last_ev, cudaEventDisableTiming));
   return m.release();
 }
 
@@ -1222,6 +1259,7 @@ int prlab_gpu_perplexity(prlab_gpu_model* m, const int32_t* tokens, int64_t n_to
     validate_policy(*policy);
     PRLAB_CUDA(cudaSetDevice(m->device));
     cudaStream_t st = m->stream;
+    StreamOrder order(*m, st);
     const int64_t V = m->V;
     // windows [off, off + len): full ones batched (bounded logits buffer), then the tail
     const int64_t nfull = n_tokens / context_len;
@@ -1322,6 +1360,7 @@ int prlab_gpu_forward(prlab_gpu_model* m, const int32_t* ids, int64_t B, int64_t
     auto& p = get_plan(*m, B, S, *policy);
     const int64_t w = m->L > 0 ? m->V : m->h;
     cudaStream_t st = m->stream;
+    StreamOrder order(*m, st);
     PRLAB_CUDA(cudaMemcpyAsync(p.ids, ids, B * S * 4, cudaMemcpyHostToDevice, st));
     const bool graph = !std::getenv("PRLAB_NO_GRAPH");
     if (p.fast && m->L > 0 && !std::getenv("PRLAB_NO_HOST_WIDEN")) {
@@ -1382,6 +1421,7 @@ int prlab_gpu_forward_ex(prlab_gpu_model* m, const int32_t* ids, int64_t B, int6
     auto& p = get_plan(*m, B, S, *policy);
     const int64_t w = m->L > 0 ? m->V : m->h;
     cudaStream_t st = m->stream;
+    StreamOrder order(*m, st);
     PRLAB_CUDA(cudaMemcpyAsync(p.ids, ids, B * S * 4, cudaMemcpyHostToDevice, st));
     FwdOpts o;
     const int64_t tap_n = m->L * B * m->H * S * S;
@@ -1448,6 +1488,7 @@ int prlab_gpu_classifier_probs(prlab_gpu_model* m, const int32_t* ids, int64_t B
     }
     auto& p = get_plan(*m, B, S, *policy);
     cudaStream_t st = m->stream;
+    StreamOrder order(*m, st);
     PRLAB_CUDA(cudaMemcpyAsync(p.ids, ids, B * S * 4, cudaMemcpyHostToDevice, st));
     FwdOpts o;
     o.hidden_only = true;
@@ -1483,6 +1524,7 @@ int prlab_gpu_forward_device(prlab_gpu_model* m, const int32_t* d_ids, int64_t B
       throw std::invalid_argument("unknown logits dtype");
     PRLAB_CUDA(cudaSetDevice(m->device));
     auto& p = get_plan(*m, B, S, *policy);
+    StreamOrder order(*m, static_cast<cudaStream_t>(stream));
     run_forward(*m, p, d_ids, d_out, out_dtype, ld, static_cast<cudaStream_t>(stream), use_graph != 0);
   });
 }
@@ -1497,6 +1539,7 @@ int prlab_gpu_forward_trunk_device(prlab_gpu_model* m, const int32_t* d_ids, int
     auto& p = get_plan(*m, B, S, *policy);
     FwdOpts o;
     o.hidden_only = true;
+    StreamOrder order(*m, static_cast<cudaStream_t>(stream));
     const int64_t n = enqueue_forward(*m, p, d_ids, nullptr, PRLAB_OUT_F32, 0, static_cast<cudaStream_t>(stream), o);
     if (kernels) *kernels = n;
   });
@@ -1554,6 +1597,7 @@ int prlab_gpu_forward_nll_device(prlab_gpu_model* m, const int32_t* d_ids, const
     if (m->L == 0) throw std::invalid_argument("forward_nll needs a model with a tied head (num_layers > 0)");
     PRLAB_CUDA(cudaSetDevice(m->device));
     auto& p = get_plan(*m, B, S, *policy);
+    StreamOrder order(*m, static_cast<cudaStream_t>(stream));
     enqueue_nll(*m, p, d_ids, d_targets, d_nll, d_argmax, static_cast<cudaStream_t>(stream), fused);
   });
 }
@@ -1571,14 +1615,49 @@ int prlab_gpu_sync_status(prlab_gpu_model* m, void* stream) {
   });
 }
 
-int prlab_gpu_forward_kernel_count(prlab_gpu_model* m, int64_t B, int64_t S, const prlab_policy* policy,
-                                   int64_t* count) {
+int prlab_gpu_forward_kernel_count_ex(prlab_gpu_model* m, int64_t B, int64_t S, const prlab_policy* policy,
+                                      int32_t out_dtype, int64_t* count) {
   return guarded([&] {
     check_forward_args(*m, B, S);
+    if (out_dtype != PRLAB_OUT_F32 && out_dtype != PRLAB_OUT_F16) throw std::invalid_argument("unknown logits dtype");
     const bool fast = fast_eligible(*m, S, *policy);
     const int64_t L = m->L;
     const bool small = fast && fwd_small_supported(B * S, S, m->h, m->f, m->hd, L);
-    *count = small ? 2 : (fast ? 1 + 7 * L + 1 + 1 : 1 + 7 * L + (L > 0 ? 2 : 1));
+    // fast path: trunk (1 persistent kernel, or embed + 7 per layer + final LN) + the head GEMM,
+    // + the fp16 -> fp32 widening kernel when fp32 logits are asked for
+    const int64_t widen = fast && out_dtype == PRLAB_OUT_F32 ? 1 : 0;
+    *count = small ? 2 + widen : (fast ? 1 + 7 * L + 1 + 1 + widen : 1 + 7 * L + (L > 0 ? 2 : 1));
+  });
+}
+
+int prlab_gpu_forward_kernel_count(prlab_gpu_model* m, int64_t B, int64_t S, const prlab_policy* policy,
+                                   int64_t* count) {
+  return prlab_gpu_forward_kernel_count_ex(m, B, S, policy, PRLAB_OUT_F16, count);
+}
+
+int prlab_gpu_debug_embedding_device(prlab_gpu_model* m, const int32_t* d_ids, int64_t B, int64_t S, int32_t path,
+                                     float* d_out, void* stream) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(m->mu);
+    check_forward_args(*m, B, S);
+    prlab_policy pol;
+    prlab_gpu_resolve_policy("hybrid", &pol);
+    if (!fast_eligible(*m, S, pol)) throw std::invalid_argument("embedding debug: shape not on the tensor-core path");
+    PRLAB_CUDA(cudaSetDevice(m->device));
+    auto& p = get_plan(*m, B, S, pol);
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    StreamOrder order(*m, st);
+    if (path == 0) {
+      embed_f32(m->tok, m->V, m->pos, static_cast<int>(m->h), d_ids, static_cast<int>(B), static_cast<int>(S), p.x,
+                m->err.at<int>(0), st);
+    } else {
+      if (!p.small) throw std::invalid_argument("embedding debug: shape not on the persistent batch-1 kernel");
+      FwdSmallPlan sp = p.sp;
+      sp.ids = d_ids;
+      sp.embed_only = 1;
+      launch_fwd_small(sp, st);
+    }
+    PRLAB_CUDA(cudaMemcpyAsync(d_out, p.x, B * S * m->h * 4, cudaMemcpyDeviceToDevice, st));
   });
 }
 

@@ -1,0 +1,176 @@
+"""North-star parity bars on the GPU (BASELINE.json north_star, BASELINE.md section 3,
+SURVEY.md section 8(d)), at the benchmark configurations themselves:
+
+  * embedding-index gathers BIT-EXACT against the reference's own embed()
+    (src/kernels.cpp:256-294, called through oracle/_ref) on the full GPT-2 / BERT tables,
+    through both hot-path gather kernels: embed_f32_kernel (multi-kernel path) and stage 0
+    of the batch-1 persistent kernel (fwd_small);
+  * C4 (GPT-2 hybrid, batch 32, seq 512) at forward level: first and last sequence vs the
+    CPU oracle (cosine >= 0.9998, zero non-finite, max-abs <= 5e-3 vs CPU hybrid);
+  * GPT-2 greedy argmax at C2 (1 x 128): fp32 path bit-exact off near-ties (gap < 1e-5);
+    hybrid agreement rate vs CPU hybrid, exact on every row whose CPU top-2 gap is >= 3e-3
+    (above the measured GPU<->CPU hybrid drift), near-tie rows reported separately;
+  * the presets' hybrid path vs CPU HYBRID (not only fp32), and the drift by depth.
+
+Every measured number is also appended to $PRLAB_PARITY_REPORT (JSON lines) when set.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_2603_28708_b200 as pg
+from oracle.oracle import PRESETS, compare_logits, split_params
+from prlab_testutil import have_reference_lib, model_params, oracle, reference
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+_MODELS = {}
+
+
+def device_model(cfg):
+    if cfg not in _MODELS:
+        _MODELS[cfg] = pg.DeviceModel(pg.ModelConfig(**cfg.__dict__), model_params(cfg))
+    return _MODELS[cfg]
+
+
+def report(**kw):
+    path = os.environ.get("PRLAB_PARITY_REPORT")
+    if path:
+        with open(path, "a") as f:
+            f.write(json.dumps(kw) + "\n")
+
+
+def embed_ref(cfg, ids, B, S):
+    """The reference's embed() itself when oracle/_ref is built, else the pinned restatement."""
+    p = dict(split_params(cfg, model_params(cfg)))
+    tok, pos = p["token_embedding"], p["position_embedding"]
+    if have_reference_lib():
+        return reference().embed(tok, pos, ids, B, S, 0), "reference embed()"
+    return oracle().embed(tok, pos, ids, B, S, 0), "oracle restatement"
+
+
+@pytest.mark.parametrize("name,B,S,paths", [
+    ("gpt2_small", 1, 128, (0, 1)),    # C2
+    ("bert_base", 1, 128, (0, 1)),     # C1 / C3 corner
+    ("bert_base", 8, 16, (0, 1)),      # batch > 1 inside the persistent kernel
+    ("bert_base", 32, 512, (0,)),      # C3 max
+    ("gpt2_small", 32, 512, (0,)),     # C4
+])
+def test_embedding_gather_bitexact(name, B, S, paths):
+    cfg = PRESETS[name]
+    m = device_model(cfg)
+    ids = oracle().random_tokens(cfg.vocab, B, S, 1234 + B + S)
+    want, src = embed_ref(cfg, ids, B, S)
+    d_ids = torch.from_numpy(ids).cuda()
+    st = torch.cuda.current_stream().cuda_stream
+    for path in paths:
+        out = torch.full((B * S, cfg.hidden), float("nan"), device="cuda")
+        m.embedding_device(d_ids.data_ptr(), B, S, path, out.data_ptr(), st)
+        m.sync_status(st)
+        got = out.cpu().numpy()
+        ndiff = int((got.view(np.uint32) != want.view(np.uint32)).sum())
+        report(test="embedding_gather", model=name, B=B, S=S, path=["embed_f32_kernel", "fwd_small stage 0"][path],
+               against=src, elements=int(got.size), bit_differences=ndiff)
+        assert ndiff == 0, f"path {path}: {ndiff} of {got.size} fp32 words differ from {src}"
+
+
+def _argmax_stats(got, cpu, near):
+    g = got.reshape(-1, got.shape[-1])
+    w = cpu.reshape(-1, cpu.shape[-1]).astype(np.float64)
+    top2 = np.sort(w, axis=1)[:, -2:]
+    gap = top2[:, 1] - top2[:, 0]
+    agree = np.argmax(g, 1) == np.argmax(w, 1)
+    clear = gap >= near
+    return {"rows": int(len(gap)), "agree": int(agree.sum()), "agreement_rate": float(agree.mean()),
+            "clear_rows": int(clear.sum()), "clear_agree": int(agree[clear].sum()),
+            "near_tie_rows": [{"row": int(r), "gap": float(gap[r]), "agree": bool(agree[r])}
+                              for r in np.nonzero(~clear)[0]]}
+
+
+def test_c2_greedy_argmax():
+    cfg = PRESETS["gpt2_small"]
+    o = oracle()
+    m = device_model(cfg)
+    p = model_params(cfg)
+    ids = o.random_tokens(cfg.vocab, 1, 128, 1234)
+    # fp32 policy: bit-exact argmax, rows with a top-2 gap < 1e-5 excluded
+    cpu32 = o.forward(cfg, p, ids, 1, 128, "fp32")
+    g32 = m.forward(ids, 1, 128, "fp32")
+    s32 = _argmax_stats(g32, cpu32, 1e-5)
+    report(test="argmax_c2", policy="fp32", **{k: v for k, v in s32.items()})
+    assert s32["clear_rows"] > 0 and s32["clear_agree"] == s32["clear_rows"], s32
+    # hybrid: agreement rate against the CPU hybrid forward (same policy)
+    cpuh = o.forward(cfg, p, ids, 1, 128, "hybrid")
+    gh = m.forward(ids, 1, 128, "hybrid")
+    sh = _argmax_stats(gh, cpuh, 3e-3)
+    report(test="argmax_c2", policy="hybrid", **sh)
+    assert sh["clear_agree"] == sh["clear_rows"], sh
+
+
+def test_c4_forward_first_last_sequence():
+    """C4 at forward level: the whole 32 x 512 batch on the device (tensor-core path: CTA-pair
+    GEMMs at M = 16384, streaming causal attention at B*H = 384), the first and last sequence
+    against per-sequence oracle runs (rows are independent)."""
+    cfg = PRESETS["gpt2_small"]
+    o = oracle()
+    m = device_model(cfg)
+    p = model_params(cfg)
+    B, S, V = 32, 512, cfg.vocab
+    ids = o.random_tokens(V, B, S, 4321)
+    ld = (V + 7) // 8 * 8
+    d_ids = torch.from_numpy(ids).cuda()
+    out = torch.empty(B * S, ld, dtype=torch.float16, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    m.forward_device(d_ids.data_ptr(), B, S, "hybrid", out.data_ptr(), pg.OUT_F16, ld, st, True)
+    m.sync_status(st)
+    assert bool(torch.isfinite(out[:, :V]).all()), "non-finite C4 logits"
+    for b in (0, B - 1):
+        got = out[b * S:(b + 1) * S, :V].float().cpu().numpy().reshape(1, S, V)
+        seq = ids[b * S:(b + 1) * S]
+        cpuh = o.forward(cfg, p, seq, 1, S, "hybrid")
+        cpu32 = o.forward(cfg, p, seq, 1, S, "fp32")
+        rh, r32 = compare_logits(cpuh, got), compare_logits(cpu32, got)
+        sh = _argmax_stats(got, cpuh, 3e-3)
+        report(test="c4_forward", seq=b, vs_cpu_hybrid=rh, vs_cpu_fp32=r32,
+               argmax_vs_cpu_hybrid={k: v for k, v in sh.items() if k != "near_tie_rows"},
+               near_tie_rows=len(sh["near_tie_rows"]))
+        assert rh["candidate_nonfinite"] == 0 and r32["candidate_nonfinite"] == 0
+        assert rh["cosine"] >= 0.9998 and r32["cosine"] >= 0.9998, (rh, r32)
+        assert rh["max_abs_error"] <= 5e-3, rh
+        assert sh["clear_agree"] == sh["clear_rows"], sh
+
+
+@pytest.mark.parametrize("name,B,S", [("gpt2_small", 1, 128), ("bert_base", 2, 64), ("gpt2_small", 2, 77),
+                                      ("bert_base", 1, 512)])
+def test_preset_hybrid_vs_cpu_hybrid(name, B, S):
+    cfg = PRESETS[name]
+    o = oracle()
+    m = device_model(cfg)
+    ids = o.random_tokens(cfg.vocab, B, S, 1234)
+    got = m.forward(ids, B, S, "hybrid")
+    cpuh = o.forward(cfg, model_params(cfg), ids, B, S, "hybrid")
+    r = compare_logits(cpuh, got)
+    report(test="preset_vs_cpu_hybrid", model=name, B=B, S=S, **r)
+    assert r["candidate_nonfinite"] == 0
+    assert r["cosine"] >= 0.9999, r
+    assert r["max_abs_error"] <= 5e-3, r
+
+
+@pytest.mark.parametrize("layers", [1, 2, 4, 8])
+def test_hybrid_drift_by_depth(layers):
+    """GPU hybrid vs CPU hybrid as the trunk deepens (build_model's canonical stream puts the
+    layers in order, so an L-layer GPT-2 shares its first layers with the 12-layer one)."""
+    cfg = PRESETS["gpt2_small"].replace(num_layers=layers)
+    o = oracle()
+    p = o.build_model(cfg)
+    m = pg.DeviceModel(pg.ModelConfig(**cfg.__dict__), p)
+    ids = o.random_tokens(cfg.vocab, 1, 128, 1234)
+    got = m.forward(ids, 1, 128, "hybrid")
+    cpuh = o.forward(cfg, p, ids, 1, 128, "hybrid")
+    r = compare_logits(cpuh, got)
+    report(test="hybrid_drift_by_depth", layers=layers, **r)
+    m.close()
+    assert r["candidate_nonfinite"] == 0 and r["cosine"] >= 0.9999 and r["max_abs_error"] <= 5e-3, r

@@ -1,13 +1,20 @@
 """Multi-process (gloo, world_size 2) coverage of the replica host logic used by
-bench.py --gpus N: batch sharding, per-replica seeds and max-over-ranks timing."""
+bench.py --gpus N: batch sharding, per-replica seeds, max-over-ranks timing -- and
+bench.py's own multi-rank branch, launched by torchrun with a CPU stand-in for the
+device step (`--stub-device`)."""
+import json
 import os
 import socket
+import subprocess
+import sys
 
 import pytest
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2603_28708_b200 import replicas
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
 def test_shard_batch_covers_exactly():
@@ -21,6 +28,18 @@ def test_shard_batch_covers_exactly():
                 pos += c
     with pytest.raises(ValueError):
         replicas.shard_batch(4, 2, 2)
+
+
+def test_rank_batch_weak_and_strong():
+    assert [replicas.rank_batch(32, 4, r, False) for r in range(4)] == [(0, 32), (32, 32), (64, 32), (96, 32)]
+    assert [replicas.rank_batch(32, 4, r, True) for r in range(4)] == [(0, 8), (8, 8), (16, 8), (24, 8)]
+    assert replicas.rank_batch(32, 1, 0, True) == (0, 32)
+
+
+def test_timed_steps_counts_exactly():
+    calls = []
+    per, mine, total = replicas.timed_steps(lambda: calls.append(1), 5, 3, replicas.WallTimer())
+    assert len(calls) == 8 and len(per) == 5 and total == mine
 
 
 def _free_port():
@@ -38,11 +57,8 @@ def _worker(rank, world, port, q):
         start, count = replicas.shard_batch(33, world, rank)
         t = replicas.max_over_ranks(1.0 + rank, dist)  # rank 1 is the slow one
         seed = replicas.replica_token_seed(1234, rank)
-        import torch
-        c = torch.tensor([count])
-        dist.all_reduce(c)
-        q.put((rank, start, count, t, seed, int(c.item()),
-               replicas.aggregate_throughput(32, world, t)))
+        gb = replicas.sum_over_ranks(count, dist)
+        q.put((rank, start, count, t, seed, int(gb), replicas.aggregate_throughput(32, world, t)))
     finally:
         dist.destroy_process_group()
 
@@ -63,3 +79,32 @@ def test_two_rank_replicas_gloo():
     assert [r[4] for r in res] == [1234, 1235]      # independent replica inputs
     assert all(r[5] == 33 for r in res)             # shards cover the global batch
     assert all(r[6] == 32.0 for r in res)           # 2 ranks x 32 seq / 2 s
+
+
+def _torchrun_bench(extra):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_free_port()),
+           os.path.join(ROOT, "bench.py"), "--gpus", "2", "--steps", "4", "--warmup", "3",
+           "--stub-device"] + extra
+    env = dict(os.environ, OMP_NUM_THREADS="1")
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env=env, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout  # rank 0 alone prints
+    return json.loads(lines[0])
+
+
+def test_bench_multirank_branch_weak():
+    line = _torchrun_bench([])
+    assert line["n_gpus"] == 2 and line["scaling"] == "weak"
+    assert line["config"]["workload"].startswith("C4")          # WORLD_SIZE > 1 -> configs[3]
+    assert line["config"]["global_batch"] == 64 and line["config"]["per_replica_batch"] == 32
+    # value = all ranks' sequences / the SLOWEST rank's time (rank 1 sleeps twice as long)
+    assert line["ms_per_step"] >= line["rank_ms"] / 4 * 1.5
+    assert abs(line["value"] - 64 * 4 / (line["ms_per_step"] * 4 / 1000.0)) < 1e-6 * line["value"]
+
+
+def test_bench_multirank_branch_strong():
+    line = _torchrun_bench(["--strong"])
+    assert line["scaling"] == "strong"
+    assert line["config"]["global_batch"] == 32 and line["config"]["per_replica_batch"] == 16
