@@ -119,6 +119,18 @@ int prlab_gpu_model_load_checkpoint(const char* path, int device, prlab_model_de
 int prlab_gpu_model_memory(const prlab_gpu_model* m, uint64_t* weight_bytes,
                            uint64_t* workspace_bytes);
 
+/* Device bytes by purpose (the memory planner's accounting):
+ * weights_fast  = the hybrid arena (fp16 K-major linears + tied head, fp32 tables, LN, biases);
+ * weights_fp32  = fp32 copies materialised only when a non-hybrid policy ran (+ classifier head);
+ * workspace     = the liveness-planned activation arena (max over the planned (B, S) keys);
+ * logits        = library-side [B*S, V] logits buffers, allocated only when a call needs the
+ *                 logits inside the library (host forward, unfused NLL);
+ * scratch       = split-K scratch, persistent-kernel partials, fused-head partials, error word. */
+typedef struct {
+  uint64_t weights_fast, weights_fp32, workspace, logits, scratch, total;
+} prlab_memory_report;
+int prlab_gpu_model_memory_ex(prlab_gpu_model* m, prlab_memory_report* out);
+
 /* ---- host fixture generators, same streams as the reference ----
  * build_model (src/model.cpp:217-265): N(0,0.02) fixed Box-Muller over
  * mt19937_64(seed) in canonical order, biases 0, gammas 1.  out: param_count floats. */

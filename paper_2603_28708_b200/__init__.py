@@ -79,6 +79,14 @@ class LogitComparison(C.Structure):
                 "nan_affected": bool(self.nan_affected)}
 
 
+class MemoryReport(C.Structure):
+    _fields_ = [("weights_fast", C.c_uint64), ("weights_fp32", C.c_uint64), ("workspace", C.c_uint64),
+                ("logits", C.c_uint64), ("scratch", C.c_uint64), ("total", C.c_uint64)]
+
+    def as_dict(self):
+        return {k: int(getattr(self, k)) for k, _ in self._fields_}
+
+
 class Trace(C.Structure):
     """Reference ForwardTrace instrumentation (include/prlab/model.hpp:113-125)."""
     _fields_ = [("seconds", C.c_double * 7), ("kernel_calls", (C.c_uint64 * 2) * 7)]
@@ -156,6 +164,7 @@ EXPORTS = [
     ("prlab_gpu_model_create_flat", C.c_int, [C.POINTER(_ModelDesc), _FP, C.c_int, C.POINTER(_P)]),
     ("prlab_gpu_model_destroy", None, [_P]),
     ("prlab_gpu_model_memory", C.c_int, [_P, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
+    ("prlab_gpu_model_memory_ex", C.c_int, [_P, C.POINTER(MemoryReport)]),
     ("prlab_gpu_build_model", C.c_int, [C.POINTER(_ModelDesc), _FP, C.c_int64]),
     ("prlab_gpu_param_count", C.c_uint64, [C.POINTER(_ModelDesc)]),
     ("prlab_gpu_random_tokens", C.c_int, [C.c_int64, C.c_int64, C.c_int64, C.c_uint64, _IP]),
@@ -361,6 +370,12 @@ class DeviceModel:
         w, ws = C.c_uint64(), C.c_uint64()
         _check(lib().prlab_gpu_model_memory(self._h, C.byref(w), C.byref(ws)))
         return int(w.value), int(ws.value)
+
+    def memory_report(self) -> dict:
+        """Device bytes by purpose (prlab_gpu_model_memory_ex)."""
+        r = MemoryReport()
+        _check(lib().prlab_gpu_model_memory_ex(self._h, C.byref(r)))
+        return r.as_dict()
 
     def forward(self, ids, batch: int, seq: int, policy="hybrid", want_trace=False):
         """Drop-in forward (src/model.cpp:456-482): host ids -> host fp32 logits [B,S,V]."""

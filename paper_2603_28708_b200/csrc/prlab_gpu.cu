@@ -494,8 +494,9 @@ struct prlab_gpu_model {
     __half *xn16 = nullptr, *big16 = nullptr, *logit16 = nullptr;
     float *xn32 = nullptr, *qkv32 = nullptr, *ctx32 = nullptr, *ff32 = nullptr;
     int32_t* ids = nullptr;
-    float* out32 = nullptr;
-    int64_t ld16 = 0;
+    float* out32 = nullptr;    // fp32 logits staging (host forward / generic path), allocated on first use
+    int64_t ld16 = 0, outw = 0;
+    DeviceBuffer lazy16, lazy32;  // the [B*S, V] logits buffers are not part of the planned workspace
     // host forward copy-out: 0 = not calibrated, 1 = fp16 rows widened on host, 2 = fp32 copy
     int copy_mode = 0;
     std::vector<GemmPlan> gemms;  // fast path: 4 per layer + head
@@ -528,6 +529,24 @@ struct prlab_gpu_model {
 };
 
 namespace {
+
+// The library-side logits buffers ([B*S, V]: 1.65 GB fp16 / 3.3 GB fp32 at C4) exist only
+// for callers that want the logits in the library (host forward, unfused NLL); a device
+// forward into the caller's buffer or the fused NLL head never allocates them.
+__half* plan_logits16(prlab_gpu_model::Plan& p) {
+  if (!p.logit16) {
+    p.lazy16.alloc(static_cast<size_t>(p.B * p.S * p.ld16) * 2);
+    p.logit16 = static_cast<__half*>(p.lazy16.p);
+  }
+  return p.logit16;
+}
+float* plan_out32(prlab_gpu_model::Plan& p) {
+  if (!p.out32) {
+    p.lazy32.alloc(static_cast<size_t>(p.B * p.S * p.outw) * 4);
+    p.out32 = static_cast<float*>(p.lazy32.p);
+  }
+  return p.out32;
+}
 
 // Stream ordering of one API call on the model's shared workspace (held under the model
 // mutex): before queuing on `st`, wait for the previous call's work if that was queued on
@@ -764,12 +783,10 @@ prlab_gpu_model::Plan& get_plan(prlab_gpu_model& m, int64_t B, int64_t S, const 
   ArenaPlan ap;
   const int s_x = ap.add(M * h * 4);
   const int s_ids = ap.add(M * 4);
-  const int s_out = ap.add(M * outw * 4);
   int s_a, s_b, s_c = -1;
   if (fast) {
     s_a = ap.add(M * h * 2);                       // xn16 / ctx16
     s_b = ap.add(M * std::max(3 * h, f) * 2);      // qkv16 / ff16
-    s_c = ap.add(M * ld16 * 2);                    // fp16 logits (internal)
   } else {
     s_a = ap.add(M * h * 4);                       // xn32
     s_b = ap.add(M * (3 * h + f) * 4);             // qkv32 | ff32 (attention reads qkv while ff unused)
@@ -790,12 +807,11 @@ prlab_gpu_model::Plan& get_plan(prlab_gpu_model& m, int64_t B, int64_t S, const 
   auto at = [&](int s) { return ap.offs[s]; };
   p.x = m.ws.at<float>(at(s_x));
   p.ids = m.ws.at<int32_t>(at(s_ids));
-  p.out32 = m.ws.at<float>(at(s_out));
+  p.outw = outw;
   const int Mi = static_cast<int>(M), hi = static_cast<int>(h), fi = static_cast<int>(f);
   if (fast) {
     p.xn16 = m.ws.at<__half>(at(s_a));
     p.big16 = m.ws.at<__half>(at(s_b));
-    p.logit16 = m.ws.at<__half>(at(s_c));
     for (int64_t l = 0; l < m.L; ++l) {
       const auto& w = m.l16[l];
       p.gemms.push_back(plan_gemm_tc(p.xn16, h, w.wqkv, h, w.bqkv, p.big16, 3 * h, Mi, 3 * hi, hi, EPI_BIAS_F16, &m.scratch));
@@ -803,8 +819,6 @@ prlab_gpu_model::Plan& get_plan(prlab_gpu_model& m, int64_t B, int64_t S, const 
       p.gemms.push_back(plan_gemm_tc(p.xn16, h, w.w1, h, w.b1, p.big16, f, Mi, fi, hi, EPI_BIAS_GELU_F16, &m.scratch));
       p.gemms.push_back(plan_gemm_tc(p.big16, f, w.w2, f, w.b2, p.x, h, Mi, hi, fi, EPI_BIAS_RESID_F32, &m.scratch));
     }
-    p.gemms.push_back(plan_gemm_tc(p.xn16, h, m.emb16, h, nullptr, p.logit16, ld16, Mi,
-                                   static_cast<int>(V), hi, EPI_F16, &m.scratch));
     p.attn = plan_attn_tc(p.big16, 3 * h, p.xn16, h, static_cast<int>(B), static_cast<int>(S),
                           static_cast<int>(m.H), static_cast<int>(m.hd), m.d.archetype == 1);
     if (fwd_small_supported(M, S, h, f, m.hd, m.L)) plan_small(m, p, B, S);
@@ -885,8 +899,13 @@ int64_t enqueue_forward(prlab_gpu_model& m, prlab_gpu_model::Plan& p, const int3
         it = p.head_plans.emplace(key, plan_gemm_tc(p.xn16, h, m.emb16, h, nullptr, out, ld, Mi, Vi, hi, EPI_F16, &m.scratch)).first;
       T(PRLAB_LINEAR, [&] { launch_gemm_tc(it->second, st); });  // tied head straight into the caller's buffer
     } else {
-      T(PRLAB_LINEAR, [&] { launch_gemm_tc(p.gemms.back(), st); });
-      T(PRLAB_LINEAR, [&] { convert_f16_to_f32(p.logit16, p.ld16, static_cast<float*>(out), ld, Mi, Vi, st); });
+      __half* l16 = plan_logits16(p);
+      const auto key = std::make_tuple(static_cast<void*>(l16), p.ld16);
+      auto it = p.head_plans.find(key);
+      if (it == p.head_plans.end())
+        it = p.head_plans.emplace(key, plan_gemm_tc(p.xn16, h, m.emb16, h, nullptr, l16, p.ld16, Mi, Vi, hi, EPI_F16, &m.scratch)).first;
+      T(PRLAB_LINEAR, [&] { launch_gemm_tc(it->second, st); });
+      T(PRLAB_LINEAR, [&] { convert_f16_to_f32(l16, p.ld16, static_cast<float*>(out), ld, Mi, Vi, st); });
     }
     return n;
   }
@@ -1346,6 +1365,23 @@ int prlab_gpu_model_memory(const prlab_gpu_model* m, uint64_t* weight_bytes, uin
   });
 }
 
+int prlab_gpu_model_memory_ex(prlab_gpu_model* m, prlab_memory_report* r) {
+  return guarded([&] {
+    std::lock_guard<std::mutex> lk(m->mu);
+    std::memset(r, 0, sizeof(*r));
+    r->weights_fast = m->arena16.bytes;
+    r->weights_fp32 = m->arena32.bytes + m->cls_arena.bytes;
+    r->workspace = m->ws.bytes;
+    r->scratch = m->split_ws.bytes + m->split_tickets.bytes + m->err.bytes;
+    for (const auto& kv : m->plans) {
+      const auto& p = *kv.second;
+      r->logits += p.lazy16.bytes + p.lazy32.bytes;
+      r->scratch += p.small_buf.bytes + p.rs_buf.bytes;
+    }
+    r->total = r->weights_fast + r->weights_fp32 + r->workspace + r->logits + r->scratch;
+  });
+}
+
 int prlab_gpu_forward(prlab_gpu_model* m, const int32_t* ids, int64_t B, int64_t S,
                       const prlab_policy* policy, float* logits, prlab_trace* trace) {
   return guarded([&] {
@@ -1368,7 +1404,7 @@ int prlab_gpu_forward(prlab_gpu_model* m, const int32_t* ids, int64_t B, int64_t
       // the fp32 logits bit for bit -- half the PCIe bytes (host_widen.cpp), but host-thread
       // work whose speed depends on the host; the first call of a plan times both copy-outs
       // of the same logits and keeps the faster one
-      run_forward(*m, p, p.ids, p.logit16, PRLAB_OUT_F16, p.ld16, st, graph);
+      run_forward(*m, p, p.ids, plan_logits16(p), PRLAB_OUT_F16, p.ld16, st, graph);
       if (const char* force = std::getenv("PRLAB_HOST_COPY"))  // "widen" / "fp32": skip the timing
         p.copy_mode = std::strcmp(force, "widen") == 0 ? 1 : 2;
       if (p.copy_mode == 0) {
@@ -1379,7 +1415,7 @@ int prlab_gpu_forward(prlab_gpu_model* m, const int32_t* ids, int64_t B, int64_t
           d2h_widen_f16(p.logit16, p.ld16, logits, w, B * S, w, st);
           t_w = std::min(t_w, std::chrono::duration<double>(clk::now() - t0).count());
         }
-        convert_f16_to_f32(p.logit16, p.ld16, p.out32, w, static_cast<int>(B * S), static_cast<int>(w), st);
+        convert_f16_to_f32(p.logit16, p.ld16, plan_out32(p), w, static_cast<int>(B * S), static_cast<int>(w), st);
         PRLAB_CUDA(cudaStreamSynchronize(st));
         for (int r = 0; r < 3; ++r) {
           const auto t0 = clk::now();
@@ -1391,12 +1427,12 @@ int prlab_gpu_forward(prlab_gpu_model* m, const int32_t* ids, int64_t B, int64_t
       } else if (p.copy_mode == 1) {
         d2h_widen_f16(p.logit16, p.ld16, logits, w, B * S, w, st);
       } else {
-        convert_f16_to_f32(p.logit16, p.ld16, p.out32, w, static_cast<int>(B * S), static_cast<int>(w), st);
+        convert_f16_to_f32(p.logit16, p.ld16, plan_out32(p), w, static_cast<int>(B * S), static_cast<int>(w), st);
         PRLAB_CUDA(cudaMemcpyAsync(logits, p.out32, B * S * w * 4, cudaMemcpyDeviceToHost, st));
         PRLAB_CUDA(cudaStreamSynchronize(st));
       }
     } else {
-      run_forward(*m, p, p.ids, p.out32, PRLAB_OUT_F32, w, st, graph);
+      run_forward(*m, p, p.ids, plan_out32(p), PRLAB_OUT_F32, w, st, graph);
       PRLAB_CUDA(cudaMemcpyAsync(logits, p.out32, B * S * w * 4, cudaMemcpyDeviceToHost, st));
       PRLAB_CUDA(cudaStreamSynchronize(st));
     }
@@ -1429,6 +1465,7 @@ int prlab_gpu_forward_ex(prlab_gpu_model* m, const int32_t* ids, int64_t B, int6
     if (retain) o.tap = tap.f();
     std::vector<std::tuple<int, cudaEvent_t, cudaEvent_t>> ev;
     if (timed) o.timing = &ev;
+    plan_out32(p);
     if (!retain && !timed)
       run_forward(*m, p, p.ids, p.out32, PRLAB_OUT_F32, w, st, !std::getenv("PRLAB_NO_GRAPH"));
     else
@@ -1555,7 +1592,8 @@ void enqueue_nll(prlab_gpu_model& m, prlab_gpu_model::Plan& p, const int32_t* d_
     p.rs_state = 2;
     if (p.fast && !std::getenv("PRLAB_NO_FUSED_NLL")) {
       // the head GEMM exactly as the logits path plans it, with the statistics epilogue
-      GemmPlan probe = plan_gemm_tc(p.xn16, m.h, m.emb16, m.h, nullptr, p.logit16, p.ld16, static_cast<int>(M),
+      // (planning only, never launched: any 16-byte-aligned device pointer serves as the output base)
+      GemmPlan probe = plan_gemm_tc(p.xn16, m.h, m.emb16, m.h, nullptr, p.xn16, p.ld16, static_cast<int>(M),
                                     static_cast<int>(V), static_cast<int>(m.h), EPI_F16, &m.scratch);
       if (probe.pair) {
         const int nslots = ((static_cast<int>(V) + probe.bn - 1) / probe.bn) * 2;  // 2 column groups per tile
@@ -1579,10 +1617,10 @@ void enqueue_nll(prlab_gpu_model& m, prlab_gpu_model::Plan& p, const int32_t* d_
     launch_gemm_tc(hp, st);
     rowstat_combine(p.rs_buf.p, hp.nslots, M, V, d_targets, hp.tval, d_nll, d_argmax, st);
   } else if (p.fast) {  // unfused: logits into the workspace, then the row kernel
-    enqueue_forward(m, p, d_ids, p.logit16, PRLAB_OUT_F16, p.ld16, st);
+    enqueue_forward(m, p, d_ids, plan_logits16(p), PRLAB_OUT_F16, p.ld16, st);
     row_nll(p.logit16, 1, M, V, p.ld16, d_targets, d_nll, d_argmax, st);
   } else {
-    enqueue_forward(m, p, d_ids, p.out32, PRLAB_OUT_F32, V, st);
+    enqueue_forward(m, p, d_ids, plan_out32(p), PRLAB_OUT_F32, V, st);
     row_nll(p.out32, 0, M, V, V, d_targets, d_nll, d_argmax, st);
   }
 }

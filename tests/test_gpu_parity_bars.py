@@ -8,8 +8,9 @@ SURVEY.md section 8(d)), at the benchmark configurations themselves:
   * C4 (GPT-2 hybrid, batch 32, seq 512) at forward level: first and last sequence vs the
     CPU oracle (cosine >= 0.9998, zero non-finite, max-abs <= 5e-3 vs CPU hybrid);
   * GPT-2 greedy argmax at C2 (1 x 128): fp32 path bit-exact off near-ties (gap < 1e-5);
-    hybrid agreement rate vs CPU hybrid, exact on every row whose CPU top-2 gap is >= 3e-3
-    (above the measured GPU<->CPU hybrid drift), near-tie rows reported separately;
+    hybrid agreement rate vs CPU hybrid, reported with the rows whose CPU top-2 gap is below
+    3e-3 listed separately, and EXACT on every row whose gap exceeds twice
+    the measured max |GPU - CPU| of that forward (no drift of two logits can swap them);
   * the presets' hybrid path vs CPU HYBRID (not only fp32), and the drift by depth.
 
 Every measured number is also appended to $PRLAB_PARITY_REPORT (JSON lines) when set.
@@ -106,8 +107,11 @@ def test_c2_greedy_argmax():
     cpuh = o.forward(cfg, p, ids, 1, 128, "hybrid")
     gh = m.forward(ids, 1, 128, "hybrid")
     sh = _argmax_stats(gh, cpuh, 3e-3)
-    report(test="argmax_c2", policy="hybrid", **sh)
-    assert sh["clear_agree"] == sh["clear_rows"], sh
+    drift = compare_logits(cpuh, gh)["max_abs_error"]
+    sx = _argmax_stats(gh, cpuh, max(3e-3, 2 * drift))
+    report(test="argmax_c2", policy="hybrid", max_abs_drift=drift, **sh,
+           beyond_2x_drift={"rows": sx["clear_rows"], "agree": sx["clear_agree"]})
+    assert sx["clear_agree"] == sx["clear_rows"], sx
 
 
 def test_c4_forward_first_last_sequence():
@@ -134,13 +138,15 @@ def test_c4_forward_first_last_sequence():
         cpu32 = o.forward(cfg, p, seq, 1, S, "fp32")
         rh, r32 = compare_logits(cpuh, got), compare_logits(cpu32, got)
         sh = _argmax_stats(got, cpuh, 3e-3)
+        sx = _argmax_stats(got, cpuh, max(3e-3, 2 * rh["max_abs_error"]))
         report(test="c4_forward", seq=b, vs_cpu_hybrid=rh, vs_cpu_fp32=r32,
                argmax_vs_cpu_hybrid={k: v for k, v in sh.items() if k != "near_tie_rows"},
-               near_tie_rows=len(sh["near_tie_rows"]))
+               near_tie_rows_gap_below_3e3=len(sh["near_tie_rows"]),
+               beyond_2x_drift={"rows": sx["clear_rows"], "agree": sx["clear_agree"]})
         assert rh["candidate_nonfinite"] == 0 and r32["candidate_nonfinite"] == 0
         assert rh["cosine"] >= 0.9998 and r32["cosine"] >= 0.9998, (rh, r32)
         assert rh["max_abs_error"] <= 5e-3, rh
-        assert sh["clear_agree"] == sh["clear_rows"], sh
+        assert sx["clear_agree"] == sx["clear_rows"], sx
 
 
 @pytest.mark.parametrize("name,B,S", [("gpt2_small", 1, 128), ("bert_base", 2, 64), ("gpt2_small", 2, 77),
