@@ -69,6 +69,7 @@ enum : int {
 
 struct FaArgs {
   int B, S, H, causal, nqt, h;
+  int unstab;  // full_fp16 fast path: unstabilised softmax (no max shift, kernels.cpp:155)
   __half* ctx;
   int64_t ld_ctx;
   long long* dbg;  // optional clock64 stamps of CTA 0, [block][8] (scripts/fa_phases.py), null = off
@@ -259,7 +260,7 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fa_kernel(const __grid_const
         // block max over both halves of the raw accumulators (round16(x * 0.125) is monotone)
         float m0 = NEG_INF, m1 = NEG_INF;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
+        for (int h = 0; h < 2 && !a.unstab; ++h) {
           const int c = 32 * h;
           if (h == 0 ? dead0 : dead1) continue;
           uint32_t v[32];
@@ -280,20 +281,23 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fa_kernel(const __grid_const
             }
           }
         }
-        float* rmax = red + (bc & 1) * 256;
-        rmax[half * 128 + r] = fmaxf(m0, m1);
-        if (ts) ts[1] = clock64();
-        named_bar_sync(1, 32 * kSoftmaxWarps);
-        if (ts) ts[2] = clock64();
-        const float mraw = fmaxf(rmax[r], rmax[128 + r]);
-        const float mblk = mraw == NEG_INF ? NEG_INF : __fmul_rn(r16(mraw), 0.125f);
-        const float mnew = fmaxf(m, mblk);
+        float mnew = 0.0f;  // unstabilised: e = exp(s) (the reference's full_fp16 softmax)
+        if (!a.unstab) {
+          float* rmax = red + (bc & 1) * 256;
+          rmax[half * 128 + r] = fmaxf(m0, m1);
+          if (ts) ts[1] = clock64();
+          named_bar_sync(1, 32 * kSoftmaxWarps);
+          if (ts) ts[2] = clock64();
+          const float mraw = fmaxf(rmax[r], rmax[128 + r]);
+          const float mblk = mraw == NEG_INF ? NEG_INF : __fmul_rn(r16(mraw), 0.125f);
+          mnew = fmaxf(m, mblk);
+        }
         // Lazy rescaling: O and l are rescaled (and m moved) only when some row of the
         // warp saw its max grow by more than kLazy; otherwise this block's exponentials use
         // the stale max, e <= e^kLazy, well inside fp16 -- and fp16 rounding is relative, so
         // P~ keeps its precision.  Saves the O round trip through TMEM on most blocks.
         constexpr float kLazy = 5.0f;
-        const bool rescale = kb > 0 && __any_sync(0xffffffffu, mnew > m + kLazy);
+        const bool rescale = !a.unstab && kb > 0 && __any_sync(0xffffffffu, mnew > m + kLazy);
         const float mold = m;
         if (kb == 0 || rescale) m = mnew;
         // e = exp(s - m), P~ = round16(e) -> TMEM
@@ -377,7 +381,9 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fa_kernel(const __grid_const
       // both partial sums visible (the next write of rsum is a unit later, behind at least
       // one block barrier that this warp reaches only after its read)
       named_bar_sync(1, 32 * kSoftmaxWarps);
-      const float lt = __fadd_rn(rsum[r], rsum[128 + r]);
+      // full_fp16: the reference sums e on the binary16 lattice -- a sum past 65504 is inf
+      // (p -> 0), an overflowed e is inf (p -> inf / inf = NaN, kernels.cpp:154-165)
+      const float lt = a.unstab ? r16(__fadd_rn(rsum[r], rsum[128 + r])) : __fadd_rn(rsum[r], rsum[128 + r]);
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[F_TFREE]);
       if (qrow < a.S) {
@@ -435,6 +441,7 @@ void launch_attn_fa(const AttnPlan& p, cudaStream_t st) {
   a.ctx = reinterpret_cast<__half*>(p.ctx);
   a.ld_ctx = p.ld_ctx;
   a.dbg = p.dbg;
+  a.unstab = p.unstab;
   const int units = p.B * p.H * a.nqt;
   const int grid = std::min(units, 2 * num_sms());
   launch_pdl(attn_fa_kernel, dim3(grid), dim3(kThreads), kFaSmemBytes, st, p.tmQKV, a);

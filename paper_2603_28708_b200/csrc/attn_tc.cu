@@ -475,7 +475,8 @@ void launch_attn_tc(const AttnPlan& p, cudaStream_t st, float* tap) {
   // resident-row kernel's 16 softmax warps per tile finish first (C3 sweep A/B,
   // profiles/r01/ab_attn_c3_sweep.txt: B=8 S=32 0.557 vs 0.590 ms, B=16 S=32 0.698 vs 0.653).
   const int nqt = (p.S + 127) / 128;
-  if (tap == nullptr && attn_fa_enabled() && (nqt > 1 || p.B * p.H > num_sms())) {
+  if (p.unstab && tap != nullptr) throw std::invalid_argument("unstabilised softmax has no score tap");
+  if (p.unstab || (tap == nullptr && attn_fa_enabled() && (nqt > 1 || p.B * p.H > num_sms()))) {
     launch_attn_fa(p, st);
     return;
   }

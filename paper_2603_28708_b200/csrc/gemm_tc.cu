@@ -46,7 +46,17 @@ struct GemmArgs {
   const int32_t* targets;  // EPI_ROWSTAT: target column per row (< 0: none)
   float* tval;             // EPI_ROWSTAT: round16 logit at the target column per row
   long long* dbg; // optional per-CTA %globaltimer stamps [grid][8] (debug), null = off
+  int acc16;      // FP16 accumulator (idesc c_format F16; full_fp16 fast path), else FP32
 };
+
+// An FP16 accumulator sits in the low half of each 32-bit TMEM cell (probed on B200,
+// scripts/ubench/probe_tmem_layout.cu): widen it so the fp32 epilogues apply unchanged
+// (exact: every binary16 value is an fp32 value).
+__device__ __forceinline__ void acc16_widen(uint32_t (&u)[32]) {
+#pragma unroll
+  for (int i = 0; i < 32; ++i)
+    u[i] = __float_as_uint(__half2float(__ushort_as_half(static_cast<unsigned short>(u[i] & 0xFFFFu))));
+}
 
 // LEAN: half-depth pipeline (~100 KB smem) so two CTAs -- this kernel's and the
 // next PDL-launched kernel's -- can be co-resident on an SM at batch-1 sizes.
@@ -267,7 +277,7 @@ __global__ void __launch_bounds__(Cfg<BN, LEAN, EPI>::THREADS, 1)
     __syncwarp();
   } else if (warp == 1) {
     // ---------------- MMA issuer ----------------
-    constexpr uint32_t idesc = idesc_f16_f32(BM, BN, 0, 0);
+    const uint32_t idesc = idesc_f16_f32(BM, BN, 0, 0) & (g.acc16 ? ~(3u << 4) : ~0u);
     uint32_t stage = 0, phase = 0, t = 0;
     for (int unit = blockIdx.x; unit < total_units; unit += gridDim.x, ++t) {
       int tile, split, kb0, kb1;
@@ -339,6 +349,7 @@ __global__ void __launch_bounds__(Cfg<BN, LEAN, EPI>::THREADS, 1)
             uint32_t u[32];
             tmem_ld32(tmem_base + ((quad * 32) << 16) + acc * BN + c + h, u);
             tmem_wait_ld();
+            if (g.acc16) acc16_widen(u);
             const float* sb = has_bias ? sbias + (c - cbase) + h : nullptr;
             if (F32OUT) {
               float v[32];
@@ -375,6 +386,7 @@ __global__ void __launch_bounds__(Cfg<BN, LEAN, EPI>::THREADS, 1)
           uint32_t u[32];
           tmem_ld32(tmem_base + ((quad * 32) << 16) + acc * BN + c, u);
           tmem_wait_ld();
+          if (g.acc16) acc16_widen(u);
           float v[32];
 #pragma unroll
           for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(u[i]);
@@ -391,6 +403,7 @@ __global__ void __launch_bounds__(Cfg<BN, LEAN, EPI>::THREADS, 1)
           uint32_t u[32];
           tmem_ld32(tmem_base + ((quad * 32) << 16) + acc * BN + c, u);
           tmem_wait_ld();
+          if (g.acc16) acc16_widen(u);
 #pragma unroll
           for (int i = 0; i < 32; i += 4)
             __stcg(reinterpret_cast<float4*>(wrow + c + i),
@@ -611,7 +624,7 @@ __global__ void __launch_bounds__(CCfg<BN>::THREADS, 1)
     }
     __syncwarp();
   } else if (warp == 1) {
-    constexpr uint32_t idesc = idesc_f16_f32(BM, BN, 0, 0);
+    const uint32_t idesc = idesc_f16_f32(BM, BN, 0, 0) & (g.acc16 ? ~(3u << 4) : ~0u);
     uint32_t stage = 0, phase = 0;
     for (int kb = kb0; kb < kb1; ++kb) {
       mbar_wait(&full[stage], phase);
@@ -642,6 +655,7 @@ __global__ void __launch_bounds__(CCfg<BN>::THREADS, 1)
       uint32_t u[32];
       tmem_ld32(tmem_base + ((quad * 32) << 16) + c, u);
       tmem_wait_ld();
+      if (g.acc16) acc16_widen(u);
       float* dst = part + r * C::PSTRIDE + c;
 #pragma unroll
       for (int i = 0; i < 32; i += 4)
@@ -939,7 +953,7 @@ __global__ void __launch_bounds__(Cfg2<BN, EPI>::THREADS, 1)
   } else if (warp == 1) {
     // ---------------- MMA issuer (leader only) ----------------
     if (leader) {
-      constexpr uint32_t idesc = idesc_f16_f32(256, BN, 0, 0);
+      const uint32_t idesc = idesc_f16_f32(256, BN, 0, 0) & (g.acc16 ? ~(3u << 4) : ~0u);
       uint32_t stage = 0, phase = 0, t = 0;
       for (int unit = pair; unit < total_units; unit += npairs, ++t) {
         const uint32_t acc = t & 1, acc_phase = (t >> 1) & 1;
@@ -1010,6 +1024,7 @@ __global__ void __launch_bounds__(Cfg2<BN, EPI>::THREADS, 1)
           uint32_t u[32];
           tmem_ld32(tmem_base + ((quad * 32) << 16) + acc * BN + c, u);
           tmem_wait_ld();
+          if (g.acc16) acc16_widen(u);
           const int col0 = n_blk * BN + c;
           float v[32];
           float cm = ninf;
@@ -1059,6 +1074,7 @@ __global__ void __launch_bounds__(Cfg2<BN, EPI>::THREADS, 1)
           uint32_t u[32];
           tmem_ld32(tmem_base + ((quad * 32) << 16) + acc * BN + c + h, u);
           tmem_wait_ld();
+          if (g.acc16) acc16_widen(u);
           const float* sb = has_bias ? sbias + (c - cbase) + h : nullptr;
           if (F32OUT) {
             float v[32];
@@ -1380,6 +1396,7 @@ void launch_gemm_tc(const GemmPlan& p, cudaStream_t st) {
   g.dbg = debug_stamps();
   g.targets = p.targets;
   g.tval = p.tval;
+  g.acc16 = p.acc16 ? 1 : 0;
   if (p.pair) {
     if (p.bn == 256)
       launch_pair_bn<256>(p, g, st);

@@ -104,6 +104,7 @@ struct GemmPlan {
   const int32_t* targets = nullptr;  // EPI_ROWSTAT
   float* tval = nullptr;
   int nslots = 0;
+  bool acc16 = false;  // FP16 accumulator (full_fp16 fast path)
 };
 // Split-K scratch: fp32 partial tiles + per-tile tickets (zero between launches).
 // One per model: kernels of one forward run in stream order, so they share it.
@@ -148,6 +149,7 @@ struct AttnPlan {
   int B, S, H, hd, causal;
   int64_t ld_qkv, ld_ctx;
   long long* dbg = nullptr;  // phase timestamps (debug)
+  int unstab = 0;            // unstabilised softmax (full_fp16 fast path, kernels.cpp:155): no max shift
 };
 bool attn_tc_supported(int S, int hd);
 AttnPlan plan_attn_tc(const void* qkv, int64_t ld_qkv, void* ctx, int64_t ld_ctx, int B, int S,
@@ -220,8 +222,9 @@ void transpose_to_f16(const float* in, int rows, int cols, __half* out, int64_t 
 void round16_inplace(float* x, int64_t n, cudaStream_t st);
 
 // fast-path LayerNorm for h % 128 == 0 (warp per row): fp32 x -> fp16 lattice (hybrid)
+// x_round (full_fp16 fast path): x itself, rounded onto the binary16 lattice in place first
 void ln_f32_to_f16(const float* x, int rows, int n, const float* gamma, const float* beta,
-                   float eps, __half* out, cudaStream_t st);
+                   float eps, __half* out, cudaStream_t st, float* x_round = nullptr);
 // fast embed for the hybrid path (fp32 add, float4)
 void embed_f32(const float* tok, int64_t vocab, const float* pos, int h, const int32_t* ids,
                int B, int S, float* out, int* err_flag, cudaStream_t st);

@@ -229,10 +229,10 @@ __global__ void simt_layernorm_kernel(const float* __restrict__ x, int rows, int
 // round16 of the next op is applied here).  One warp per row, n = 128*VPT,
 // row held in registers (two-pass mean / variance like the reference).
 template <int VPT>
-__global__ void __launch_bounds__(256) ln_f16_kernel(const float* __restrict__ x, int rows,
+__global__ void __launch_bounds__(256) ln_f16_kernel(const float* x, int rows,
                                                      const float* __restrict__ gamma,
                                                      const float* __restrict__ beta, float eps,
-                                                     __half* __restrict__ out) {
+                                                     __half* __restrict__ out, float* x_round) {
   // Persistent warps over rows (grid-stride, as many blocks as are co-resident), the next
   // row's loads issued before the current row's reductions, so DRAM stays busy through the
   // reduction and store phases (C4: 15.2 -> 14.2 us per call; a TMA bulk-copy ring of 4
@@ -256,6 +256,17 @@ __global__ void __launch_bounds__(256) ln_f16_kernel(const float* __restrict__ x
     float4 v[VPT];
 #pragma unroll
     for (int i = 0; i < VPT; ++i) v[i] = nxt[i];
+    if (x_round) {
+      // full_fp16 fast path: the residual stream lives on the binary16 lattice (Residual
+      // class F16E, kernels.cpp:237-254): the fp32 sum the residual GEMM added in L2 is
+      // rounded here, once, before anything reads it -- round16(x + y) exactly
+      float4* w = reinterpret_cast<float4*>(x_round + static_cast<int64_t>(row) * n);
+#pragma unroll
+      for (int i = 0; i < VPT; ++i) {
+        v[i] = make_float4(r16(v[i].x), r16(v[i].y), r16(v[i].z), r16(v[i].w));
+        w[lane + 32 * i] = v[i];
+      }
+    }
     if (row + stride < rows) {
       const float4* in = reinterpret_cast<const float4*>(x + static_cast<int64_t>(row + stride) * n);
 #pragma unroll
@@ -505,7 +516,7 @@ void simt_layernorm(const float* x, int rows, int n, const float* gamma, const f
 // persistent warps: as many 256-thread blocks as are co-resident (register-bound)
 template <int VPT>
 void launch_ln(const float* x, int rows, const float* gamma, const float* beta, float eps, __half* out,
-               cudaStream_t st) {
+               cudaStream_t st, float* x_round) {
   static int per_sm_dev[64] = {};
   int& per_sm = per_sm_dev[current_device() & 63];
   if (per_sm == 0) {
@@ -514,19 +525,20 @@ void launch_ln(const float* x, int rows, const float* gamma, const float* beta, 
     per_sm = std::max(1, v);
   }
   const int grid = std::min((rows + 7) / 8, num_sms() * per_sm);
-  launch_pdl(ln_f16_kernel<VPT>, dim3(grid), dim3(256), 0, st, x, rows, gamma, beta, eps, out);
+  launch_pdl(ln_f16_kernel<VPT>, dim3(grid), dim3(256), 0, st, x, rows, gamma, beta, eps, out, x_round);
 }
 
 void ln_f32_to_f16(const float* x, int rows, int n, const float* gamma, const float* beta,
-                   float eps, __half* out, cudaStream_t st) {
+                   float eps, __half* out, cudaStream_t st, float* x_round) {
   switch (n) {
-    case 128: launch_ln<1>(x, rows, gamma, beta, eps, out, st); break;
-    case 256: launch_ln<2>(x, rows, gamma, beta, eps, out, st); break;
-    case 384: launch_ln<3>(x, rows, gamma, beta, eps, out, st); break;
-    case 512: launch_ln<4>(x, rows, gamma, beta, eps, out, st); break;
-    case 768: launch_ln<6>(x, rows, gamma, beta, eps, out, st); break;
-    case 1024: launch_ln<8>(x, rows, gamma, beta, eps, out, st); break;
+    case 128: launch_ln<1>(x, rows, gamma, beta, eps, out, st, x_round); break;
+    case 256: launch_ln<2>(x, rows, gamma, beta, eps, out, st, x_round); break;
+    case 384: launch_ln<3>(x, rows, gamma, beta, eps, out, st, x_round); break;
+    case 512: launch_ln<4>(x, rows, gamma, beta, eps, out, st, x_round); break;
+    case 768: launch_ln<6>(x, rows, gamma, beta, eps, out, st, x_round); break;
+    case 1024: launch_ln<8>(x, rows, gamma, beta, eps, out, st, x_round); break;
     default:
+      if (x_round) throw std::invalid_argument("fp16-lattice LayerNorm needs h in {128..1024, step 128}");
       simt_layernorm(x, rows, n, gamma, beta, eps, Kcfg{0, 0, 1}, nullptr, out, 0, st);
       return;
   }

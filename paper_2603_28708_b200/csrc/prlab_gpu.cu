@@ -197,6 +197,14 @@ bool is_hybrid(const prlab_policy& p) {
   }
   return true;
 }
+// The built-in full_fp16 assignment (src/policy.cpp:55): every class {F16E, F16E}, unstabilised.
+bool is_full_fp16(const prlab_policy& p) {
+  for (int i = 0; i < PRLAB_NUM_OP_CLASSES; ++i) {
+    const prlab_kcfg& c = p.cls[i];
+    if (c.compute != 1 || c.accum != 1 || c.stabilized) return false;
+  }
+  return true;
+}
 uint64_t policy_key(const prlab_policy& p) {
   uint64_t k = 0;
   for (int i = 0; i < PRLAB_NUM_OP_CLASSES; ++i)
@@ -489,6 +497,7 @@ struct prlab_gpu_model {
   struct Plan {
     int64_t B = 0, S = 0;
     bool fast = false;
+    bool fp16 = false;  // full_fp16 on the tensor cores (fast16_eligible)
     prlab_policy pol{};
     float* x = nullptr;
     __half *xn16 = nullptr, *big16 = nullptr, *logit16 = nullptr;
@@ -571,12 +580,26 @@ struct StreamOrder {
 };
 
 // Fast (tensor-core) path eligibility: the hybrid policy and TMA-friendly extents.
-bool fast_eligible(const prlab_gpu_model& m, int64_t S, const prlab_policy& pol) {
-  if (!is_hybrid(pol) || m.L < 1) return false;
+bool tc_shape_ok(const prlab_gpu_model& m, int64_t S) {
+  if (m.L < 1) return false;
   if (m.h % 128 != 0 || m.h > 1024 || m.f % 64 != 0) return false;
   if (!attn_tc_supported(static_cast<int>(S), static_cast<int>(m.hd))) return false;
   if (std::getenv("PRLAB_FORCE_GENERIC")) return false;
   return true;
+}
+bool fast_eligible(const prlab_gpu_model& m, int64_t S, const prlab_policy& pol) {
+  return is_hybrid(pol) && tc_shape_ok(m, S);
+}
+// full_fp16 on the tensor cores (C5 speed arm): FP16 accumulators, the residual stream and
+// every op output on the binary16 lattice, unstabilised softmax.  It rounds once per
+// 16-wide MMA step instead of after every product (the reference's per-MAC emulation,
+// src/kernels.cpp:56-66), so it is selected only when per-MAC exactness is not asked for:
+// `exact` plans (retain_scores) and PRLAB_FP16_EXACT=1 keep the exact SIMT emulation that
+// reproduces the reference's known-answer tests.
+bool fast16_eligible(const prlab_gpu_model& m, int64_t S, const prlab_policy& pol, bool exact) {
+  if (exact || !is_full_fp16(pol) || !tc_shape_ok(m, S)) return false;
+  const char* e = std::getenv("PRLAB_FP16_EXACT");
+  return e == nullptr || std::atoi(e) == 0;
 }
 
 void h2d(void* dst, const float* src, size_t n) {
@@ -767,12 +790,14 @@ void plan_small(prlab_gpu_model& m, prlab_gpu_model::Plan& p, int64_t B, int64_t
   p.small = true;
 }
 
-prlab_gpu_model::Plan& get_plan(prlab_gpu_model& m, int64_t B, int64_t S, const prlab_policy& pol) {
-  const auto key = std::make_tuple(B, S, policy_key(pol));
+prlab_gpu_model::Plan& get_plan(prlab_gpu_model& m, int64_t B, int64_t S, const prlab_policy& pol,
+                                bool exact = false) {
+  const bool fast16 = fast16_eligible(m, S, pol, exact);
+  const auto key = std::make_tuple(B, S, policy_key(pol) | (fast16 ? 1ull << 40 : 0ull));
   auto it = m.plans.find(key);
   if (it != m.plans.end()) return *it->second;
 
-  const bool fast = fast_eligible(m, S, pol);
+  const bool fast = fast_eligible(m, S, pol) || fast16;
   if (!fast) ensure_f32(m);
   const int64_t M = B * S, h = m.h, f = m.f, V = m.V;
   const int64_t outw = m.L > 0 ? V : h;
@@ -803,6 +828,7 @@ prlab_gpu_model::Plan& get_plan(prlab_gpu_model& m, int64_t B, int64_t S, const 
   p.S = S;
   p.pol = pol;
   p.fast = fast;
+  p.fp16 = fast16;
   p.ld16 = ld16;
   auto at = [&](int s) { return ap.offs[s]; };
   p.x = m.ws.at<float>(at(s_x));
@@ -821,7 +847,12 @@ prlab_gpu_model::Plan& get_plan(prlab_gpu_model& m, int64_t B, int64_t S, const 
     }
     p.attn = plan_attn_tc(p.big16, 3 * h, p.xn16, h, static_cast<int>(B), static_cast<int>(S),
                           static_cast<int>(m.H), static_cast<int>(m.hd), m.d.archetype == 1);
-    if (fwd_small_supported(M, S, h, f, m.hd, m.L)) plan_small(m, p, B, S);
+    if (fast16) {
+      for (auto& g : p.gemms) g.acc16 = true;
+      p.attn.unstab = 1;
+    } else if (fwd_small_supported(M, S, h, f, m.hd, m.L)) {
+      plan_small(m, p, B, S);
+    }
   } else {
     p.xn32 = m.ws.at<float>(at(s_a));
     p.qkv32 = m.ws.at<float>(at(s_b));
@@ -875,19 +906,23 @@ int64_t enqueue_forward(prlab_gpu_model& m, prlab_gpu_model::Plan& p, const int3
     launch_fwd_small(sp, st);
     n += 1;
   } else if (p.fast) {
-    T(PRLAB_EMBEDDING, [&] { embed_f32(m.tok, V, m.pos, hi, ids, Bi, Si, p.x, err, st); });
+    float* xr = p.fp16 ? p.x : nullptr;  // full_fp16: LN rounds the residual stream in place first
+    if (p.fp16)  // embed with every operand conformed to binary16 (kernels.cpp:256-294, F16E)
+      T(PRLAB_EMBEDDING, [&] { simt_embed(m.tok, V, m.pos, hi, ids, Bi, Si, Kcfg{1, 1, 0}, p.x, err, st); });
+    else
+      T(PRLAB_EMBEDDING, [&] { embed_f32(m.tok, V, m.pos, hi, ids, Bi, Si, p.x, err, st); });
     for (int64_t l = 0; l < L; ++l) {
       const auto& w = m.l16[l];
       float* tap = o.tap ? o.tap + l * tap_stride : nullptr;
-      T(PRLAB_LAYERNORM, [&] { ln_f32_to_f16(p.x, Mi, hi, w.ln1g, w.ln1b, 1e-5f, p.xn16, st); });  // LN1
+      T(PRLAB_LAYERNORM, [&] { ln_f32_to_f16(p.x, Mi, hi, w.ln1g, w.ln1b, 1e-5f, p.xn16, st, xr); });  // LN1
       T(PRLAB_LINEAR, [&] { launch_gemm_tc(p.gemms[4 * l + 0], st); });                          // QKV (+bias)
       T(PRLAB_ATTENTION_SCORE_MATMUL, [&] { launch_attn_tc(p.attn, st, tap); });                // -> ctx (xn16)
       T(PRLAB_LINEAR, [&] { launch_gemm_tc(p.gemms[4 * l + 1], st); });                          // Wo + residual
-      T(PRLAB_LAYERNORM, [&] { ln_f32_to_f16(p.x, Mi, hi, w.ln2g, w.ln2b, 1e-5f, p.xn16, st); });  // LN2
+      T(PRLAB_LAYERNORM, [&] { ln_f32_to_f16(p.x, Mi, hi, w.ln2g, w.ln2b, 1e-5f, p.xn16, st, xr); });  // LN2
       T(PRLAB_LINEAR, [&] { launch_gemm_tc(p.gemms[4 * l + 2], st); });                          // FFN1 + GELU
       T(PRLAB_LINEAR, [&] { launch_gemm_tc(p.gemms[4 * l + 3], st); });                          // FFN2 + residual
     }
-    T(PRLAB_LAYERNORM, [&] { ln_f32_to_f16(p.x, Mi, hi, m.lnfg, m.lnfb, 1e-5f, p.xn16, st); });
+    T(PRLAB_LAYERNORM, [&] { ln_f32_to_f16(p.x, Mi, hi, m.lnfg, m.lnfb, 1e-5f, p.xn16, st, xr); });
   }
   if (p.fast) {
     if (o.hidden_only) return n;  // forward_hidden: r16(final LN) in xn16 (the Linear lattice)
@@ -897,6 +932,7 @@ int64_t enqueue_forward(prlab_gpu_model& m, prlab_gpu_model::Plan& p, const int3
       auto it = p.head_plans.find(key);
       if (it == p.head_plans.end())
         it = p.head_plans.emplace(key, plan_gemm_tc(p.xn16, h, m.emb16, h, nullptr, out, ld, Mi, Vi, hi, EPI_F16, &m.scratch)).first;
+      it->second.acc16 = p.fp16;
       T(PRLAB_LINEAR, [&] { launch_gemm_tc(it->second, st); });  // tied head straight into the caller's buffer
     } else {
       __half* l16 = plan_logits16(p);
@@ -904,6 +940,7 @@ int64_t enqueue_forward(prlab_gpu_model& m, prlab_gpu_model::Plan& p, const int3
       auto it = p.head_plans.find(key);
       if (it == p.head_plans.end())
         it = p.head_plans.emplace(key, plan_gemm_tc(p.xn16, h, m.emb16, h, nullptr, l16, p.ld16, Mi, Vi, hi, EPI_F16, &m.scratch)).first;
+      it->second.acc16 = p.fp16;
       T(PRLAB_LINEAR, [&] { launch_gemm_tc(it->second, st); });
       T(PRLAB_LINEAR, [&] { convert_f16_to_f32(l16, p.ld16, static_cast<float*>(out), ld, Mi, Vi, st); });
     }
@@ -1454,7 +1491,7 @@ int prlab_gpu_forward_ex(prlab_gpu_model* m, const int32_t* ids, int64_t B, int6
     const bool retain = (flags & PRLAB_FWD_RETAIN_SCORES) != 0, timed = (flags & PRLAB_FWD_TIMED) != 0;
     if (retain && scores == nullptr) throw std::invalid_argument("retain_scores needs a scores buffer");
     PRLAB_CUDA(cudaSetDevice(m->device));
-    auto& p = get_plan(*m, B, S, *policy);
+    auto& p = get_plan(*m, B, S, *policy, retain);  // the score tap needs the exact (stabilised-order) kernels
     const int64_t w = m->L > 0 ? m->V : m->h;
     cudaStream_t st = m->stream;
     StreamOrder order(*m, st);
@@ -1601,6 +1638,7 @@ void enqueue_nll(prlab_gpu_model& m, prlab_gpu_model::Plan& p, const int32_t* d_
         p.rs_plan = plan_gemm_tc(p.xn16, m.h, m.emb16, m.h, nullptr, p.rs_buf.p, 8, static_cast<int>(M),
                                  static_cast<int>(V), static_cast<int>(m.h), EPI_ROWSTAT, &m.scratch, probe.bn);
         p.rs_plan.nslots = nslots;
+        p.rs_plan.acc16 = p.fp16;
         p.rs_plan.tval =
             reinterpret_cast<float*>(static_cast<char*>(p.rs_buf.p) + static_cast<size_t>(nslots) * M * 16);
         p.rs_state = p.rs_plan.pair ? 1 : 2;
@@ -1658,9 +1696,9 @@ int prlab_gpu_forward_kernel_count_ex(prlab_gpu_model* m, int64_t B, int64_t S, 
   return guarded([&] {
     check_forward_args(*m, B, S);
     if (out_dtype != PRLAB_OUT_F32 && out_dtype != PRLAB_OUT_F16) throw std::invalid_argument("unknown logits dtype");
-    const bool fast = fast_eligible(*m, S, *policy);
+    const bool fast = fast_eligible(*m, S, *policy) || fast16_eligible(*m, S, *policy, false);
     const int64_t L = m->L;
-    const bool small = fast && fwd_small_supported(B * S, S, m->h, m->f, m->hd, L);
+    const bool small = fast_eligible(*m, S, *policy) && fwd_small_supported(B * S, S, m->h, m->f, m->hd, L);
     // fast path: trunk (1 persistent kernel, or embed + 7 per layer + final LN) + the head GEMM,
     // + the fp16 -> fp32 widening kernel when fp32 logits are asked for
     const int64_t widen = fast && out_dtype == PRLAB_OUT_F32 ? 1 : 0;

@@ -1,5 +1,6 @@
 #!/usr/bin/env python3
-"""C5 precision ablation on the B200: fp32 vs full_fp16 vs hybrid at seq 512 for
+"""C5 precision ablation on the B200: fp32 vs full_fp16 (tensor-core fast path and the exact
+per-MAC emulation) vs hybrid at seq 512 for
 BERT-base and GPT-2 -- device latency (CUDA-graph replay, p50), fidelity against the
 GPU fp32 forward (cosine / max abs), and the NaN rate over adversarial models
 (make_adversarial_model restated in oracle/, target max score 30, 5 seeds).
@@ -60,14 +61,19 @@ def main():
             for pol in adv_nan:
                 adv_nan[pol] += int(not np.isfinite(am.forward(probe, 1, 32, pol)).all())
             am.close()
-        for pol in ["fp32", "full_fp16", "hybrid"]:
+        for pol, exact in [("fp32", 0), ("full_fp16", 0), ("full_fp16", 1), ("hybrid", 0)]:
+            # full_fp16: tensor-core FP16 accumulators (default) or the exact per-MAC emulation
+            os.environ["PRLAB_FP16_EXACT"] = str(exact)
             ms = time_policy(model, cfg, 1, S, pol)
             got = model.forward(ids, 1, S, pol)
             r = compare_logits(base, got)
-            print(json.dumps({"model": name, "seq": S, "batch": 1, "policy": pol, "p50_ms": round(ms, 4),
+            tag = pol + ("_exact_emulation" if exact else "")
+            print(json.dumps({"model": name, "seq": S, "batch": 1, "policy": tag, "p50_ms": round(ms, 4),
+                              "kernels": model.kernel_count(1, S, pol),
                               "cosine_vs_gpu_fp32": r["cosine"], "max_abs_vs_gpu_fp32": r["max_abs_error"],
                               "nonfinite": r["candidate_nonfinite"],
-                              "adversarial_nan_rate": adv_nan[pol] / 5.0}), flush=True)
+                              "adversarial_nan_rate": adv_nan[pol] / 5.0 if not exact else None}), flush=True)
+        os.environ.pop("PRLAB_FP16_EXACT", None)
         model.close()
 
 
