@@ -1026,6 +1026,8 @@ void run_forward(prlab_gpu_model& m, prlab_gpu_model::Plan& p, const int32_t* d_
   const auto key = std::make_tuple(static_cast<const void*>(d_ids), d_out, out_dtype, ld);
   auto it = p.graphs.find(key);
   if (it == p.graphs.end()) {
+    // buffers the recording needs are allocated before the capture (no cudaMalloc inside it)
+    if (p.fast && out_dtype == PRLAB_OUT_F32) plan_logits16(p);
     // capture on a private stream so a legacy-default caller stream still works
     cudaStream_t cap;
     PRLAB_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
