@@ -291,6 +291,9 @@ int prlab_gpu_debug_embedding_device(prlab_gpu_model* m, const int32_t* d_ids, i
                                      int32_t path, float* d_out, void* stream);
 /* Debug: per-stage %globaltimer stamps of the batch-1 persistent forward, [stage][grid][2]. */
 int prlab_gpu_debug_small_stamps(long long* dbg);
+/* Debug: phase stamps of the cluster batch-1 kernel, [cluster][CTA 0 / 15][layer][16]
+ * (%globaltimer; slot 15 = cycles the MMA issuer waited for weights in that layer). */
+int prlab_gpu_debug_cluster_stamps(long long* dbg);
 
 #ifdef __cplusplus
 }

@@ -219,6 +219,7 @@ EXPORTS = [
                                                  C.c_int64, C.c_int32, _P]),
     ("prlab_gpu_debug_gemm_stamps", C.c_int, [_P]),
     ("prlab_gpu_debug_small_stamps", C.c_int, [_P]),
+    ("prlab_gpu_debug_cluster_stamps", C.c_int, [_P]),
     ("prlab_gpu_attention_f16_device_dbg", C.c_int, [_P, _P, C.c_int64, C.c_int64, C.c_int64,
                                                      C.c_int64, C.c_int32, _P, _P]),
 ]

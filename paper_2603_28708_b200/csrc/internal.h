@@ -142,6 +142,31 @@ size_t fwd_small_workspace_floats(int64_t M, int64_t h, int64_t f);
 void launch_fwd_small(const FwdSmallPlan& p, cudaStream_t st);
 long long*& small_debug_stamps();  // [stage][grid][2] globaltimer stamps target (debug; null = off)
 
+// --- batch-1 forward_hidden on 16-CTA clusters owning 32-row blocks (fwd_cluster.cu) ---
+struct FwdClusterPlan {
+  int M, S, L, V, causal;
+  const void* host_lw;            // host array of per-layer {ln1g, ln1b, ln2g, ln2b, bqkv, bo, b1, b2}
+  CUtensorMap ctx_map;            // ctx rows [12 kb][128 rows][64], box 32 rows x 12 kb
+  const uint8_t* wstream;         // per-CTA weight streams (build_cluster_stream), L x 888 units of 16 KB
+  const float *tok, *pos, *lnfg, *lnfb;
+  const int32_t* ids;
+  int* err;
+  float* xg;
+  __half* ctxg;
+  __half* kvg;
+  float* part;
+  unsigned* flags;
+  __half* xn16;
+  int embed_only = 0;
+};
+bool fwd_cluster_supported(int64_t M, int64_t S, int64_t h, int64_t f, int64_t H, int64_t L);
+size_t fwd_cluster_workspace_bytes(int64_t L);
+size_t cluster_stream_bytes_per_layer();
+void build_cluster_stream(const __half* wqkv, const __half* wo, const __half* w1, const __half* w2, void* dst,
+                          cudaStream_t st);
+void launch_fwd_cluster(const FwdClusterPlan& p, cudaStream_t st);
+long long*& cluster_debug_stamps();  // [cluster][2][L][16] globaltimer phase stamps (debug; null = off)
+
 // --- fused tensor-core attention (hybrid, head_dim 64, seq <= 512) ---
 struct AttnPlan {
   CUtensorMap tmQKV;

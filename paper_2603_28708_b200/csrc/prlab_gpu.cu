@@ -481,6 +481,7 @@ struct prlab_gpu_model {
   DeviceBuffer cls_arena;
   float *pool_wt = nullptr, *pool_b = nullptr, *cls_wt = nullptr, *cls_b = nullptr;
 
+  DeviceBuffer cl_stream;  // batch-1 cluster kernel: per-CTA weight streams (built with its first plan)
   DeviceBuffer err;  // device error word (bad token ids)
   DeviceBuffer split_ws, split_tickets;
   SplitScratch scratch;
@@ -516,6 +517,11 @@ struct prlab_gpu_model {
     DeviceBuffer small_buf;  // ctx16 + scratch + barrier counter
     std::vector<CUtensorMap> small_maps;
     std::vector<std::array<const void*, 12>> small_lw;
+    // batch-1 shapes on 16-CTA clusters (fwd_cluster.cu); preferred over fwd_small when supported
+    bool cluster = false;
+    FwdClusterPlan cp{};
+    DeviceBuffer cl_buf;
+    std::vector<std::array<const float*, 8>> cl_lw;
     std::map<std::tuple<const void*, void*, int, int64_t>, cudaGraphExec_t> graphs;
     std::map<std::tuple<void*, int64_t>, GemmPlan> head_plans;
     // fused head statistics (prlab_gpu_forward_nll_device): 0 = not planned, 1 = fused, 2 = unfused
@@ -790,6 +796,53 @@ void plan_small(prlab_gpu_model& m, prlab_gpu_model::Plan& p, int64_t B, int64_t
   p.small = true;
 }
 
+// Cluster plan: per-layer weight maps (3D k-block views, boxes of 64 / 48 rows x one
+// k-block), the ctx map (32 rows x 12 k-blocks), and the L2 exchange buffers.
+void plan_cluster(prlab_gpu_model& m, prlab_gpu_model::Plan& p, int64_t B, int64_t S) {
+  const int64_t M = B * S, h = m.h, L = m.L;
+  if (m.cl_stream.p == nullptr) {  // once per model: every CTA rank's weights in consumption order
+    const size_t per = cluster_stream_bytes_per_layer();
+    m.cl_stream.alloc(per * static_cast<size_t>(L));
+    for (int64_t l = 0; l < L; ++l) {
+      const auto& w = m.l16[l];
+      build_cluster_stream(w.wqkv, w.wo, w.w1, w.w2, static_cast<char*>(m.cl_stream.p) + per * l, nullptr);
+    }
+    PRLAB_CUDA(cudaDeviceSynchronize());
+  }
+  ArenaPlan ap;
+  const int s_xg = ap.add(128 * h * 4), s_ctx = ap.add(128 * h * 2), s_kv = ap.add(L * 128 * 2 * h * 2),
+            s_part = ap.add(4 * 16 * h * 32 * 4), s_flags = ap.add(L * 4 * 16 * 4);
+  p.cl_buf.alloc(ap.total);
+  char* base = static_cast<char*>(p.cl_buf.p);
+  p.cl_lw.assign(static_cast<size_t>(L), {});
+  for (int64_t l = 0; l < L; ++l) {
+    const auto& w = m.l16[l];
+    p.cl_lw[l] = {w.ln1g, w.ln1b, w.ln2g, w.ln2b, w.bqkv, w.bo, w.b1, w.b2};
+  }
+  __half* ctxg = reinterpret_cast<__half*>(base + ap.offs[s_ctx]);
+  FwdClusterPlan& cp = p.cp;
+  cp.ctx_map = make_tmap_f16_3d(ctxg, 64, 128, h / 64, h, 64, 64, 32, static_cast<uint32_t>(h / 64));
+  cp.wstream = static_cast<const uint8_t*>(m.cl_stream.p);
+  cp.M = static_cast<int>(M);
+  cp.S = static_cast<int>(S);
+  cp.L = static_cast<int>(L);
+  cp.V = static_cast<int>(m.V);
+  cp.causal = m.d.archetype == 1;
+  cp.host_lw = p.cl_lw.data();
+  cp.tok = m.tok;
+  cp.pos = m.pos;
+  cp.lnfg = m.lnfg;
+  cp.lnfb = m.lnfb;
+  cp.err = m.err.at<int>(0);
+  cp.xg = reinterpret_cast<float*>(base + ap.offs[s_xg]);
+  cp.ctxg = ctxg;
+  cp.kvg = reinterpret_cast<__half*>(base + ap.offs[s_kv]);
+  cp.part = reinterpret_cast<float*>(base + ap.offs[s_part]);
+  cp.flags = reinterpret_cast<unsigned*>(base + ap.offs[s_flags]);
+  cp.xn16 = p.xn16;
+  p.cluster = true;
+}
+
 prlab_gpu_model::Plan& get_plan(prlab_gpu_model& m, int64_t B, int64_t S, const prlab_policy& pol,
                                 bool exact = false) {
   const bool fast16 = fast16_eligible(m, S, pol, exact);
@@ -852,6 +905,7 @@ prlab_gpu_model::Plan& get_plan(prlab_gpu_model& m, int64_t B, int64_t S, const 
       p.attn.unstab = 1;
     } else if (fwd_small_supported(M, S, h, f, m.hd, m.L)) {
       plan_small(m, p, B, S);
+      if (fwd_cluster_supported(M, S, h, f, m.H, m.L)) plan_cluster(m, p, B, S);
     }
   } else {
     p.xn32 = m.ws.at<float>(at(s_a));
@@ -901,9 +955,15 @@ int64_t enqueue_forward(prlab_gpu_model& m, prlab_gpu_model::Plan& p, const int3
   const int64_t tap_stride = B * m.H * S * S;
   if (p.fast && p.small && !o.tap && !o.timing) {
     // batch-1 shapes: embed .. final LN as one cooperative kernel (fwd_small.cu)
-    FwdSmallPlan sp = p.sp;
-    sp.ids = ids;
-    launch_fwd_small(sp, st);
+    if (p.cluster) {
+      FwdClusterPlan cp = p.cp;
+      cp.ids = ids;
+      launch_fwd_cluster(cp, st);
+    } else {
+      FwdSmallPlan sp = p.sp;
+      sp.ids = ids;
+      launch_fwd_small(sp, st);
+    }
     n += 1;
   } else if (p.fast) {
     float* xr = p.fp16 ? p.x : nullptr;  // full_fp16: LN rounds the residual stream in place first
@@ -1410,6 +1470,7 @@ int prlab_gpu_model_memory_ex(prlab_gpu_model* m, prlab_memory_report* r) {
     std::memset(r, 0, sizeof(*r));
     r->weights_fast = m->arena16.bytes;
     r->weights_fp32 = m->arena32.bytes + m->cls_arena.bytes;
+    r->weights_fast += m->cl_stream.bytes;  // the batch-1 cluster kernel's re-tiled fp16 linears
     r->workspace = m->ws.bytes;
     r->scratch = m->split_ws.bytes + m->split_tickets.bytes + m->err.bytes;
     for (const auto& kv : m->plans) {
@@ -1728,12 +1789,20 @@ int prlab_gpu_debug_embedding_device(prlab_gpu_model* m, const int32_t* d_ids, i
     if (path == 0) {
       embed_f32(m->tok, m->V, m->pos, static_cast<int>(m->h), d_ids, static_cast<int>(B), static_cast<int>(S), p.x,
                 m->err.at<int>(0), st);
-    } else {
+    } else if (path == 1) {
       if (!p.small) throw std::invalid_argument("embedding debug: shape not on the persistent batch-1 kernel");
       FwdSmallPlan sp = p.sp;
       sp.ids = d_ids;
       sp.embed_only = 1;
       launch_fwd_small(sp, st);
+    } else {
+      if (!p.cluster) throw std::invalid_argument("embedding debug: shape not on the cluster batch-1 kernel");
+      FwdClusterPlan cp = p.cp;
+      cp.ids = d_ids;
+      cp.embed_only = 1;
+      launch_fwd_cluster(cp, st);
+      PRLAB_CUDA(cudaMemcpyAsync(d_out, cp.xg, B * S * m->h * 4, cudaMemcpyDeviceToDevice, st));
+      return;
     }
     PRLAB_CUDA(cudaMemcpyAsync(d_out, p.x, B * S * m->h * 4, cudaMemcpyDeviceToDevice, st));
   });
@@ -1883,6 +1952,10 @@ int prlab_gpu_linear_f16_device_ex(const void* A, const void* Wt, const float* b
 
 int prlab_gpu_debug_small_stamps(long long* dbg) {
   return guarded([&] { small_debug_stamps() = dbg; });
+}
+
+int prlab_gpu_debug_cluster_stamps(long long* dbg) {
+  return guarded([&] { cluster_debug_stamps() = dbg; });
 }
 
 int prlab_gpu_debug_gemm_stamps(long long* dbg) {
