@@ -14,7 +14,11 @@
  * after the previous call's work on the same model (event wait when the stream differs),
  * because all calls share the model's workspace.  Calls on distinct models run
  * concurrently.  A stream that is being captured by the CALLER is not ordered (the
- * caller's graph defines the order).
+ * caller's graph defines the order).  prlab_gpu_forward (hybrid, logits widened on the
+ * host, logits <= 512 MB) holds the model's mutex only while it enqueues its compute into
+ * one of two model-owned logits slots; its copy-out then runs on the slot's own stream with
+ * the mutex released, so a concurrent caller's compute overlaps it (at most two calls in
+ * flight; each call returns exactly its own logits).
  *
  * Errors: every function returns PRLAB_OK (0) or a status; the thread-local
  * message is available from prlab_gpu_last_error().  The status maps onto the

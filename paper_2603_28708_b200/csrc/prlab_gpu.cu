@@ -486,6 +486,18 @@ struct prlab_gpu_model {
   DeviceBuffer split_ws, split_tickets;
   SplitScratch scratch;
   cudaStream_t stream = nullptr;  // private stream of the host (drop-in) forward
+  // Host forward copy-out slots (prlab_gpu_forward, hybrid, logits widened on the host): the
+  // call enqueues its compute under `mu` into slot s's device logits, releases `mu`, and copies
+  // slot s out on the slot's own stream -- a concurrent caller's compute overlaps that copy-out.
+  // A slot's mutex is held from before its compute is enqueued until its copy-out finished.
+  struct HostSlot {
+    std::mutex mu;
+    DeviceBuffer buf;
+    cudaStream_t cs = nullptr;
+    cudaEvent_t ready = nullptr;  // the slot's logits are written (recorded on the compute stream)
+  };
+  HostSlot hslot[2];
+  uint64_t hslot_next = 0;
   // Every call shares the workspace below (activations, split-K scratch, the persistent
   // kernel's grid-barrier counter, graphs): work queued on a stream other than the previous
   // call's waits on this event, recorded after that call's work (see StreamOrder).
@@ -533,6 +545,10 @@ struct prlab_gpu_model {
 
   ~prlab_gpu_model() {
     drop_plans();
+    for (auto& hs : hslot) {
+      if (hs.cs) cudaStreamDestroy(hs.cs);
+      if (hs.ready) cudaEventDestroy(hs.ready);
+    }
     if (stream) cudaStreamDestroy(stream);
     if (last_ev) cudaEventDestroy(last_ev);
   }
@@ -1482,9 +1498,56 @@ int prlab_gpu_model_memory_ex(prlab_gpu_model* m, prlab_memory_report* r) {
   });
 }
 
+// Overlapped host forward (hybrid, logits widened on the host, calibrated plan): returns false
+// (nothing done) when the call must take the serial path below.  Phase 1 under the model lock:
+// ids H2D + forward into slot s's device logits on the compute stream; phase 2 outside it: the
+// slot's copy-out (chunked fp16 D2H + host widening, host_widen.cpp) on the slot's stream.
+bool forward_overlapped(prlab_gpu_model* m, const int32_t* ids, int64_t B, int64_t S, const prlab_policy* policy,
+                        float* logits, prlab_trace* trace) {
+  if (std::getenv("PRLAB_NO_HOST_OVERLAP") || std::getenv("PRLAB_NO_HOST_WIDEN") || std::getenv("PRLAB_HOST_COPY"))
+    return false;
+  std::unique_lock<std::mutex> lk(m->mu);
+  validate_policy(*policy);
+  check_forward_args(*m, B, S);
+  if (m->L == 0) return false;
+  auto it = m->plans.find(std::make_tuple(B, S, policy_key(*policy)));
+  if (it == m->plans.end() || !it->second->fast || it->second->copy_mode != 1) return false;
+  auto& p = *it->second;
+  const size_t bytes = static_cast<size_t>(B * S * p.ld16) * 2;
+  if (bytes > (static_cast<size_t>(512) << 20)) return false;  // C4-sized logits: one buffer, serial path
+  for (int64_t i = 0; i < B * S; ++i)  // embed(), src/kernels.cpp:278-283
+    if (ids[i] < 0 || ids[i] >= m->V)
+      throw std::out_of_range("token id " + std::to_string(ids[i]) + " outside vocab of " + std::to_string(m->V));
+  PRLAB_CUDA(cudaSetDevice(m->device));
+  auto& hs = m->hslot[m->hslot_next++ & 1];
+  // waits only for this slot's previous copy-out (which never takes the model lock)
+  std::unique_lock<std::mutex> sl(hs.mu);
+  if (!hs.cs) {
+    PRLAB_CUDA(cudaStreamCreateWithFlags(&hs.cs, cudaStreamNonBlocking));
+    PRLAB_CUDA(cudaEventCreateWithFlags(&hs.ready, cudaEventDisableTiming));
+  }
+  if (hs.buf.bytes < bytes) hs.buf.alloc(bytes);  // the slot's last copy-out completed
+  __half* dlog = static_cast<__half*>(hs.buf.p);
+  const int64_t w = m->V, ld16 = p.ld16;
+  const bool graph = !std::getenv("PRLAB_NO_GRAPH");
+  {
+    cudaStream_t st = m->stream;
+    StreamOrder order(*m, st);
+    PRLAB_CUDA(cudaMemcpyAsync(p.ids, ids, B * S * 4, cudaMemcpyHostToDevice, st));
+    run_forward(*m, p, p.ids, dlog, PRLAB_OUT_F16, ld16, st, graph);
+    PRLAB_CUDA(cudaEventRecord(hs.ready, st));
+  }
+  if (trace) fill_calls(*m, B, *policy, trace);
+  lk.unlock();
+  PRLAB_CUDA(cudaStreamWaitEvent(hs.cs, hs.ready, 0));
+  d2h_widen_f16(dlog, ld16, logits, w, B * S, w, hs.cs);
+  return true;
+}
+
 int prlab_gpu_forward(prlab_gpu_model* m, const int32_t* ids, int64_t B, int64_t S,
                       const prlab_policy* policy, float* logits, prlab_trace* trace) {
   return guarded([&] {
+    if (forward_overlapped(m, ids, B, S, policy, logits, trace)) return;
     std::lock_guard<std::mutex> lk(m->mu);
     validate_policy(*policy);
     check_forward_args(*m, B, S);

@@ -80,3 +80,35 @@ def test_two_models_two_threads():
     for i in range(2):
         assert np.array_equal(results[i], want[i])
         models[i].close()
+
+
+@pytest.mark.parametrize("B,S", [(1, 128), (2, 64)])
+def test_one_model_concurrent_host_callers(B, S):
+    """prlab_gpu_forward from three host threads on one model (the overlapped two-phase path:
+    compute under the model lock into one of two logits slots, copy-out outside it): every
+    call returns exactly the logits of its own ids, equal to a serial call's, while the
+    copy-outs of one call overlap another call's compute."""
+    cfg = PRESETS["gpt2_small"].replace(num_layers=2)
+    m = pg.DeviceModel(pg.ModelConfig(**cfg.__dict__), model_params(cfg))
+    V = cfg.vocab
+    ids = [oracle().random_tokens(V, B, S, 40 + i) for i in range(3)]
+    want = [m.forward(x, B, S, "hybrid") for x in ids]  # first call calibrates the copy-out
+    assert m.host_copy_mode(B, S, "hybrid") in (1, 2)
+    errors, bad = [], []
+
+    def run(i):
+        try:
+            for rep in range(12):
+                got = m.forward(ids[i], B, S, "hybrid")
+                if not np.array_equal(got, want[i]):
+                    bad.append((i, rep))
+        except Exception as e:  # pragma: no cover
+            errors.append(e)
+    ths = [threading.Thread(target=run, args=(i,)) for i in range(3)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    assert not errors, errors
+    assert not bad, bad
+    m.close()
