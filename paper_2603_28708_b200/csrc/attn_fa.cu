@@ -414,6 +414,333 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fa_kernel(const __grid_const
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// Row-owner variant (default): one softmax thread per query row (warps 0..3 = TMEM lane
+// quadrants), the whole 128-key S block loaded from TMEM as packed round16 scores (masked keys
+// become -inf halves, so the exponent pass needs no masking) and S released (SFREE) right after
+// the load -- the next block's Q.K^T then runs under this block's exponentials.  The block max
+// is taken from registers (no second TMEM read, no cross-warp barrier); the lazy running-max /
+// O-rescale logic and every rounding point are those of attn_fa_kernel above.
+// Measured per-block chain of attn_fa_kernel (scripts/fa_phases.py, C4): max pass 512 cycles,
+// exp pass 2 966, wake-up 360, next-S wait ~1 340 = 4.8 K cycles against a MUFU floor of ~1 K.
+// ---------------------------------------------------------------------------------------
+// TPR threads per query row: 1 (4 softmax warps, 168 registers) or 2 (8 softmax warps, each half
+// of the row's keys; the halves' block maxima meet in shared memory behind a 64-thread pairwise
+// named barrier -- more warps to hide the TMEM / MUFU latencies at 2 CTAs per SM)
+template <int TPR>
+constexpr int row_threads() { return 128 * TPR + 64; }  // + TMA warp + MMA warp
+enum : int {
+  R_QFULL = 0, R_QEMPTY = 2, R_KFULL = 4, R_KEMPTY = 6, R_VFULL = 8, R_VEMPTY = 10,
+  R_SFULL = 12,   // S block in TMEM
+  R_SFREE = 13,   // softmax warps: S read (into registers)
+  R_PREADY = 14,  // softmax warps: P in TMEM, O rescaled
+  R_OFULL = 15,   // last P.V of the unit done
+  R_TFREE = 16,   // softmax warps: O read by the epilogue
+  R_PVDONE = 17,  // P.V of a block done: P columns and O free
+  R_COUNT = 18
+};
+
+__device__ __forceinline__ uint32_t h2_max(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("max.f16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+
+template <int TPR>
+__global__ void __launch_bounds__(row_threads<TPR>(), 2) attn_fa_row_kernel(const __grid_constant__ CUtensorMap tm, const FaArgs a) {
+  constexpr int kRowWarps = 4 * TPR, NC = 4 / TPR;  // softmax warps, 32-key chunks per thread
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~static_cast<uintptr_t>(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + FaSmem::BAR);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + R_COUNT);
+  const uint32_t warp = warp_id(), lane = lane_id();
+  constexpr uint32_t kTmaWarp = kRowWarps, kMmaWarp = kRowWarps + 1;
+
+  if (warp == kTmaWarp && lane == 0) {
+    tma_prefetch_desc(&tm);
+    for (int i = 0; i < R_COUNT; ++i)
+      mbar_init(&bars[i], (i == R_SFREE || i == R_PREADY || i == R_TFREE) ? kRowWarps : 1);
+    fence_barrier_init();
+  }
+  if (warp == kMmaWarp) {
+    tmem_alloc(tmem_slot, kTmemCols);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  pdl_trigger();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == kTmaWarp) {
+    // ---------------- TMA producer: per unit Q, then K/V blocks in consumption order
+    if (lane == 0) {
+      pdl_wait();  // q/k/v are written by the upstream QKV GEMM
+      uint32_t qc = 0, kc = 0;
+      for (int it = 0, u; (u = fa_unit_at(a, it)) >= 0; ++it, ++qc) {
+        int b, head, qt, nkb;
+        fa_decode(a, u, b, head, qt, nkb);
+        const uint32_t qs = qc & 1;
+        mbar_wait(&bars[R_QEMPTY + qs], ((qc >> 1) & 1) ^ 1);
+        mbar_expect_tx(&bars[R_QFULL + qs], kTile);
+        tma_load_3d(smem + FaSmem::Q + qs * kTile, &tm, &bars[R_QFULL + qs], head * 64, qt * 128, b);
+        for (int kb = 0; kb < nkb; ++kb, ++kc) {
+          const uint32_t s = kc & 1, ph = ((kc >> 1) & 1) ^ 1;
+          mbar_wait(&bars[R_KEMPTY + s], ph);
+          mbar_expect_tx(&bars[R_KFULL + s], kTile);
+          tma_load_3d(smem + FaSmem::K + s * kTile, &tm, &bars[R_KFULL + s], a.h + head * 64, kb * 128, b);
+          mbar_wait(&bars[R_VEMPTY + s], ph);
+          mbar_expect_tx(&bars[R_VFULL + s], kTile);
+          tma_load_3d(smem + FaSmem::V + s * kTile, &tm, &bars[R_VFULL + s], 2 * a.h + head * 64, kb * 128, b);
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == kMmaWarp) {
+    // ---------------- MMA issuer: S_kb+1 as soon as the softmax has S_kb in registers (SFREE),
+    // P.V_kb once it wrote P (PREADY)
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = idesc_f16_f32(128, 128, 0, 0);
+      constexpr uint32_t idesc_o = idesc_f16_f32(128, 64, 0, 1);
+      uint32_t qc = 0, kc = 0, bc = 0;
+      auto issue_s = [&](uint32_t q0, uint32_t kcount, bool last_of_unit, uint32_t qs) {
+        const uint32_t s = kcount & 1;
+        mbar_wait(&bars[R_KFULL + s], (kcount >> 1) & 1);
+        tc_fence_after();
+        const uint32_t k0 = smem_u32(smem + FaSmem::K + s * kTile);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          umma_f16_ss(tmem + kColS, sw128_desc(q0 + k * 32, 0, 1024), sw128_desc(k0 + k * 32, 0, 1024), idesc_s,
+                      k != 0);
+        umma_commit(&bars[R_SFULL]);
+        umma_commit(&bars[R_KEMPTY + s]);
+        if (last_of_unit) umma_commit(&bars[R_QEMPTY + qs]);
+      };
+      for (int it = 0, u; (u = fa_unit_at(a, it)) >= 0; ++it, ++qc) {
+        int b, head, qt, nkb;
+        fa_decode(a, u, b, head, qt, nkb);
+        const uint32_t qs = qc & 1;
+        mbar_wait(&bars[R_QFULL + qs], (qc >> 1) & 1);
+        const uint32_t q0 = smem_u32(smem + FaSmem::Q + qs * kTile);
+        if (bc > 0) mbar_wait_spin(&bars[R_SFREE], (bc - 1) & 1);  // previous block's S was read
+        issue_s(q0, kc, nkb == 1, qs);
+        for (int kb = 0; kb < nkb; ++kb, ++kc, ++bc) {
+          const uint32_t s = kc & 1, ph = (kc >> 1) & 1;
+          if (kb + 1 < nkb) {
+            mbar_wait_spin(&bars[R_SFREE], bc & 1);
+            issue_s(q0, kc + 1, kb + 2 == nkb, qs);
+          }
+          mbar_wait_spin(&bars[R_PREADY], bc & 1);
+          long long* ms = (a.dbg && blockIdx.x == 0 && bc < 32) ? a.dbg + bc * 8 : nullptr;
+          if (ms) ms[4] = clock64();
+          if (kb == 0 && qc > 0) mbar_wait(&bars[R_TFREE], (qc - 1) & 1);
+          mbar_wait(&bars[R_VFULL + s], ph);
+          tc_fence_after();
+          const uint32_t v0 = smem_u32(smem + FaSmem::V + s * kTile);
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)  // 16 keys per MMA = 8 packed TMEM columns of P
+            umma_f16_ts_fa(tmem + kColO, tmem + kColP + 8 * kk, sw128_desc(v0 + kk * 2048, 128 * 128, 1024), idesc_o,
+                           (kb | kk) != 0);
+          umma_commit(&bars[R_PVDONE]);
+          umma_commit(&bars[R_VEMPTY + s]);
+          if (kb == nkb - 1) umma_commit(&bars[R_OFULL]);
+          if (ms) ms[5] = clock64();
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- softmax + epilogue: thread = query row (TMEM lane)
+    const uint32_t quad = warp & 3, half = warp >> 2;  // half: which NC chunks of a block (TPR = 2)
+    const int r = static_cast<int>(quad * 32 + lane);
+    float* red = reinterpret_cast<float*>(smem + FaSmem::RED);
+    const uint32_t lane_addr = tmem + ((quad * 32) << 16);
+    const float NEG_INF = __int_as_float(0xff800000);
+    constexpr uint32_t NEG_INF2 = 0xFC00FC00u;  // (-inf, -inf) as f16x2
+    constexpr float LOG2E = 1.4426950408889634f;
+    uint32_t qc = 0, bc = 0;
+    for (int it = 0, u; (u = fa_unit_at(a, it)) >= 0; ++it, ++qc) {
+      int b, head, qt, nkb;
+      fa_decode(a, u, b, head, qt, nkb);
+      const int qrow = qt * 128 + r;
+      const int row_lo = qt * 128 + static_cast<int>(quad) * 32, row_hi = row_lo + 31;  // this warp's rows
+      const int key_lim = a.causal ? min(a.S - 1, qrow) : a.S - 1;  // last key this row sees
+      float m = NEG_INF, l = 0.0f;
+      for (int kb = 0; kb < nkb; ++kb, ++bc) {
+        mbar_wait(&bars[R_SFULL], bc & 1);
+        long long* ts = (a.dbg && blockIdx.x == 0 && warp == 0 && lane == 0 && bc < 32) ? a.dbg + bc * 8 : nullptr;
+        if (ts) ts[0] = clock64();
+        tc_fence_after();
+        const int key0 = kb * 128;
+        // per 32-key chunk (warp-uniform): dead = no key of the chunk is visible to any row of
+        // the warp; full = every key visible to every row of the warp
+        uint32_t sp[16 * NC];  // round16 scores, packed pairs; masked keys -inf
+        uint32_t hm[4] = {NEG_INF2, NEG_INF2, NEG_INF2, NEG_INF2};  // independent max chains
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc) {
+          const int c = static_cast<int>(half) * NC + cc;
+          const int k0c = key0 + 32 * c;
+          const bool dead = k0c >= a.S || (a.causal && k0c > row_hi);
+          if (dead) {
+#pragma unroll
+            for (int i = 0; i < 16; ++i) sp[16 * cc + i] = NEG_INF2;
+            continue;
+          }
+          uint32_t w[32];
+          tmem_ld32(lane_addr + kColS + 32 * c, w);
+          tmem_wait_ld();
+          if (ts && cc == 0) ts[6] = clock64();
+          if (k0c + 32 <= a.S && (!a.causal || k0c + 31 <= row_lo)) {  // warp-uniform: no masking
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const uint32_t hv = h2_pack_rn(__uint_as_float(w[2 * i]), __uint_as_float(w[2 * i + 1]));
+              sp[16 * cc + i] = hv;
+              hm[i & 3] = h2_max(hm[i & 3], hv);
+            }
+          } else {  // keys j > lim are masked: branch-free selects
+#pragma unroll
+            for (int i = 0; i < 16; ++i) {
+              const int j = k0c + 2 * i;
+              const uint32_t hv = h2_pack_rn(__uint_as_float(w[2 * i]), __uint_as_float(w[2 * i + 1]));
+              const uint32_t keep = (j <= key_lim ? 0x0000FFFFu : 0u) | (j + 1 <= key_lim ? 0xFFFF0000u : 0u);
+              const uint32_t mv = (hv & keep) | (NEG_INF2 & ~keep);
+              sp[16 * cc + i] = mv;
+              hm[i & 3] = h2_max(hm[i & 3], mv);
+            }
+          }
+        }
+        const uint32_t hmax = h2_max(h2_max(hm[0], hm[1]), h2_max(hm[2], hm[3]));
+        if (ts) ts[7] = clock64();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars[R_SFREE]);  // the next Q.K^T may overwrite S now
+        if (ts) ts[1] = clock64();
+        float mnew = 0.0f;  // unstabilised: e = exp(s) (the reference's full_fp16 softmax)
+        if (!a.unstab) {
+          float h0, h1;
+          h2_unpack(hmax, h0, h1);
+          float mraw = fmaxf(h0, h1);  // = round16(max acc): round16 is monotone
+          if constexpr (TPR == 2) {  // the other half of the row: shared memory + pairwise barrier
+            float* rmax = red + (bc & 1) * 256;  // by block parity: a fast pair may write the next block's first
+            rmax[half * 128 + r] = mraw;
+            named_bar_sync(1 + quad, 64);
+            mraw = fmaxf(rmax[r], rmax[128 + r]);
+          }
+          const float mblk = mraw == NEG_INF ? NEG_INF : __fmul_rn(mraw, 0.125f);
+          mnew = fmaxf(m, mblk);
+        }
+        constexpr float kLazy = 5.0f;  // see attn_fa_kernel
+        const bool rescale = !a.unstab && kb > 0 && __any_sync(0xffffffffu, mnew > m + kLazy);
+        const float mold = m;
+        if (kb == 0 || rescale) m = mnew;
+        // e = exp(s - m), P~ = round16(e), in registers before the wait for the previous P.V
+        // (s = round16(acc) * 2^-3, the 2^-3 in the FMA); four independent partial sums
+        const float ml = __fmul_rn(m, LOG2E);
+        const uint64_t nm = f2_pack(-ml, -ml);
+        const uint64_t kl8 = f2_pack(0.125f * LOG2E, 0.125f * LOG2E);
+        uint64_t sum2[2] = {f2_pack(0.0f, 0.0f), f2_pack(0.0f, 0.0f)};
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc) {
+          const int c = static_cast<int>(half) * NC + cc;
+          const int k0c = key0 + 32 * c;
+          if (k0c >= a.S || (a.causal && k0c > row_hi)) {  // dead chunk: P~ = 0
+#pragma unroll
+            for (int i = 0; i < 16; ++i) sp[16 * cc + i] = 0u;
+            continue;
+          }
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            float s0, s1, x0, x1;
+            h2_unpack(sp[16 * cc + i], s0, s1);
+            f2_unpack(f2_fma(f2_pack(s0, s1), kl8, nm), x0, x1);
+            const float e0 = ex2_approx(x0), e1 = ex2_approx(x1);  // ex2(-inf) = 0: masked keys
+            sum2[i & 1] = f2_add(sum2[i & 1], f2_pack(e0, e1));
+            sp[16 * cc + i] = h2_pack_rn(e0, e1);  // P~ replaces the score in place
+          }
+        }
+        if (bc > 0) mbar_wait(&bars[R_PVDONE], (bc - 1) & 1);  // P columns and O free
+        tc_fence_after();
+        if (ts) ts[2] = clock64();
+        if (rescale) {
+          const float sc = ex2_approx(__fmul_rn(__fsub_rn(mold, m), LOG2E));
+          l = __fmul_rn(l, sc);
+          const uint64_t sc2 = f2_pack(sc, sc);
+#pragma unroll
+          for (int hh = 0; hh < 2 / TPR; ++hh) {  // this thread's O columns
+            const uint32_t oc = kColO + 32 * (static_cast<uint32_t>(half) + hh);
+            uint32_t o[32];
+            tmem_ld32(lane_addr + oc, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; i += 2) {
+              float x0, x1;
+              f2_unpack(f2_mul(f2_pack(__uint_as_float(o[i]), __uint_as_float(o[i + 1])), sc2), x0, x1);
+              o[i] = __float_as_uint(x0);
+              o[i + 1] = __float_as_uint(x1);
+            }
+            tmem_st32(lane_addr + oc, o);
+          }
+        }
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc)
+          tmem_st16(lane_addr + kColP + 16 * (static_cast<uint32_t>(half) * NC + cc), *reinterpret_cast<uint32_t(*)[16]>(sp + 16 * cc));
+        float sa, sb, sc_, sd;
+        f2_unpack(sum2[0], sa, sb);
+        f2_unpack(sum2[1], sc_, sd);
+        l = __fadd_rn(l, __fadd_rn(__fadd_rn(sa, sb), __fadd_rn(sc_, sd)));
+        tmem_wait_st();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bars[R_PREADY]);
+        if (ts) ts[3] = clock64();
+      }
+      // epilogue: o = round16(O / l) -> ctx row (this thread's 64 / TPR halves)
+      if constexpr (TPR == 2) red[512 + half * 128 + r] = l;
+      mbar_wait(&bars[R_OFULL], qc & 1);
+      tc_fence_after();
+      uint32_t o[64 / TPR];
+#pragma unroll
+      for (int hh = 0; hh < 2 / TPR; ++hh)
+        tmem_ld32(lane_addr + kColO + 32 * (static_cast<uint32_t>(half) + hh), *reinterpret_cast<uint32_t(*)[32]>(o + 32 * hh));
+      tmem_wait_ld();
+      tc_fence_before();
+      if constexpr (TPR == 2) {  // both partial sums visible; the next rsum write is a unit (and a pair barrier) later
+        named_bar_sync(1 + quad, 64);
+        l = __fadd_rn(red[512 + r], red[512 + 128 + r]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[R_TFREE]);
+      // full_fp16: the reference sums e on the binary16 lattice (kernels.cpp:154-165)
+      const float lt = a.unstab ? r16(l) : l;
+      if (qrow < a.S) {
+        const float inv = __frcp_rn(lt);
+        const uint64_t inv2 = f2_pack(inv, inv);
+        uint4* dst = reinterpret_cast<uint4*>(a.ctx + (static_cast<int64_t>(b) * a.S + qrow) * a.ld_ctx + head * 64 +
+                                              half * 32);
+#pragma unroll
+        for (int q = 0; q < 8 / TPR; ++q) {
+          uint32_t pk[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            float x0, x1;
+            f2_unpack(f2_mul(f2_pack(__uint_as_float(o[8 * q + 2 * i]), __uint_as_float(o[8 * q + 2 * i + 1])), inv2),
+                      x0, x1);
+            pk[i] = h2_pack_rn(x0, x1);
+          }
+          dst[q] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == kMmaWarp) {
+    tc_fence_after();
+    tmem_dealloc(tmem, kTmemCols);
+  }
+}
+
 }  // namespace
 
 bool attn_fa_enabled() {
@@ -430,7 +757,15 @@ void launch_attn_fa(const AttnPlan& p, cudaStream_t st) {
   once_per_device(mu, done, [] {
     PRLAB_CUDA(cudaFuncSetAttribute(attn_fa_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kFaSmemBytes)));
+    PRLAB_CUDA(cudaFuncSetAttribute(attn_fa_row_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kFaSmemBytes)));
+    PRLAB_CUDA(cudaFuncSetAttribute(attn_fa_row_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kFaSmemBytes)));
   });
+  static const int row = [] {  // threads per row of the row-owner kernel (0: half-row kernel)
+    const char* e = std::getenv("PRLAB_ATTN_ROW");
+    return e == nullptr ? 2 : std::atoi(e);
+  }();
   FaArgs a;
   a.B = p.B;
   a.S = p.S;
@@ -444,7 +779,12 @@ void launch_attn_fa(const AttnPlan& p, cudaStream_t st) {
   a.unstab = p.unstab;
   const int units = p.B * p.H * a.nqt;
   const int grid = std::min(units, 2 * num_sms());
-  launch_pdl(attn_fa_kernel, dim3(grid), dim3(kThreads), kFaSmemBytes, st, p.tmQKV, a);
+  if (row == 2)
+    launch_pdl(attn_fa_row_kernel<2>, dim3(grid), dim3(row_threads<2>()), kFaSmemBytes, st, p.tmQKV, a);
+  else if (row == 1)
+    launch_pdl(attn_fa_row_kernel<1>, dim3(grid), dim3(row_threads<1>()), kFaSmemBytes, st, p.tmQKV, a);
+  else
+    launch_pdl(attn_fa_kernel, dim3(grid), dim3(kThreads), kFaSmemBytes, st, p.tmQKV, a);
 }
 
 }  // namespace prlab_gpu

@@ -31,7 +31,10 @@ def main():
             break
         rows.append({"pass1": d[b, 1] - d[b, 0], "max_bar": d[b, 2] - d[b, 1], "pass2_to_ready": d[b, 3] - d[b, 2],
                      "ready_to_mma_seen": d[b, 4] - d[b, 3], "mma_issue": d[b, 5] - d[b, 4],
-                     "issue_to_next_s_seen": d[b + 1, 0] - d[b, 5], "block_total": d[b + 1, 0] - d[b, 0]})
+                     "issue_to_next_s_seen": d[b + 1, 0] - d[b, 5], "block_total": d[b + 1, 0] - d[b, 0],
+                     # row-owner kernel: first chunk loaded, all chunks packed (0 / unused otherwise)
+                     "row_first_chunk": d[b, 6] - d[b, 0] if d[b, 6] else 0,
+                     "row_all_chunks": d[b, 7] - d[b, 0] if d[b, 7] else 0})
     avg = {k: round(float(np.median([r[k] for r in rows])), 1) for k in rows[0]}
     print(json.dumps({"B": B, "S": S, "blocks": len(rows), "median_cycles": avg}))
 
