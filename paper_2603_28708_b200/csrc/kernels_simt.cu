@@ -381,6 +381,120 @@ __global__ void simt_attention_kernel(const float* __restrict__ q, const float* 
   }
 }
 
+// ---------------------------------------------------------------------------
+// fp32-policy attention (att = F32/F32, softmax F32 stabilised; hd 64, S <= 512, no tap):
+// register-tiled two-pass form.  One CTA per (b, head, 64-query block): scores
+// s = (q . k) * scale (causal -inf after scaling, model.cpp:405-413) for the whole key range
+// into shared memory, exact softmax p = e / sum with e = expf(s - max) (kernels.cpp:127-168),
+// then ctx = P . V.  The same operations as simt_attention_kernel in fp32; only the summation
+// orders differ (4x4 register tiles, fmaf, warp-tree row sums) -- the fp32 parity budget
+// (1e-3 relative) is the reference's own fp32-vs-fp32 contract.  One warp per query row
+// with sequential sums (simt_attention_kernel) measured 859 us per layer at BERT s512.
+// ---------------------------------------------------------------------------
+constexpr int kAtQ = 64, kAtD = 64, kAtPad = 68;
+__global__ void __launch_bounds__(256) attn_f32_tiled_kernel(const float* __restrict__ q, const float* __restrict__ k,
+                                                             const float* __restrict__ v, int64_t ld_in,
+                                                             float* __restrict__ ctx, int64_t ld_ctx, int S, int H,
+                                                             float scale, int causal) {
+  extern __shared__ __align__(16) float sh[];
+  float* sQt = sh;                      // [d][q]  (transposed, padded)
+  float* sKV = sQt + kAtD * kAtPad;     // K tile transposed [d][key], then V tile [key][d]
+  float* sS = sKV + kAtD * kAtPad;      // [q][S + 4] scores / probabilities
+  const int ldS = S + 4;
+  const int qb = blockIdx.x, head = blockIdx.y, b = blockIdx.z;
+  const int q0 = qb * kAtQ, nq = min(kAtQ, S - q0);
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int kend = causal ? min(S, q0 + nq) : S;  // keys any query of the block sees
+  const float* qbase = q + (static_cast<int64_t>(b) * S) * ld_in + head * kAtD;
+  const float* kbase = k + (static_cast<int64_t>(b) * S) * ld_in + head * kAtD;
+  const float* vbase = v + (static_cast<int64_t>(b) * S) * ld_in + head * kAtD;
+  for (int e = tid; e < kAtQ * kAtD; e += 256) {
+    const int r = e >> 6, d = e & 63;
+    sQt[d * kAtPad + r] = r < nq ? qbase[static_cast<int64_t>(q0 + r) * ld_in + d] : 0.0f;
+  }
+  // ---- scores, 64 keys at a time
+  for (int j0 = 0; j0 < kend; j0 += 64) {
+    __syncthreads();  // sKV free (previous tile's readers done); sQt visible
+    for (int e = tid; e < 64 * kAtD; e += 256) {
+      const int r = e >> 6, d = e & 63;
+      sKV[d * kAtPad + r] = j0 + r < S ? kbase[static_cast<int64_t>(j0 + r) * ld_in + d] : 0.0f;
+    }
+    __syncthreads();
+    float acc[4][4] = {};
+#pragma unroll 8
+    for (int d = 0; d < kAtD; ++d) {
+      const float4 a4 = *reinterpret_cast<const float4*>(sQt + d * kAtPad + 4 * ty);
+      const float4 b4 = *reinterpret_cast<const float4*>(sKV + d * kAtPad + 4 * tx);
+      const float a[4] = {a4.x, a4.y, a4.z, a4.w}, bb[4] = {b4.x, b4.y, b4.z, b4.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int jj = 0; jj < 4; ++jj) acc[i][jj] = fmaf(a[i], bb[jj], acc[i][jj]);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int qi = 4 * ty + i;
+#pragma unroll
+      for (int jj = 0; jj < 4; ++jj) {
+        const int j = j0 + 4 * tx + jj;
+        if (j < kend) {
+          const float sv = __fmul_rn(acc[i][jj], scale);
+          sS[qi * ldS + j] = (causal && j > q0 + qi) ? __int_as_float(0xff800000) : sv;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // ---- softmax per row: warp w -> rows w, w + 8, ...
+  {
+    const int w = tid >> 5, lane = tid & 31;
+    for (int r = w; r < nq; r += 8) {
+      float* row = sS + r * ldS;
+      float mx = __int_as_float(0xff800000);
+      for (int j = lane; j < kend; j += 32) mx = fmaxf(mx, row[j]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      float sum = 0.0f;
+      for (int j = lane; j < kend; j += 32) {
+        const float e = expf(__fsub_rn(row[j], mx));
+        row[j] = e;
+        sum = __fadd_rn(sum, e);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum = __fadd_rn(sum, __shfl_xor_sync(0xffffffffu, sum, o));
+      for (int j = lane; j < kend; j += 32) row[j] = __fdiv_rn(row[j], sum);
+    }
+  }
+  // ---- ctx = P . V, 64 keys at a time; thread: queries 4ty.., dims 4tx..
+  float o[4][4] = {};
+  for (int j0 = 0; j0 < kend; j0 += 64) {
+    __syncthreads();  // probabilities written / previous V tile consumed
+    for (int e = tid; e < 64 * kAtD; e += 256) {
+      const int r = e >> 6, d = e & 63;
+      sKV[r * kAtPad + d] = j0 + r < S ? vbase[static_cast<int64_t>(j0 + r) * ld_in + d] : 0.0f;
+    }
+    __syncthreads();
+    const int jn = min(64, kend - j0);
+    for (int jj = 0; jj < jn; ++jj) {
+      const float4 v4 = *reinterpret_cast<const float4*>(sKV + jj * kAtPad + 4 * tx);
+      const float vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const float pv = sS[(4 * ty + i) * ldS + j0 + jj];
+#pragma unroll
+        for (int dd = 0; dd < 4; ++dd) o[i][dd] = fmaf(pv, vv[dd], o[i][dd]);
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int qi = 4 * ty + i;
+    if (qi < nq)
+      *reinterpret_cast<float4*>(ctx + (static_cast<int64_t>(b) * S + q0 + qi) * ld_ctx + head * kAtD + 4 * tx) =
+          make_float4(o[i][0], o[i][1], o[i][2], o[i][3]);
+  }
+}
+
 // per-op softmax (kernels.cpp:127-168): one warp per row, sequential sum.
 __global__ void simt_softmax_kernel(const float* __restrict__ x, int64_t rows, int64_t n, Kcfg cfg,
                                     float* __restrict__ out) {
@@ -547,6 +661,21 @@ void ln_f32_to_f16(const float* x, int rows, int n, const float* gamma, const fl
 void simt_attention(const float* q, const float* k, const float* v, int64_t ld_in, float* ctx,
                     int64_t ld_ctx, int B, int S, int H, int hd, float scale, int causal, Kcfg att,
                     Kcfg sm, float* tap, cudaStream_t st) {
+  // plain fp32 configs: the register-tiled kernel (same operations, other summation order)
+  if (tap == nullptr && hd == kAtD && S <= 512 && att.compute == 0 && att.accum == 0 && sm.compute == 0 &&
+      sm.accum == 0 && sm.stabilized && ld_in % 4 == 0 && ld_ctx % 4 == 0 && !std::getenv("PRLAB_NO_ATTN_F32_TILED")) {
+    const size_t shm = static_cast<size_t>(2 * kAtD * kAtPad + kAtQ * (S + 4)) * sizeof(float);
+    static std::mutex mu;
+    static uint64_t done = 0;
+    once_per_device(mu, done, [] {
+      PRLAB_CUDA(cudaFuncSetAttribute(attn_f32_tiled_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      static_cast<int>((2 * kAtD * kAtPad + kAtQ * (512 + 4)) * sizeof(float))));
+    });
+    attn_f32_tiled_kernel<<<dim3((S + kAtQ - 1) / kAtQ, H, B), 256, shm, st>>>(q, k, v, ld_in, ctx, ld_ctx, S, H, scale,
+                                                                                causal);
+    PRLAB_CUDA(cudaGetLastError());
+    return;
+  }
   const int warps = 4;
   const size_t shmem = static_cast<size_t>(warps) * (S + hd) * sizeof(float);
   {
