@@ -275,6 +275,12 @@ int prlab_gpu_linear_f16_device(const void* A, const void* Wt, const float* bias
 int prlab_gpu_linear_f16_device_ex(const void* A, const void* Wt, const float* bias, void* out,
                                    int64_t M, int64_t N, int64_t K, int64_t ldo, int32_t epi,
                                    int32_t bn, int32_t splits, int32_t lean, void* stream);
+/* fp32-policy linear on the tensor cores (3xTF32, gemm_tf32.cu), device pointers:
+ * out[M, N] (row pitch N) = epi(A[M, K] . Wt[N, K]^T), epi 0 = + bias (bias may be null),
+ * 1 = GELU(+ bias) with exact erf, 2 = resid + (acc + bias) (resid [M, N], may alias out).
+ * Replaces the fp32 linear_bias of src/kernels.cpp:40-83 under the fp32 policy; K % 32 == 0. */
+int prlab_gpu_linear_f32_device(const float* A, const float* Wt, const float* bias, float* out, int64_t M,
+                                int64_t N, int64_t K, int32_t epi, const float* resid, void* stream);
 /* Fused hybrid attention on tensor cores: qkv fp16 [B*S, 3h] (q|k|v), ctx fp16 [B*S, h]. */
 int prlab_gpu_attention_f16_device(const void* qkv, void* ctx, int64_t batch, int64_t seq,
                                    int64_t heads, int64_t head_dim, int32_t causal,

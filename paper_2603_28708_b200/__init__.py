@@ -215,6 +215,8 @@ EXPORTS = [
     ("prlab_gpu_linear_f16_device_ex", C.c_int, [_P, _P, _P, _P, C.c_int64, C.c_int64, C.c_int64,
                                                  C.c_int64, C.c_int32, C.c_int32, C.c_int32,
                                                  C.c_int32, _P]),
+    ("prlab_gpu_linear_f32_device", C.c_int, [_P, _P, _P, _P, C.c_int64, C.c_int64, C.c_int64,
+                                              C.c_int32, _P, _P]),
     ("prlab_gpu_attention_f16_device", C.c_int, [_P, _P, C.c_int64, C.c_int64, C.c_int64,
                                                  C.c_int64, C.c_int32, _P]),
     ("prlab_gpu_debug_gemm_stamps", C.c_int, [_P]),
@@ -586,6 +588,13 @@ def linear_f16_device_ex(A, Wt, bias, out, M, N, K, ldo, epi, bn=0, splits=0, le
                                                 C.c_void_p(_ptr(bias)), C.c_void_p(_ptr(out)), M,
                                                 N, K, ldo, epi, bn, splits, lean,
                                                 C.c_void_p(stream)))
+
+
+def linear_f32_device(A, Wt, bias, out, M, N, K, epi=0, resid=None, stream=0):
+    """fp32-policy linear on the tensor cores (3xTF32): out = epi(A . Wt^T)."""
+    _check(lib().prlab_gpu_linear_f32_device(C.c_void_p(_ptr(A)), C.c_void_p(_ptr(Wt)), C.c_void_p(_ptr(bias)),
+                                             C.c_void_p(_ptr(out)), M, N, K, epi, C.c_void_p(_ptr(resid)),
+                                             C.c_void_p(stream)))
 
 
 def attention_f16_device(qkv, ctx, B, S, H, hd, causal, stream=0):

@@ -187,6 +187,15 @@ void configure_attn_tc();
 bool attn_fa_enabled();
 void launch_attn_fa(const AttnPlan& p, cudaStream_t st);
 
+// --- fp32-policy linears on the tensor cores: 3xTF32 tcgen05 GEMM (gemm_tf32.cu) ---
+// lo = w - trunc19(w) (the part of each fp32 value kind::tf32 drops)
+void split_lo(const float* w, float* lo, int64_t n, cudaStream_t st);
+bool gemm_tf32_ok(const float* A, int64_t lda, const float* W, int64_t ldw, int64_t K);
+// out = epi(A . W^T): op 0 (+bias), 1 GELU (exact erf), 2 residual (out = resid + v); fp32
+void gemm_tf32(const float* A, int64_t lda, const float* W, const float* Wlo, int64_t ldw, float* out, int64_t ldo,
+               int M, int N, int K, const float* bias, int op, const float* resid, float* ws, size_t ws_floats,
+               cudaStream_t st);
+
 // --- SIMT kernels (any shape, any policy; fp32 storage) ---
 struct Kcfg {
   int compute, accum, stabilized;

@@ -475,6 +475,15 @@ struct prlab_gpu_model {
   };
   std::vector<L32> l32;
   bool have32 = false;
+  // 3xTF32 residues w - trunc19(w) of the fp32 linears and the tied head (gemm_tf32.cu),
+  // built with the first plan of a plain-fp32 policy
+  DeviceBuffer arena32lo;
+  struct L32lo {
+    float *wqkv, *wo, *w1, *w2;
+  };
+  std::vector<L32lo> l32lo;
+  float* tok_lo = nullptr;
+  bool have32lo = false;
 
   // encoder classifier head (pooler [h,h], classifier [h,2]) as fp32 W^T + biases,
   // uploaded on the first classifier_probs call
@@ -758,6 +767,36 @@ void ensure_f32(prlab_gpu_model& m) {
   m.have32 = true;
 }
 
+// fp32 policy on the tensor cores: linear / activation / residual classes all plain fp32
+bool tf32_policy(const prlab_policy& pol) {
+  auto f32 = [&](int c) { return pol.cls[c].compute == PRLAB_F32 && pol.cls[c].accum == PRLAB_F32; };
+  return f32(PRLAB_LINEAR) && f32(PRLAB_ACTIVATION) && f32(PRLAB_RESIDUAL);
+}
+
+void ensure_f32lo(prlab_gpu_model& m) {
+  if (m.have32lo) return;
+  ensure_f32(m);
+  const int64_t h = m.h, f = m.f, L = m.L;
+  const int64_t per = 3 * h * h + h * h + f * h + h * f;
+  m.arena32lo.alloc(static_cast<size_t>(per * L + m.V * h) * 4 + 1024);
+  float* base = static_cast<float*>(m.arena32lo.p);
+  m.l32lo.resize(L);
+  for (int64_t l = 0; l < L; ++l) {
+    float* b = base + per * l;
+    auto& lo = m.l32lo[l];
+    const auto& w = m.l32[l];
+    lo = {b, b + 3 * h * h, b + 4 * h * h, b + 4 * h * h + f * h};
+    split_lo(w.wqkv_t, lo.wqkv, 3 * h * h, nullptr);
+    split_lo(w.wo_t, lo.wo, h * h, nullptr);
+    split_lo(w.w1_t, lo.w1, f * h, nullptr);
+    split_lo(w.w2_t, lo.w2, h * f, nullptr);
+  }
+  m.tok_lo = base + per * L;
+  split_lo(m.tok, m.tok_lo, m.V * h, nullptr);
+  PRLAB_CUDA(cudaDeviceSynchronize());
+  m.have32lo = true;
+}
+
 // Batch-1 plan: tensor maps (activations box 128 x 64, weights box 32 x 64) and the
 // the fp32 partials (per-head Wo, FFN2 K splits) and the grid-barrier counter live in
 // one device buffer.
@@ -867,7 +906,10 @@ prlab_gpu_model::Plan& get_plan(prlab_gpu_model& m, int64_t B, int64_t S, const 
   if (it != m.plans.end()) return *it->second;
 
   const bool fast = fast_eligible(m, S, pol) || fast16;
-  if (!fast) ensure_f32(m);
+  if (!fast) {
+    ensure_f32(m);
+    if (tf32_policy(pol) && !std::getenv("PRLAB_NO_TF32X3")) ensure_f32lo(m);
+  }
   const int64_t M = B * S, h = m.h, f = m.f, V = m.V;
   const int64_t outw = m.L > 0 ? V : h;
   const int64_t ld16 = (V + 7) / 8 * 8;
@@ -1031,22 +1073,32 @@ int64_t enqueue_forward(prlab_gpu_model& m, prlab_gpu_model::Plan& p, const int3
              res = K(pol.cls[PRLAB_RESIDUAL]);
   T(PRLAB_EMBEDDING, [&] { simt_embed(m.tok, V, m.pos, hi, ids, Bi, Si, emb, p.x, err, st); });
   const float scale = 1.0f / std::sqrt(static_cast<float>(m.hd));
+  // plain-fp32 linears on the tensor cores (3xTF32, gemm_tf32.cu) when the residues exist
+  const bool tc32 = m.have32lo && tf32_policy(pol) && !std::getenv("PRLAB_NO_TF32X3");
+  auto lin_gemm = [&](const float* A, int64_t lda, const float* W, const float* Wlo, int64_t ldw, float* out,
+                      int64_t ldo, int Mi_, int Ni_, int Ki_, const float* bias, int op, const float* resid) {
+    if (tc32 && Wlo != nullptr && gemm_tf32_ok(A, lda, W, ldw, Ki_))
+      gemm_tf32(A, lda, W, Wlo, ldw, out, ldo, Mi_, Ni_, Ki_, bias, op, resid, m.scratch.ws, m.scratch.ws_floats, st);
+    else
+      simt_gemm(A, lda, W, ldw, out, ldo, Mi_, Ni_, Ki_, lin, SimtGemmEpi{bias, op, act, res, resid}, st);
+  };
   for (int64_t l = 0; l < L; ++l) {
     const auto& w16 = m.l16[l];
     const auto& w = m.l32[l];
+    const auto* wl = tc32 ? &m.l32lo[l] : nullptr;
     float* tap = o.tap ? o.tap + l * tap_stride : nullptr;
     T(PRLAB_LAYERNORM, [&] { simt_layernorm(p.x, Mi, hi, w16.ln1g, w16.ln1b, 1e-5f, ln, p.xn32, nullptr, 0, st); });
     T(PRLAB_LINEAR, [&] {
-      simt_gemm(p.xn32, h, w.wqkv_t, h, p.qkv32, 3 * h, Mi, 3 * hi, hi, lin, SimtGemmEpi{w.bqkv, 0, act, res, nullptr}, st);
+      lin_gemm(p.xn32, h, w.wqkv_t, wl ? wl->wqkv : nullptr, h, p.qkv32, 3 * h, Mi, 3 * hi, hi, w.bqkv, 0, nullptr);
     });
     T(PRLAB_ATTENTION_SCORE_MATMUL, [&] {
       simt_attention(p.qkv32, p.qkv32 + h, p.qkv32 + 2 * h, 3 * h, p.ctx32, h, Bi, Si, static_cast<int>(m.H),
                      static_cast<int>(m.hd), scale, m.d.archetype == 1, att, sm, tap, st);
     });
-    T(PRLAB_LINEAR, [&] { simt_gemm(p.ctx32, h, w.wo_t, h, p.x, h, Mi, hi, hi, lin, SimtGemmEpi{w.bo, 2, act, res, p.x}, st); });
+    T(PRLAB_LINEAR, [&] { lin_gemm(p.ctx32, h, w.wo_t, wl ? wl->wo : nullptr, h, p.x, h, Mi, hi, hi, w.bo, 2, p.x); });
     T(PRLAB_LAYERNORM, [&] { simt_layernorm(p.x, Mi, hi, w16.ln2g, w16.ln2b, 1e-5f, ln, p.xn32, nullptr, 0, st); });
-    T(PRLAB_LINEAR, [&] { simt_gemm(p.xn32, h, w.w1_t, h, p.ff32, f, Mi, fi, hi, lin, SimtGemmEpi{w.b1, 1, act, res, nullptr}, st); });
-    T(PRLAB_LINEAR, [&] { simt_gemm(p.ff32, f, w.w2_t, f, p.x, h, Mi, hi, fi, lin, SimtGemmEpi{w.b2, 2, act, res, p.x}, st); });
+    T(PRLAB_LINEAR, [&] { lin_gemm(p.xn32, h, w.w1_t, wl ? wl->w1 : nullptr, h, p.ff32, f, Mi, fi, hi, w.b1, 1, nullptr); });
+    T(PRLAB_LINEAR, [&] { lin_gemm(p.ff32, f, w.w2_t, wl ? wl->w2 : nullptr, f, p.x, h, Mi, hi, fi, w.b2, 2, p.x); });
   }
   if (o.hidden_only) {
     // forward_hidden: zero layers -> the embeddings (p.x), else the final LN in xn32
@@ -1063,9 +1115,7 @@ int64_t enqueue_forward(prlab_gpu_model& m, prlab_gpu_model::Plan& p, const int3
   } else {
     T(PRLAB_LAYERNORM, [&] { simt_layernorm(p.x, Mi, hi, m.lnfg, m.lnfb, 1e-5f, ln, p.xn32, nullptr, 0, st); });
     // tied head: logits = hidden . E^T, E [V, h] is already K-major (model.cpp:469-480)
-    T(PRLAB_LINEAR, [&] {
-      simt_gemm(p.xn32, h, m.tok, h, dst, ld, Mi, Vi, hi, lin, SimtGemmEpi{nullptr, 0, act, res, nullptr}, st);
-    });
+    T(PRLAB_LINEAR, [&] { lin_gemm(p.xn32, h, m.tok, tc32 ? m.tok_lo : nullptr, h, dst, ld, Mi, Vi, hi, nullptr, 0, nullptr); });
   }
   return n;
 }
@@ -2010,6 +2060,23 @@ int prlab_gpu_linear_f16_device_ex(const void* A, const void* Wt, const float* b
     const GemmPlan p = plan_gemm_tc(A, K_, Wt, K_, bias, out, ldo, static_cast<int>(M), static_cast<int>(N),
                                     static_cast<int>(K_), epi, &global_split_scratch(), bn, splits, lean);
     launch_gemm_tc(p, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int prlab_gpu_linear_f32_device(const float* A, const float* Wt, const float* bias, float* out, int64_t M, int64_t N,
+                                int64_t K_, int32_t epi, const float* resid, void* stream) {
+  return guarded([&] {
+    if (epi < 0 || epi > 2) throw std::invalid_argument("unknown epilogue");
+    if (M < 1 || N < 1 || K_ < 1) throw std::invalid_argument("empty linear");
+    if (epi == 2 && resid == nullptr) throw std::invalid_argument("residual epilogue needs resid");
+    if (!gemm_tf32_ok(A, K_, Wt, K_, K_)) throw std::invalid_argument("tf32 linear: K % 32 and 16-byte alignment");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    TmpDev lo(static_cast<size_t>(N * K_) * 4);
+    split_lo(Wt, lo.f(), N * K_, st);
+    auto& sc = global_split_scratch();
+    gemm_tf32(A, K_, Wt, lo.f(), K_, out, N, static_cast<int>(M), static_cast<int>(N), static_cast<int>(K_), bias, epi,
+              resid, sc.ws, sc.ws_floats, st);
+    PRLAB_CUDA(cudaStreamSynchronize(st));  // the residue buffer is freed on return
   });
 }
 
