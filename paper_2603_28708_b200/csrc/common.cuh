@@ -382,6 +382,13 @@ __device__ __forceinline__ void tma_load_2d_pair(void* dst, const CUtensorMap* m
       "l"(reinterpret_cast<uint64_t>(m)), "r"(to_leader(smem_u32(bar))), "r"(c0), "r"(c1)
       : "memory");
 }
+__device__ __forceinline__ void tma_load_3d_pair(void* dst, const CUtensorMap* m, uint64_t* bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, "
+      "%4, %5}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(to_leader(smem_u32(bar))), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
 // Pair TMA load multicast to the CTAs in `mask` (cluster-relative ranks): each
 // destination receives the box at the same shared offset and the transaction bytes
 // complete on the mbarrier of its pair's leader (same offset).

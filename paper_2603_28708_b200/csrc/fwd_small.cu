@@ -55,10 +55,10 @@ struct SmemL {
 constexpr int kRowH = 72;    // fp16 row stride (halves) of K / V / Q / ctx
 constexpr int kRowP = 136;   // fp16 row stride of P
 constexpr int kRowS = 132;   // fp32 row stride of the scores
-__host__ __device__ constexpr uint32_t att_bytes(int h) {
-  return static_cast<uint32_t>(h) * 128 + (2 * 128 + 2 * kQB) * kRowH * 2 + kQB * kRowS * 4 + kQB * kRowP * 2;
+__host__ __device__ constexpr uint32_t att_bytes(int h, int qb) {
+  return static_cast<uint32_t>(h) * 128 + (2 * 128 + 2 * qb) * kRowH * 2 + qb * kRowS * 4 + qb * kRowP * 2;
 }
-static_assert(att_bytes(1024) <= SmemL::BAR, "attention scratch");
+static_assert(att_bytes(1024, 16) <= SmemL::BAR && att_bytes(768, 32) <= SmemL::BAR, "attention scratch");
 
 struct LayerW {
   const float *ln1g, *ln1b, *ln2g, *ln2b;  // fp32 [h]
@@ -209,12 +209,23 @@ struct Ctl {
 // Weights (B) of one task into smem: issued by the producer thread as soon as the
 // previous task's MMAs have consumed sB -- at the end of the previous stage, so the
 // DRAM latency of the weights hides under the grid barrier.
-template <int NT>
+// PAIR (M in (128, 256], CTA pairs of a 2-CTA cluster, cta_group::2 MMAs issued by the leader):
+// each CTA loads half of the task's NT weight rows (rows n0 + rank * NT/2) into the same
+// offset; the transaction bytes complete on the leader's barrier, the peer arrives remotely.
+template <int NT, bool PAIR>
 __device__ void load_b(Ctl& c, uint8_t* smem, const CUtensorMap* mB, int n0, int k0, int nkb) {
   if (threadIdx.x == 4 * 32) {
-    mbar_wait(c.accempty, (c.tc & 1) ^ 1);  // previous task's MMAs done reading sB
-    mbar_expect_tx(c.bfull, static_cast<uint32_t>(nkb) * NT * 128);
-    tma_load_3d(smem + SmemL::B, mB, c.bfull, 0, n0, k0 / 64);  // the task's whole B: one request
+    if (!PAIR) {
+      mbar_wait(c.accempty, (c.tc & 1) ^ 1);  // previous task's MMAs done reading sB
+      mbar_expect_tx(c.bfull, static_cast<uint32_t>(nkb) * NT * 128);
+      tma_load_3d(smem + SmemL::B, mB, c.bfull, 0, n0, k0 / 64);  // the task's whole B: one request
+    } else {
+      const uint32_t rank = cluster_ctarank() & 1;
+      if (c.tc > 0) mbar_wait(c.accfull, (c.tc - 1) & 1);  // the pair's previous MMAs read this sB
+      if (rank == 0) mbar_expect_tx(c.bfull, static_cast<uint32_t>(nkb) * NT * 128);  // both halves
+      tma_load_3d_pair(smem + SmemL::B, mB, c.bfull, 0, n0 + static_cast<int>(rank) * (NT / 2), k0 / 64);
+      if (rank != 0) mbar_arrive_cluster(to_leader(smem_u32(c.bfull)));
+    }
   }
   c.bpref = 1;
 }
@@ -222,14 +233,15 @@ __device__ void load_b(Ctl& c, uint8_t* smem, const CUtensorMap* mB, int n0, int
 // One GEMM task: D[128 x NT] = A[:, k0:k0+64*nkb] . B[n0:n0+NT, same]^T, then `EPI`.
 // EPI 0: fp32 partial -> out32 (row pitch ld32); 1: round16(gelu(round16(round16(acc) + b)))
 // -> out16; 2: round16(round16(acc) + b) -> out16.
-template <int NT, int EPI, int KP>
+template <int NT, int EPI, int KP, bool PAIR = false>
 __device__ void gemm_task(const SmallArgs& a, uint8_t* smem, Ctl& c, const CUtensorMap* mA, const CUtensorMap* mB,
                           int n0, int k0, int nkb, float* out32, int64_t ld32, const float* bias, __half* out16,
                           int64_t ld16) {
   const uint32_t warp = warp_id(), lane = lane_id();
+  const uint32_t rank = PAIR ? (cluster_ctarank() & 1) : 0;  // PAIR: this CTA's 128 token rows
   uint8_t* sA = smem + SmemL::A;
   uint8_t* sB = smem + SmemL::B;
-  if (!c.bpref) load_b<NT>(c, smem, mB, n0, k0, nkb);
+  if (!c.bpref) load_b<NT, PAIR>(c, smem, mB, n0, k0, nkb);
   c.bpref = 0;
   if (warp == 4) {
     if (lane == 0) {
@@ -237,17 +249,23 @@ __device__ void gemm_task(const SmallArgs& a, uint8_t* smem, Ctl& c, const CUten
       for (int kb = 0; kb < nkb; kb += KP) {  // one request of KP k-blocks per ring slot
         const uint32_t u = c.kc + kb / KP, st = u % kStages;
         mbar_wait(&c.empty[st], ((u / kStages) & 1) ^ 1);
-        mbar_expect_tx(&c.full[st], KP * kABytes);
-        tma_load_3d(sA + st * kKPR * kABytes, mA, &c.full[st], 0, 0, k0 / 64 + kb);
+        if (!PAIR) {
+          mbar_expect_tx(&c.full[st], KP * kABytes);
+          tma_load_3d(sA + st * kKPR * kABytes, mA, &c.full[st], 0, 0, k0 / 64 + kb);
+        } else {
+          if (rank == 0) mbar_expect_tx(&c.full[st], 2 * KP * kABytes);  // both CTAs' rows
+          tma_load_3d_pair(sA + st * kKPR * kABytes, mA, &c.full[st], 0, static_cast<int>(rank) * 128, k0 / 64 + kb);
+          if (rank != 0) mbar_arrive_cluster(to_leader(smem_u32(&c.full[st])));
+        }
       }
     }
     __syncwarp();
-  } else if (warp == 5) {
+  } else if (warp == 5 && rank == 0) {
     if (lane == 0) {
       long long* gs = (a.dbg && blockIdx.x == 0 && c.tc < 64) ? a.dbg + 220000 + c.tc * 8 : nullptr;
       if (gs) gs[0] = globaltimer();
-      constexpr uint32_t idesc = idesc_f16_f32(128, NT, 0, 0);
-      mbar_wait(c.accempty, (c.tc & 1) ^ 1);  // epilogue of the previous task read TMEM
+      constexpr uint32_t idesc = idesc_f16_f32(PAIR ? 256 : 128, NT, 0, 0);
+      mbar_wait(c.accempty, (c.tc & 1) ^ 1);  // epilogue of the previous task read TMEM (PAIR: both CTAs')
       mbar_wait(c.bfull, c.tc & 1);
       if (gs) gs[1] = globaltimer();
       tc_fence_after();
@@ -258,15 +276,28 @@ __device__ void gemm_task(const SmallArgs& a, uint8_t* smem, Ctl& c, const CUten
         tc_fence_after();
 #pragma unroll
         for (int j = 0; j < KP; ++j) {
-          const uint32_t a0 = smem_u32(sA + (st * kKPR + j) * kABytes), b0 = smem_u32(sB + (kb + j) * (NT * 128));  // the 3D box packs k-blocks at NT rows
+          // the 3D box packs k-blocks at NT rows (PAIR: NT / 2 rows per CTA)
+          const uint32_t a0 = smem_u32(sA + (st * kKPR + j) * kABytes),
+                         b0 = smem_u32(sB + (kb + j) * ((PAIR ? NT / 2 : NT) * 128));
 #pragma unroll
-          for (int kk = 0; kk < 4; ++kk)
-            umma_f16_ss(c.tmem, sw128_desc(a0 + kk * 32, 0, 1024), sw128_desc(b0 + kk * 32, 0, 1024), idesc,
-                        (kb | j | kk) != 0);
+          for (int kk = 0; kk < 4; ++kk) {
+            if (PAIR)
+              umma_f16_ss_pair(c.tmem, sw128_desc(a0 + kk * 32, 0, 1024), sw128_desc(b0 + kk * 32, 0, 1024), idesc,
+                               (kb | j | kk) != 0);
+            else
+              umma_f16_ss(c.tmem, sw128_desc(a0 + kk * 32, 0, 1024), sw128_desc(b0 + kk * 32, 0, 1024), idesc,
+                          (kb | j | kk) != 0);
+          }
         }
-        umma_commit(&c.empty[st]);
+        if (PAIR)
+          umma_commit_pair(&c.empty[st]);  // both CTAs' A slots are free
+        else
+          umma_commit(&c.empty[st]);
       }
-      umma_commit(c.accfull);
+      if (PAIR)
+        umma_commit_pair(c.accfull);
+      else
+        umma_commit(c.accfull);
       if (gs) gs[3] = globaltimer();
     }
     __syncwarp();
@@ -303,8 +334,13 @@ __device__ void gemm_task(const SmallArgs& a, uint8_t* smem, Ctl& c, const CUten
     tmem_wait_ld();
     tc_fence_before();
     __syncwarp();
-    if (lane == 0) mbar_arrive(c.accempty);
-    const int row = static_cast<int>(quad * 32 + lane);
+    if (lane == 0) {
+      if (PAIR)
+        mbar_arrive_cluster(to_leader(smem_u32(c.accempty)));  // the leader's MMAs reuse both TMEMs
+      else
+        mbar_arrive(c.accempty);
+    }
+    const int row = static_cast<int>(rank * 128 + quad * 32 + lane);
     if (row < a.M) {
       if (EPI == 0) {
         float4* o = reinterpret_cast<float4*>(out32 + static_cast<int64_t>(row) * ld32 + c0);
@@ -361,8 +397,10 @@ __device__ __forceinline__ void mma16816(float (&d)[4], const uint32_t (&a)[4], 
 // head's Wo partial ctx_h . Wo[:, head cols]^T -> part[head][rows] in fp32; the RLN2
 // stage sums the heads' partials in head order.  q/k/v come from the QKV stage's fp16
 // output (pitch 3h).
+template <int QB>  // queries per task: 16 (one m16 row block) or 32 (two; CTA-pair mode, M > 128)
 __device__ void attn_wo_task(const SmallArgs& a, uint8_t* smem, const CUtensorMap* mWo, uint64_t* wo_bar,
                              uint32_t wo_phase, int b, int hh, int q0, long long* ts) {
+  constexpr int MB = QB / 16;
   // ts (debug, thread 0 only): [0] start [1] q/k/v staged [2] scores [3] softmax [4] ctx [5] Wo landed [6] done
   if (ts) ts[0] = globaltimer();
   const int h = a.h, S = a.S;
@@ -371,10 +409,10 @@ __device__ void attn_wo_task(const SmallArgs& a, uint8_t* smem, const CUtensorMa
   __half* sK = reinterpret_cast<__half*>(smem + h * 128);
   __half* sV = sK + 128 * kRowH;
   __half* sQ = sV + 128 * kRowH;
-  __half* sC = sQ + kQB * kRowH;
-  float* sS = reinterpret_cast<float*>(sC + kQB * kRowH);
-  __half* sP = reinterpret_cast<__half*>(sS + kQB * kRowS);
-  const int kv = a.causal ? min(S, q0 + kQB) : S;  // keys this block can see
+  __half* sC = sQ + QB * kRowH;
+  float* sS = reinterpret_cast<float*>(sC + QB * kRowH);
+  __half* sP = reinterpret_cast<__half*>(sS + QB * kRowS);
+  const int kv = a.causal ? min(S, q0 + QB) : S;  // keys this block can see
   const int kvp = (kv + 15) & ~15;
   __syncthreads();  // the previous task's readers are done with the scratch
   if (threadIdx.x == 0) {  // the head's Wo column slice: h rows x 64 (128 B), 256-row boxes
@@ -398,7 +436,7 @@ __device__ void attn_wo_task(const SmallArgs& a, uint8_t* smem, const CUtensorMa
       }
     }
     const int qi = threadIdx.x >> 3, qc8 = (threadIdx.x & 7) * 8;
-    if (threadIdx.x < kQB * 8 && q0 + qi < S)
+    if (threadIdx.x < QB * 8 && q0 + qi < S)
       qq = *reinterpret_cast<const uint4*>(base + static_cast<int64_t>(q0 + qi) * 3 * h + qc8);
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
@@ -408,53 +446,57 @@ __device__ void attn_wo_task(const SmallArgs& a, uint8_t* smem, const CUtensorMa
         *reinterpret_cast<uint4*>(sV + j * kRowH + c8) = vv[u];
       }
     }
-    if (threadIdx.x < kQB * 8) *reinterpret_cast<uint4*>(sQ + qi * kRowH + qc8) = qq;
+    if (threadIdx.x < QB * 8) *reinterpret_cast<uint4*>(sQ + qi * kRowH + qc8) = qq;
   }
   __syncthreads();
   if (ts) ts[1] = globaltimer();
   const int g = lane >> 2, t4 = lane & 3;
-  // scores: warp w -> keys [16w, 16w + 16)
+  // scores: warp w -> keys [16w, 16w + 16), every 16-query row block
   if (static_cast<int>(warp) * 16 < kvp) {
-    float acc[2][4] = {};
 #pragma unroll
-    for (int ks = 0; ks < 4; ++ks) {
-      uint32_t af[4], bf[4];
-      ldsm_x4(smem_u32(sQ + (lane & 15) * kRowH + ks * 16 + (lane >> 4) * 8), af);
-      ldsm_x4(smem_u32(sK + (warp * 16 + (lane & 7) + (lane >> 4) * 8) * kRowH + ks * 16 + ((lane >> 3) & 1) * 8), bf);
-      mma16816(acc[0], af, bf[0], bf[1]);
-      mma16816(acc[1], af, bf[2], bf[3]);
-    }
+    for (int mb = 0; mb < MB; ++mb) {
+      float acc[2][4] = {};
 #pragma unroll
-    for (int nt = 0; nt < 2; ++nt)
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int r = g + (e >> 1) * 8, j = warp * 16 + nt * 8 + 2 * t4 + (e & 1);
-        const bool valid = j < kv && (!a.causal || j <= q0 + r);
-        sS[r * kRowS + j] = valid ? r16(__fmul_rn(acc[nt][e], 0.125f)) : __int_as_float(0xff800000);
+      for (int ks = 0; ks < 4; ++ks) {
+        uint32_t af[4], bf[4];
+        ldsm_x4(smem_u32(sQ + (mb * 16 + (lane & 15)) * kRowH + ks * 16 + (lane >> 4) * 8), af);
+        ldsm_x4(smem_u32(sK + (warp * 16 + (lane & 7) + (lane >> 4) * 8) * kRowH + ks * 16 + ((lane >> 3) & 1) * 8), bf);
+        mma16816(acc[0], af, bf[0], bf[1]);
+        mma16816(acc[1], af, bf[2], bf[3]);
       }
+#pragma unroll
+      for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int r = mb * 16 + g + (e >> 1) * 8, j = warp * 16 + nt * 8 + 2 * t4 + (e & 1);
+          const bool valid = j < kv && (!a.causal || j <= q0 + r);
+          sS[r * kRowS + j] = valid ? r16(__fmul_rn(acc[nt][e], 0.125f)) : __int_as_float(0xff800000);
+        }
+    }
   }
   __syncthreads();
   if (ts) ts[2] = globaltimer();
-  // softmax: warp w -> rows 2w, 2w + 1 (interleaved); lane -> keys lane + 32c
+  // softmax: warp w -> rows w * QB/8 .. (interleaved); lane -> keys lane + 32c
   {
-    float sc[2][4], mx[2], sum[2], e[2][4];
+    constexpr int RW = QB / 8;  // rows per warp
+    float sc[RW][4], mx[RW], sum[RW], e[RW][4];
 #pragma unroll
-    for (int rr = 0; rr < 2; ++rr) {
+    for (int rr = 0; rr < RW; ++rr) {
       mx[rr] = __int_as_float(0xff800000);
 #pragma unroll
       for (int c4 = 0; c4 < 4; ++c4) {
         const int j = c4 * 32 + lane;
-        sc[rr][c4] = j < kvp ? sS[(warp * 2 + rr) * kRowS + j] : __int_as_float(0xff800000);
+        sc[rr][c4] = j < kvp ? sS[(warp * RW + rr) * kRowS + j] : __int_as_float(0xff800000);
         mx[rr] = fmaxf(mx[rr], sc[rr][c4]);
       }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-      for (int rr = 0; rr < 2; ++rr) mx[rr] = fmaxf(mx[rr], __shfl_xor_sync(0xffffffffu, mx[rr], o));
+      for (int rr = 0; rr < RW; ++rr) mx[rr] = fmaxf(mx[rr], __shfl_xor_sync(0xffffffffu, mx[rr], o));
     constexpr float LOG2E = 1.4426950408889634f;
 #pragma unroll
-    for (int rr = 0; rr < 2; ++rr) {
+    for (int rr = 0; rr < RW; ++rr) {
       const float mxl = __fmul_rn(mx[rr], LOG2E);
       sum[rr] = 0.0f;
 #pragma unroll
@@ -466,43 +508,46 @@ __device__ void attn_wo_task(const SmallArgs& a, uint8_t* smem, const CUtensorMa
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
-      for (int rr = 0; rr < 2; ++rr) sum[rr] = __fadd_rn(sum[rr], __shfl_xor_sync(0xffffffffu, sum[rr], o));
+      for (int rr = 0; rr < RW; ++rr) sum[rr] = __fadd_rn(sum[rr], __shfl_xor_sync(0xffffffffu, sum[rr], o));
 #pragma unroll
-    for (int rr = 0; rr < 2; ++rr) {
+    for (int rr = 0; rr < RW; ++rr) {
       const float inv = __frcp_rn(sum[rr]);
 #pragma unroll
       for (int c4 = 0; c4 < 4; ++c4) {
         const int j = c4 * 32 + lane;
-        if (j < kvp) sP[(warp * 2 + rr) * kRowP + j] = __float2half_rn(__fmul_rn(e[rr][c4], inv));
+        if (j < kvp) sP[(warp * RW + rr) * kRowP + j] = __float2half_rn(__fmul_rn(e[rr][c4], inv));
       }
     }
   }
   __syncthreads();
   if (ts) ts[3] = globaltimer();
-  // ctx = round16(P . V): warp w -> dims [8w, 8w + 8)
-  {
+  // ctx = round16(P . V): warp w -> dims [8w, 8w + 8), every row block
+#pragma unroll
+  for (int mb = 0; mb < MB; ++mb) {
     float o[4] = {};
     for (int ks = 0; ks < kvp / 16; ++ks) {
       uint32_t af[4], bf[2];
-      ldsm_x4(smem_u32(sP + (lane & 15) * kRowP + ks * 16 + (lane >> 4) * 8), af);
+      ldsm_x4(smem_u32(sP + (mb * 16 + (lane & 15)) * kRowP + ks * 16 + (lane >> 4) * 8), af);
       ldsm_x2_trans(smem_u32(sV + (ks * 16 + (lane & 15)) * kRowH + warp * 8), bf);
       mma16816(o, af, bf[0], bf[1]);
     }
-    *reinterpret_cast<__half2*>(sC + g * kRowH + warp * 8 + 2 * t4) = __floats2half2_rn(o[0], o[1]);
-    *reinterpret_cast<__half2*>(sC + (g + 8) * kRowH + warp * 8 + 2 * t4) = __floats2half2_rn(o[2], o[3]);
+    *reinterpret_cast<__half2*>(sC + (mb * 16 + g) * kRowH + warp * 8 + 2 * t4) = __floats2half2_rn(o[0], o[1]);
+    *reinterpret_cast<__half2*>(sC + (mb * 16 + g + 8) * kRowH + warp * 8 + 2 * t4) = __floats2half2_rn(o[2], o[3]);
   }
   __syncthreads();
   if (ts) ts[4] = globaltimer();
-  // Wo partial: out[16][h] = ctx . WoSlice^T; warp w -> n-tiles [w * h/64, (w+1) * h/64) (pairs)
-  {
+  // Wo partial: out[QB][h] = ctx . WoSlice^T; warp w -> n-tiles [w * h/64, (w+1) * h/64) (pairs)
+  mbar_wait(wo_bar, wo_phase);
+  if (ts) ts[5] = globaltimer();
+#pragma unroll
+  for (int mb = 0; mb < MB; ++mb) {
     uint32_t af[4][4];
 #pragma unroll
-    for (int ks = 0; ks < 4; ++ks) ldsm_x4(smem_u32(sC + (lane & 15) * kRowH + ks * 16 + (lane >> 4) * 8), af[ks]);
-    mbar_wait(wo_bar, wo_phase);
-    if (ts) ts[5] = globaltimer();
+    for (int ks = 0; ks < 4; ++ks)
+      ldsm_x4(smem_u32(sC + (mb * 16 + (lane & 15)) * kRowH + ks * 16 + (lane >> 4) * 8), af[ks]);
     const int per_warp = h / 64;  // n-tiles of 8 columns per warp (h / 8 tiles over 8 warps)
     float* outp = a.part + static_cast<int64_t>(hh) * a.M * h;
-    const int row0 = b * S + q0;
+    const int row0 = b * S + q0 + mb * 16, qr = q0 + mb * 16;
 #pragma unroll 2
     for (int p2 = 0; p2 < per_warp; p2 += 2) {
       const int n0 = (warp * per_warp + p2) * 8;
@@ -519,9 +564,9 @@ __device__ void attn_wo_task(const SmallArgs& a, uint8_t* smem, const CUtensorMa
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt) {
         const int col = n0 + nt * 8 + 2 * t4;
-        if (q0 + g < S)
+        if (qr + g < S)
           *reinterpret_cast<float2*>(outp + static_cast<int64_t>(row0 + g) * h + col) = make_float2(d[nt][0], d[nt][1]);
-        if (q0 + g + 8 < S)
+        if (qr + g + 8 < S)
           *reinterpret_cast<float2*>(outp + static_cast<int64_t>(row0 + g + 8) * h + col) =
               make_float2(d[nt][2], d[nt][3]);
       }
@@ -568,6 +613,93 @@ __device__ void residual_ln_row(const SmallArgs& a, int r, int nsplit, const flo
   if (ts && threadIdx.x == 0) ts[2] = globaltimer();
 }
 
+// PAIR = false: M <= 128, one CTA per GEMM task.  PAIR = true: 128 < M <= 256 on 2-CTA clusters,
+// GEMM tasks per CTA pair (cta_group::2, M = 256: each CTA its 128 token rows, half the weight
+// tile), so a task's MMA chain and per-CTA activation bytes stay those of M = 128; attention
+// and row stages are per CTA as before.
+// Two rows at once (M > grid): threads [0, 128) row r0, [128, 256) row r1 (if r1 >= 0), VPT
+// consecutive columns per thread (h = 128 VPT); the same operations as residual_ln_row /
+// ln_row, with each half's block sums over its 4 warps (named barrier per half).
+template <int MAXSP, int VPT>
+__device__ void residual_ln_rows2(const SmallArgs& a, int r0, int r1, int nsplit, const float* bias, const float* g,
+                                  const float* b, float* red, bool final_out) {
+  const int h = a.h, half = threadIdx.x >> 7, t = threadIdx.x & 127, c = VPT * t;
+  const int r = half ? r1 : r0;
+  const bool act = r >= 0;
+  const uint32_t wid = (threadIdx.x >> 5) & 3, lane = threadIdx.x & 31;
+  float* rh = red + 8 + 8 * half;  // [2][4] partials per half (red[0..7] is ln_row's)
+  float xv[VPT];
+  float gv[VPT], bv[VPT];
+  if (act) {
+    // partial sums in split order, streamed (the compiler keeps as many loads in flight as
+    // registers allow; holding all MAXSP x VPT values spills)
+    float psum[VPT];
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) psum[i] = 0.0f;
+#pragma unroll 4
+    for (int sp = 0; sp < nsplit; ++sp)
+#pragma unroll
+      for (int i = 0; i < VPT; i += 2) {
+        const float2 v2 = __ldcg(reinterpret_cast<const float2*>(a.part + (static_cast<int64_t>(sp) * a.M + r) * h + c + i));
+        psum[i] = __fadd_rn(psum[i], v2.x);
+        psum[i + 1] = __fadd_rn(psum[i + 1], v2.y);
+      }
+    float xo[VPT], bs[VPT];
+#pragma unroll
+    for (int i = 0; i < VPT; i += 2) {
+      const float2 x2 = *reinterpret_cast<const float2*>(a.x + static_cast<int64_t>(r) * h + c + i);
+      const float2 b2 = *reinterpret_cast<const float2*>(bias + c + i);
+      const float2 g2 = *reinterpret_cast<const float2*>(g + c + i);
+      const float2 e2 = *reinterpret_cast<const float2*>(b + c + i);
+      xo[i] = x2.x;
+      xo[i + 1] = x2.y;
+      bs[i] = b2.x;
+      bs[i + 1] = b2.y;
+      gv[i] = g2.x;
+      gv[i + 1] = g2.y;
+      bv[i] = e2.x;
+      bv[i + 1] = e2.y;
+    }
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) xv[i] = __fadd_rn(xo[i], r16(__fadd_rn(r16(psum[i]), bs[i])));
+#pragma unroll
+    for (int i = 0; i < VPT; i += 2)
+      *reinterpret_cast<float2*>(a.x + static_cast<int64_t>(r) * h + c + i) = make_float2(xv[i], xv[i + 1]);
+  }
+  auto half_sum = [&](float v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    named_bar_sync(2 + half, 128);
+    if (lane == 0) rh[wid] = v;
+    named_bar_sync(2 + half, 128);
+    return (rh[0] + rh[1]) + (rh[2] + rh[3]);  // fixed order
+  };
+  float s = 0.0f;
+  if (act)
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) s = __fadd_rn(s, xv[i]);
+  const float mean = __fdiv_rn(half_sum(s), static_cast<float>(h));
+  float q = 0.0f;
+  if (act)
+#pragma unroll
+    for (int i = 0; i < VPT; ++i) {
+      const float d = __fsub_rn(xv[i], mean);
+      q = __fmaf_rn(d, d, q);
+    }
+  const float var = __fdiv_rn(half_sum(q), static_cast<float>(h));
+  const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(var, 1e-5f)));
+  if (act) {
+    __half* out = a.xn16 + static_cast<int64_t>(r) * h + c;
+#pragma unroll
+    for (int i = 0; i < VPT; i += 2)
+      *reinterpret_cast<uint32_t*>(out + i) =
+          h2_pack_rn(__fadd_rn(__fmul_rn(gv[i], __fmul_rn(__fsub_rn(xv[i], mean), inv)), bv[i]),
+                     __fadd_rn(__fmul_rn(gv[i + 1], __fmul_rn(__fsub_rn(xv[i + 1], mean), inv)), bv[i + 1]));
+  }
+  (void)final_out;
+}
+
+template <bool PAIR>
 __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_constant__ SmallArgs a) {
   // no static shared memory in this kernel: the dynamic window starts 1024-aligned, and
   // indexing it directly keeps every access in the shared state space (LDS/STS)
@@ -575,8 +707,8 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
   const int h = a.h, f = a.f, M = a.M, S = a.S, H = a.H;
   const uint32_t warp = warp_id(), lane = lane_id();
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SmemL::BAR);
-  float* red = reinterpret_cast<float*>(bars + 16);  // [8]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(red + 8);
+  float* red = reinterpret_cast<float*>(bars + 16);  // [8] ln_row, [8..24) residual_ln_rows2
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(red + 24);
   Ctl c;
   c.full = bars;
   c.empty = bars + kStages;
@@ -587,18 +719,24 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
   uint32_t n_att = 0;                         // attention tasks run by this CTA (wo_bar phase)
   if (threadIdx.x == 0) {
     for (int i = 0; i < kStages; ++i) {
-      mbar_init(&c.full[i], 1);
+      mbar_init(&c.full[i], PAIR ? 2 : 1);  // PAIR: both CTAs' producers arrive on the leader's
       mbar_init(&c.empty[i], 1);
     }
-    mbar_init(c.bfull, 1);
+    mbar_init(c.bfull, PAIR ? 2 : 1);
     mbar_init(c.accfull, 1);
-    mbar_init(c.accempty, 8);  // every warp reads its TMEM slice
+    mbar_init(c.accempty, PAIR ? 16 : 8);  // every warp (PAIR: of both CTAs) reads its TMEM slice
     mbar_init(wo_bar, 1);
     fence_barrier_init();
   }
+  if (PAIR) cluster_sync_all();  // barrier inits visible to the peer before any remote arrival
   if (warp == 5) {
-    tmem_alloc(tslot, 32);
-    tmem_relinquish();
+    if (PAIR) {
+      tmem_alloc_pair(tslot, 64);
+      tmem_relinquish_pair();
+    } else {
+      tmem_alloc(tslot, 32);
+      tmem_relinquish();
+    }
   }
   if (warp == 6)
     for (int i = lane; i < 2 + 4 * a.L; i += 32) tma_prefetch_desc(&a.maps[i]);
@@ -612,22 +750,25 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
   unsigned target = 0;
   const CUtensorMap* mXn = a.maps + 0;
   const CUtensorMap* mFf = a.maps + 1;
-  // task geometry (same on every CTA)
-  const int t_qkv = 3 * h / 16;                    // N=16 tiles, full K -> fp16 q/k/v
-  const int t_ffn1 = f / kTileN;                   // N=32 tiles, full K, GELU
-  const int t_ffn2 = (h / kTileN) * a.split_ffn2;  // N=32 tiles x K splits -> partials
+  // task geometry (same on every CTA; PAIR: per CTA pair, N per pair task)
+  constexpr int NQ = PAIR ? 32 : 16, N1 = PAIR ? 64 : kTileN, N2 = PAIR ? 64 : kTileN;
+  const int gid = PAIR ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+  const int gn = PAIR ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
+  const int t_qkv = 3 * h / NQ;                 // full K -> fp16 q/k/v
+  const int t_ffn1 = f / N1;                    // full K, GELU
+  const int t_ffn2 = (h / N2) * a.split_ffn2;   // tiles x K splits -> partials
   const int kb_ffn2 = f / 64 / a.split_ffn2;
   auto pre_qkv = [&](int l) {
-    if (static_cast<int>(blockIdx.x) < t_qkv) load_b<16>(c, smem, a.maps + 2 + 4 * l + 0, blockIdx.x * 16, 0, h / 64);
+    if (gid < t_qkv) load_b<NQ, PAIR>(c, smem, a.maps + 2 + 4 * l + 0, gid * NQ, 0, h / 64);
   };
   auto pre_ffn1 = [&](int l) {
-    if (static_cast<int>(blockIdx.x) < t_ffn1) load_b<kTileN>(c, smem, a.maps + 2 + 4 * l + 2, blockIdx.x * kTileN, 0, h / 64);
+    if (gid < t_ffn1) load_b<N1, PAIR>(c, smem, a.maps + 2 + 4 * l + 2, gid * N1, 0, h / 64);
   };
   auto pre_ffn2 = [&](int l) {
-    const int t = blockIdx.x;
+    const int t = gid;
     if (t < t_ffn2)
-      load_b<kTileN>(c, smem, a.maps + 2 + 4 * l + 3, (t / a.split_ffn2) * kTileN, (t % a.split_ffn2) * kb_ffn2 * 64,
-                     kb_ffn2);
+      load_b<N2, PAIR>(c, smem, a.maps + 2 + 4 * l + 3, (t / a.split_ffn2) * N2, (t % a.split_ffn2) * kb_ffn2 * 64,
+                       kb_ffn2);
   };
 
   // ---- stage 0: embedding gather (bit-exact fp32 tok + pos) + LN1 of layer 0
@@ -663,12 +804,15 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
       prefetch_layer_weights(a, a.lw[l + 1]);
     }
     // ---- QKV: N=16 tiles, full K, round16(round16(acc) + b) -> fp16 q|k|v (ff16 buffer)
-    for (int t = blockIdx.x; t < t_qkv; t += gridDim.x)
-      gemm_task<16, 2, 4>(a, smem, c, mXn, mW + 0, t * 16, 0, h / 64, nullptr, 0, w.bqkv, a.ff16, 3 * h);
+    for (int t = gid; t < t_qkv; t += gn)
+      gemm_task<NQ, 2, 4, PAIR>(a, smem, c, mXn, mW + 0, t * NQ, 0, h / 64, nullptr, 0, w.bqkv, a.ff16, 3 * h);
     grid_sync(a.gbar, target, a.dbg);
     // ---- attention + Wo: (batch, head, 16-query block) tasks, head partials -> part[head]
     {
-      const int nqb = (S + kQB - 1) / kQB;
+      // PAIR (M > 128): 32-query tasks -- at most 96 for S <= 128, one round on 148 CTAs
+      const bool q32 = PAIR && h <= 768;  // (the 32-query scratch fits for h <= 768)
+      const int QB = q32 ? 32 : kQB;
+      const int nqb = (S + QB - 1) / QB;
       long long* ats = (a.dbg && blockIdx.x == 0 && threadIdx.x == 0) ? a.dbg + 210000 + l * 8 : nullptr;
       if (ats) ats[0] = globaltimer();
       for (int t = blockIdx.x; t < a.B * H * nqb; t += gridDim.x) {
@@ -677,7 +821,10 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         // debug stamps: the heaviest causal task of head 0 (last query block)
         long long* ts = (a.dbg && qb == nqb - 1 && hh == 0 && b == 0 && threadIdx.x == 0) ? a.dbg + 230000 + l * 8 : nullptr;
-        attn_wo_task(a, smem, mW + 1, wo_bar, n_att & 1, b, hh, qb * kQB, ts);
+        if (q32)
+          attn_wo_task<32>(a, smem, mW + 1, wo_bar, n_att & 1, b, hh, qb * QB, ts);
+        else
+          attn_wo_task<kQB>(a, smem, mW + 1, wo_bar, n_att & 1, b, hh, qb * QB, ts);
         ++n_att;
       }
       if (ats) ats[1] = globaltimer();
@@ -688,39 +835,56 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
     }
     grid_sync(a.gbar, target, a.dbg);
     // ---- residual + LN2: x += round16(round16(sum over heads of the Wo partials) + bo)
-    for (int r = blockIdx.x; r < M; r += gridDim.x)
-      residual_ln_row<16>(a, r, H, w.bo, w.ln2g, w.ln2b, red,
-                          (a.dbg && blockIdx.x == 0) ? a.dbg + 200000 + l * 8 : nullptr);
+    if (PAIR && M > static_cast<int>(gridDim.x) && h == 768 && H <= 12) {  // two rows per CTA at once
+      for (int r = blockIdx.x; r < M; r += 2 * gridDim.x)
+        residual_ln_rows2<12, 6>(a, r, r + static_cast<int>(gridDim.x) < M ? r + static_cast<int>(gridDim.x) : -1, H,
+                                 w.bo, w.ln2g, w.ln2b, red, false);
+    } else {
+      for (int r = blockIdx.x; r < M; r += gridDim.x)
+        residual_ln_row<16>(a, r, H, w.bo, w.ln2g, w.ln2b, red,
+                            (a.dbg && blockIdx.x == 0) ? a.dbg + 200000 + l * 8 : nullptr);
+    }
     grid_sync(a.gbar, target, a.dbg);
     // ---- FFN1 + GELU, full K
-    for (int t = blockIdx.x; t < t_ffn1; t += gridDim.x)
-      gemm_task<kTileN, 1, 4>(a, smem, c, mXn, mW + 2, t * kTileN, 0, h / 64, nullptr, 0, w.b1, a.ff16, f);
+    for (int t = gid; t < t_ffn1; t += gn)
+      gemm_task<N1, 1, 4, PAIR>(a, smem, c, mXn, mW + 2, t * N1, 0, h / 64, nullptr, 0, w.b1, a.ff16, f);
     pre_ffn2(l);
     grid_sync(a.gbar, target, a.dbg);
     // ---- FFN2: partials over K splits
-    for (int t = blockIdx.x; t < t_ffn2; t += gridDim.x)
-      gemm_task<kTileN, 0, 4>(a, smem, c, mFf, mW + 3, (t / a.split_ffn2) * kTileN, (t % a.split_ffn2) * kb_ffn2 * 64,
-                           kb_ffn2, a.part + static_cast<int64_t>(t % a.split_ffn2) * M * h, h, nullptr, nullptr, 0);
+    for (int t = gid; t < t_ffn2; t += gn)
+      gemm_task<N2, 0, 4, PAIR>(a, smem, c, mFf, mW + 3, (t / a.split_ffn2) * N2, (t % a.split_ffn2) * kb_ffn2 * 64,
+                                kb_ffn2, a.part + static_cast<int64_t>(t % a.split_ffn2) * M * h, h, nullptr, nullptr,
+                                0);
     if (l + 1 < a.L) pre_qkv(l + 1);
     grid_sync(a.gbar, target, a.dbg);
     // ---- residual + LN1 of the next layer (or the final LN)
     {
       const float* g = l + 1 < a.L ? a.lw[l + 1].ln1g : a.lnfg;
       const float* bb = l + 1 < a.L ? a.lw[l + 1].ln1b : a.lnfb;
-      for (int r = blockIdx.x; r < M; r += gridDim.x) residual_ln_row<8>(a, r, a.split_ffn2, w.b2, g, bb, red);
+      if (PAIR && M > static_cast<int>(gridDim.x) && h == 768) {
+        for (int r = blockIdx.x; r < M; r += 2 * gridDim.x)
+          residual_ln_rows2<8, 6>(a, r, r + static_cast<int>(gridDim.x) < M ? r + static_cast<int>(gridDim.x) : -1,
+                                  a.split_ffn2, w.b2, g, bb, red, false);
+      } else {
+        for (int r = blockIdx.x; r < M; r += gridDim.x) residual_ln_row<8>(a, r, a.split_ffn2, w.b2, g, bb, red);
+      }
     }
     if (l + 1 < a.L) grid_sync(a.gbar, target, a.dbg);
   }
   pdl_trigger();
   tc_fence_before();
   __syncthreads();
+  if (PAIR) cluster_sync_all();  // the peer's remote arrivals / MMAs on this CTA are done
   if (warp == 5) {
     tc_fence_after();
-    tmem_dealloc(c.tmem, 32);
+    if (PAIR)
+      tmem_dealloc_pair(c.tmem, 64);
+    else
+      tmem_dealloc(c.tmem, 32);
   }
 }
 
-constexpr size_t kSmem = SmemL::BAR + 16 * 8 + 8 * 4 + 16;
+constexpr size_t kSmem = SmemL::BAR + 16 * 8 + 24 * 4 + 16;
 static_assert(kSmem <= 227 * 1024, "fwd_small smem");
 
 
@@ -733,7 +897,8 @@ long long*& small_debug_stamps() {
 
 bool fwd_small_supported(int64_t M, int64_t S, int64_t h, int64_t f, int64_t hd, int64_t L) {
   if (std::getenv("PRLAB_NO_FWD_SMALL")) return false;
-  return L <= kMaxLayers && M >= 1 && M <= 128 && S <= 128 && hd == 64 && L >= 1 && h % 256 == 0 && h <= 1024 && f % 512 == 0 &&
+  const int64_t max_m = std::getenv("PRLAB_NO_SMALL_PAIR") ? 128 : 256;  // 128 < M <= 256: CTA-pair kernel
+  return L <= kMaxLayers && M >= 1 && M <= max_m && S <= 128 && hd == 64 && L >= 1 && h % 256 == 0 && h <= 1024 && f % 512 == 0 &&
          h / 64 <= kMaxKB && (f / 512) <= 8 && (f / 512) * 64 <= kMaxKB * 64;
 }
 
@@ -746,7 +911,9 @@ void launch_fwd_small(const FwdSmallPlan& p, cudaStream_t st) {
   static std::mutex mu;
   static uint64_t done = 0;
   once_per_device(mu, done, [] {
-    PRLAB_CUDA(cudaFuncSetAttribute(fwd_small_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    PRLAB_CUDA(cudaFuncSetAttribute(fwd_small_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kSmem)));
+    PRLAB_CUDA(cudaFuncSetAttribute(fwd_small_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kSmem)));
   });
   // 28 KB of kernel parameters, copied at launch: one per host thread (models driven from
@@ -780,17 +947,25 @@ void launch_fwd_small(const FwdSmallPlan& p, cudaStream_t st) {
   a.gbar = p.gbar;
   a.dbg = small_debug_stamps();
   PRLAB_CUDA(cudaMemsetAsync(p.gbar, 0, sizeof(unsigned), st));
+  const bool pair = p.M > 128;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(num_sms());
+  cfg.gridDim = dim3(pair ? num_sms() & ~1 : num_sms());
   cfg.blockDim = dim3(kThreads);
   cfg.dynamicSmemBytes = kSmem;
   cfg.stream = st;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeCooperative;
   attr[0].val.cooperative = 1;
+  attr[1].id = cudaLaunchAttributeClusterDimension;
+  attr[1].val.clusterDim.x = 2;
+  attr[1].val.clusterDim.y = 1;
+  attr[1].val.clusterDim.z = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  PRLAB_CUDA(cudaLaunchKernelEx(&cfg, fwd_small_kernel, a));
+  cfg.numAttrs = pair ? 2 : 1;
+  if (pair)
+    PRLAB_CUDA(cudaLaunchKernelEx(&cfg, fwd_small_kernel<true>, a));
+  else
+    PRLAB_CUDA(cudaLaunchKernelEx(&cfg, fwd_small_kernel<false>, a));
 }
 
 }  // namespace prlab_gpu

@@ -19,7 +19,7 @@ PER = len(NAMES)  # stages per layer
 
 def main():
     cfg = pg.ModelConfig.preset(sys.argv[1] if len(sys.argv) > 1 else "gpt2_small")
-    B, S = 1, 128
+    B, S = int(os.environ.get("B", 1)), int(os.environ.get("S", 128))
     m = pg.DeviceModel(cfg, pg.build_model(cfg))
     ids = torch.from_numpy(pg.random_tokens(cfg.vocab, B, S, 3)).cuda()
     V = cfg.vocab
@@ -36,7 +36,7 @@ def main():
     torch.cuda.synchronize()
     pg._check(pg.lib().prlab_gpu_debug_small_stamps(None))
     raw = dbg.cpu().numpy().astype(np.float64)
-    d = raw[: nst * 148 * 2].reshape(nst, 148, 2)
+    d = raw[: nst * 148 * 2].reshape(nst, 148, 2)  # (the pair grid is 148 CTAs too)
     rl = raw[200000:200000 + 8 * cfg.num_layers].reshape(cfg.num_layers, 8)
     arrive_max = d[:, :, 0].max(1)
     release_min = np.where(d[:, :, 1] > 0, d[:, :, 1], np.inf).min(1)

@@ -1,6 +1,7 @@
 """The batch-1 persistent forward (fwd_small.cu: forward_hidden as one cooperative
-kernel with grid barriers, used for B*S <= 128) against the multi-kernel tensor-core
-path and the CPU oracle, decoder (causal) and encoder shapes, including ragged M."""
+kernel with grid barriers, used for B*S <= 128, and on CTA pairs for 128 < B*S <= 256)
+against the multi-kernel tensor-core path and the CPU oracle, decoder (causal) and encoder
+shapes, including ragged M."""
 import os
 
 import numpy as np
@@ -18,7 +19,9 @@ BERT_SMALLV = GPT2_SMALLV.replace(archetype=0, seed=1)
 
 
 @pytest.mark.parametrize("cfg", [GPT2_SMALLV, BERT_SMALLV], ids=["gpt2", "bert"])
-@pytest.mark.parametrize("B,S", [(1, 128), (1, 1), (1, 37), (2, 64), (4, 32), (3, 17)])
+@pytest.mark.parametrize("B,S", [(1, 128), (1, 1), (1, 37), (2, 64), (4, 32), (3, 17),
+                                 # 128 < B*S <= 256: the CTA-pair kernel (2-CTA clusters, M = 256 MMAs)
+                                 (2, 128), (4, 64), (8, 32), (3, 77), (2, 65)])
 def test_fwd_small_matches_multikernel_and_oracle(cfg, B, S, monkeypatch):
     o = oracle()
     p = model_params(cfg)
@@ -54,15 +57,16 @@ def test_fwd_small_bad_token_reported():
     m.close()
 
 
-def test_fwd_small_repeatable_under_back_to_back_launches():
+@pytest.mark.parametrize("B,S", [(1, 128), (2, 128)], ids=["single", "pair"])
+def test_fwd_small_repeatable_under_back_to_back_launches(B, S):
     """Race detector for the grid-barrier protocol (release/acquire + the TMA thread's
-    proxy fence): 200 back-to-back forwards of a 12-layer model on one stream must give
+    proxy fence) and, at B*S > 128, the CTA-pair protocol (remote arrivals, multicast
+    commits): 200 back-to-back forwards of a 12-layer model on one stream must give
     bit-identical logits -- a stale operand read in any of the ~85 stages would not."""
     import torch
     cfg = GPT2_SMALLV.replace(num_layers=12)
     o = oracle()
     m = pg.DeviceModel(pg.ModelConfig(**cfg.__dict__), model_params(cfg))
-    B, S = 1, 128
     ids = torch.as_tensor(o.random_tokens(cfg.vocab, B, S, 11).reshape(-1), dtype=torch.int32, device="cuda")
     width = (cfg.vocab + 7) // 8 * 8
     outs = torch.empty(200, B * S, width, dtype=torch.float16, device="cuda")
