@@ -4,8 +4,10 @@
   * tcgen05 GEMMs: one-CTA (TMA ring + TMEM double buffer), CTA pair (cta_group::2,
     multicast commits), cluster split-K (DSMEM reduction), every epilogue;
   * attention: exact two-pass (attn_tc) and streaming (attn_fa) kernels, causal and not;
-  * the batch-1 persistent kernel (grid barrier, per-stage TMA/MMA protocol) and the
-    multi-kernel forward (PDL chain) through the drop-in forward, hybrid and full_fp16."""
+  * the batch-1 persistent kernel (grid barrier, per-stage TMA/MMA protocol), its CTA-pair
+    variant (128 < B*S <= 256: cta_group::2 tasks, remote arrivals, multicast commits) and the
+    multi-kernel forward (PDL chain) through the drop-in forward, hybrid and full_fp16;
+  * the fp32 policy: 3xTF32 GEMMs (converter warps, split-K reduce) and the tiled attention."""
 import os
 import sys
 
@@ -39,9 +41,9 @@ for (B, S, causal) in [(1, 128, 1), (2, 96, 0), (1, 256, 1), (1, 384, 0)]:
     print("attention", B, S, causal, "ok", flush=True)
 cfg = pg.ModelConfig.preset("gpt2_small").replace(num_layers=2, vocab=4096)
 m = pg.DeviceModel(cfg, pg.build_model(cfg))
-for (B, S) in [(1, 64), (2, 160)]:
+for (B, S) in [(1, 64), (2, 96), (2, 160)]:
     ids = pg.random_tokens(cfg.vocab, B, S, 3)
-    for pol in ("hybrid", "full_fp16"):
+    for pol in ("hybrid", "full_fp16", "fp32"):
         out = m.forward(ids, B, S, pol)
         assert np.isfinite(out).all()
     print("forward", B, S, "ok", flush=True)
