@@ -180,3 +180,30 @@ def test_hybrid_drift_by_depth(layers):
     report(test="hybrid_drift_by_depth", layers=layers, **r)
     m.close()
     assert r["candidate_nonfinite"] == 0 and r["cosine"] >= 0.9999 and r["max_abs_error"] <= 5e-3, r
+
+
+@pytest.mark.parametrize("name", ["bert_base", "gpt2_small"])
+def test_c1_fp32_forward_within_1e3(name):
+    """C1 (BERT-base fp32, batch 1, seq 128 -- the reference's CPU-runnable config) and the
+    same shape on GPT-2: the fp32 policy (3xTF32 tensor-core linears, tiled fp32 attention)
+    against the CPU fp32 forward, max|gpu - cpu| / max|cpu| <= 1e-3 (north star), argmax
+    identical off near-ties (top-2 gap < 1e-5)."""
+    cfg = PRESETS[name]
+    o = oracle()
+    p = model_params(cfg)
+    m = device_model(cfg)
+    ids = o.random_tokens(cfg.vocab, 1, 128, 2024)
+    got = m.forward(ids, 1, 128, "fp32").astype(np.float64)
+    want = o.forward(cfg, p, ids, 1, 128, "fp32").astype(np.float64)
+    rel = float(np.abs(got - want).max() / np.abs(want).max())
+    w = want.reshape(-1, want.shape[-1])
+    g = got.reshape(-1, got.shape[-1])
+    top2 = np.sort(w, axis=1)[:, -2:]
+    clear = (top2[:, 1] - top2[:, 0]) >= 1e-5
+    agree = (w.argmax(1) == g.argmax(1))
+    report(test="c1_fp32", model=name, rel_err_vs_max=rel, max_abs=float(np.abs(got - want).max()),
+           argmax_rows=int(len(agree)), argmax_agree=int(agree.sum()), clear_rows=int(clear.sum()),
+           clear_agree=int((agree & clear).sum()))
+    assert np.isfinite(got).all()
+    assert rel <= 1e-3, rel
+    assert (agree | ~clear).all()
