@@ -47,7 +47,7 @@ struct FaSmem {
   // float [3][2][128]: partial row max per half (double-buffered by block parity: a fast
   // warp may write the next block's before a slow one read this one's), partial row sums
   static constexpr uint32_t RED = V + 2 * kTile;
-  static constexpr uint32_t BAR = RED + 3 * 256 * 4;
+  static constexpr uint32_t BAR = RED + 6 * 256 * 4;  // row kernel TPR 4: rmax 2 x 4 x 128, rsum 4 x 128
   static constexpr uint32_t TOTAL = BAR + 256;
 };
 constexpr size_t kFaSmemBytes = 1024 + FaSmem::TOTAL;
@@ -424,9 +424,10 @@ __global__ void __launch_bounds__(kThreads, 2) attn_fa_kernel(const __grid_const
 // Measured per-block chain of attn_fa_kernel (scripts/fa_phases.py, C4): max pass 512 cycles,
 // exp pass 2 966, wake-up 360, next-S wait ~1 340 = 4.8 K cycles against a MUFU floor of ~1 K.
 // ---------------------------------------------------------------------------------------
-// TPR threads per query row: 1 (4 softmax warps, 168 registers) or 2 (8 softmax warps, each half
+// TPR threads per query row: 1 (4 softmax warps, 162 registers) or 2 (8 softmax warps, each half
 // of the row's keys; the halves' block maxima meet in shared memory behind a 64-thread pairwise
-// named barrier -- more warps to hide the TMEM / MUFU latencies at 2 CTAs per SM)
+// named barrier -- more warps to hide the TMEM / MUFU latencies at 2 CTAs per SM).  The code is
+// written for TPR = 4 too; measured slower (59 vs 48 us at C4: 56 registers, a 4-warp barrier).
 template <int TPR>
 constexpr int row_threads() { return 128 * TPR + 64; }  // + TMA warp + MMA warp
 enum : int {
@@ -552,7 +553,8 @@ __global__ void __launch_bounds__(row_threads<TPR>(), 2) attn_fa_row_kernel(cons
     __syncwarp();
   } else {
     // ---------------- softmax + epilogue: thread = query row (TMEM lane)
-    const uint32_t quad = warp & 3, half = warp >> 2;  // half: which NC chunks of a block (TPR = 2)
+    const uint32_t quad = warp & 3, half = warp >> 2;  // half: which NC chunks of a block (TPR > 1)
+    constexpr int OC = 64 / TPR;  // this thread's O columns
     const int r = static_cast<int>(quad * 32 + lane);
     float* red = reinterpret_cast<float*>(smem + FaSmem::RED);
     const uint32_t lane_addr = tmem + ((quad * 32) << 16);
@@ -588,7 +590,12 @@ __global__ void __launch_bounds__(row_threads<TPR>(), 2) attn_fa_row_kernel(cons
             continue;
           }
           uint32_t w[32];
-          tmem_ld32(lane_addr + kColS + 32 * c, w);
+          if constexpr (TPR == 4) {  // register budget (56 at 2 x 576 threads): two 16-column loads
+            tmem_ld16(lane_addr + kColS + 32 * c, *reinterpret_cast<uint32_t(*)[16]>(w));
+            tmem_ld16(lane_addr + kColS + 32 * c + 16, *reinterpret_cast<uint32_t(*)[16]>(w + 16));
+          } else {
+            tmem_ld32(lane_addr + kColS + 32 * c, w);
+          }
           tmem_wait_ld();
           if (ts && cc == 0) ts[6] = clock64();
           if (k0c + 32 <= a.S && (!a.causal || k0c + 31 <= row_lo)) {  // warp-uniform: no masking
@@ -621,11 +628,12 @@ __global__ void __launch_bounds__(row_threads<TPR>(), 2) attn_fa_row_kernel(cons
           float h0, h1;
           h2_unpack(hmax, h0, h1);
           float mraw = fmaxf(h0, h1);  // = round16(max acc): round16 is monotone
-          if constexpr (TPR == 2) {  // the other half of the row: shared memory + pairwise barrier
-            float* rmax = red + (bc & 1) * 256;  // by block parity: a fast pair may write the next block's first
+          if constexpr (TPR > 1) {  // the row's other parts: shared memory + a barrier of the row's warps
+            float* rmax = red + (bc & 1) * 512;  // by block parity: a fast group may write the next block's first
             rmax[half * 128 + r] = mraw;
-            named_bar_sync(1 + quad, 64);
-            mraw = fmaxf(rmax[r], rmax[128 + r]);
+            named_bar_sync(1 + quad, 32 * TPR);
+#pragma unroll
+            for (int q = 0; q < TPR; ++q) mraw = fmaxf(mraw, rmax[q * 128 + r]);
           }
           const float mblk = mraw == NEG_INF ? NEG_INF : __fmul_rn(mraw, 0.125f);
           mnew = fmaxf(m, mblk);
@@ -667,19 +675,19 @@ __global__ void __launch_bounds__(row_threads<TPR>(), 2) attn_fa_row_kernel(cons
           l = __fmul_rn(l, sc);
           const uint64_t sc2 = f2_pack(sc, sc);
 #pragma unroll
-          for (int hh = 0; hh < 2 / TPR; ++hh) {  // this thread's O columns
-            const uint32_t oc = kColO + 32 * (static_cast<uint32_t>(half) + hh);
-            uint32_t o[32];
-            tmem_ld32(lane_addr + oc, o);
+          for (int hh = 0; hh < OC / 16; ++hh) {  // this thread's O columns, 16 at a time
+            const uint32_t oc = kColO + OC * static_cast<uint32_t>(half) + 16 * hh;
+            uint32_t o[16];
+            tmem_ld16(lane_addr + oc, o);
             tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 32; i += 2) {
+            for (int i = 0; i < 16; i += 2) {
               float x0, x1;
               f2_unpack(f2_mul(f2_pack(__uint_as_float(o[i]), __uint_as_float(o[i + 1])), sc2), x0, x1);
               o[i] = __float_as_uint(x0);
               o[i + 1] = __float_as_uint(x1);
             }
-            tmem_st32(lane_addr + oc, o);
+            tmem_st16(lane_addr + oc, o);
           }
         }
 #pragma unroll
@@ -696,18 +704,21 @@ __global__ void __launch_bounds__(row_threads<TPR>(), 2) attn_fa_row_kernel(cons
         if (ts) ts[3] = clock64();
       }
       // epilogue: o = round16(O / l) -> ctx row (this thread's 64 / TPR halves)
-      if constexpr (TPR == 2) red[512 + half * 128 + r] = l;
+      if constexpr (TPR > 1) red[1024 + half * 128 + r] = l;
       mbar_wait(&bars[R_OFULL], qc & 1);
       tc_fence_after();
-      uint32_t o[64 / TPR];
+      uint32_t o[OC];
 #pragma unroll
-      for (int hh = 0; hh < 2 / TPR; ++hh)
-        tmem_ld32(lane_addr + kColO + 32 * (static_cast<uint32_t>(half) + hh), *reinterpret_cast<uint32_t(*)[32]>(o + 32 * hh));
+      for (int hh = 0; hh < OC / 16; ++hh)
+        tmem_ld16(lane_addr + kColO + OC * static_cast<uint32_t>(half) + 16 * hh, *reinterpret_cast<uint32_t(*)[16]>(o + 16 * hh));
       tmem_wait_ld();
       tc_fence_before();
-      if constexpr (TPR == 2) {  // both partial sums visible; the next rsum write is a unit (and a pair barrier) later
-        named_bar_sync(1 + quad, 64);
-        l = __fadd_rn(red[512 + r], red[512 + 128 + r]);
+      if constexpr (TPR > 1) {  // every part's sum visible; the next rsum write is a unit (and a row barrier) later
+        named_bar_sync(1 + quad, 32 * TPR);
+        float lt2 = red[1024 + r];
+#pragma unroll
+        for (int q = 1; q < TPR; ++q) lt2 = __fadd_rn(lt2, red[1024 + q * 128 + r]);
+        l = lt2;
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[R_TFREE]);
@@ -717,9 +728,9 @@ __global__ void __launch_bounds__(row_threads<TPR>(), 2) attn_fa_row_kernel(cons
         const float inv = __frcp_rn(lt);
         const uint64_t inv2 = f2_pack(inv, inv);
         uint4* dst = reinterpret_cast<uint4*>(a.ctx + (static_cast<int64_t>(b) * a.S + qrow) * a.ld_ctx + head * 64 +
-                                              half * 32);
+                                              half * OC);
 #pragma unroll
-        for (int q = 0; q < 8 / TPR; ++q) {
+        for (int q = 0; q < OC / 8; ++q) {
           uint32_t pk[4];
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
