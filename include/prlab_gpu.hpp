@@ -102,6 +102,9 @@ DeviceModel& device_model_for(const Model& m, int device = 0) {
 // prlab::forward (model.cpp:456-482): same signature, same ForwardTrace fields
 // (logits [B,S,V] fp32 storage; kernel_calls per class/dtype; seconds per class from
 // CUDA events like the reference's timed() wrappers; layer_scores when retained).
+// Filling `seconds` per op class times every kernel separately, so this path does not run the
+// fused batch-1 trunk: latency / throughput callers (bench.cpp's benchmark_forward) should use
+// forward_untimed below, which runs the captured fast path (and overlaps concurrent callers).
 template <class Model, class TokenBatch, class PrecisionPolicy>
 auto forward(const Model& model, const TokenBatch& tokens, const PrecisionPolicy& policy,
              bool retain_scores = false) {
@@ -130,6 +133,24 @@ auto forward(const Model& model, const TokenBatch& tokens, const PrecisionPolicy
       trace.layer_scores.push_back(std::move(t));
     }
   }
+  return trace;
+}
+
+// forward() without the per-class timing: the same logits (ForwardTrace::kernel_calls filled,
+// seconds left zero), through the fused / graph-captured fast path -- what a latency or
+// throughput caller wants.  Safe from several threads on one model (prlab_gpu_forward).
+template <class Model, class TokenBatch, class PrecisionPolicy>
+auto forward_untimed(const Model& model, const TokenBatch& tokens, const PrecisionPolicy& policy) {
+  DeviceModel& dm = device_model_for(model);
+  const prlab_policy pol = to_c_policy(policy);
+  decltype(prlab::forward(model, tokens, policy)) trace;
+  const int64_t w = dm.layers() > 0 ? dm.vocab() : dm.hidden();
+  trace.logits.shape = {tokens.batch, tokens.seq, w};
+  trace.logits.data.resize(static_cast<size_t>(tokens.batch * tokens.seq * w));
+  prlab_trace tr{};
+  check(prlab_gpu_forward(dm.get(), tokens.ids.data(), tokens.batch, tokens.seq, &pol, trace.logits.data.data(), &tr));
+  for (int c = 0; c < PRLAB_NUM_OP_CLASSES; ++c)
+    for (int d = 0; d < 2; ++d) trace.kernel_calls[static_cast<size_t>(c)][static_cast<size_t>(d)] = tr.kernel_calls[c][d];
   return trace;
 }
 

@@ -8,9 +8,12 @@
 // Built by oracle/Makefile into oracle/_ref/dropin_test; run on the GPU box by
 // tests/test_gpu_dropin.py.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <stdexcept>
+#include <thread>
+#include <vector>
 
 #include "prlab/fidelity.hpp"
 #include "prlab/kernels.hpp"
@@ -101,6 +104,37 @@ int main() {
       dec = true;
     }
     CHECK(dec, "classifier_probs on a decoder -> std::invalid_argument");
+  }
+
+  // --- concurrent callers (the reference's free functions are safe on distinct data,
+  //     SPEC.md:118-119): four threads x 8 forwards on one model through forward_untimed
+  //     (the fused path with the overlapped copy-out); every call equals its serial result
+  {
+    std::vector<TokenBatch> tb;
+    std::vector<std::vector<float>> want;
+    for (int t = 0; t < 4; ++t) {
+      tb.push_back(random_tokens(model.config.vocab, 1, 128, 500 + t));
+      want.push_back(gpu::forward_untimed(model, tb.back(), resolve_policy("hybrid")).logits.data);
+    }
+    std::atomic<int> mismatches{0}, errors{0};
+    std::vector<std::thread> th;
+    for (int t = 0; t < 4; ++t)
+      th.emplace_back([&, t] {
+        try {
+          for (int r = 0; r < 8; ++r)
+            if (gpu::forward_untimed(model, tb[t], resolve_policy("hybrid")).logits.data != want[t]) ++mismatches;
+        } catch (const std::exception&) {
+          ++errors;
+        }
+      });
+    for (auto& x : th) x.join();
+    const auto timed = gpu::forward(model, tb[0], resolve_policy("hybrid"));
+    double md = 0.0;
+    for (size_t i = 0; i < want[0].size(); ++i) md = std::max(md, std::fabs(static_cast<double>(timed.logits.data[i]) - want[0][i]));
+    std::printf("       concurrent: %d mismatches, %d errors; timed vs untimed max |diff| %.3e\n", mismatches.load(),
+                errors.load(), md);
+    CHECK(mismatches == 0 && errors == 0, "4 concurrent callers x 8 forwards return their serial logits");
+    CHECK(md <= 2e-2, "forward (instrumented) and forward_untimed (fused) agree");
   }
 
   // --- exceptions: same types as the reference
