@@ -300,3 +300,4 @@ def test_linear_f32_tensor_core_vs_fp64(M, N, K, epi):
     # noise floor err32 ~ 4e-7; rounding the residues to nearest tf32 does not change it) --
     # 400x inside the fp32 policy's 1e-3 contract; a plain 1xTF32 GEMM sits near 1e-3
     assert err <= max(8 * err32, 5e-6), (err, err32)
+
