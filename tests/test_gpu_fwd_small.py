@@ -16,6 +16,8 @@ pytestmark = pytest.mark.gpu
 GPT2_SMALLV = ModelConfig(archetype=1, num_layers=2, hidden=768, heads=12, ffn=3072, vocab=4096,
                           max_positions=512, seed=0)
 BERT_SMALLV = GPT2_SMALLV.replace(archetype=0, seed=1)
+# GPT-2-medium-shaped (h 1024, 16 heads, ffn 4096): the largest hidden size the trunk takes
+GPT2_MEDIUMV = GPT2_SMALLV.replace(hidden=1024, heads=16, ffn=4096, seed=2)
 
 
 @pytest.mark.parametrize("cfg", [GPT2_SMALLV, BERT_SMALLV], ids=["gpt2", "bert"])
@@ -23,6 +25,17 @@ BERT_SMALLV = GPT2_SMALLV.replace(archetype=0, seed=1)
                                  # 128 < B*S <= 256: the CTA-pair kernel (2-CTA clusters, M = 256 MMAs)
                                  (2, 128), (4, 64), (8, 32), (3, 77), (2, 65)])
 def test_fwd_small_matches_multikernel_and_oracle(cfg, B, S, monkeypatch):
+    _check_small(cfg, B, S, monkeypatch)
+
+
+@pytest.mark.parametrize("B,S", [(1, 128), (2, 100)], ids=["single", "pair"])
+def test_fwd_small_h1024(B, S, monkeypatch):
+    """h = 1024 (16 heads, ffn 4096): 16 k-block weight slabs, 16-query attention tasks and
+    one-row stages in the pair kernel (the 32-query / two-row variants are h = 768 only)."""
+    _check_small(GPT2_MEDIUMV, B, S, monkeypatch)
+
+
+def _check_small(cfg, B, S, monkeypatch):
     o = oracle()
     p = model_params(cfg)
     ids = o.random_tokens(cfg.vocab, B, S, 5 + B + S)
