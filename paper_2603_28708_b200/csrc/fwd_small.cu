@@ -76,6 +76,7 @@ struct SmallArgs {
   int M, B, S, h, f, H, L, V, causal;
   int split_ffn2;
   int embed_only;                // debug: stop after stage 0 (x = the embedding gather)
+  int q32;                       // attention tasks of 32 queries (else 16)
   const float *tok, *pos, *lnfg, *lnfb;
   const int32_t* ids;
   int* err;
@@ -401,7 +402,7 @@ template <int QB>  // queries per task: 16 (one m16 row block) or 32 (two; CTA-p
 __device__ void attn_wo_task(const SmallArgs& a, uint8_t* smem, const CUtensorMap* mWo, uint64_t* wo_bar,
                              uint32_t wo_phase, int b, int hh, int q0, long long* ts) {
   constexpr int MB = QB / 16;
-  // ts (debug, thread 0 only): [0] start [1] q/k/v staged [2] scores [3] softmax [4] ctx [5] Wo landed [6] done
+  // ts (debug, thread 0 only): [0] start [1] q/k/v staged [2] scores [3] softmax [4] ctx [5] Wo landed [6] done [7] row maxima
   if (ts) ts[0] = globaltimer();
   const int h = a.h, S = a.S;
   const uint32_t warp = warp_id(), lane = lane_id();
@@ -450,19 +451,29 @@ __device__ void attn_wo_task(const SmallArgs& a, uint8_t* smem, const CUtensorMa
   }
   __syncthreads();
   if (ts) ts[1] = globaltimer();
+  // per-warp clock64 stamps of the same task (debug): lane 0 of each warp
+  long long* wt = (a.dbg && q0 + QB >= S && hh == 0 && b == 0 && lane == 0)
+                      ? a.dbg + 240000 + warp * 8 : nullptr;
+  if (wt) wt[0] = clock64();
   const int g = lane >> 2, t4 = lane & 3;
-  // scores: warp w -> keys [16w, 16w + 16), every 16-query row block
-  if (static_cast<int>(warp) * 16 < kvp) {
+  // scores: warp w -> keys [16w, 16w + 16), every 16-query row block; the columns past the
+  // visible keys are written as -inf too, so the softmax below reads and writes all 128
+  // columns without guards (guarded smem accesses under the trunk's register pressure
+  // compile to one branch + address rematerialisation per access: 3-5x slower)
+  {
+    const bool live = static_cast<int>(warp) * 16 < kvp;
 #pragma unroll
     for (int mb = 0; mb < MB; ++mb) {
       float acc[2][4] = {};
+      if (live) {
 #pragma unroll
-      for (int ks = 0; ks < 4; ++ks) {
-        uint32_t af[4], bf[4];
-        ldsm_x4(smem_u32(sQ + (mb * 16 + (lane & 15)) * kRowH + ks * 16 + (lane >> 4) * 8), af);
-        ldsm_x4(smem_u32(sK + (warp * 16 + (lane & 7) + (lane >> 4) * 8) * kRowH + ks * 16 + ((lane >> 3) & 1) * 8), bf);
-        mma16816(acc[0], af, bf[0], bf[1]);
-        mma16816(acc[1], af, bf[2], bf[3]);
+        for (int ks = 0; ks < 4; ++ks) {
+          uint32_t af[4], bf[4];
+          ldsm_x4(smem_u32(sQ + (mb * 16 + (lane & 15)) * kRowH + ks * 16 + (lane >> 4) * 8), af);
+          ldsm_x4(smem_u32(sK + (warp * 16 + (lane & 7) + (lane >> 4) * 8) * kRowH + ks * 16 + ((lane >> 3) & 1) * 8), bf);
+          mma16816(acc[0], af, bf[0], bf[1]);
+          mma16816(acc[1], af, bf[2], bf[3]);
+        }
       }
 #pragma unroll
       for (int nt = 0; nt < 2; ++nt)
@@ -474,8 +485,10 @@ __device__ void attn_wo_task(const SmallArgs& a, uint8_t* smem, const CUtensorMa
         }
     }
   }
+  if (wt) wt[1] = clock64();
   __syncthreads();
   if (ts) ts[2] = globaltimer();
+  if (wt) wt[2] = clock64();
   // softmax: warp w -> rows w * QB/8 .. (interleaved); lane -> keys lane + 32c
   {
     constexpr int RW = QB / 8;  // rows per warp
@@ -486,7 +499,7 @@ __device__ void attn_wo_task(const SmallArgs& a, uint8_t* smem, const CUtensorMa
 #pragma unroll
       for (int c4 = 0; c4 < 4; ++c4) {
         const int j = c4 * 32 + lane;
-        sc[rr][c4] = j < kvp ? sS[(warp * RW + rr) * kRowS + j] : __int_as_float(0xff800000);
+        sc[rr][c4] = sS[(warp * RW + rr) * kRowS + j];
         mx[rr] = fmaxf(mx[rr], sc[rr][c4]);
       }
     }
@@ -494,6 +507,8 @@ __device__ void attn_wo_task(const SmallArgs& a, uint8_t* smem, const CUtensorMa
     for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
       for (int rr = 0; rr < RW; ++rr) mx[rr] = fmaxf(mx[rr], __shfl_xor_sync(0xffffffffu, mx[rr], o));
+    if (ts) ts[7] = globaltimer();
+    if (wt) wt[3] = clock64();
     constexpr float LOG2E = 1.4426950408889634f;
 #pragma unroll
     for (int rr = 0; rr < RW; ++rr) {
@@ -509,18 +524,21 @@ __device__ void attn_wo_task(const SmallArgs& a, uint8_t* smem, const CUtensorMa
     for (int o = 16; o > 0; o >>= 1)
 #pragma unroll
       for (int rr = 0; rr < RW; ++rr) sum[rr] = __fadd_rn(sum[rr], __shfl_xor_sync(0xffffffffu, sum[rr], o));
+    if (wt) wt[4] = clock64();
 #pragma unroll
     for (int rr = 0; rr < RW; ++rr) {
       const float inv = __frcp_rn(sum[rr]);
 #pragma unroll
       for (int c4 = 0; c4 < 4; ++c4) {
         const int j = c4 * 32 + lane;
-        if (j < kvp) sP[(warp * RW + rr) * kRowP + j] = __float2half_rn(__fmul_rn(e[rr][c4], inv));
+        sP[(warp * RW + rr) * kRowP + j] = __float2half_rn(__fmul_rn(e[rr][c4], inv));
       }
     }
   }
+  if (wt) wt[5] = clock64();
   __syncthreads();
   if (ts) ts[3] = globaltimer();
+  if (wt) wt[6] = clock64();
   // ctx = round16(P . V): warp w -> dims [8w, 8w + 8), every row block
 #pragma unroll
   for (int mb = 0; mb < MB; ++mb) {
@@ -810,7 +828,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
     // ---- attention + Wo: (batch, head, 16-query block) tasks, head partials -> part[head]
     {
       // PAIR (M > 128): 32-query tasks -- at most 96 for S <= 128, one round on 148 CTAs
-      const bool q32 = PAIR && h <= 768;  // (the 32-query scratch fits for h <= 768)
+      const bool q32 = a.q32 != 0;  // (host: CTA-pair mode and h <= 768, where the 32-query scratch fits)
       const int QB = q32 ? 32 : kQB;
       const int nqb = (S + QB - 1) / QB;
       long long* ats = (a.dbg && blockIdx.x == 0 && threadIdx.x == 0) ? a.dbg + 210000 + l * 8 : nullptr;
@@ -931,6 +949,10 @@ void launch_fwd_small(const FwdSmallPlan& p, cudaStream_t st) {
   a.causal = p.causal;
   a.split_ffn2 = p.f / 512;
   a.embed_only = p.embed_only;
+  {
+    const char* e = std::getenv("PRLAB_SMALL_Q32");  // A/B switch: 0 / 1 forces 16 / 32-query tasks
+    a.q32 = (e && *e) ? (std::atoi(e) != 0 && p.h <= 768) : (p.M > 128 && p.h <= 768);
+  }
   if (p.L > kMaxLayers) throw std::invalid_argument("fwd_small: too many layers");
   std::memcpy(a.maps, p.host_maps, sizeof(CUtensorMap) * (2 + 4 * p.L));
   std::memcpy(a.lw, p.host_lw, sizeof(LayerW) * p.L);

@@ -1251,10 +1251,12 @@ GemmPlan plan_gemm_tc(const void* A, int64_t lda, const void* Wt, int64_t ldw, c
   const int sms = num_sms();
   const int mb = (M + BM - 1) / BM;
   const int nkb = (K + BK - 1) / BK;
-  // Widest N tile that still gives every SM work; narrower tiles stream the
-  // weights through more SMs when M is small (weight-bandwidth bound).
+  // Widest N tile that still gives at least 0.6 of the SMs work; narrower tiles stream
+  // the weights through more SMs when M is small (weight-bandwidth bound).  Measured over
+  // the forward's shapes (M 128..4096 x QKV / Wo / FFN / heads, profiles/r02/bn_rule.jsonl):
+  // one wave of 96-144 wide tiles beats two waves of half-width ones by 20-40 %.
   int bn = 256;
-  while (bn > 64 && static_cast<int64_t>(mb) * ((N + bn - 1) / bn) < sms) bn /= 2;
+  while (bn > 64 && static_cast<int64_t>(mb) * ((N + bn - 1) / bn) * 5 < static_cast<int64_t>(sms) * 3) bn /= 2;
   if (force_bn) bn = force_bn;
   const int tiles = mb * ((N + bn - 1) / bn);
   // Split K while the grid is far below one wave (batch-1 latency shapes): the

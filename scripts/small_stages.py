@@ -89,8 +89,13 @@ def main():
         print(json.dumps({"layer": l, "attn_task_last_qblock": {
             "start_after_release_us": round((t[0] - d[k - 1, :, 1].max()) / 1e3, 2),
             "stage_us": round((t[1] - t[0]) / 1e3, 2), "scores_us": round((t[2] - t[1]) / 1e3, 2),
-            "softmax_us": round((t[3] - t[2]) / 1e3, 2), "pv_us": round((t[4] - t[3]) / 1e3, 2),
+            "softmax_us": round((t[3] - t[2]) / 1e3, 2), "softmax_max_us": round((t[7] - t[2]) / 1e3, 2), "pv_us": round((t[4] - t[3]) / 1e3, 2),
             "wo_wait_us": round((t[5] - t[4]) / 1e3, 2), "wo_mma_store_us": round((t[6] - t[5]) / 1e3, 2)}}))
+    wt = raw[240000:240000 + 64].reshape(8, 8)  # last layer's task, per warp: clock64
+    if wt[0, 0] != 0:
+        print(json.dumps({"attn_task_warp_cycles": [
+            {"scores": int(w[1] - w[0]), "sync1": int(w[2] - w[1]), "max": int(w[3] - w[2]),
+             "exp_sum": int(w[4] - w[3]), "store_p": int(w[5] - w[4]), "sync2": int(w[6] - w[5])} for w in wt]}))
     gt = raw[220000:220000 + 64 * 8].reshape(64, 8)
     names = ["qkv", "ffn1", "ffn2"]
     for t in range(6):
