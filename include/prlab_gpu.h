@@ -197,7 +197,10 @@ int prlab_gpu_classifier_probs(prlab_gpu_model* m, const int32_t* ids, int64_t b
                                const prlab_policy* policy, float* probs);
 
 /* Device-resident form: d_ids [B*S] int32 on the device, logits written to
- * d_out with row pitch `ld` elements (ld >= V) in out_dtype.  Asynchronous on
+ * d_out with row pitch `ld` elements (ld >= V) in out_dtype (columns V .. ld-1 are
+ * scratch: the head's TMA store may fill them up to the next 16-byte boundary; fp32
+ * logits with ld % 4 == 0 come straight from the head's epilogue, other pitches through
+ * per-thread stores).  Asynchronous on
  * `stream` (cudaStream_t; NULL = legacy default).  With use_graph != 0 the
  * forward is captured once per (B,S,policy,out) key and replayed as a CUDA
  * graph.  Ids are validated on the device; an out-of-range id is reported by
@@ -265,8 +268,10 @@ int prlab_gpu_embed(const float* tok, int64_t vocab, const float* pos, int64_t n
  * Hybrid Linear on tensor cores (tcgen05): out = epi(round16(A.W^T)), A fp16
  * [M,K] row-major, Wt fp16 [N,K] row-major (K-major), bias fp32 [N] or NULL.
  * epi: 0 = bias -> fp16 out; 1 = bias+GELU -> fp16 out; 2 = bias then fp32
- * residual add in place into out (fp32 [M,N]); 3 = no bias -> fp16 out.
- * ldo = row pitch of out in elements. */
+ * residual add in place into out (fp32 [M,N]); 3 = no bias -> fp16 out; 5 = no bias ->
+ * fp32 out holding the binary16 value round16(acc) (the tied head with fp32 logits).
+ * ldo = row pitch of out in elements; when ldo > N the TMA-store epilogue may write the
+ * row padding up to the next 16-byte boundary (never past ldo). */
 int prlab_gpu_linear_f16_device(const void* A, const void* Wt, const float* bias, void* out,
                                 int64_t M, int64_t N, int64_t K, int64_t ldo, int32_t epi,
                                 void* stream);

@@ -83,12 +83,16 @@ struct Cfg {
   static constexpr size_t SMEM = 1024 + BIAS_OFF + BIAS_BYTES;
 };
 
+// epilogues with a bias operand / an fp32 output tile
+__host__ __device__ constexpr bool epi_bias(int epi) { return epi != EPI_F16 && epi != EPI_F16_F32; }
+__host__ __device__ constexpr bool epi_f32out(int epi) { return epi == EPI_BIAS_RESID_F32 || epi == EPI_F16_F32; }
+
 // Pairs go through the packed pipes: cvt.rn.f16x2 (= round16 of both lanes), then the
 // bias add as a binary16 RNE add (= round16(round16(acc) + b) since b is on the lattice).
 template <int EPI>
 __device__ __forceinline__ uint32_t epilogue_pair(float a0, float a1, float b0, float b1) {
   uint32_t h = h2_pack_rn(a0, a1);
-  if (EPI != EPI_F16) {
+  if (epi_bias(EPI)) {
     h = h2_add_rn(h, h2_pack_rn(b0, b1));  // exact repack: biases are pre-rounded (0 when absent)
     if (EPI == EPI_BIAS_GELU_F16) {
       float x0, x1;
@@ -102,7 +106,7 @@ __device__ __forceinline__ uint32_t epilogue_pair(float a0, float a1, float b0, 
 template <int EPI>
 __device__ __forceinline__ uint32_t epilogue_pair(float a0, float a1, const float* sbias, int i) {
   float b0 = 0.0f, b1 = 0.0f;
-  if (EPI != EPI_F16 && sbias != nullptr) {
+  if (epi_bias(EPI) && sbias != nullptr) {
     const float2 b = *reinterpret_cast<const float2*>(sbias + i);
     b0 = b.x;
     b1 = b.y;
@@ -135,6 +139,15 @@ __device__ __forceinline__ void epilogue_chunk(const float (&acc)[32], const Gem
     } else {
       for (int i = 0; i < 32; ++i)
         if (col0 + i < g.N) o[i] = __fadd_rn(o[i], v[i]);
+    }
+  } else if (EPI == EPI_F16_F32) {
+    float* o = reinterpret_cast<float*>(g.out) + static_cast<int64_t>(row) * g.ldo + col0;
+    if (full && (g.ldo % 4) == 0) {
+#pragma unroll
+      for (int i = 0; i < 32; i += 4) *reinterpret_cast<float4*>(o + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+    } else {
+      for (int i = 0; i < 32; ++i)
+        if (col0 + i < g.N) o[i] = v[i];
     }
   } else {
     __half* o = reinterpret_cast<__half*>(g.out) + static_cast<int64_t>(row) * g.ldo + col0;
@@ -320,7 +333,7 @@ __global__ void __launch_bounds__(Cfg<BN, LEAN, EPI>::THREADS, 1)
       tile_coords(g, tile, m_blk, n_blk);
       const uint32_t acc = t & 1, acc_phase = (t >> 1) & 1;
       // stage this warp's bias slice while the accumulator is still being produced
-      const bool has_bias = EPI != EPI_F16 && g.bias != nullptr;
+      const bool has_bias = epi_bias(EPI) && g.bias != nullptr;
       if (has_bias) {
         __syncwarp();
         for (int c = lane; c < C::COLS_PER_WARP; c += 32) {
@@ -332,10 +345,12 @@ __global__ void __launch_bounds__(Cfg<BN, LEAN, EPI>::THREADS, 1)
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const int row = m_blk * BM + r;
-      if (g.splits == 1 && g.tma_store) {
+      // (fp32 logits with unaligned rows: staged like the TMA store, written by the warp
+      // one row at a time -- 128-byte coalesced rows instead of one row per lane)
+      if (g.splits == 1 && (g.tma_store || EPI == EPI_F16_F32)) {
         // fp16 out: 64-column store chunks (2 TMEM loads); fp32 residual: 32-column
         // chunks added into x by the TMA engine (cp.reduce.async.bulk .add.f32)
-        constexpr bool F32OUT = EPI == EPI_BIAS_RESID_F32;
+        constexpr bool F32OUT = epi_f32out(EPI);
         constexpr int SC = F32OUT ? 32 : 64;
         uint8_t* ebuf = smem + C::EPI_OFF + (warp - 2) * 2 * 4096;
 #pragma unroll 1
@@ -367,10 +382,23 @@ __global__ void __launch_bounds__(Cfg<BN, LEAN, EPI>::THREADS, 1)
                     make_uint4(pk[4 * j], pk[4 * j + 1], pk[4 * j + 2], pk[4 * j + 3]);
             }
           }
+          if (EPI == EPI_F16_F32 && !g.tma_store) {
+            __syncwarp();
+            const int col = n_blk * BN + c + static_cast<int>(lane);
+            const int row0 = m_blk * BM + static_cast<int>(quad) * 32;
+            float* o = reinterpret_cast<float*>(g.out) + static_cast<int64_t>(row0) * g.ldo + col;
+#pragma unroll 4
+            for (int rr = 0; rr < 32; ++rr)
+              if (row0 + rr < g.M && col < g.N)
+                o[static_cast<int64_t>(rr) * g.ldo] =
+                    *reinterpret_cast<const float*>(buf + rr * 128 + ((((lane >> 2) ^ (rr & 7))) << 4) + (lane & 3) * 4);
+            __syncwarp();  // the staging buffer is rewritten by the next chunk
+            continue;
+          }
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            if (F32OUT)
+            if (EPI == EPI_BIAS_RESID_F32)
               tma_reduce_add_2d(&tmC, buf, n_blk * BN + c, m_blk * BM + quad * 32);
             else
               tma_store_2d(&tmC, buf, n_blk * BN + c, m_blk * BM + quad * 32);
@@ -989,7 +1017,7 @@ __global__ void __launch_bounds__(Cfg2<BN, EPI>::THREADS, 1)
     float* sbias = reinterpret_cast<float*>(smem + C::BIAS_OFF) + (warp - 2) * C::COLS_PER_WARP;
     const uint32_t tempty_leader = to_leader(smem_u32(&tempty[0]));
     uint8_t* ebuf = smem + C::EPI_OFF + (warp - 2) * C::NBUF * 4096;
-    constexpr bool F32OUT = EPI == EPI_BIAS_RESID_F32;
+    constexpr bool F32OUT = epi_f32out(EPI);
     constexpr int SC = F32OUT ? 32 : 64;
     uint32_t t = 0, store_k = 0;
     for (int unit = pair; unit < total_units; unit += npairs, ++t) {
@@ -997,7 +1025,7 @@ __global__ void __launch_bounds__(Cfg2<BN, EPI>::THREADS, 1)
       coords(unit, mp, n_blk);
       const int m_blk = 2 * mp + static_cast<int>(rank);
       const uint32_t acc = t & 1, acc_phase = (t >> 1) & 1;
-      const bool has_bias = EPI != EPI_F16 && g.bias != nullptr;
+      const bool has_bias = epi_bias(EPI) && g.bias != nullptr;
       if (has_bias) {
         __syncwarp();
         for (int c = lane; c < C::COLS_PER_WARP; c += 32) {
@@ -1095,7 +1123,7 @@ __global__ void __launch_bounds__(Cfg2<BN, EPI>::THREADS, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          if (F32OUT)
+          if (EPI == EPI_BIAS_RESID_F32)
             tma_reduce_add_2d(&tmC, buf, n_blk * BN + c, m_blk * BM + quad * 32);
           else
             tma_store_2d(&tmC, buf, n_blk * BN + c, m_blk * BM + quad * 32);
@@ -1132,6 +1160,7 @@ void configure_pair_bn() {
   configure_pair_one<BN, EPI_BIAS_RESID_F32>();
   configure_pair_one<BN, EPI_F16>();
   configure_pair_one<BN, EPI_ROWSTAT>();
+  configure_pair_one<BN, EPI_F16_F32>();
 }
 
 template <int BN, int EPI>
@@ -1164,6 +1193,7 @@ void launch_pair_bn(const GemmPlan& p, const GemmArgs& g, cudaStream_t st) {
     case EPI_BIAS_RESID_F32: launch_pair_one<BN, EPI_BIAS_RESID_F32>(p, g, st); break;
     case EPI_F16: launch_pair_one<BN, EPI_F16>(p, g, st); break;
     case EPI_ROWSTAT: launch_pair_one<BN, EPI_ROWSTAT>(p, g, st); break;
+    case EPI_F16_F32: launch_pair_one<BN, EPI_F16_F32>(p, g, st); break;
     default: throw std::invalid_argument("unknown gemm epilogue");
   }
 }
@@ -1180,6 +1210,7 @@ void configure_bn() {
   configure_one<BN, LEAN, EPI_BIAS_GELU_F16>();
   configure_one<BN, LEAN, EPI_BIAS_RESID_F32>();
   configure_one<BN, LEAN, EPI_F16>();
+  configure_one<BN, LEAN, EPI_F16_F32>();
 }
 
 template <int BN, bool LEAN, int EPI>
@@ -1195,6 +1226,7 @@ void launch_bn(const GemmPlan& p, const GemmArgs& g, cudaStream_t st) {
     case EPI_BIAS_GELU_F16: launch_one<BN, LEAN, EPI_BIAS_GELU_F16>(p, g, st); break;
     case EPI_BIAS_RESID_F32: launch_one<BN, LEAN, EPI_BIAS_RESID_F32>(p, g, st); break;
     case EPI_F16: launch_one<BN, LEAN, EPI_F16>(p, g, st); break;
+    case EPI_F16_F32: launch_one<BN, LEAN, EPI_F16_F32>(p, g, st); break;
     default: throw std::invalid_argument("unknown gemm epilogue");
   }
 }
@@ -1271,6 +1303,7 @@ GemmPlan plan_gemm_tc(const void* A, int64_t lda, const void* Wt, int64_t ldw, c
     splits = std::min(std::abs(force_splits), nkb);
     cluster = force_splits > 0 && splits > 1;  // negative: the global-workspace split-K path
   }
+  if (epi == EPI_F16_F32) cluster = false;  // (the cluster split-K kernel has no fp32-widening epilogue)
   if (splits > 1) {
     const int kps = (nkb + splits - 1) / splits;
     splits = (nkb + kps - 1) / kps;
@@ -1322,7 +1355,7 @@ GemmPlan plan_gemm_tc(const void* A, int64_t lda, const void* Wt, int64_t ldw, c
   }
   p.tmA = make_tmap_f16_2d(A, M, K, lda, BM, BK);
   // TMA-store epilogue when the output rows are 16-byte aligned (TMA clips the M/N tails)
-  const bool f32out = epi == EPI_BIAS_RESID_F32;
+  const bool f32out = epi_f32out(epi);
   const int64_t row_bytes = ldo * (f32out ? 4 : 2);
   p.tma_store = !std::getenv("PRLAB_NO_TMA_STORE") && (row_bytes % 16 == 0) &&
                 (reinterpret_cast<uintptr_t>(out) % 16 == 0);

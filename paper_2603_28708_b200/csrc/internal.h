@@ -84,6 +84,7 @@ enum GemmEpi : int {
   // (max, sum exp(v - max), first argmax column, non-finite flag), one slot per
   // (n-block, epilogue column group); tval[row] = v at targets[row].  Pair kernel only.
   EPI_ROWSTAT = 4,
+  EPI_F16_F32 = 5,        // round16(acc)                           -> fp32 (the binary16 value, widened)
 };
 struct GemmPlan {
   CUtensorMap tmA, tmB, tmC;  // tmC: output map for the TMA-store epilogue

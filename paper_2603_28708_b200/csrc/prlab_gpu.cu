@@ -544,7 +544,7 @@ struct prlab_gpu_model {
     DeviceBuffer cl_buf;
     std::vector<std::array<const float*, 8>> cl_lw;
     std::map<std::tuple<const void*, void*, int, int64_t>, cudaGraphExec_t> graphs;
-    std::map<std::tuple<void*, int64_t>, GemmPlan> head_plans;
+    std::map<std::tuple<void*, int64_t, int>, GemmPlan> head_plans;  // (out, ld, epilogue)
     // fused head statistics (prlab_gpu_forward_nll_device): 0 = not planned, 1 = fused, 2 = unfused
     int rs_state = 0;
     GemmPlan rs_plan{};
@@ -1050,21 +1050,21 @@ int64_t enqueue_forward(prlab_gpu_model& m, prlab_gpu_model::Plan& p, const int3
     if (o.hidden_only) return n;  // forward_hidden: r16(final LN) in xn16 (the Linear lattice)
     if (out_dtype == PRLAB_OUT_F16) {
       if (ld % 8 != 0) throw std::invalid_argument("fp16 logits need a row pitch that is a multiple of 8");
-      const auto key = std::make_tuple(out, ld);
+      const auto key = std::make_tuple(out, ld, static_cast<int>(EPI_F16));
       auto it = p.head_plans.find(key);
       if (it == p.head_plans.end())
         it = p.head_plans.emplace(key, plan_gemm_tc(p.xn16, h, m.emb16, h, nullptr, out, ld, Mi, Vi, hi, EPI_F16, &m.scratch)).first;
       it->second.acc16 = p.fp16;
       T(PRLAB_LINEAR, [&] { launch_gemm_tc(it->second, st); });  // tied head straight into the caller's buffer
     } else {
-      __half* l16 = plan_logits16(p);
-      const auto key = std::make_tuple(static_cast<void*>(l16), p.ld16);
+      // fp32 logits straight from the head's epilogue (the widened binary16 values; TMA
+      // store when the rows are 16-byte aligned), no fp16 staging buffer
+      const auto key = std::make_tuple(out, ld, static_cast<int>(EPI_F16_F32));
       auto it = p.head_plans.find(key);
       if (it == p.head_plans.end())
-        it = p.head_plans.emplace(key, plan_gemm_tc(p.xn16, h, m.emb16, h, nullptr, l16, p.ld16, Mi, Vi, hi, EPI_F16, &m.scratch)).first;
+        it = p.head_plans.emplace(key, plan_gemm_tc(p.xn16, h, m.emb16, h, nullptr, out, ld, Mi, Vi, hi, EPI_F16_F32, &m.scratch)).first;
       it->second.acc16 = p.fp16;
       T(PRLAB_LINEAR, [&] { launch_gemm_tc(it->second, st); });
-      T(PRLAB_LINEAR, [&] { convert_f16_to_f32(l16, p.ld16, static_cast<float*>(out), ld, Mi, Vi, st); });
     }
     return n;
   }
@@ -1879,10 +1879,9 @@ int prlab_gpu_forward_kernel_count_ex(prlab_gpu_model* m, int64_t B, int64_t S, 
     const bool fast = fast_eligible(*m, S, *policy) || fast16_eligible(*m, S, *policy, false);
     const int64_t L = m->L;
     const bool small = fast_eligible(*m, S, *policy) && fwd_small_supported(B * S, S, m->h, m->f, m->hd, L);
-    // fast path: trunk (1 persistent kernel, or embed + 7 per layer + final LN) + the head GEMM,
-    // + the fp16 -> fp32 widening kernel when fp32 logits are asked for
-    const int64_t widen = fast && out_dtype == PRLAB_OUT_F32 ? 1 : 0;
-    *count = small ? 2 + widen : (fast ? 1 + 7 * L + 1 + 1 + widen : 1 + 7 * L + (L > 0 ? 2 : 1));
+    // fast path: trunk (1 persistent kernel, or embed + 7 per layer + final LN) + the head GEMM
+    // (fp16 or fp32 logits straight from its epilogue)
+    *count = small ? 2 : (fast ? 1 + 7 * L + 1 + 1 : 1 + 7 * L + (L > 0 ? 2 : 1));
   });
 }
 
@@ -2048,7 +2047,7 @@ int prlab_gpu_embed(const float* tok, int64_t vocab, const float* pos, int64_t n
 int prlab_gpu_linear_f16_device(const void* A, const void* Wt, const float* bias, void* out, int64_t M,
                                 int64_t N, int64_t K_, int64_t ldo, int32_t epi, void* stream) {
   return guarded([&] {
-    if (epi < 0 || epi > 3) throw std::invalid_argument("unknown epilogue");
+    if (epi < 0 || epi > 5 || epi == EPI_ROWSTAT) throw std::invalid_argument("unknown epilogue");
     const GemmPlan p = plan_gemm_tc(A, K_, Wt, K_, bias, out, ldo, static_cast<int>(M), static_cast<int>(N),
                                     static_cast<int>(K_), epi, &global_split_scratch());
     launch_gemm_tc(p, static_cast<cudaStream_t>(stream));
@@ -2059,7 +2058,7 @@ int prlab_gpu_linear_f16_device_ex(const void* A, const void* Wt, const float* b
                                    int64_t N, int64_t K_, int64_t ldo, int32_t epi, int32_t bn, int32_t splits,
                                    int32_t lean, void* stream) {
   return guarded([&] {
-    if (epi < 0 || epi > 3) throw std::invalid_argument("unknown epilogue");
+    if (epi < 0 || epi > 5 || epi == EPI_ROWSTAT) throw std::invalid_argument("unknown epilogue");
     if (bn != 0 && bn != 64 && bn != 128 && bn != 256) throw std::invalid_argument("bn must be 64, 128 or 256");
     const GemmPlan p = plan_gemm_tc(A, K_, Wt, K_, bias, out, ldo, static_cast<int>(M), static_cast<int>(N),
                                     static_cast<int>(K_), epi, &global_split_scratch(), bn, splits, lean);

@@ -17,7 +17,7 @@ pol = os.environ.get("POLICY", "hybrid")
 m = pg.DeviceModel(cfg, pg.build_model(cfg))
 ids = torch.from_numpy(pg.random_tokens(cfg.vocab, B, S, 11)).cuda()
 f16 = os.environ.get("OUT", "f32") == "f16"
-ld = (cfg.vocab + 7) // 8 * 8 if f16 else cfg.vocab
+ld = (cfg.vocab + 7) // 8 * 8 if f16 else int(os.environ.get("LD32", (cfg.vocab + 3) // 4 * 4))
 out = torch.empty(B * S, ld, device="cuda", dtype=torch.float16 if f16 else torch.float32)
 st = torch.cuda.current_stream()
 run = lambda: m.forward_device(ids.data_ptr(), B, S, pol, out.data_ptr(), pg.OUT_F16 if f16 else pg.OUT_F32, ld, st.cuda_stream, True)

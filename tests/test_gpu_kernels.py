@@ -301,3 +301,32 @@ def test_linear_f32_tensor_core_vs_fp64(M, N, K, epi):
     # 400x inside the fp32 policy's 1e-3 contract; a plain 1xTF32 GEMM sits near 1e-3
     assert err <= max(8 * err32, 5e-6), (err, err32)
 
+
+
+# ---- fp32 logits straight from the head epilogue (EPI 5 = widened round16(acc)) ----
+@pytest.mark.parametrize("M,N,ldo,bn,splits,lean", [
+    (128, 30522, 30524, 0, 0, 0),     # C2/C3 head shape, 16-byte rows: TMA-store epilogue
+    (256, 30522, 30522, 0, 0, 0),     # unaligned rows: per-thread stores
+    (640, 50257, 50260, 256, 1, 2),   # CTA-pair kernel, M tail
+    (200, 768, 768, 64, -3, 1),       # global-workspace split-K, lean pipeline
+    (200, 768, 768, 128, 3, -1),      # (cluster split-K request: falls back to one split)
+    (1, 96, 96, 0, 0, 0),
+])
+def test_tc_linear_f32_logits_match_f16(M, N, ldo, bn, splits, lean):
+    """epi 5 writes exactly float(epi 3's fp16 value) into an fp32 buffer, on every kernel
+    variant and store path, and leaves the pitch padding past the 16-byte chunk untouched."""
+    K = 768
+    g = torch.Generator(device="cuda").manual_seed(M + N)
+    A = (torch.randn(M, K, device="cuda", generator=g) * 0.5).half()
+    Wt = (torch.randn(N, K, device="cuda", generator=g) * 0.05).half()
+    ld16 = (N + 7) // 8 * 8
+    o16 = torch.empty(M, ld16, device="cuda", dtype=torch.float16)
+    pg.linear_f16_device_ex(A, Wt, None, o16, M, N, K, ld16, 3, bn, splits, lean)
+    o32 = torch.full((M, ldo), float("nan"), device="cuda", dtype=torch.float32)
+    pg.linear_f16_device_ex(A, Wt, None, o32, M, N, K, ldo, 5, bn, splits, lean)
+    torch.cuda.synchronize()
+    assert torch.equal(o32[:, :N], o16[:, :N].float())
+    # the TMA store writes whole 16-byte chunks: at most up to the next 4-float boundary
+    assert torch.isnan(o32[:, (N + 3) // 4 * 4:]).all()
+    with pytest.raises(ValueError):
+        pg.linear_f16_device(A, Wt, None, o32, M, N, K, ldo, 4)  # row statistics: not an output epilogue
