@@ -1039,43 +1039,76 @@ __global__ void __launch_bounds__(Cfg2<BN, EPI>::THREADS, 1)
       if constexpr (EPI == EPI_ROWSTAT) {
         // Fused log-softmax statistics of this thread's row over the warp's columns
         // (logits v = round16(acc), exactly the values EPI_F16 would store): running max
-        // with rescaled fp32 sum of expf(v - max) (expf like row_nll), the first column of
-        // the maximum (strict >, ascending columns), the target's value.
+        // with a rescaled fp32 sum of 2^((v - max) log2 e) (ex2.approx, packed fp32x2
+        // subtract/scale), the first column of the maximum (strict >, ascending columns:
+        // the chunk is rescanned only when its max is a new record), the target's value.
+        // Non-finite rows: a NaN anywhere reaches the sum, +inf the max.  ~8 issue slots per
+        // element (the per-element argmax / NaN / target tests cost ~20).
         const int row = m_blk * BM + static_cast<int>(quad) * 32 + static_cast<int>(lane);
         const int32_t tgt = (g.targets != nullptr && row < g.M) ? g.targets[row] : -1;
         const float ninf = __int_as_float(0xff800000);
-        float mx = ninf, sum = 0.0f, best = ninf;
+        constexpr float L2E = 1.4426950408889634f;
+        constexpr int NCH = C::COLS_PER_WARP / 32;
+        float mx = ninf, sum = 0.0f;
         int bidx = 0x7fffffff;
-        bool bad = false;
-#pragma unroll 1
-        for (int c = cbase; c < cbase + C::COLS_PER_WARP; c += 32) {
+        bool nan_seen = false;
+        const uint32_t tbase = tmem_base + ((quad * 32) << 16) + acc * BN;
+        auto load_chunk = [&](int k, float (&v)[32]) {
           uint32_t u[32];
-          tmem_ld32(tmem_base + ((quad * 32) << 16) + acc * BN + c, u);
+          tmem_ld32(tbase + cbase + k * 32, u);
           tmem_wait_ld();
           if (g.acc16) acc16_widen(u);
-          const int col0 = n_blk * BN + c;
-          float v[32];
-          float cm = ninf;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            v[j] = col0 + j < g.N ? __half2float(__float2half_rn(__uint_as_float(u[j]))) : ninf;
-            bad |= isnan(v[j]) || v[j] == __int_as_float(0x7f800000);
-            cm = fmaxf(cm, v[j]);
-            if (v[j] > best) {
-              best = v[j];
-              bidx = col0 + j;
-            }
-            if (col0 + j == tgt) g.tval[row] = v[j];
+          for (int q = 0; q < 16; ++q)
+            h2_unpack(h2_pack_rn(__uint_as_float(u[2 * q]), __uint_as_float(u[2 * q + 1])), v[2 * q], v[2 * q + 1]);
+          const int col0 = n_blk * BN + cbase + k * 32;
+          if (col0 + 32 > g.N) {  // (warp-uniform: the vocabulary tail)
+#pragma unroll
+            for (int q = 0; q < 32; ++q)
+              if (col0 + q >= g.N) v[q] = ninf;
+          }
+        };
+#pragma unroll
+        for (int k = 0; k < NCH; ++k) {
+          float v[32];
+          load_chunk(k, v);
+          const int col0 = n_blk * BN + cbase + k * 32;
+          float m4[4] = {v[0], v[1], v[2], v[3]};
+#pragma unroll
+          for (int q = 4; q < 32; ++q) m4[q & 3] = fmaxf(m4[q & 3], v[q]);
+          const float cm = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
+          const unsigned kt = static_cast<unsigned>(tgt - col0);
+          if (kt < 32u) {
+            float tv = v[0];
+#pragma unroll
+            for (int q = 1; q < 32; ++q) tv = kt == static_cast<unsigned>(q) ? v[q] : tv;
+            g.tval[row] = tv;
           }
           if (cm > mx) {
-            sum = mx == ninf ? 0.0f : sum * expf(mx - cm);
+            int jj = 31;
+#pragma unroll
+            for (int q = 31; q >= 0; --q) jj = v[q] == cm ? q : jj;
+            bidx = col0 + jj;
+            sum = mx == ninf ? 0.0f : sum * ex2_approx(__fmul_rn(__fsub_rn(mx, cm), L2E));
             mx = cm;
           }
           if (mx != ninf) {
+            const uint64_t nm = f2_pack(-mx, -mx), l2 = f2_pack(L2E, L2E);
+            float s4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-            for (int j = 0; j < 32; ++j) sum += expf(v[j] - mx);
+            for (int q = 0; q < 16; ++q) {
+              float d0, d1;
+              f2_unpack(f2_mul(f2_add(f2_pack(v[2 * q], v[2 * q + 1]), nm), l2), d0, d1);
+              s4[(2 * q) & 3] += ex2_approx(d0);
+              s4[(2 * q + 1) & 3] += ex2_approx(d1);
+            }
+            sum += (s4[0] + s4[1]) + (s4[2] + s4[3]);
+          } else {
+#pragma unroll
+            for (int q = 0; q < 32; ++q) nan_seen |= v[q] != v[q];
           }
         }
+        const bool bad = nan_seen || sum != sum || mx == __int_as_float(0x7f800000);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
