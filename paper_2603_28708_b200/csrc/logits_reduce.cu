@@ -152,46 +152,81 @@ __global__ void __launch_bounds__(kThreads) compare_rows_kernel(const TB* __rest
   if (threadIdx.x == 0) out[6] = static_cast<double>(bad);
 }
 
-// Fold of the LM head's fused row statistics (gemm_tc.cu EPI_ROWSTAT): one thread per
-// row walks its slots in column order -- slot-major layout, so a warp's loads cover 32
-// consecutive rows -- max M and the first column reaching it (strict >: lowest index on
-// ties, as row_nll), denominator sum_p s_p * exp(m_p - M) in double, then the NLL of the
-// target exactly as row_nll forms it (0 without a target, NaN for a non-finite row).
-__global__ void __launch_bounds__(kThreads) rowstat_combine_kernel(const float4* __restrict__ stat, int nslots,
-                                                                   int64_t rows, int64_t n,
-                                                                   const int32_t* __restrict__ targets,
-                                                                   const float* __restrict__ tval,
-                                                                   double* __restrict__ nll, int32_t* __restrict__ amax) {
-  const int64_t r = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x;
-  if (r >= rows) return;
-  float mx = __int_as_float(0xff800000);
+// Fold of the LM head's fused row statistics (gemm_tc.cu EPI_ROWSTAT): a CTA owns 32 rows;
+// its 8 warps split the slots (warp w: slots w, w + 8, ...) so every load is one 512-byte
+// run of 32 consecutive rows (slot-major layout).  Per thread: running max with the first
+// column reaching it (slots in column order, strict >) and the denominator
+// sum_p s_p * exp(m_p - m) in double, rescaled when m grows; the 8 partials of a row then
+// merge through shared memory (max, lowest column on ties, den * exp(m_w - M)).  The NLL
+// of the target is formed exactly as row_nll does (0 without a target, NaN for a
+// non-finite row).
+constexpr int kFoldRows = 32, kFoldWarps = 8;
+__global__ void __launch_bounds__(kFoldRows * kFoldWarps) rowstat_combine_kernel(
+    const float4* __restrict__ stat, int nslots, int64_t rows, int64_t n, const int32_t* __restrict__ targets,
+    const float* __restrict__ tval, double* __restrict__ nll, int32_t* __restrict__ amax) {
+  __shared__ float s_mx[kFoldWarps][kFoldRows];
+  __shared__ int s_idx[kFoldWarps][kFoldRows];
+  __shared__ double s_den[kFoldWarps][kFoldRows];
+  __shared__ int s_bad[kFoldWarps][kFoldRows];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t r = static_cast<int64_t>(blockIdx.x) * kFoldRows + lane;
+  const float ninf = __int_as_float(0xff800000);
+  float mx = ninf;
   int idx = 0x7fffffff;
+  double den = 0.0;
   bool bad = false;
-  for (int p = 0; p < nslots; ++p) {
-    const float4 q = stat[static_cast<int64_t>(p) * rows + r];
-    bad |= q.w != 0.0f;
-    if (q.x > mx) {
-      mx = q.x;
-      idx = __float_as_int(q.z);
+  if (r < rows) {
+    for (int p = w; p < nslots; p += kFoldWarps) {
+      const float4 q = __ldcs(stat + static_cast<int64_t>(p) * rows + r);
+      bad |= q.w != 0.0f;
+      if (q.x == ninf) continue;  // an all-masked slot (vocabulary tail)
+      if (q.x > mx) {
+        den = mx == ninf ? 0.0 : den * exp(static_cast<double>(mx) - static_cast<double>(q.x));
+        mx = q.x;
+        idx = __float_as_int(q.z);
+      }
+      den += static_cast<double>(q.y) * exp(static_cast<double>(q.x) - static_cast<double>(mx));
     }
   }
-  if (amax != nullptr) amax[r] = idx;
+  s_mx[w][lane] = mx;
+  s_idx[w][lane] = idx;
+  s_den[w][lane] = den;
+  s_bad[w][lane] = bad;
+  __syncthreads();
+  if (w != 0 || r >= rows) return;
+  // merge in warp order: slots of warp v precede those of warp v+1 only within a stride,
+  // so ties resolve on the column index itself
+  float M = ninf;
+  int I = 0x7fffffff;
+  bool B = false;
+#pragma unroll
+  for (int v = 0; v < kFoldWarps; ++v) {
+    const float m = s_mx[v][lane];
+    const int id = s_idx[v][lane];
+    B |= s_bad[v][lane] != 0;
+    if (m > M || (m == M && m != ninf && id < I)) {
+      M = m;
+      I = id;
+    }
+  }
+  if (amax != nullptr) amax[r] = I;
   if (nll == nullptr) return;
   const int32_t t = targets != nullptr ? targets[r] : -1;
   if (t < 0 || t >= n) {
     nll[r] = 0.0;
     return;
   }
-  if (!isfinite(mx) || bad) {
+  if (!isfinite(M) || B) {
     nll[r] = __longlong_as_double(0x7ff8000000000000ll);
     return;
   }
-  double den = 0.0;
-  for (int p = 0; p < nslots; ++p) {
-    const float4 q = stat[static_cast<int64_t>(p) * rows + r];
-    if (q.x != __int_as_float(0xff800000)) den += static_cast<double>(q.y) * exp(static_cast<double>(q.x) - mx);
+  double D = 0.0;
+#pragma unroll
+  for (int v = 0; v < kFoldWarps; ++v) {
+    const float m = s_mx[v][lane];
+    if (m != ninf) D += s_den[v][lane] * exp(static_cast<double>(m) - static_cast<double>(M));
   }
-  nll[r] = -((static_cast<double>(tval[r]) - mx) - log(den));
+  nll[r] = -((static_cast<double>(tval[r]) - M) - log(D));
 }
 
 }  // namespace
@@ -199,7 +234,7 @@ __global__ void __launch_bounds__(kThreads) rowstat_combine_kernel(const float4*
 void rowstat_combine(const void* stat, int nslots, int64_t rows, int64_t n, const int32_t* targets,
                      const float* tval, double* nll, int32_t* amax, cudaStream_t st) {
   if (rows <= 0) return;
-  rowstat_combine_kernel<<<static_cast<unsigned>((rows + kThreads - 1) / kThreads), kThreads, 0, st>>>(
+  rowstat_combine_kernel<<<static_cast<unsigned>((rows + kFoldRows - 1) / kFoldRows), kFoldRows * kFoldWarps, 0, st>>>(
       static_cast<const float4*>(stat), nslots, rows, n, targets, tval, nll, amax);
   PRLAB_CUDA(cudaGetLastError());
 }
