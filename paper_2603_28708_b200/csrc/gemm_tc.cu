@@ -1108,15 +1108,31 @@ __global__ void __launch_bounds__(Cfg2<BN, EPI>::THREADS, 1)
             for (int q = 0; q < 32; ++q) nan_seen |= v[q] != v[q];
           }
         }
-        const bool bad = nan_seen || sum != sum || mx == __int_as_float(0x7f800000);
+        bool bad = nan_seen || sum != sum || mx == __int_as_float(0x7f800000);
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive_cluster(tempty_leader + acc * 8);
-        if (row < g.M) {
-          const int slot = n_blk * (C::EPI_WARPS / 4) + ((static_cast<int>(warp) - 2) >> 2);
-          reinterpret_cast<float4*>(g.out)[static_cast<int64_t>(slot) * g.M + row] =
-              make_float4(mx, sum, __int_as_float(bidx), bad ? 1.0f : 0.0f);
+        // the two column groups of a TMEM lane quadrant (warps q and q + 4) merge through
+        // shared memory (double-buffered by tile parity: one barrier per tile), so the head
+        // writes one slot per n-block and row: half the bytes for the fold kernel
+        static_assert(C::EPI_WARPS == 8, "row statistics: two column groups per quadrant");
+        const int grp = (static_cast<int>(warp) - 2) >> 2;
+        float4* xch = reinterpret_cast<float4*>(smem + C::EPI_OFF) + ((t & 1) * 4 + quad) * 32;
+        if (grp == 1) xch[lane] = make_float4(mx, sum, __int_as_float(bidx), bad ? 1.0f : 0.0f);
+        named_bar_sync(8 + quad, 64);
+        if (grp == 1) continue;
+        const float4 o = xch[lane];
+        if (o.x > mx) {  // (ties keep group 0: its columns come first)
+          sum = (mx == ninf ? 0.0f : sum * ex2_approx(__fmul_rn(__fsub_rn(mx, o.x), L2E))) + o.y;
+          mx = o.x;
+          bidx = __float_as_int(o.z);
+        } else if (o.x != ninf) {
+          sum += o.y * ex2_approx(__fmul_rn(__fsub_rn(o.x, mx), L2E));
         }
+        bad |= o.w != 0.0f || sum != sum;
+        if (row < g.M)
+          reinterpret_cast<float4*>(g.out)[static_cast<int64_t>(n_blk) * g.M + row] =
+              make_float4(mx, sum, __int_as_float(bidx), bad ? 1.0f : 0.0f);
         continue;
       }
 #pragma unroll 1

@@ -82,7 +82,7 @@ enum GemmEpi : int {
   // per-row statistics of round16(acc) instead of the values (the LM head's fused
   // log-softmax / argmax): out = float4 [nslots][M] partials
   // (max, sum exp(v - max), first argmax column, non-finite flag), one slot per
-  // (n-block, epilogue column group); tval[row] = v at targets[row].  Pair kernel only.
+  // n-block; tval[row] = v at targets[row].  Pair kernel only.
   EPI_ROWSTAT = 4,
   EPI_F16_F32 = 5,        // round16(acc)                           -> fp32 (the binary16 value, widened)
 };

@@ -1813,7 +1813,7 @@ void enqueue_nll(prlab_gpu_model& m, prlab_gpu_model::Plan& p, const int32_t* d_
       GemmPlan probe = plan_gemm_tc(p.xn16, m.h, m.emb16, m.h, nullptr, p.xn16, p.ld16, static_cast<int>(M),
                                     static_cast<int>(V), static_cast<int>(m.h), EPI_F16, &m.scratch);
       if (probe.pair) {
-        const int nslots = ((static_cast<int>(V) + probe.bn - 1) / probe.bn) * 2;  // 2 column groups per tile
+        const int nslots = (static_cast<int>(V) + probe.bn - 1) / probe.bn;  // one slot per n-block (gemm_tc.cu)
         p.rs_buf.alloc(static_cast<size_t>(nslots) * M * 16 + M * 4);
         p.rs_plan = plan_gemm_tc(p.xn16, m.h, m.emb16, m.h, nullptr, p.rs_buf.p, 8, static_cast<int>(M),
                                  static_cast<int>(V), static_cast<int>(m.h), EPI_ROWSTAT, &m.scratch, probe.bn);
