@@ -518,19 +518,36 @@ __global__ void __launch_bounds__(row_threads<TPR>(), 2) attn_fa_row_kernel(cons
         umma_commit(&bars[R_KEMPTY + s]);
         if (last_of_unit) umma_commit(&bars[R_QEMPTY + qs]);
       };
-      for (int it = 0, u; (u = fa_unit_at(a, it)) >= 0; ++it, ++qc) {
-        int b, head, qt, nkb;
-        fa_decode(a, u, b, head, qt, nkb);
+      // The next block's Q.K^T is issued as soon as the softmax has read S -- across unit
+      // boundaries too (the next unit's Q is double-buffered), so a unit's first S is ready
+      // when the softmax warps come back from the previous unit's epilogue.
+      auto q_addr = [&](uint32_t qcount) { return smem_u32(smem + FaSmem::Q + (qcount & 1) * kTile); };
+      int u = fa_unit_at(a, 0);
+      int nkb = 0;
+      if (u >= 0) {
+        int b_, h_, qt_;
+        fa_decode(a, u, b_, h_, qt_, nkb);
+        mbar_wait(&bars[R_QFULL], 0);
+        issue_s(q_addr(0), 0, nkb == 1, 0);
+      }
+      for (int it = 0; u >= 0; ++it, ++qc) {
         const uint32_t qs = qc & 1;
-        mbar_wait(&bars[R_QFULL + qs], (qc >> 1) & 1);
-        const uint32_t q0 = smem_u32(smem + FaSmem::Q + qs * kTile);
-        if (bc > 0) mbar_wait_spin(&bars[R_SFREE], (bc - 1) & 1);  // previous block's S was read
-        issue_s(q0, kc, nkb == 1, qs);
+        const uint32_t q0 = q_addr(qc);
+        const int un = fa_unit_at(a, it + 1);  // the next unit (its first S is issued from here)
+        int nkb_next = 0;
+        if (un >= 0) {
+          int b_, h_, qt_;
+          fa_decode(a, un, b_, h_, qt_, nkb_next);
+        }
         for (int kb = 0; kb < nkb; ++kb, ++kc, ++bc) {
           const uint32_t s = kc & 1, ph = (kc >> 1) & 1;
           if (kb + 1 < nkb) {
             mbar_wait_spin(&bars[R_SFREE], bc & 1);
             issue_s(q0, kc + 1, kb + 2 == nkb, qs);
+          } else if (un >= 0) {
+            mbar_wait_spin(&bars[R_SFREE], bc & 1);
+            mbar_wait(&bars[R_QFULL + (qs ^ 1)], ((qc + 1) >> 1) & 1);
+            issue_s(q_addr(qc + 1), kc + 1, nkb_next == 1, qs ^ 1);
           }
           mbar_wait_spin(&bars[R_PREADY], bc & 1);
           long long* ms = (a.dbg && blockIdx.x == 0 && bc < 32) ? a.dbg + bc * 8 : nullptr;
@@ -548,6 +565,8 @@ __global__ void __launch_bounds__(row_threads<TPR>(), 2) attn_fa_row_kernel(cons
           if (kb == nkb - 1) umma_commit(&bars[R_OFULL]);
           if (ms) ms[5] = clock64();
         }
+        u = un;
+        nkb = nkb_next;
       }
     }
     __syncwarp();
@@ -562,6 +581,51 @@ __global__ void __launch_bounds__(row_threads<TPR>(), 2) attn_fa_row_kernel(cons
     constexpr uint32_t NEG_INF2 = 0xFC00FC00u;  // (-inf, -inf) as f16x2
     constexpr float LOG2E = 1.4426950408889634f;
     uint32_t qc = 0, bc = 0;
+    // A unit's epilogue (o = round16(O / l) -> ctx) runs after the NEXT unit's first block has
+    // its exponentials in registers: the wait for the unit's last P.V (OFULL) then hides behind
+    // that block's S load and exponent pass instead of stalling the row between units.
+    struct Pending { float l; int64_t dst; bool live; } pe{0.0f, 0, false};
+    auto epilogue = [&](uint32_t qcount) {
+      if constexpr (TPR > 1) red[1024 + half * 128 + r] = pe.l;
+      mbar_wait(&bars[R_OFULL], qcount & 1);
+      tc_fence_after();
+      uint32_t o[OC];
+#pragma unroll
+      for (int hh = 0; hh < OC / 16; ++hh)
+        tmem_ld16(lane_addr + kColO + OC * static_cast<uint32_t>(half) + 16 * hh, *reinterpret_cast<uint32_t(*)[16]>(o + 16 * hh));
+      tmem_wait_ld();
+      tc_fence_before();
+      float l = pe.l;
+      if constexpr (TPR > 1) {  // every part's sum visible; the next rsum write is a unit (and a row barrier) later
+        named_bar_sync(1 + quad, 32 * TPR);
+        float lt2 = red[1024 + r];
+#pragma unroll
+        for (int q = 1; q < TPR; ++q) lt2 = __fadd_rn(lt2, red[1024 + q * 128 + r]);
+        l = lt2;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[R_TFREE]);
+      // full_fp16: the reference sums e on the binary16 lattice (kernels.cpp:154-165)
+      const float lt = a.unstab ? r16(l) : l;
+      if (pe.dst >= 0) {
+        const float inv = __frcp_rn(lt);
+        const uint64_t inv2 = f2_pack(inv, inv);
+        uint4* dst = reinterpret_cast<uint4*>(a.ctx + pe.dst);
+#pragma unroll
+        for (int q = 0; q < OC / 8; ++q) {
+          uint32_t pk[4];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            float x0, x1;
+            f2_unpack(f2_mul(f2_pack(__uint_as_float(o[8 * q + 2 * i]), __uint_as_float(o[8 * q + 2 * i + 1])), inv2),
+                      x0, x1);
+            pk[i] = h2_pack_rn(x0, x1);
+          }
+          dst[q] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        }
+      }
+      pe.live = false;
+    };
     for (int it = 0, u; (u = fa_unit_at(a, it)) >= 0; ++it, ++qc) {
       int b, head, qt, nkb;
       fa_decode(a, u, b, head, qt, nkb);
@@ -667,6 +731,7 @@ __global__ void __launch_bounds__(row_threads<TPR>(), 2) attn_fa_row_kernel(cons
             sp[16 * cc + i] = h2_pack_rn(e0, e1);  // P~ replaces the score in place
           }
         }
+        if (pe.live) epilogue(qc - 1);  // (kb == 0: the previous unit's O, then TFREE)
         if (bc > 0) mbar_wait(&bars[R_PVDONE], (bc - 1) & 1);  // P columns and O free
         tc_fence_after();
         if (ts) ts[2] = clock64();
@@ -703,46 +768,12 @@ __global__ void __launch_bounds__(row_threads<TPR>(), 2) attn_fa_row_kernel(cons
         if (lane == 0) mbar_arrive(&bars[R_PREADY]);
         if (ts) ts[3] = clock64();
       }
-      // epilogue: o = round16(O / l) -> ctx row (this thread's 64 / TPR halves)
-      if constexpr (TPR > 1) red[1024 + half * 128 + r] = l;
-      mbar_wait(&bars[R_OFULL], qc & 1);
-      tc_fence_after();
-      uint32_t o[OC];
-#pragma unroll
-      for (int hh = 0; hh < OC / 16; ++hh)
-        tmem_ld16(lane_addr + kColO + OC * static_cast<uint32_t>(half) + 16 * hh, *reinterpret_cast<uint32_t(*)[16]>(o + 16 * hh));
-      tmem_wait_ld();
-      tc_fence_before();
-      if constexpr (TPR > 1) {  // every part's sum visible; the next rsum write is a unit (and a row barrier) later
-        named_bar_sync(1 + quad, 32 * TPR);
-        float lt2 = red[1024 + r];
-#pragma unroll
-        for (int q = 1; q < TPR; ++q) lt2 = __fadd_rn(lt2, red[1024 + q * 128 + r]);
-        l = lt2;
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[R_TFREE]);
-      // full_fp16: the reference sums e on the binary16 lattice (kernels.cpp:154-165)
-      const float lt = a.unstab ? r16(l) : l;
-      if (qrow < a.S) {
-        const float inv = __frcp_rn(lt);
-        const uint64_t inv2 = f2_pack(inv, inv);
-        uint4* dst = reinterpret_cast<uint4*>(a.ctx + (static_cast<int64_t>(b) * a.S + qrow) * a.ld_ctx + head * 64 +
-                                              half * OC);
-#pragma unroll
-        for (int q = 0; q < OC / 8; ++q) {
-          uint32_t pk[4];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) {
-            float x0, x1;
-            f2_unpack(f2_mul(f2_pack(__uint_as_float(o[8 * q + 2 * i]), __uint_as_float(o[8 * q + 2 * i + 1])), inv2),
-                      x0, x1);
-            pk[i] = h2_pack_rn(x0, x1);
-          }
-          dst[q] = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        }
-      }
+      // epilogue deferred (see Pending): this thread's 64 / TPR columns of the ctx row
+      pe.l = l;
+      pe.dst = qrow < a.S ? (static_cast<int64_t>(b) * a.S + qrow) * a.ld_ctx + head * 64 + half * OC : -1;
+      pe.live = true;
     }
+    if (pe.live) epilogue(qc - 1);
   }
   tc_fence_before();
   __syncthreads();

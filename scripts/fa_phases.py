@@ -36,6 +36,9 @@ def main():
                      "row_first_chunk": d[b, 6] - d[b, 0] if d[b, 6] else 0,
                      "row_all_chunks": d[b, 7] - d[b, 0] if d[b, 7] else 0})
     avg = {k: round(float(np.median([r[k] for r in rows])), 1) for k in rows[0]}
+    n = int((d[:, 0] > 0).sum())
+    print(json.dumps({"cta0_blocks": n, "s_seen_deltas": [int(d[i + 1, 0] - d[i, 0]) for i in range(n - 1)],
+                      "span_cycles": int(d[n - 1, 3] - d[0, 0])}))
     print(json.dumps({"B": B, "S": S, "blocks": len(rows), "median_cycles": avg}))
 
 
