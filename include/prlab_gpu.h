@@ -286,7 +286,9 @@ int prlab_gpu_linear_f16_device_ex(const void* A, const void* Wt, const float* b
  * Replaces the fp32 linear_bias of src/kernels.cpp:40-83 under the fp32 policy; K % 32 == 0. */
 int prlab_gpu_linear_f32_device(const float* A, const float* Wt, const float* bias, float* out, int64_t M,
                                 int64_t N, int64_t K, int32_t epi, const float* resid, void* stream);
-/* Fused hybrid attention on tensor cores: qkv fp16 [B*S, 3h] (q|k|v), ctx fp16 [B*S, h]. */
+/* Fused hybrid attention on tensor cores: qkv fp16 [B*S, 3h] (q|k|v), ctx fp16 [B*S, h].
+ * The streaming kernel's dynamic unit counter is per host thread and device: one host thread
+ * must not have two of these calls in flight on different streams at once. */
 int prlab_gpu_attention_f16_device(const void* qkv, void* ctx, int64_t batch, int64_t seq,
                                    int64_t heads, int64_t head_dim, int32_t causal,
                                    void* stream);

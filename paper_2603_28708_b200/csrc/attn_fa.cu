@@ -25,6 +25,12 @@
 // tile); causal units are ordered by key-block count and dealt in a snake over the CTAs.
 #include <cstdlib>
 
+#include <algorithm>
+#include <map>
+#include <queue>
+#include <tuple>
+#include <vector>
+
 #include "common.cuh"
 #include "internal.h"
 
@@ -48,7 +54,7 @@ struct FaSmem {
   // warp may write the next block's before a slow one read this one's), partial row sums
   static constexpr uint32_t RED = V + 2 * kTile;
   static constexpr uint32_t BAR = RED + 6 * 256 * 4;  // row kernel TPR 4: rmax 2 x 4 x 128, rsum 4 x 128
-  static constexpr uint32_t TOTAL = BAR + 256;
+  static constexpr uint32_t TOTAL = BAR + 512;
 };
 constexpr size_t kFaSmemBytes = 1024 + FaSmem::TOTAL;
 
@@ -68,6 +74,8 @@ enum : int {
 };
 
 struct FaArgs {
+  int* work;         // dynamic unit counter [2] (next unit, CTAs done; zero between launches) or null
+  const int* sched;  // balanced static schedule ([grid + 1] offsets, then unit ids; attn_fa_schedule) or null
   int B, S, H, causal, nqt, h;
   int unstab;  // full_fp16 fast path: unstabilised softmax (no max shift, kernels.cpp:155)
   __half* ctx;
@@ -114,6 +122,10 @@ __device__ __forceinline__ float fmax3_fa(float a, float b, float c) {
 
 // unit u -> (b, head, qt); causal: all last tiles first (most key blocks), snake over CTAs
 __device__ __forceinline__ int fa_unit_at(const FaArgs& a, int k) {
+  if (a.sched != nullptr) {
+    const int o0 = __ldg(a.sched + blockIdx.x), o1 = __ldg(a.sched + blockIdx.x + 1);
+    return o0 + k < o1 ? __ldg(a.sched + gridDim.x + 1 + o0 + k) : -1;
+  }
   const int n = a.B * a.H * a.nqt;
   const int g = static_cast<int>(gridDim.x), c = static_cast<int>(blockIdx.x);
   const int u = k * g + ((k & 1) ? g - 1 - c : c);
@@ -438,7 +450,9 @@ enum : int {
   R_OFULL = 15,   // last P.V of the unit done
   R_TFREE = 16,   // softmax warps: O read by the epilogue
   R_PVDONE = 17,  // P.V of a block done: P columns and O free
-  R_COUNT = 18
+  R_UFULL = 18,   // [4] unit ring (dynamic schedule): id published by the TMA warp
+  R_UEMPTY = 22,  // [4] unit ring: read by the MMA thread and every softmax warp
+  R_COUNT = 26
 };
 
 __device__ __forceinline__ uint32_t h2_max(uint32_t a, uint32_t b) {
@@ -461,7 +475,9 @@ __global__ void __launch_bounds__(row_threads<TPR>(), 2) attn_fa_row_kernel(cons
   if (warp == kTmaWarp && lane == 0) {
     tma_prefetch_desc(&tm);
     for (int i = 0; i < R_COUNT; ++i)
-      mbar_init(&bars[i], (i == R_SFREE || i == R_PREADY || i == R_TFREE) ? kRowWarps : 1);
+      mbar_init(&bars[i], (i == R_SFREE || i == R_PREADY || i == R_TFREE) ? kRowWarps
+                          : (i >= R_UEMPTY && i < R_UEMPTY + 4)      ? 1 + kRowWarps
+                                                                      : 1);
     fence_barrier_init();
   }
   if (warp == kMmaWarp) {
@@ -473,13 +489,39 @@ __global__ void __launch_bounds__(row_threads<TPR>(), 2) attn_fa_row_kernel(cons
   tc_fence_after();
   pdl_trigger();
   const uint32_t tmem = *tmem_slot;
+  if (a.dbg && threadIdx.x == 0) a.dbg[256 + 2 * blockIdx.x] = globaltimer();  // per-CTA span (debug)
+  // Dynamic schedule (a.work): the TMA warp claims units (heavy first: unit ids are ordered by
+  // key-block count) from a global counter and publishes them through a 4-entry ring, so the two
+  // CTAs of an SM -- which the warp scheduler does not serve equally -- and every SM finish
+  // together.  Consumers read each entry once and release it at once.
+  volatile int* uring = reinterpret_cast<volatile int*>(tmem_slot + 1);
+  const int n_units = a.B * a.H * a.nqt;
+  auto unit_claim = [&](int k) -> int {  // TMA warp, lane 0
+    if (a.work == nullptr) return fa_unit_at(a, k);
+    const int slot = k & 3;
+    mbar_wait(&bars[R_UEMPTY + slot], ((k >> 2) & 1) ^ 1);
+    int u = atomicAdd(a.work, 1);
+    if (u >= n_units) u = -1;
+    uring[slot] = u;
+    mbar_arrive(&bars[R_UFULL + slot]);
+    return u;
+  };
+  auto unit_read = [&](int k, bool warp_wide) -> int {  // MMA thread (warp_wide false) / softmax warps
+    if (a.work == nullptr) return fa_unit_at(a, k);
+    const int slot = k & 3;
+    mbar_wait(&bars[R_UFULL + slot], (k >> 2) & 1);
+    const int u = uring[slot];
+    if (warp_wide) __syncwarp();
+    if (!warp_wide || lane == 0) mbar_arrive(&bars[R_UEMPTY + slot]);
+    return u;
+  };
 
   if (warp == kTmaWarp) {
     // ---------------- TMA producer: per unit Q, then K/V blocks in consumption order
     if (lane == 0) {
       pdl_wait();  // q/k/v are written by the upstream QKV GEMM
       uint32_t qc = 0, kc = 0;
-      for (int it = 0, u; (u = fa_unit_at(a, it)) >= 0; ++it, ++qc) {
+      for (int it = 0, u; (u = unit_claim(it)) >= 0; ++it, ++qc) {
         int b, head, qt, nkb;
         fa_decode(a, u, b, head, qt, nkb);
         const uint32_t qs = qc & 1;
@@ -522,7 +564,7 @@ __global__ void __launch_bounds__(row_threads<TPR>(), 2) attn_fa_row_kernel(cons
       // boundaries too (the next unit's Q is double-buffered), so a unit's first S is ready
       // when the softmax warps come back from the previous unit's epilogue.
       auto q_addr = [&](uint32_t qcount) { return smem_u32(smem + FaSmem::Q + (qcount & 1) * kTile); };
-      int u = fa_unit_at(a, 0);
+      int u = unit_read(0, false);
       int nkb = 0;
       if (u >= 0) {
         int b_, h_, qt_;
@@ -533,14 +575,17 @@ __global__ void __launch_bounds__(row_threads<TPR>(), 2) attn_fa_row_kernel(cons
       for (int it = 0; u >= 0; ++it, ++qc) {
         const uint32_t qs = qc & 1;
         const uint32_t q0 = q_addr(qc);
-        const int un = fa_unit_at(a, it + 1);  // the next unit (its first S is issued from here)
-        int nkb_next = 0;
-        if (un >= 0) {
-          int b_, h_, qt_;
-          fa_decode(a, un, b_, h_, qt_, nkb_next);
-        }
+        int un = -1, nkb_next = 0;  // the next unit: read at this unit's last block (the TMA warp
+                                    // publishes it only after issuing this unit's last loads)
         for (int kb = 0; kb < nkb; ++kb, ++kc, ++bc) {
           const uint32_t s = kc & 1, ph = (kc >> 1) & 1;
+          if (kb + 1 == nkb) {
+            un = unit_read(it + 1, false);
+            if (un >= 0) {
+              int b_, h_, qt_;
+              fa_decode(a, un, b_, h_, qt_, nkb_next);
+            }
+          }
           if (kb + 1 < nkb) {
             mbar_wait_spin(&bars[R_SFREE], bc & 1);
             issue_s(q0, kc + 1, kb + 2 == nkb, qs);
@@ -626,7 +671,7 @@ __global__ void __launch_bounds__(row_threads<TPR>(), 2) attn_fa_row_kernel(cons
       }
       pe.live = false;
     };
-    for (int it = 0, u; (u = fa_unit_at(a, it)) >= 0; ++it, ++qc) {
+    for (int it = 0, u; (u = unit_read(it, true)) >= 0; ++it, ++qc) {
       int b, head, qt, nkb;
       fa_decode(a, u, b, head, qt, nkb);
       const int qrow = qt * 128 + r;
@@ -777,6 +822,15 @@ __global__ void __launch_bounds__(row_threads<TPR>(), 2) attn_fa_row_kernel(cons
   }
   tc_fence_before();
   __syncthreads();
+  if (a.dbg && threadIdx.x == 0) a.dbg[257 + 2 * blockIdx.x] = globaltimer();
+  if (a.work != nullptr && threadIdx.x == 0) {  // the last CTA out re-arms the counter for the next launch
+    __threadfence();
+    if (atomicAdd(a.work + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+      a.work[0] = 0;
+      a.work[1] = 0;
+      __threadfence();
+    }
+  }
   if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc(tmem, kTmemCols);
@@ -791,6 +845,51 @@ bool attn_fa_enabled() {
     return e == nullptr || std::atoi(e) != 0;
   }();
   return on;
+}
+
+// Balanced static schedule for the persistent grid: units (b, head, q-tile) cost their
+// key-block count plus ~half a block of per-unit overhead (the Q load, the epilogue and the
+// pipeline refill at a unit boundary); longest-processing-time-first onto the least-loaded
+// CTA, each CTA's list heavy first.  The serpentine order it replaces gave C4 CTAs 12-14
+// blocks in 5-6 units, and the 14-block / 6-unit CTAs finished 7 us after the rest
+// (scripts/fa_phases.py).  Built at plan time, cached per (device, shape, grid).
+const int* attn_fa_schedule(int B, int S, int H, int causal) {
+  static std::mutex mu;
+  static std::map<std::tuple<int, int, int, int, int>, int*> cache;
+  int dev = 0;
+  PRLAB_CUDA(cudaGetDevice(&dev));
+  const int nqt = (S + 127) / 128, items = B * H, n = items * nqt;
+  const int grid = std::min(n, 2 * num_sms());
+  std::lock_guard<std::mutex> lk(mu);
+  const auto key = std::make_tuple(dev, B * H, nqt, causal, grid);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  auto nkb = [&](int u) { const int qt = nqt - 1 - u / items; return causal ? qt + 1 : nqt; };
+  std::vector<int> order(n);
+  for (int u = 0; u < n; ++u) order[u] = u;
+  std::stable_sort(order.begin(), order.end(), [&](int x, int y) { return nkb(x) > nkb(y); });
+  using Load = std::pair<double, int>;  // (cost, cta): min-heap, ties to the lower CTA index
+  std::priority_queue<Load, std::vector<Load>, std::greater<Load>> heap;
+  for (int c = 0; c < grid; ++c) heap.push({0.0, c});
+  std::vector<std::vector<int>> lists(grid);
+  for (int u : order) {
+    const Load l = heap.top();
+    heap.pop();
+    lists[l.second].push_back(u);
+    heap.push({l.first + nkb(u) + 0.5, l.second});
+  }
+  std::vector<int> host(grid + 1 + n);
+  int o = 0;
+  for (int c = 0; c < grid; ++c) {
+    host[c] = o;
+    for (int u : lists[c]) host[grid + 1 + o++] = u;
+  }
+  host[grid] = o;
+  int* d = nullptr;
+  PRLAB_CUDA(cudaMalloc(&d, host.size() * sizeof(int)));
+  PRLAB_CUDA(cudaMemcpy(d, host.data(), host.size() * sizeof(int), cudaMemcpyHostToDevice));
+  cache.emplace(key, d);
+  return d;
 }
 
 void launch_attn_fa(const AttnPlan& p, cudaStream_t st) {
@@ -821,6 +920,8 @@ void launch_attn_fa(const AttnPlan& p, cudaStream_t st) {
   a.unstab = p.unstab;
   const int units = p.B * p.H * a.nqt;
   const int grid = std::min(units, 2 * num_sms());
+  a.sched = std::getenv("PRLAB_ATTN_SERPENTINE") ? nullptr : p.fa_sched;
+  a.work = (row == 2 || row == 1) && !std::getenv("PRLAB_ATTN_STATIC") ? p.fa_work : nullptr;  // (row kernels only)
   if (row == 2)
     launch_pdl(attn_fa_row_kernel<2>, dim3(grid), dim3(row_threads<2>()), kFaSmemBytes, st, p.tmQKV, a);
   else if (row == 1)

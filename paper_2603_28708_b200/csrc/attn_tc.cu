@@ -457,6 +457,7 @@ AttnPlan plan_attn_tc(const void* qkv, int64_t ld_qkv, void* ctx, int64_t ld_ctx
   p.causal = causal;
   p.ld_qkv = ld_qkv;
   p.ld_ctx = ld_ctx;
+  if (attn_fa_enabled()) p.fa_sched = attn_fa_schedule(B, S, H, causal);
   return p;
 }
 

@@ -176,6 +176,8 @@ struct AttnPlan {
   int64_t ld_qkv, ld_ctx;
   long long* dbg = nullptr;  // phase timestamps (debug)
   int unstab = 0;            // unstabilised softmax (full_fp16 fast path, kernels.cpp:155): no max shift
+  const int* fa_sched = nullptr;  // streaming kernel's balanced unit schedule (attn_fa_schedule)
+  int* fa_work = nullptr;         // its dynamic-schedule counter [2] (zeroed; owned by the caller's plan)
 };
 bool attn_tc_supported(int S, int hd);
 AttnPlan plan_attn_tc(const void* qkv, int64_t ld_qkv, void* ctx, int64_t ld_ctx, int B, int S,
@@ -187,6 +189,8 @@ void configure_attn_tc();
 // dispatches to it when no tap is requested unless PRLAB_ATTN_FA=0
 bool attn_fa_enabled();
 void launch_attn_fa(const AttnPlan& p, cudaStream_t st);
+// device table of the streaming kernel's per-CTA unit lists (built once per shape, at plan time)
+const int* attn_fa_schedule(int B, int S, int H, int causal);
 
 // --- fp32-policy linears on the tensor cores: 3xTF32 tcgen05 GEMM (gemm_tf32.cu) ---
 // lo = w - trunc19(w) (the part of each fp32 value kind::tf32 drops)

@@ -548,6 +548,7 @@ struct prlab_gpu_model {
     // fused head statistics (prlab_gpu_forward_nll_device): 0 = not planned, 1 = fused, 2 = unfused
     int rs_state = 0;
     GemmPlan rs_plan{};
+    DeviceBuffer attn_work;  // the streaming attention's dynamic-schedule counter (int [2])
     DeviceBuffer rs_buf;  // float4 [nslots][M] partials + float [M] target logits
   };
   std::map<std::tuple<int64_t, int64_t, uint64_t>, std::unique_ptr<Plan>> plans;
@@ -962,6 +963,9 @@ prlab_gpu_model::Plan& get_plan(prlab_gpu_model& m, int64_t B, int64_t S, const 
     }
     p.attn = plan_attn_tc(p.big16, 3 * h, p.xn16, h, static_cast<int>(B), static_cast<int>(S),
                           static_cast<int>(m.H), static_cast<int>(m.hd), m.d.archetype == 1);
+    p.attn_work.alloc(2 * sizeof(int));
+    PRLAB_CUDA(cudaMemset(p.attn_work.p, 0, 2 * sizeof(int)));
+    p.attn.fa_work = static_cast<int*>(p.attn_work.p);
     if (fast16) {
       for (auto& g : p.gemms) g.acc16 = true;
       p.attn.unstab = 1;
@@ -2106,6 +2110,17 @@ int prlab_gpu_attention_f16_device_dbg(const void* qkv, void* ctx, int64_t B, in
     AttnPlan p = plan_attn_tc(qkv, 3 * H * hd, ctx, H * hd, static_cast<int>(B), static_cast<int>(S),
                               static_cast<int>(H), static_cast<int>(hd), causal);
     p.dbg = dbg;
+    // the dynamic-schedule counter: one per host thread and device (this building block's calls
+    // from one thread are stream-ordered by contract; see prlab_gpu.h)
+    thread_local std::map<int, int*> work;
+    int dev = 0;
+    PRLAB_CUDA(cudaGetDevice(&dev));
+    int*& w = work[dev];
+    if (w == nullptr) {
+      PRLAB_CUDA(cudaMalloc(&w, 2 * sizeof(int)));
+      PRLAB_CUDA(cudaMemset(w, 0, 2 * sizeof(int)));
+    }
+    p.fa_work = w;
     launch_attn_tc(p, static_cast<cudaStream_t>(stream));
   });
 }

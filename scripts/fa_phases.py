@@ -20,11 +20,41 @@ def main():
     ctx = torch.empty(B * S, H * hd, device="cuda", dtype=torch.float16)
     for _ in range(3):
         pg.attention_f16_device(qkv, ctx, B, S, H, hd, 1)
-    dbg = torch.zeros(32 * 8, dtype=torch.int64, device="cuda")
+    dbg = torch.zeros(256 + 2 * 1024, dtype=torch.int64, device="cuda")
     pg._check(pg.lib().prlab_gpu_attention_f16_device_dbg(C.c_void_p(qkv.data_ptr()), C.c_void_p(ctx.data_ptr()),
                                                           B, S, H, hd, 1, None, C.c_void_p(dbg.data_ptr())))
     torch.cuda.synchronize()
-    d = dbg.cpu().numpy().reshape(32, 8).astype(np.float64)
+    raw = dbg.cpu().numpy().astype(np.float64)
+    d = raw[:256].reshape(32, 8)
+    sp = raw[256:].reshape(-1, 2)
+    sp = sp[sp[:, 0] > 0]
+    if len(sp):
+        t0 = sp[:, 0].min()
+        st, en = (sp[:, 0] - t0) / 1e3, (sp[:, 1] - t0) / 1e3
+        print(json.dumps({"ctas": len(sp), "start_us_max": round(float(st.max()), 2),
+                          "end_us": {"min": round(float(en.min()), 2), "median": round(float(np.median(en)), 2),
+                                     "p90": round(float(np.percentile(en, 90)), 2), "max": round(float(en.max()), 2)},
+                          "cta0_end_us": round(float(en[0]), 2)}))
+        # static schedule (attn_fa.cu fa_unit_at / fa_decode): blocks and units per CTA vs end time
+        g, items, nqt = len(sp), B * H, (S + 127) // 128
+        n = items * nqt
+        loads = []
+        for c in range(g):
+            blocks = units = 0
+            for k in range(64):
+                u = k * g + ((g - 1 - c) if (k & 1) else c)
+                if u >= n:
+                    break
+                qt = nqt - 1 - u // items
+                blocks += qt + 1
+                units += 1
+            loads.append((blocks, units))
+        by = {}
+        for c in range(g):
+            by.setdefault(loads[c], []).append(en[c])
+        print(json.dumps({"end_us_by_blocks_units": {f"{k[0]}b/{k[1]}u": round(float(np.mean(v)), 2) for k, v in sorted(by.items())},
+                          "sm_pair_end_us": [round(float(max(en[c], en[c + g // 2])), 1) for c in range(0, g // 2, 16)],
+                          "end_first_half_vs_second": [round(float(np.mean(en[:g // 2])), 2), round(float(np.mean(en[g // 2:])), 2)]}))
     rows = []
     for b in range(1, 31):
         if d[b, 0] == 0 or d[b + 1, 0] == 0:
