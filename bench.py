@@ -224,7 +224,8 @@ def run_reference_arm(args, wl):
 # ---------------------------------------------------------------------------
 # our arm
 # ---------------------------------------------------------------------------
-def kernel_profile(pg, torch, cfg, B, S, stream, reps=20, causal=1, model=None, d_ids=None, policy="hybrid"):
+def kernel_profile(pg, torch, cfg, B, S, stream, reps=20, causal=1, model=None, d_ids=None, policy="hybrid",
+                   nll_head=False):
     """Per-kernel device times of one forward's kernels (inputs resident): each kernel
     replayed `reps` times from a CUDA graph, CUDA events on the stream it runs on.
     With `model` given and a batch-1 shape (forward = the persistent trunk kernel + the
@@ -241,6 +242,7 @@ def kernel_profile(pg, torch, cfg, B, S, stream, reps=20, causal=1, model=None, 
     ctx = torch.empty(M, h, device=dev, dtype=torch.float16)
     L = cfg.num_layers
     ld_head = (V + 7) // 8 * 8
+    stats = torch.empty(((V + 255) // 256) * M * 4, device=dev) if nll_head else None
     small = model is not None and model.kernel_count(B, S, policy) == 2
     fl = pg.flop_count(cfg, B, S)
     # trunk: every layer's fp16 weights streamed from HBM once (they exceed L2 across the
@@ -260,6 +262,10 @@ def kernel_profile(pg, torch, cfg, B, S, stream, reps=20, causal=1, model=None, 
                       L, 2 * (M * f + h * f) + 8 * M * h, 2 * M * h * f),
         "gemm_head": (lambda st: pg.linear_f16_device(A, W, None, out16, M, V, h, ld_head, 3, st),
                       1, 2 * (M * h + V * h + M * V), 2 * M * h * V),
+        # the forward_nll step's head: log-softmax statistics fused into the epilogue, no logits
+        # (one float4 per row and 256-column n-block)
+        "gemm_head_nll": (lambda st: pg.linear_f16_device_ex(A, W, None, stats, M, V, h, M, 4, 256, 1, 2, st),
+                          1, 2 * (M * h + V * h) + 16 * M * ((V + 255) // 256), 2 * M * h * V),
         "attention": (lambda st: pg.attention_f16_device(qkv, ctx, B, S, H, hd, causal, st),
                       L, 2 * (M * 3 * h + M * h), 4 * B * S * S * h),
     }
@@ -267,6 +273,7 @@ def kernel_profile(pg, torch, cfg, B, S, stream, reps=20, causal=1, model=None, 
         items = {k: items[k] for k in ("fwd_small", "gemm_head")}
     else:
         del items["fwd_small"]
+        del items["gemm_head" if nll_head else "gemm_head_nll"]
     res = {}
     # each kernel is replayed `reps` times from one CUDA graph (as in the forward: PDL-chained,
     # no host launch gaps), timed with CUDA events on the stream the kernels run on
@@ -528,7 +535,7 @@ def run_ours(args, wl):
     prof, roof, cpu, c4ref = {}, None, None, None
     if env.rank == 0 and not args.no_profile:
         prof = kernel_profile(pg, torch, w.cfg, count, S, w.sp, causal=int(w.cfg.archetype == 1),
-                              model=w.model, d_ids=w.d_ids, policy=policy)
+                              model=w.model, d_ids=w.d_ids, policy=policy, nll_head=w.nll_mode)
         roof = roofline_of(prof, pk, wl)
 
     # ---- CPU baseline: the reference on this host (rank 0, N=1 only) ----

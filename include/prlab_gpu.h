@@ -276,7 +276,10 @@ int prlab_gpu_linear_f16_device(const void* A, const void* Wt, const float* bias
                                 int64_t M, int64_t N, int64_t K, int64_t ldo, int32_t epi,
                                 void* stream);
 /* Same with an explicit tile configuration (tuning sweeps): bn in {0 (auto), 64, 128, 256},
- * splits (0 = auto), lean (0 = auto, 1 = half-depth pipeline, -1 = full depth). */
+ * splits (0 = auto), lean (0 = auto, 1 = half-depth pipeline, -1 = full depth).  epi 4 (the
+ * LM head's fused log-softmax statistics, CTA-pair kernel only, M >= 512): out = float4
+ * [ceil(N / BN)][M] per-row (max, sum exp(v - max), first argmax column, non-finite flag)
+ * partials, no targets -- the head kernel of forward_nll_device, for timing. */
 int prlab_gpu_linear_f16_device_ex(const void* A, const void* Wt, const float* bias, void* out,
                                    int64_t M, int64_t N, int64_t K, int64_t ldo, int32_t epi,
                                    int32_t bn, int32_t splits, int32_t lean, void* stream);

@@ -2062,7 +2062,7 @@ int prlab_gpu_linear_f16_device_ex(const void* A, const void* Wt, const float* b
                                    int64_t N, int64_t K_, int64_t ldo, int32_t epi, int32_t bn, int32_t splits,
                                    int32_t lean, void* stream) {
   return guarded([&] {
-    if (epi < 0 || epi > 5 || epi == EPI_ROWSTAT) throw std::invalid_argument("unknown epilogue");
+    if (epi < 0 || epi > 5) throw std::invalid_argument("unknown epilogue");
     if (bn != 0 && bn != 64 && bn != 128 && bn != 256) throw std::invalid_argument("bn must be 64, 128 or 256");
     const GemmPlan p = plan_gemm_tc(A, K_, Wt, K_, bias, out, ldo, static_cast<int>(M), static_cast<int>(N),
                                     static_cast<int>(K_), epi, &global_split_scratch(), bn, splits, lean);
