@@ -330,3 +330,28 @@ def test_tc_linear_f32_logits_match_f16(M, N, ldo, bn, splits, lean):
     assert torch.isnan(o32[:, (N + 3) // 4 * 4:]).all()
     with pytest.raises(ValueError):
         pg.linear_f16_device(A, Wt, None, o32, M, N, K, ldo, 4)  # row statistics: not an output epilogue
+
+
+@pytest.mark.parametrize("B,S,causal", [(3, 384, 1), (5, 200, 0), (32, 512, 1), (1, 129, 1)])
+def test_streaming_attention_dynamic_schedule(B, S, causal, monkeypatch):
+    """The streaming kernel's dynamically claimed units (per-thread counter, re-armed by the
+    last CTA of each launch) give the same ctx bit for bit as the static schedule, launch
+    after launch, with shapes interleaved on the same counter."""
+    H, hd = 12, 64
+    g = torch.Generator(device="cuda").manual_seed(B * S + causal)
+    qkv = (torch.randn(B * S, 3 * H * hd, device="cuda", generator=g) * 1.5).half()
+    other = (torch.randn(2 * 256, 3 * H * hd, device="cuda", generator=g)).half()
+    octx = torch.empty(2 * 256, H * hd, device="cuda", dtype=torch.float16)
+    outs = []
+    for _ in range(3):
+        ctx = torch.full((B * S, H * hd), float("nan"), device="cuda", dtype=torch.float16)
+        pg.attention_f16_device(qkv, ctx, B, S, H, hd, causal)
+        pg.attention_f16_device(other, octx, 2, 256, H, hd, 1)  # another shape on the same counter
+        outs.append(ctx)
+    monkeypatch.setenv("PRLAB_ATTN_STATIC", "1")
+    ref = torch.full((B * S, H * hd), float("nan"), device="cuda", dtype=torch.float16)
+    pg.attention_f16_device(qkv, ref, B, S, H, hd, causal)
+    torch.cuda.synchronize()
+    assert torch.isfinite(ref.float()).all()
+    for o in outs:
+        assert torch.equal(o, ref)
