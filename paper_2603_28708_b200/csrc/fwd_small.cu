@@ -84,6 +84,8 @@ struct SmallArgs {
   __half *xn16, *ff16;
   float* part;                   // fp32 partial sums [split][M][h] (split = head for Wo, K split for FFN2)
   unsigned* gbar;                // grid barrier counter (zeroed before each launch)
+  unsigned* qkv_flags;           // per QKV task: completions so far (zeroed before each launch), or null
+                                 // when a grid barrier separates QKV from attention
   long long* dbg;                // optional [stage][grid][2] globaltimer (arrive, release)
 };
 
@@ -822,9 +824,18 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
       prefetch_layer_weights(a, a.lw[l + 1]);
     }
     // ---- QKV: N=16 tiles, full K, round16(round16(acc) + b) -> fp16 q|k|v (ff16 buffer)
-    for (int t = gid; t < t_qkv; t += gn)
+    // QKV -> attention without a grid barrier (a.qkv_flags): each task releases a counter once
+    // its q/k/v columns are stored (both CTAs of a pair count), and an attention task acquires
+    // only the 12 (pair: 6) tasks holding its head's q, k and v -- one L2 hop instead of the
+    // barrier's two, and no wait for unrelated heads
+    for (int t = gid; t < t_qkv; t += gn) {
       gemm_task<NQ, 2, 4, PAIR>(a, smem, c, mXn, mW + 0, t * NQ, 0, h / 64, nullptr, 0, w.bqkv, a.ff16, 3 * h);
-    grid_sync(a.gbar, target, a.dbg);
+      if (a.qkv_flags) {
+        __syncthreads();  // every thread's q/k/v stores precede the release
+        if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.qkv_flags + t) : "memory");
+      }
+    }
+    if (!a.qkv_flags) grid_sync(a.gbar, target, a.dbg);
     // ---- attention + Wo: (batch, head, 16-query block) tasks, head partials -> part[head]
     {
       // PAIR (M > 128): 32-query tasks -- at most 96 for S <= 128, one round on 148 CTAs
@@ -839,6 +850,23 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         // debug stamps: the heaviest causal task of head 0 (last query block)
         long long* ts = (a.dbg && qb == nqb - 1 && hh == 0 && b == 0 && threadIdx.x == 0) ? a.dbg + 230000 + l * 8 : nullptr;
+        if (a.qkv_flags) {  // this head's q | k | v column tasks are stored (acquire; attn_wo_task's
+                            // opening __syncthreads orders the whole CTA's loads after it)
+          constexpr int PER = 64 / NQ;
+          if (static_cast<int>(threadIdx.x) < 3 * PER) {
+            const int sec = static_cast<int>(threadIdx.x) / PER, j = static_cast<int>(threadIdx.x) % PER;
+            const unsigned* f = a.qkv_flags + (sec * h + hh * 64) / NQ + j;
+            const unsigned want = static_cast<unsigned>(l + 1) * (PAIR ? 2u : 1u);
+            const long long t0 = clock64();
+            while (ld_acquire(f) < want) {
+              if (clock64() - t0 > (1ll << 32)) {
+                printf("prlab_gpu watchdog: qkv flag timeout block %d task %d want %u\n", blockIdx.x,
+                       static_cast<int>(f - a.qkv_flags), want);
+                __trap();
+              }
+            }
+          }
+        }
         if (q32)
           attn_wo_task<32>(a, smem, mW + 1, wo_bar, n_att & 1, b, hh, qb * QB, ts);
         else
@@ -903,6 +931,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
 }
 
 constexpr size_t kSmem = SmemL::BAR + 16 * 8 + 24 * 4 + 16;
+static_assert(16 + 3 * 1024 / 16 <= (kBarRegionBytes / 4), "QKV flags fit the barrier region");
 static_assert(kSmem <= 227 * 1024, "fwd_small smem");
 
 
@@ -967,8 +996,9 @@ void launch_fwd_small(const FwdSmallPlan& p, cudaStream_t st) {
   a.ff16 = p.ff16;
   a.part = p.scratch;
   a.gbar = p.gbar;
+  a.qkv_flags = std::getenv("PRLAB_SMALL_QKV_BARRIER") ? nullptr : p.gbar + 16;  // (the bar region's tail)
   a.dbg = small_debug_stamps();
-  PRLAB_CUDA(cudaMemsetAsync(p.gbar, 0, sizeof(unsigned), st));
+  PRLAB_CUDA(cudaMemsetAsync(p.gbar, 0, kBarRegionBytes, st));  // the barrier counter and the QKV flags
   const bool pair = p.M > 128;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(pair ? num_sms() & ~1 : num_sms());

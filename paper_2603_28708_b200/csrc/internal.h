@@ -135,9 +135,10 @@ struct FwdSmallPlan {
   float* x;
   __half *xn16, *ff16;
   float* scratch;            // fwd_small_workspace_floats()
-  unsigned* gbar;
+  unsigned* gbar;            // kBarRegionBytes: the grid barrier counter, then per-QKV-task flags
   int embed_only = 0;        // debug: stop after the embedding stage (x = tok + pos)
 };
+constexpr size_t kBarRegionBytes = 64 + 4 * 512;
 bool fwd_small_supported(int64_t M, int64_t S, int64_t h, int64_t f, int64_t hd, int64_t L);
 size_t fwd_small_workspace_floats(int64_t M, int64_t h, int64_t f);
 void launch_fwd_small(const FwdSmallPlan& p, cudaStream_t st);

@@ -805,7 +805,7 @@ void plan_small(prlab_gpu_model& m, prlab_gpu_model::Plan& p, int64_t B, int64_t
   const int64_t M = B * S, h = m.h, f = m.f, L = m.L;
   ArenaPlan ap;
   const int s_scr = ap.add(fwd_small_workspace_floats(M, h, f) * 4);
-  const int s_bar = ap.add(64);
+  const int s_bar = ap.add(kBarRegionBytes);
   p.small_buf.alloc(ap.total);
   char* base = static_cast<char*>(p.small_buf.p);
   auto& maps = p.small_maps;
