@@ -84,8 +84,12 @@ struct SmallArgs {
   __half *xn16, *ff16;
   float* part;                   // fp32 partial sums [split][M][h] (split = head for Wo, K split for FFN2)
   unsigned* gbar;                // grid barrier counter (zeroed before each launch)
-  unsigned* qkv_flags;           // per QKV task: completions so far (zeroed before each launch), or null
-                                 // when a grid barrier separates QKV from attention
+  // Stage hand-offs without grid barriers (null: barriers): per-task completion counters,
+  // zeroed before each launch, released by the producing CTA(s) after their stores.
+  unsigned* qkv_flags;           // per QKV task (q|k|v columns of all rows)
+  unsigned* qkv_done;            // all QKV tasks (the row stage may overwrite xn16 after it)
+  unsigned* attn_flags;          // per attention task (b, head, query block): its Wo partial rows
+  unsigned* ffn1_flags;          // per FFN1 task: its GELU output columns
   long long* dbg;                // optional [stage][grid][2] globaltimer (arrive, release)
 };
 
@@ -832,7 +836,10 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
       gemm_task<NQ, 2, 4, PAIR>(a, smem, c, mXn, mW + 0, t * NQ, 0, h / 64, nullptr, 0, w.bqkv, a.ff16, 3 * h);
       if (a.qkv_flags) {
         __syncthreads();  // every thread's q/k/v stores precede the release
-        if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.qkv_flags + t) : "memory");
+        if (threadIdx.x == 0) {
+          asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.qkv_flags + t) : "memory");
+          asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.qkv_done) : "memory");
+        }
       }
     }
     if (!a.qkv_flags) grid_sync(a.gbar, target, a.dbg);
@@ -872,6 +879,10 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
         else
           attn_wo_task<kQB>(a, smem, mW + 1, wo_bar, n_att & 1, b, hh, qb * QB, ts);
         ++n_att;
+        if (a.qkv_flags) {  // this task's Wo partial rows are stored
+          __syncthreads();
+          if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.attn_flags + t) : "memory");
+        }
       }
       if (ats) ats[1] = globaltimer();
       // the scratch (generic writes) overlaps the B region the FFN1 weights are fetched into
@@ -879,28 +890,78 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
       __syncthreads();
       pre_ffn1(l);
     }
-    grid_sync(a.gbar, target, a.dbg);
+    if (!a.qkv_flags) grid_sync(a.gbar, target, a.dbg);
+    // rows of a query block wait for its H attention tasks (and for every QKV task: the row
+    // stage rewrites xn16, the QKV GEMMs' A operand)
+    auto wait_row = [&](int r, int tid0) {
+      const int QB = a.q32 ? 32 : kQB, nqb = (S + QB - 1) / QB;
+      const int i = static_cast<int>(threadIdx.x) - tid0;
+      if (r < 0 || i < 0 || i > H) return;
+      const unsigned* f = i < H ? a.attn_flags + ((r / S) * H + i) * nqb + (r % S) / QB : a.qkv_done;
+      const unsigned want = i < H ? static_cast<unsigned>(l + 1)
+                                  : static_cast<unsigned>((l + 1) * t_qkv) * (PAIR ? 2u : 1u);
+      const long long t0 = clock64();
+      while (ld_acquire(f) < want) {
+        if (clock64() - t0 > (1ll << 32)) {
+          printf("prlab_gpu watchdog: row flag timeout block %d row %d slot %d\n", blockIdx.x, r, i);
+          __trap();
+        }
+      }
+    };
     // ---- residual + LN2: x += round16(round16(sum over heads of the Wo partials) + bo)
     if (PAIR && M > static_cast<int>(gridDim.x) && h == 768 && H <= 12) {  // two rows per CTA at once
-      for (int r = blockIdx.x; r < M; r += 2 * gridDim.x)
-        residual_ln_rows2<12, 6>(a, r, r + static_cast<int>(gridDim.x) < M ? r + static_cast<int>(gridDim.x) : -1, H,
-                                 w.bo, w.ln2g, w.ln2b, red, false);
+      for (int r = blockIdx.x; r < M; r += 2 * gridDim.x) {
+        const int r2 = r + static_cast<int>(gridDim.x) < M ? r + static_cast<int>(gridDim.x) : -1;
+        if (a.qkv_flags) {
+          wait_row(r, 0);
+          wait_row(r2, 32);
+          __syncthreads();
+        }
+        residual_ln_rows2<12, 6>(a, r, r2, H, w.bo, w.ln2g, w.ln2b, red, false);
+      }
     } else {
-      for (int r = blockIdx.x; r < M; r += gridDim.x)
+      for (int r = blockIdx.x; r < M; r += gridDim.x) {
+        if (a.qkv_flags) {
+          wait_row(r, 0);
+          __syncthreads();
+        }
         residual_ln_row<16>(a, r, H, w.bo, w.ln2g, w.ln2b, red,
                             (a.dbg && blockIdx.x == 0) ? a.dbg + 200000 + l * 8 : nullptr);
+      }
     }
     grid_sync(a.gbar, target, a.dbg);
     // ---- FFN1 + GELU, full K
-    for (int t = gid; t < t_ffn1; t += gn)
+    for (int t = gid; t < t_ffn1; t += gn) {
       gemm_task<N1, 1, 4, PAIR>(a, smem, c, mXn, mW + 2, t * N1, 0, h / 64, nullptr, 0, w.b1, a.ff16, f);
+      if (a.qkv_flags) {  // this task's GELU columns are stored
+        __syncthreads();
+        if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(a.ffn1_flags + t) : "memory");
+      }
+    }
     pre_ffn2(l);
-    grid_sync(a.gbar, target, a.dbg);
-    // ---- FFN2: partials over K splits
-    for (int t = gid; t < t_ffn2; t += gn)
+    if (!a.qkv_flags) grid_sync(a.gbar, target, a.dbg);
+    // ---- FFN2: partials over K splits (a split waits only for the FFN1 tasks of its K range;
+    // gemm_task's TMA warp fences the generic->async proxy before loading them)
+    for (int t = gid; t < t_ffn2; t += gn) {
+      if (a.qkv_flags) {
+        const int per = kb_ffn2 * 64 / N1, i = static_cast<int>(threadIdx.x);
+        if (i < per) {
+          const unsigned* fl = a.ffn1_flags + (t % a.split_ffn2) * per + i;
+          const unsigned want = static_cast<unsigned>(l + 1) * (PAIR ? 2u : 1u);
+          const long long t0 = clock64();
+          while (ld_acquire(fl) < want) {
+            if (clock64() - t0 > (1ll << 32)) {
+              printf("prlab_gpu watchdog: ffn1 flag timeout block %d task %d\n", blockIdx.x, static_cast<int>(fl - a.ffn1_flags));
+              __trap();
+            }
+          }
+        }
+        __syncthreads();
+      }
       gemm_task<N2, 0, 4, PAIR>(a, smem, c, mFf, mW + 3, (t / a.split_ffn2) * N2, (t % a.split_ffn2) * kb_ffn2 * 64,
                                 kb_ffn2, a.part + static_cast<int64_t>(t % a.split_ffn2) * M * h, h, nullptr, nullptr,
                                 0);
+    }
     if (l + 1 < a.L) pre_qkv(l + 1);
     grid_sync(a.gbar, target, a.dbg);
     // ---- residual + LN1 of the next layer (or the final LN)
@@ -931,7 +992,9 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
 }
 
 constexpr size_t kSmem = SmemL::BAR + 16 * 8 + 24 * 4 + 16;
-static_assert(16 + 3 * 1024 / 16 <= (kBarRegionBytes / 4), "QKV flags fit the barrier region");
+static_assert(kFlagFfn1 - kFlagQkv >= 3 * 1024 / 16 && kFlagAttn - kFlagFfn1 >= 4096 / 32 &&
+                  kFlagAttn + 256 * 16 <= kBarRegionBytes / 4,
+              "per-task flags fit the barrier region (max tasks: QKV 3h/16, FFN1 f/32, attention B*H*ceil(S/16))");
 static_assert(kSmem <= 227 * 1024, "fwd_small smem");
 
 
@@ -996,7 +1059,13 @@ void launch_fwd_small(const FwdSmallPlan& p, cudaStream_t st) {
   a.ff16 = p.ff16;
   a.part = p.scratch;
   a.gbar = p.gbar;
-  a.qkv_flags = std::getenv("PRLAB_SMALL_QKV_BARRIER") ? nullptr : p.gbar + 16;  // (the bar region's tail)
+  {  // the bar region: [0] grid barrier, [1] QKV-done counter, then the per-task flags
+    const bool barriers = std::getenv("PRLAB_SMALL_BARRIERS") || std::getenv("PRLAB_SMALL_QKV_BARRIER");
+    a.qkv_flags = barriers ? nullptr : p.gbar + kFlagQkv;
+    a.qkv_done = p.gbar + 1;
+    a.ffn1_flags = p.gbar + kFlagFfn1;
+    a.attn_flags = p.gbar + kFlagAttn;
+  }
   a.dbg = small_debug_stamps();
   PRLAB_CUDA(cudaMemsetAsync(p.gbar, 0, kBarRegionBytes, st));  // the barrier counter and the QKV flags
   const bool pair = p.M > 128;

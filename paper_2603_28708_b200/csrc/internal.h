@@ -138,7 +138,8 @@ struct FwdSmallPlan {
   unsigned* gbar;            // kBarRegionBytes: the grid barrier counter, then per-QKV-task flags
   int embed_only = 0;        // debug: stop after the embedding stage (x = tok + pos)
 };
-constexpr size_t kBarRegionBytes = 64 + 4 * 512;
+constexpr int kFlagQkv = 16, kFlagFfn1 = kFlagQkv + 512, kFlagAttn = kFlagFfn1 + 256;  // u32 offsets
+constexpr size_t kBarRegionBytes = 4 * (kFlagAttn + 4096);
 bool fwd_small_supported(int64_t M, int64_t S, int64_t h, int64_t f, int64_t hd, int64_t L);
 size_t fwd_small_workspace_floats(int64_t M, int64_t h, int64_t f);
 void launch_fwd_small(const FwdSmallPlan& p, cudaStream_t st);

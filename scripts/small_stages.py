@@ -10,6 +10,10 @@ import sys
 import numpy as np
 import torch
 
+# the stage timeline needs a grid barrier at every stage boundary (the default trunk hands
+# QKV -> attention -> RLN2 and FFN1 -> FFN2 over per-task flags instead)
+os.environ.setdefault("PRLAB_SMALL_BARRIERS", "1")
+
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2603_28708_b200 as pg  # noqa: E402
 
