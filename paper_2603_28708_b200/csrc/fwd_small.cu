@@ -88,6 +88,9 @@ struct SmallArgs {
   // zeroed before each launch, released by the producing CTA(s) after their stores.
   unsigned* qkv_flags;           // per QKV task (q|k|v columns of all rows)
   unsigned* qkv_done;            // all QKV tasks (the row stage may overwrite xn16 after it)
+  unsigned* rows1_done;          // embed+LN1 / RLN1 rows done (the QKV GEMMs' A operand)
+  unsigned* rows2_done;          // RLN2 rows done (the FFN1 GEMMs' A operand)
+  unsigned* ffn2_done;           // FFN2 tasks done (every K split partial of every row)
   unsigned* attn_flags;          // per attention task (b, head, query block): its Wo partial rows
   unsigned* ffn1_flags;          // per FFN1 task: its GELU output columns
   long long* dbg;                // optional [stage][grid][2] globaltimer (arrive, release)
@@ -772,6 +775,25 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
   c.tc = 0;
   c.bpref = 0;
   unsigned target = 0;
+  const bool flags = a.qkv_flags != nullptr;  // stage hand-offs through counters, not grid barriers
+  auto release_add = [&](unsigned* ctr, unsigned n) {  // this CTA's stores, then +n (all threads call)
+    __syncthreads();
+    if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(ctr), "r"(n) : "memory");
+  };
+  auto wait_ge = [&](const unsigned* ctr, unsigned want) {  // all threads call
+    if (threadIdx.x == 0) {
+      const long long t0 = clock64();
+      while (ld_acquire(ctr) < want) {
+        if (clock64() - t0 > (1ll << 32)) {
+          printf("prlab_gpu watchdog: stage counter timeout block %d slot %d want %u seen %u\n", blockIdx.x,
+                 static_cast<int>(ctr - a.gbar), want, ld_acquire(ctr));
+          __trap();
+        }
+      }
+    }
+    __syncthreads();
+  };
+  const unsigned pairx = PAIR ? 2u : 1u;  // CTAs counting each pair task
   const CUtensorMap* mXn = a.maps + 0;
   const CUtensorMap* mFf = a.maps + 1;
   // task geometry (same on every CTA; PAIR: per CTA pair, N per pair task)
@@ -818,7 +840,11 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
     }
     ln_row(xv, act, h, a.lw[0].ln1g, a.lw[0].ln1b, a.xn16 + static_cast<int64_t>(r) * h, red);
   }
-  grid_sync(a.gbar, target, a.dbg);
+  if (!flags) {
+    grid_sync(a.gbar, target, a.dbg);
+  } else if (static_cast<int>(blockIdx.x) < M) {
+    release_add(a.rows1_done, static_cast<unsigned>((M - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1));
+  }
 
   for (int l = 0; l < (a.embed_only ? 0 : a.L); ++l) {
     const LayerW& w = a.lw[l];
@@ -832,6 +858,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
     // its q/k/v columns are stored (both CTAs of a pair count), and an attention task acquires
     // only the 12 (pair: 6) tasks holding its head's q, k and v -- one L2 hop instead of the
     // barrier's two, and no wait for unrelated heads
+    if (flags && gid < t_qkv) wait_ge(a.rows1_done, static_cast<unsigned>(M * (l + 1)));  // every xn16 row
     for (int t = gid; t < t_qkv; t += gn) {
       gemm_task<NQ, 2, 4, PAIR>(a, smem, c, mXn, mW + 0, t * NQ, 0, h / 64, nullptr, 0, w.bqkv, a.ff16, 3 * h);
       if (a.qkv_flags) {
@@ -929,7 +956,14 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
                             (a.dbg && blockIdx.x == 0) ? a.dbg + 200000 + l * 8 : nullptr);
       }
     }
-    grid_sync(a.gbar, target, a.dbg);
+    const unsigned my_rows = static_cast<int>(blockIdx.x) < M
+                                 ? static_cast<unsigned>((M - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1)
+                                 : 0u;
+    if (!flags)
+      grid_sync(a.gbar, target, a.dbg);
+    else if (my_rows)
+      release_add(a.rows2_done, my_rows);
+    if (flags && gid < t_ffn1) wait_ge(a.rows2_done, static_cast<unsigned>(M * (l + 1)));  // every LN2 row
     // ---- FFN1 + GELU, full K
     for (int t = gid; t < t_ffn1; t += gn) {
       gemm_task<N1, 1, 4, PAIR>(a, smem, c, mXn, mW + 2, t * N1, 0, h / 64, nullptr, 0, w.b1, a.ff16, f);
@@ -961,9 +995,13 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
       gemm_task<N2, 0, 4, PAIR>(a, smem, c, mFf, mW + 3, (t / a.split_ffn2) * N2, (t % a.split_ffn2) * kb_ffn2 * 64,
                                 kb_ffn2, a.part + static_cast<int64_t>(t % a.split_ffn2) * M * h, h, nullptr, nullptr,
                                 0);
+      if (flags) release_add(a.ffn2_done, 1u);
     }
     if (l + 1 < a.L) pre_qkv(l + 1);
-    grid_sync(a.gbar, target, a.dbg);
+    if (!flags)
+      grid_sync(a.gbar, target, a.dbg);
+    else if (my_rows)
+      wait_ge(a.ffn2_done, static_cast<unsigned>(t_ffn2 * (l + 1)) * pairx);  // every K-split partial
     // ---- residual + LN1 of the next layer (or the final LN)
     {
       const float* g = l + 1 < a.L ? a.lw[l + 1].ln1g : a.lnfg;
@@ -976,7 +1014,11 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
         for (int r = blockIdx.x; r < M; r += gridDim.x) residual_ln_row<8>(a, r, a.split_ffn2, w.b2, g, bb, red);
       }
     }
-    if (l + 1 < a.L) grid_sync(a.gbar, target, a.dbg);
+    if (!flags) {
+      if (l + 1 < a.L) grid_sync(a.gbar, target, a.dbg);
+    } else if (my_rows && l + 1 < a.L) {
+      release_add(a.rows1_done, my_rows);
+    }
   }
   pdl_trigger();
   tc_fence_before();
@@ -1063,6 +1105,9 @@ void launch_fwd_small(const FwdSmallPlan& p, cudaStream_t st) {
     const bool barriers = std::getenv("PRLAB_SMALL_BARRIERS") || std::getenv("PRLAB_SMALL_QKV_BARRIER");
     a.qkv_flags = barriers ? nullptr : p.gbar + kFlagQkv;
     a.qkv_done = p.gbar + 1;
+    a.rows1_done = p.gbar + 2;
+    a.rows2_done = p.gbar + 3;
+    a.ffn2_done = p.gbar + 4;
     a.ffn1_flags = p.gbar + kFlagFfn1;
     a.attn_flags = p.gbar + kFlagAttn;
   }
