@@ -630,8 +630,13 @@ __global__ void __launch_bounds__(row_threads<TPR>(), 2) attn_fa_row_kernel(cons
     // its exponentials in registers: the wait for the unit's last P.V (OFULL) then hides behind
     // that block's S load and exponent pass instead of stalling the row between units.
     struct Pending { float l; int64_t dst; bool live; } pe{0.0f, 0, false};
+    // the row's partial sums meet in shared memory, double-buffered by unit parity: a CTA's last
+    // unit may be a single block, and then no block-max barrier separates one epilogue's reads
+    // from the next epilogue's writes (compute-sanitizer racecheck)
+    static_assert(TPR == 1 || 1024 + 2 * TPR * 128 <= 6 * 256, "rsum double buffer fits the RED region");
     auto epilogue = [&](uint32_t qcount) {
-      if constexpr (TPR > 1) red[1024 + half * 128 + r] = pe.l;
+      float* rsum = red + 1024 + (qcount & 1) * (TPR * 128);
+      if constexpr (TPR > 1) rsum[half * 128 + r] = pe.l;
       mbar_wait(&bars[R_OFULL], qcount & 1);
       tc_fence_after();
       uint32_t o[OC];
@@ -643,9 +648,9 @@ __global__ void __launch_bounds__(row_threads<TPR>(), 2) attn_fa_row_kernel(cons
       float l = pe.l;
       if constexpr (TPR > 1) {  // every part's sum visible; the next rsum write is a unit (and a row barrier) later
         named_bar_sync(1 + quad, 32 * TPR);
-        float lt2 = red[1024 + r];
+        float lt2 = rsum[r];
 #pragma unroll
-        for (int q = 1; q < TPR; ++q) lt2 = __fadd_rn(lt2, red[1024 + q * 128 + r]);
+        for (int q = 1; q < TPR; ++q) lt2 = __fadd_rn(lt2, rsum[q * 128 + r]);
         l = lt2;
       }
       __syncwarp();
