@@ -794,6 +794,11 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
     __syncthreads();
   };
   const unsigned pairx = PAIR ? 2u : 1u;  // CTAs counting each pair task
+  // debug (flag mode): per-CTA end time of each stage, [layer][6][grid] (scripts/flag_timeline.py)
+  auto stamp = [&](int l, int stage) {
+    if (a.dbg && flags && threadIdx.x == 0)
+      a.dbg[250000 + (static_cast<int64_t>(l) * 6 + stage) * gridDim.x + blockIdx.x] = globaltimer();
+  };
   const CUtensorMap* mXn = a.maps + 0;
   const CUtensorMap* mFf = a.maps + 1;
   // task geometry (same on every CTA; PAIR: per CTA pair, N per pair task)
@@ -869,6 +874,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
         }
       }
     }
+    stamp(l, 0);
     if (!a.qkv_flags) grid_sync(a.gbar, target, a.dbg);
     // ---- attention + Wo: (batch, head, 16-query block) tasks, head partials -> part[head]
     {
@@ -912,6 +918,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
         }
       }
       if (ats) ats[1] = globaltimer();
+      stamp(l, 1);
       // the scratch (generic writes) overlaps the B region the FFN1 weights are fetched into
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       __syncthreads();
@@ -956,6 +963,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
                             (a.dbg && blockIdx.x == 0) ? a.dbg + 200000 + l * 8 : nullptr);
       }
     }
+    stamp(l, 2);
     const unsigned my_rows = static_cast<int>(blockIdx.x) < M
                                  ? static_cast<unsigned>((M - 1 - static_cast<int>(blockIdx.x)) / static_cast<int>(gridDim.x) + 1)
                                  : 0u;
@@ -973,6 +981,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
       }
     }
     pre_ffn2(l);
+    stamp(l, 3);
     if (!a.qkv_flags) grid_sync(a.gbar, target, a.dbg);
     // ---- FFN2: partials over K splits (a split waits only for the FFN1 tasks of its K range;
     // gemm_task's TMA warp fences the generic->async proxy before loading them)
@@ -998,6 +1007,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
       if (flags) release_add(a.ffn2_done, 1u);
     }
     if (l + 1 < a.L) pre_qkv(l + 1);
+    stamp(l, 4);
     if (!flags)
       grid_sync(a.gbar, target, a.dbg);
     else if (my_rows)
@@ -1019,6 +1029,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
     } else if (my_rows && l + 1 < a.L) {
       release_add(a.rows1_done, my_rows);
     }
+    stamp(l, 5);
   }
   pdl_trigger();
   tc_fence_before();
