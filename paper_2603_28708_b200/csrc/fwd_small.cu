@@ -566,36 +566,47 @@ __device__ void attn_wo_task(const SmallArgs& a, uint8_t* smem, const CUtensorMa
   // Wo partial: out[QB][h] = ctx . WoSlice^T; warp w -> n-tiles [w * h/64, (w+1) * h/64) (pairs)
   mbar_wait(wo_bar, wo_phase);
   if (ts) ts[5] = globaltimer();
+  // every row block's ctx fragments stay in registers, so each Wo fragment is loaded once for
+  // all of them (QB = 32: half the ldmatrix traffic of a row-block-outer loop)
+  uint32_t af[MB][4][4];
 #pragma unroll
-  for (int mb = 0; mb < MB; ++mb) {
-    uint32_t af[4][4];
+  for (int mb = 0; mb < MB; ++mb)
 #pragma unroll
     for (int ks = 0; ks < 4; ++ks)
-      ldsm_x4(smem_u32(sC + (mb * 16 + (lane & 15)) * kRowH + ks * 16 + (lane >> 4) * 8), af[ks]);
+      ldsm_x4(smem_u32(sC + (mb * 16 + (lane & 15)) * kRowH + ks * 16 + (lane >> 4) * 8), af[mb][ks]);
+  {
     const int per_warp = h / 64;  // n-tiles of 8 columns per warp (h / 8 tiles over 8 warps)
     float* outp = a.part + static_cast<int64_t>(hh) * a.M * h;
-    const int row0 = b * S + q0 + mb * 16, qr = q0 + mb * 16;
-#pragma unroll 2
+    constexpr int kUnroll = MB == 1 ? 2 : 1;  // two independent column pairs in flight for one row block
+#pragma unroll kUnroll
     for (int p2 = 0; p2 < per_warp; p2 += 2) {
       const int n0 = (warp * per_warp + p2) * 8;
-      float d[2][4] = {};
+      float d[MB][2][4] = {};
       const int n = n0 + (lane & 7) + (lane >> 4) * 8;
 #pragma unroll
       for (int ks = 0; ks < 4; ++ks) {
         uint32_t bf[4];
         const int chunk = ks * 2 + ((lane >> 3) & 1);
         ldsm_x4(smem_u32(sWo + n * 128 + ((chunk ^ (n & 7)) << 4)), bf);
-        mma16816(d[0], af[ks], bf[0], bf[1]);
-        mma16816(d[1], af[ks], bf[2], bf[3]);
+#pragma unroll
+        for (int mb = 0; mb < MB; ++mb) {
+          mma16816(d[mb][0], af[mb][ks], bf[0], bf[1]);
+          mma16816(d[mb][1], af[mb][ks], bf[2], bf[3]);
+        }
       }
 #pragma unroll
-      for (int nt = 0; nt < 2; ++nt) {
-        const int col = n0 + nt * 8 + 2 * t4;
-        if (qr + g < S)
-          *reinterpret_cast<float2*>(outp + static_cast<int64_t>(row0 + g) * h + col) = make_float2(d[nt][0], d[nt][1]);
-        if (qr + g + 8 < S)
-          *reinterpret_cast<float2*>(outp + static_cast<int64_t>(row0 + g + 8) * h + col) =
-              make_float2(d[nt][2], d[nt][3]);
+      for (int mb = 0; mb < MB; ++mb) {
+        const int row0 = b * S + q0 + mb * 16, qr = q0 + mb * 16;
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) {
+          const int col = n0 + nt * 8 + 2 * t4;
+          if (qr + g < S)
+            *reinterpret_cast<float2*>(outp + static_cast<int64_t>(row0 + g) * h + col) =
+                make_float2(d[mb][nt][0], d[mb][nt][1]);
+          if (qr + g + 8 < S)
+            *reinterpret_cast<float2*>(outp + static_cast<int64_t>(row0 + g + 8) * h + col) =
+                make_float2(d[mb][nt][2], d[mb][nt][3]);
+        }
       }
     }
   }
