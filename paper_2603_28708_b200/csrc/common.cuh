@@ -255,6 +255,51 @@ __device__ __forceinline__ void bulk_wait() {
 }
 
 // ---------------------------------------------------------------------------
+// Hybrid LayerNorm of one row held by a warp (lane owns float4 columns lane + 32 i, n =
+// 128 VPT): two-pass fp32 mean / population variance like layernorm_lastdim
+// (src/kernels.cpp:170-219), y = gamma ((x - mean) inv) + beta, round16 -> fp16 row.
+// Shared by the standalone LN kernel and the GEMM epilogues that fuse it (one summation
+// order, so both paths give the same bits).
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ float ln_warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+template <int VPT>
+__device__ __forceinline__ void ln_row_f16(const float4 (&v)[VPT], int lane, const float* __restrict__ gamma,
+                                           const float* __restrict__ beta, float eps, __half* __restrict__ out_row) {
+  constexpr int n = 128 * VPT;
+  float s = 0.0f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+  s = ln_warp_sum(s);
+  const float mean = __fdiv_rn(s, static_cast<float>(n));
+  float vs = 0.0f;
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const float a = __fsub_rn(v[i].x, mean), b = __fsub_rn(v[i].y, mean);
+    const float c = __fsub_rn(v[i].z, mean), d = __fsub_rn(v[i].w, mean);
+    vs += (__fmul_rn(a, a) + __fmul_rn(b, b)) + (__fmul_rn(c, c) + __fmul_rn(d, d));
+  }
+  vs = ln_warp_sum(vs);
+  const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(vs, static_cast<float>(n)), eps)));
+  const float4* g4 = reinterpret_cast<const float4*>(gamma);
+  const float4* b4 = reinterpret_cast<const float4*>(beta);
+  uint2* o = reinterpret_cast<uint2*>(out_row);
+#pragma unroll
+  for (int i = 0; i < VPT; ++i) {
+    const float4 g = __ldg(g4 + lane + 32 * i), b = __ldg(b4 + lane + 32 * i);
+    const float y0 = __fadd_rn(__fmul_rn(g.x, __fmul_rn(__fsub_rn(v[i].x, mean), inv)), b.x);
+    const float y1 = __fadd_rn(__fmul_rn(g.y, __fmul_rn(__fsub_rn(v[i].y, mean), inv)), b.y);
+    const float y2 = __fadd_rn(__fmul_rn(g.z, __fmul_rn(__fsub_rn(v[i].z, mean), inv)), b.z);
+    const float y3 = __fadd_rn(__fmul_rn(g.w, __fmul_rn(__fsub_rn(v[i].w, mean), inv)), b.w);
+    __half2 h01 = __floats2half2_rn(y0, y1), h23 = __floats2half2_rn(y2, y3);
+    o[lane + 32 * i] = make_uint2(*reinterpret_cast<uint32_t*>(&h01), *reinterpret_cast<uint32_t*>(&h23));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // tcgen05 (5th-gen tensor cores, TMEM)
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {

@@ -250,8 +250,6 @@ __global__ void __launch_bounds__(256) ln_f16_kernel(const float* x, int rows,
 #pragma unroll
     for (int i = 0; i < VPT; ++i) nxt[i] = __ldg(in + lane + 32 * i);
   }
-  const float4* g4 = reinterpret_cast<const float4*>(gamma);
-  const float4* b4 = reinterpret_cast<const float4*>(beta);
   for (; row < rows; row += stride) {
     float4 v[VPT];
 #pragma unroll
@@ -272,31 +270,7 @@ __global__ void __launch_bounds__(256) ln_f16_kernel(const float* x, int rows,
 #pragma unroll
       for (int i = 0; i < VPT; ++i) nxt[i] = __ldg(in + lane + 32 * i);
     }
-    float s = 0.0f;
-#pragma unroll
-    for (int i = 0; i < VPT; ++i) s += (v[i].x + v[i].y) + (v[i].z + v[i].w);
-    s = warp_sum(s);
-    const float mean = __fdiv_rn(s, static_cast<float>(n));
-    float vs = 0.0f;
-#pragma unroll
-    for (int i = 0; i < VPT; ++i) {
-      const float a = __fsub_rn(v[i].x, mean), b = __fsub_rn(v[i].y, mean);
-      const float c = __fsub_rn(v[i].z, mean), d = __fsub_rn(v[i].w, mean);
-      vs += (__fmul_rn(a, a) + __fmul_rn(b, b)) + (__fmul_rn(c, c) + __fmul_rn(d, d));
-    }
-    vs = warp_sum(vs);
-    const float inv = __fdiv_rn(1.0f, __fsqrt_rn(__fadd_rn(__fdiv_rn(vs, static_cast<float>(n)), eps)));
-    uint2* o = reinterpret_cast<uint2*>(out + static_cast<int64_t>(row) * n);
-#pragma unroll
-    for (int i = 0; i < VPT; ++i) {
-      const float4 g = __ldg(g4 + lane + 32 * i), b = __ldg(b4 + lane + 32 * i);
-      const float y0 = __fadd_rn(__fmul_rn(g.x, __fmul_rn(__fsub_rn(v[i].x, mean), inv)), b.x);
-      const float y1 = __fadd_rn(__fmul_rn(g.y, __fmul_rn(__fsub_rn(v[i].y, mean), inv)), b.y);
-      const float y2 = __fadd_rn(__fmul_rn(g.z, __fmul_rn(__fsub_rn(v[i].z, mean), inv)), b.z);
-      const float y3 = __fadd_rn(__fmul_rn(g.w, __fmul_rn(__fsub_rn(v[i].w, mean), inv)), b.w);
-      __half2 h01 = __floats2half2_rn(y0, y1), h23 = __floats2half2_rn(y2, y3);
-      o[lane + 32 * i] = make_uint2(*reinterpret_cast<uint32_t*>(&h01), *reinterpret_cast<uint32_t*>(&h23));
-    }
+    ln_row_f16<VPT>(v, lane, gamma, beta, eps, out + static_cast<int64_t>(row) * n);
   }
 }
 
