@@ -875,6 +875,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
     // only the 12 (pair: 6) tasks holding its head's q, k and v -- one L2 hop instead of the
     // barrier's two, and no wait for unrelated heads
     if (flags && gid < t_qkv) wait_ge(a.rows1_done, static_cast<unsigned>(M * (l + 1)));  // every xn16 row
+    if (a.dbg && flags && threadIdx.x == 0) a.dbg[262000 + l * gridDim.x + blockIdx.x] = globaltimer();  // (debug)
     for (int t = gid; t < t_qkv; t += gn) {
       gemm_task<NQ, 2, 4, PAIR>(a, smem, c, mXn, mW + 0, t * NQ, 0, h / 64, nullptr, 0, w.bqkv, a.ff16, 3 * h);
       if (a.qkv_flags) {

@@ -45,6 +45,11 @@ for l in range(L):
 agg = {}
 for r in rows:
     agg.setdefault(r["stage"], []).append(r["last_us"])
+qw = dbg.cpu().numpy()[262000:262000 + L * G].astype(np.float64).reshape(L, G)
+if qw[1].max() > 0:  # QKV CTAs released from the rows wait, after the previous layer's last RLN1 row
+    rel = [(qw[l][qw[l] > 0] - last[l - 1, 5]) / 1e3 for l in range(1, L)]
+    print(json.dumps({"qkv_wait_release_after_last_rln1_us": {"median": round(float(np.median(np.concatenate(rel))), 2),
+                                                               "max": round(float(np.max(np.concatenate(rel))), 2)}}))
 print(json.dumps({"total_us": round((last[-1, 5] - t0) / 1e3, 1),
                   "per_stage_last_us_avg": {k: round(float(np.mean(v)), 2) for k, v in agg.items()}}))
 for r in rows[6:12]:
