@@ -28,6 +28,13 @@ def test_fwd_small_matches_multikernel_and_oracle(cfg, B, S, monkeypatch):
     _check_small(cfg, B, S, monkeypatch)
 
 
+@pytest.mark.parametrize("B,S", [(128, 1), (200, 1), (37, 3)], ids=["single-128x1", "pair-200x1", "pair-37x3"])
+def test_fwd_small_many_short_sequences(B, S, monkeypatch):
+    """Many one-to-three-token sequences: the most attention tasks / per-task flags the
+    barrier-free trunk has to track (B * heads * query blocks)."""
+    _check_small(GPT2_SMALLV, B, S, monkeypatch)
+
+
 @pytest.mark.parametrize("B,S", [(1, 128), (2, 100)], ids=["single", "pair"])
 def test_fwd_small_h1024(B, S, monkeypatch):
     """h = 1024 (16 heads, ffn 4096): 16 k-block weight slabs, 16-query attention tasks and
