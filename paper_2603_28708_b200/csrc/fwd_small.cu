@@ -984,6 +984,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
     else if (my_rows)
       release_add(a.rows2_done, my_rows);
     if (flags && gid < t_ffn1) wait_ge(a.rows2_done, static_cast<unsigned>(M * (l + 1)));  // every LN2 row
+    if (a.dbg && flags && threadIdx.x == 0) a.dbg[264000 + l * gridDim.x + blockIdx.x] = globaltimer();  // (debug)
     // ---- FFN1 + GELU, full K
     for (int t = gid; t < t_ffn1; t += gn) {
       gemm_task<N1, 1, 4, PAIR>(a, smem, c, mXn, mW + 2, t * N1, 0, h / 64, nullptr, 0, w.b1, a.ff16, f);

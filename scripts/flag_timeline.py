@@ -50,7 +50,23 @@ if qw[1].max() > 0:  # QKV CTAs released from the rows wait, after the previous 
     rel = [(qw[l][qw[l] > 0] - last[l - 1, 5]) / 1e3 for l in range(1, L)]
     print(json.dumps({"qkv_wait_release_after_last_rln1_us": {"median": round(float(np.median(np.concatenate(rel))), 2),
                                                                "max": round(float(np.max(np.concatenate(rel))), 2)}}))
+fw = dbg.cpu().numpy()[264000:264000 + L * G].astype(np.float64).reshape(L, G)
+if fw[1].max() > 0:  # FFN1 CTAs released from the RLN2-rows wait, and their task end (stage 3 stamp)
+    rel = np.concatenate([(fw[l][fw[l] > 0] - last[l, 2]) / 1e3 for l in range(1, L)])
+    dur = np.concatenate([(d[l, 3][fw[l] > 0] - fw[l][fw[l] > 0]) / 1e3 for l in range(1, L)])
+    print(json.dumps({"ffn1_wait_release_after_last_rln2_us": {"median": round(float(np.median(rel)), 2),
+                                                                "max": round(float(rel.max()), 2)},
+                      "ffn1_task_us": {"median": round(float(np.median(dur)), 2), "p90": round(float(np.percentile(dur, 90)), 2),
+                                       "max": round(float(dur.max()), 2)}}))
 print(json.dumps({"total_us": round((last[-1, 5] - t0) / 1e3, 1),
                   "per_stage_last_us_avg": {k: round(float(np.mean(v)), 2) for k, v in agg.items()}}))
 for r in rows[6:12]:
     print(json.dumps(r))
+gt = dbg.cpu().numpy()[220000:220000 + 64 * 8].astype(np.float64).reshape(64, 8)
+for t in range(3, 9):  # CTA 0's GEMM tasks of layer 1 (qkv, ffn1, ffn2): phases after the task start
+    g = gt[t]
+    if g[0] == 0:
+        break
+    print(json.dumps({"gemm_task_cta0": ["qkv", "ffn1", "ffn2"][t % 3], "b_ready_us": round((g[1] - g[0]) / 1e3, 2),
+                      "first_a_us": round((g[2] - g[0]) / 1e3, 2), "mma_issued_us": round((g[3] - g[0]) / 1e3, 2),
+                      "acc_ready_us": round((g[4] - g[0]) / 1e3, 2), "epilogue_done_us": round((g[5] - g[0]) / 1e3, 2)}))
