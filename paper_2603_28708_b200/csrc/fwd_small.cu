@@ -108,6 +108,18 @@ __device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
   asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
+// Spin (acquire) until *ctr >= want -- one stage hand-off counter; a protocol bug traps after
+// ~2 s instead of hanging the GPU (what: 0 QKV task, 1 row, 2 FFN1 task, 3 stage counter).
+__device__ __forceinline__ void spin_acquire(const unsigned* ctr, unsigned want, int what, int idx) {
+  const long long t0 = clock64();
+  while (ld_acquire(ctr) < want) {
+    if (clock64() - t0 > (1ll << 32)) {
+      printf("prlab_gpu watchdog: hand-off timeout (kind %d, index %d) block %d want %u seen %u\n", what, idx,
+             blockIdx.x, want, ld_acquire(ctr));
+      __trap();
+    }
+  }
+}
 
 // all CTAs are co-resident (cooperative launch, one CTA per SM).  Arrive = one
 // red.release.gpu (cumulative over the CTA's writes ordered by the bar.sync before it),
@@ -792,16 +804,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
     if (threadIdx.x == 0) asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(ctr), "r"(n) : "memory");
   };
   auto wait_ge = [&](const unsigned* ctr, unsigned want) {  // all threads call
-    if (threadIdx.x == 0) {
-      const long long t0 = clock64();
-      while (ld_acquire(ctr) < want) {
-        if (clock64() - t0 > (1ll << 32)) {
-          printf("prlab_gpu watchdog: stage counter timeout block %d slot %d want %u seen %u\n", blockIdx.x,
-                 static_cast<int>(ctr - a.gbar), want, ld_acquire(ctr));
-          __trap();
-        }
-      }
-    }
+    if (threadIdx.x == 0) spin_acquire(ctr, want, 3, static_cast<int>(ctr - a.gbar));
     __syncthreads();
   };
   const unsigned pairx = PAIR ? 2u : 1u;  // CTAs counting each pair task
@@ -907,16 +910,8 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
           constexpr int PER = 64 / NQ;
           if (static_cast<int>(threadIdx.x) < 3 * PER) {
             const int sec = static_cast<int>(threadIdx.x) / PER, j = static_cast<int>(threadIdx.x) % PER;
-            const unsigned* f = a.qkv_flags + (sec * h + hh * 64) / NQ + j;
-            const unsigned want = static_cast<unsigned>(l + 1) * (PAIR ? 2u : 1u);
-            const long long t0 = clock64();
-            while (ld_acquire(f) < want) {
-              if (clock64() - t0 > (1ll << 32)) {
-                printf("prlab_gpu watchdog: qkv flag timeout block %d task %d want %u\n", blockIdx.x,
-                       static_cast<int>(f - a.qkv_flags), want);
-                __trap();
-              }
-            }
+            const int task = (sec * h + hh * 64) / NQ + j;
+            spin_acquire(a.qkv_flags + task, static_cast<unsigned>(l + 1) * (PAIR ? 2u : 1u), 0, task);
           }
         }
         if (q32)
@@ -946,13 +941,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
       const unsigned* f = i < H ? a.attn_flags + ((r / S) * H + i) * nqb + (r % S) / QB : a.qkv_done;
       const unsigned want = i < H ? static_cast<unsigned>(l + 1)
                                   : static_cast<unsigned>((l + 1) * t_qkv) * (PAIR ? 2u : 1u);
-      const long long t0 = clock64();
-      while (ld_acquire(f) < want) {
-        if (clock64() - t0 > (1ll << 32)) {
-          printf("prlab_gpu watchdog: row flag timeout block %d row %d slot %d\n", blockIdx.x, r, i);
-          __trap();
-        }
-      }
+      spin_acquire(f, want, 1, r);
     };
     // ---- residual + LN2: x += round16(round16(sum over heads of the Wo partials) + bo)
     if (PAIR && M > static_cast<int>(gridDim.x) && h == 768 && H <= 12) {  // two rows per CTA at once
@@ -1002,15 +991,8 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
       if (a.qkv_flags) {
         const int per = kb_ffn2 * 64 / N1, i = static_cast<int>(threadIdx.x);
         if (i < per) {
-          const unsigned* fl = a.ffn1_flags + (t % a.split_ffn2) * per + i;
-          const unsigned want = static_cast<unsigned>(l + 1) * (PAIR ? 2u : 1u);
-          const long long t0 = clock64();
-          while (ld_acquire(fl) < want) {
-            if (clock64() - t0 > (1ll << 32)) {
-              printf("prlab_gpu watchdog: ffn1 flag timeout block %d task %d\n", blockIdx.x, static_cast<int>(fl - a.ffn1_flags));
-              __trap();
-            }
-          }
+          const int task = (t % a.split_ffn2) * per + i;
+          spin_acquire(a.ffn1_flags + task, static_cast<unsigned>(l + 1) * (PAIR ? 2u : 1u), 2, task);
         }
         __syncthreads();
       }
