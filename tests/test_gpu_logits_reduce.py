@@ -11,6 +11,7 @@ host restatements:
     value; the reference's validation errors.
 """
 import numpy as np
+import torch
 import pytest
 
 import paper_2603_28708_b200 as pg
@@ -179,3 +180,45 @@ def test_perplexity_fused_head_matches_unfused(monkeypatch):
     assert np.isfinite(a) and abs(a - b) <= 1e-6 * b, (a, b)
     fused.close()
     plain.close()
+
+
+@pytest.mark.parametrize("policy", ["full_fp16", "hybrid"])
+def test_forward_nll_fused_nonfinite_rows(policy, monkeypatch):
+    """The fused statistics epilogue on an adversarial model (fidelity.cpp:282-312): full_fp16's
+    unstabilised softmax poisons rows with NaN / inf; the fused head must flag exactly the rows
+    the logits + row_nll path flags (NaN NLL), give the same argmax and the same NLL elsewhere.
+    The NaN / inf tests are folded into the running sum / max there, not done per element."""
+    from oracle.oracle import make_adversarial_params
+    cfg = PRESETS["gpt2_small"].replace(num_layers=1, seed=3)
+    o = oracle()
+    probe = o.random_tokens(cfg.vocab, 1, 32, 5)
+    adv = make_adversarial_params(o, cfg, probe, 1, 32, 30.0)
+    B, S = 16, 32
+    M, V = B * S, cfg.vocab
+    ids = np.tile(probe, (B, 1)).astype(np.int32).ravel()
+    ids[32:] = o.random_tokens(V, B - 1, S, 9).ravel()  # first sequence = the probe itself
+    tg = np.roll(ids, -1).astype(np.int32)
+    d_ids, d_tg = torch.from_numpy(ids).cuda(), torch.from_numpy(tg).cuda()
+    res = []
+    for fused_on in (True, False):
+        if not fused_on:
+            monkeypatch.setenv("PRLAB_NO_FUSED_NLL", "1")
+        m = pg.DeviceModel(pg.ModelConfig(**cfg.__dict__), adv)
+        nll = torch.full((M,), -7.0, dtype=torch.float64, device="cuda")
+        am = torch.full((M,), -7, dtype=torch.int32, device="cuda")
+        f = m.forward_nll_device(d_ids.data_ptr(), d_tg.data_ptr(), B, S, policy, nll.data_ptr(), am.data_ptr())
+        torch.cuda.synchronize()
+        m.sync_status()
+        assert f == fused_on
+        res.append((nll.cpu().numpy(), am.cpu().numpy()))
+        m.close()
+    monkeypatch.delenv("PRLAB_NO_FUSED_NLL")
+    (a, am_a), (b, am_b) = res
+    bad_a, bad_b = ~np.isfinite(a), ~np.isfinite(b)
+    assert np.array_equal(bad_a, bad_b)
+    if policy == "full_fp16":
+        assert bad_a.any()  # the mechanism fired
+    else:
+        assert not bad_a.any()
+    assert np.array_equal(am_a[~bad_a], am_b[~bad_b])
+    assert np.max(np.abs(a[~bad_a] - b[~bad_b]), initial=0.0) <= 2e-6
