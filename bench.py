@@ -622,7 +622,7 @@ def run_stub(args, wl, env):
     preset, B, S, policy, desc = WORKLOADS[wl]
     start, count = replicas.rank_batch(B, env.world, env.rank, args.strong)
     a = np.ones((64, 64), np.float32)
-    delay = 0.002 * (1 + env.rank)  # rank 1 is the slow one: the max must win
+    delay = 0.002 * (1 + 3 * env.rank)  # rank 1 is 4x slower: the max must win (a margin load can't erase)
 
     def step():
         for _ in range(count):
