@@ -348,6 +348,9 @@ __device__ void gemm_task(const SmallArgs& a, uint8_t* smem, Ctl& c, const CUten
     const uint32_t taddr = c.tmem + ((quad * 32) << 16) + half * NH;
     if constexpr (NH == 8) {
       tmem_ld8(taddr, u);
+    } else if constexpr (NH == 24) {
+      tmem_ld16(taddr, *reinterpret_cast<uint32_t(*)[16]>(u));
+      tmem_ld8(taddr + 16, *reinterpret_cast<uint32_t(*)[8]>(u + 16));
     } else if constexpr (NH == 16) {
       tmem_ld16(taddr, u);
     } else {
@@ -749,7 +752,9 @@ __device__ void residual_ln_rows2(const SmallArgs& a, int r0, int r1, int nsplit
   (void)final_out;
 }
 
-template <bool PAIR>
+// N1P: the CTA-pair kernel's FFN1 task width (64, or 48 when it divides ffn: 64 tasks on the
+// 74 pairs instead of 48, a quarter less GELU epilogue per CTA)
+template <bool PAIR, int N1P = 64>
 __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_constant__ SmallArgs a) {
   // no static shared memory in this kernel: the dynamic window starts 1024-aligned, and
   // indexing it directly keeps every access in the shared state space (LDS/STS)
@@ -816,7 +821,7 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
   const CUtensorMap* mXn = a.maps + 0;
   const CUtensorMap* mFf = a.maps + 1;
   // task geometry (same on every CTA; PAIR: per CTA pair, N per pair task)
-  constexpr int NQ = PAIR ? 32 : 16, N1 = PAIR ? 64 : kTileN, N2 = PAIR ? 64 : kTileN;
+  constexpr int NQ = PAIR ? 32 : 16, N1 = PAIR ? N1P : kTileN, N2 = PAIR ? 64 : kTileN;
   const int gid = PAIR ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
   const int gn = PAIR ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
   const int t_qkv = 3 * h / NQ;                 // full K -> fp16 q/k/v
@@ -989,9 +994,11 @@ __global__ void __launch_bounds__(kThreads, 1) fwd_small_kernel(const __grid_con
     // gemm_task's TMA warp fences the generic->async proxy before loading them)
     for (int t = gid; t < t_ffn2; t += gn) {
       if (a.qkv_flags) {
-        const int per = kb_ffn2 * 64 / N1, i = static_cast<int>(threadIdx.x);
-        if (i < per) {
-          const int task = (t % a.split_ffn2) * per + i;
+        // the FFN1 tasks whose columns overlap this split's K range
+        const int c0 = (t % a.split_ffn2) * kb_ffn2 * 64, t_lo = c0 / N1, t_hi = (c0 + kb_ffn2 * 64 - 1) / N1;
+        const int i = static_cast<int>(threadIdx.x);
+        if (i <= t_hi - t_lo) {
+          const int task = t_lo + i;
           spin_acquire(a.ffn1_flags + task, static_cast<unsigned>(l + 1) * (PAIR ? 2u : 1u), 2, task);
         }
         __syncthreads();
@@ -1060,6 +1067,10 @@ bool fwd_small_supported(int64_t M, int64_t S, int64_t h, int64_t f, int64_t hd,
          h / 64 <= kMaxKB && (f / 512) <= 8 && (f / 512) * 64 <= kMaxKB * 64;
 }
 
+int fwd_small_pair_n1(int64_t f) {  // the CTA-pair kernel's FFN1 task width
+  return (f % 48 == 0 && !std::getenv("PRLAB_SMALL_N1_64")) ? 48 : 64;
+}
+
 size_t fwd_small_workspace_floats(int64_t M, int64_t h, int64_t f) {
   const int64_t heads = h / 64, sp_ffn2 = f / 512;  // Wo partials per head, FFN2 K splits
   return static_cast<size_t>(std::max(heads, sp_ffn2) * M * h + 64);
@@ -1072,6 +1083,8 @@ void launch_fwd_small(const FwdSmallPlan& p, cudaStream_t st) {
     PRLAB_CUDA(cudaFuncSetAttribute(fwd_small_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kSmem)));
     PRLAB_CUDA(cudaFuncSetAttribute(fwd_small_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    static_cast<int>(kSmem)));
+    PRLAB_CUDA(cudaFuncSetAttribute(fwd_small_kernel<true, 48>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                     static_cast<int>(kSmem)));
   });
   // 28 KB of kernel parameters, copied at launch: one per host thread (models driven from
@@ -1135,7 +1148,10 @@ void launch_fwd_small(const FwdSmallPlan& p, cudaStream_t st) {
   cfg.attrs = attr;
   cfg.numAttrs = pair ? 2 : 1;
   if (pair)
-    PRLAB_CUDA(cudaLaunchKernelEx(&cfg, fwd_small_kernel<true>, a));
+    if (fwd_small_pair_n1(p.f) == 48)
+      PRLAB_CUDA(cudaLaunchKernelEx(&cfg, fwd_small_kernel<true, 48>, a));
+    else
+      PRLAB_CUDA(cudaLaunchKernelEx(&cfg, fwd_small_kernel<true>, a));
   else
     PRLAB_CUDA(cudaLaunchKernelEx(&cfg, fwd_small_kernel<false>, a));
 }

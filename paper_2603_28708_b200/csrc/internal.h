@@ -142,6 +142,7 @@ constexpr int kFlagQkv = 16, kFlagFfn1 = kFlagQkv + 512, kFlagAttn = kFlagFfn1 +
 constexpr size_t kBarRegionBytes = 4 * (kFlagAttn + 4096);
 bool fwd_small_supported(int64_t M, int64_t S, int64_t h, int64_t f, int64_t hd, int64_t L);
 size_t fwd_small_workspace_floats(int64_t M, int64_t h, int64_t f);
+int fwd_small_pair_n1(int64_t f);
 void launch_fwd_small(const FwdSmallPlan& p, cudaStream_t st);
 long long*& small_debug_stamps();  // [stage][grid][2] globaltimer stamps target (debug; null = off)
 

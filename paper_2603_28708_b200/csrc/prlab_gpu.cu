@@ -822,13 +822,14 @@ void plan_small(prlab_gpu_model& m, prlab_gpu_model::Plan& p, int64_t B, int64_t
   for (int64_t l = 0; l < L; ++l) {
     const auto& w = m.l16[l];
     // per-task weight boxes: QKV N = 16, FFN1 / FFN2 N = 32 (M > 128, CTA pairs: each CTA half of
-    // the pair's N = 32 / 64 / 64 -- fwd_small.cu)
+    // the pair's N = 32 / 48 (64 when ffn % 48 != 0) / 64 -- fwd_small.cu)
     const bool pair = M > 128;
     maps.push_back(kblk(w.wqkv, 3 * h, h, 16, static_cast<uint32_t>(h / 64)));
     maps.push_back(make_tmap_f16_2d(w.wo, h, h, h, 256, 64));  // a head's Wo column slice, 256 rows per box
-    maps.push_back(kblk(w.w1, f, h, 32, static_cast<uint32_t>(h / 64)));
+    maps.push_back(kblk(w.w1, f, h, pair ? static_cast<uint32_t>(fwd_small_pair_n1(f) / 2) : 32u,
+                        static_cast<uint32_t>(h / 64)));  // (pair: each CTA half of the task's N)
     maps.push_back(kblk(w.w2, h, f, 32, static_cast<uint32_t>(kb_ffn2)));
-    (void)pair;  // the same boxes: a pair's N is twice the single-CTA N
+    // (QKV / FFN2: the same boxes serve both kernels -- a pair's N is twice the single-CTA N)
     p.small_lw[l] = {w.ln1g, w.ln1b, w.ln2g, w.ln2b, w.bqkv, w.bo, w.b1, w.b2, w.wqkv, w.wo, w.w1, w.w2};
   }
   FwdSmallPlan& sp = p.sp;
