@@ -100,3 +100,25 @@ def test_fwd_small_repeatable_under_back_to_back_launches(B, S):
     bad = [(i) for i in range(1, outs.shape[0]) if not torch.equal(outs[i], ref)]
     assert not bad, f"{len(bad)} of {outs.shape[0] - 1} repeats differ (first {bad[:5]})"
     m.close()
+
+
+@pytest.mark.parametrize("B,S", [(1, 128), (2, 96), (5, 13)], ids=["single", "pair", "ragged"])
+def test_fwd_small_counter_handoffs_match_grid_barriers(B, S, monkeypatch):
+    """The barrier-free trunk (per-task release counters) and the same kernel with a grid
+    barrier at every stage boundary (PRLAB_SMALL_BARRIERS=1) compute the same logits bit for
+    bit: only the synchronisation differs."""
+    cfg = GPT2_SMALLV
+    p = model_params(cfg)
+    ids = oracle().random_tokens(cfg.vocab, B, S, 17 + B)
+    flags = pg.DeviceModel(pg.ModelConfig(**cfg.__dict__), p)
+    a = flags.forward(ids, B, S, "hybrid")
+    # (read when the launch is recorded: a fresh model captures its forward graph with it set)
+    monkeypatch.setenv("PRLAB_SMALL_BARRIERS", "1")
+    barriers = pg.DeviceModel(pg.ModelConfig(**cfg.__dict__), p)
+    b = barriers.forward(ids, B, S, "hybrid")
+    b2 = barriers.forward(ids, B, S, "hybrid")
+    monkeypatch.delenv("PRLAB_SMALL_BARRIERS")
+    assert np.isfinite(a).all()
+    assert np.array_equal(a, b) and np.array_equal(b, b2)
+    flags.close()
+    barriers.close()
